@@ -1,0 +1,187 @@
+/*
+ * gfm_b200 -- C ABI of the B200-native (sm_100a) gfmkit training hot path.
+ *
+ * The reference (gfmkit, /root/reference/pkg/src/gfmkit) is pure Python +
+ * numpy and has no FFI; each entry point below replaces the numpy operation
+ * cited beside it (file:line relative to that package).  INTEGRATION.md shows
+ * the ctypes binding a gfmkit maintainer would add.
+ *
+ * Conventions
+ *  - Every function is stream-ordered on `stream` (a cudaStream_t passed as
+ *    void*), works on caller-owned DEVICE buffers, allocates nothing, and
+ *    returns 0 or a nonzero status (cudaError_t value, or GFM_EINVAL);
+ *    gfm_last_error() then holds a message (thread-local).
+ *  - Indices are int32.  Floating buffers are float32 (GFM_F32) or float64
+ *    (GFM_F64) per the `dtype` argument; positions are always float64.
+ *  - Node features are row-major [n_nodes][H].  A batch is a dst-sorted CSR
+ *    (rowptr[N+1], col_src[E], edge_dst[E], edge_w[E], edge_dx[E][3]) plus the
+ *    src-sorted CSC view (csc_ptr[N+1], csc_eid[E] = CSR position,
+ *    csc_dst[E]); CSR order equals the reference's stable dst sort
+ *    (model.py:260) so argmax indices and segment orders agree.
+ *  - Functions that size grids from an upper bound `e_cap` read the actual
+ *    edge count from rowptr[n_nodes] on the device (CUDA-graph friendly).
+ *  - Results are deterministic: no floating-point atomics; every reduction
+ *    has a fixed order chosen from shapes only.
+ */
+#ifndef GFM_B200_H
+#define GFM_B200_H
+
+#include <stddef.h>
+
+#if defined(__GNUC__)
+#define GFM_API __attribute__((visibility("default")))
+#else
+#define GFM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFM_ABI_VERSION 1
+
+enum { GFM_F32 = 0, GFM_F64 = 1 };
+enum { GFM_EINVAL = -1 };
+/* aggregation parts (bit order = column-block order of the output) */
+enum { GFM_PART_SUM = 1, GFM_PART_MEAN = 2, GFM_PART_MAX = 4, GFM_PART_STD = 8 };
+enum { GFM_FLAG_SCALAR = 1 }; /* force the scalar (numpy-order) kernels */
+
+/* ---- housekeeping ---------------------------------------------------- */
+GFM_API int gfm_abi_version(void);
+GFM_API const char* gfm_last_error(void);
+GFM_API int gfm_device_sm_count(void);
+GFM_API int gfm_stream_sync(void* stream);
+
+/* ---- K1/K2: batch geometry (preprocess.py:90-104, model.py:234-285) --- */
+/* gnode[i] = graph of node i (model.py:243) */
+GFM_API int gfm_graph_of_node(const int* node_offsets, int n_graphs, int* gnode, void* stream);
+/* out[0..n] = exclusive prefix sum of in[0..n) (np.cumsum, model.py:238) */
+GFM_API size_t gfm_scan_workspace_bytes(int n);
+GFM_API int gfm_exclusive_scan(const int* in, int n, int* out, void* workspace, void* stream);
+/* Radius graph replacing build_cutoff_edges (preprocess.py:90-104), emitted
+ * directly as the dst-sorted CSR make_batch builds (model.py:256-267).  The
+ * float64 predicate sqrt((dx^2+dy^2)+dz^2) <= rc is bit-exact against numpy.
+ * cells: NULL or per-graph orthorhombic box [n_graphs][3] (minimum image,
+ * needs rc < L/2); max_nbr > 0 keeps the max_nbr nearest sources per
+ * destination by (distance, source index).  Two passes: count -> scan ->
+ * fill. */
+GFM_API int gfm_radius_count(const double* pos, const int* node_offsets, const int* gnode, int n_nodes,
+                     const double* cells, double rc, int max_nbr, int* deg, void* stream);
+GFM_API int gfm_radius_fill(const double* pos, const int* node_offsets, const int* gnode, int n_nodes,
+                    const double* cells, double rc, int max_nbr, const int* rowptr, int* col_src,
+                    int* edge_dst, void* edge_w, void* edge_dx, int dtype, void* stream);
+/* make_batch for arbitrary record edge lists (model.py:245-267): stable dst
+ * sort -> CSR (order[p] = original edge index, model.py:260), w/dx from
+ * float64 positions (+ optional per-edge periodic shift), and the stable src
+ * sort -> CSC.  src/dst are global node ids in original order; edge_offsets
+ * [n_graphs+1] delimit each graph's edges. */
+GFM_API size_t gfm_csr_workspace_bytes(int n_nodes, int n_edges, int n_graphs);
+GFM_API int gfm_csr_build(const int* src, const int* dst, const int* edge_offsets, int n_graphs,
+                  const double* pos, const double* shift, int n_nodes, int n_edges, int* rowptr,
+                  int* col_src, int* edge_dst, void* edge_w, void* edge_dx, int* order,
+                  int* csc_ptr, int* csc_eid, int* csc_dst, int dtype, void* workspace,
+                  void* stream);
+/* CSC view of a CSR produced by gfm_radius_fill (workspace sized by
+ * gfm_csr_workspace_bytes(n_nodes, e_cap, n_graphs)). */
+GFM_API int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* edge_dst,
+                     const int* node_offsets, int n_graphs, int n_nodes, int e_cap, int* csc_ptr,
+                     int* csc_eid, int* csc_dst, void* workspace, void* stream);
+
+/* ---- K3/K4/K11: embedding and aggregation (model.py:293-341, 351-356) - */
+/* h = emb[z - 1] (model.py:351) */
+GFM_API int gfm_embed(const int* z, int n, const void* emb, int H, void* h, int dtype, void* stream);
+/* number of column blocks for a parts mask */
+GFM_API int gfm_agg_parts_count(int parts);
+/* agg[N][K*H] = per-dst reduction of msg = h[src] * w over the CSR rows
+ * (_aggregate, model.py:293-322; std/pna are extensions).  argmax [N][H]
+ * (max part) holds the first CSR position attaining the max; stat_mean
+ * [N][H] (std part) keeps the mean for the backward. */
+GFM_API int gfm_agg_fwd(const void* h, int n_nodes, int H, const int* rowptr, const int* col_src,
+                const void* edge_w, int parts, void* agg, int* argmax, void* stat_mean, int dtype,
+                int flags, void* stream);
+/* Backward as a CSC gather, no atomics (_aggregate_backward model.py:325-341
+ * + np.add.at(dh_in, src, dmsg * w) model.py:561): dh holds dz W on entry;
+ * out = (dh + gather) [* (1 - gate^2) when gate != NULL, model.py:553]. */
+GFM_API size_t gfm_agg_bwd_workspace_bytes(int n_nodes, int H, int parts, int dtype);
+GFM_API int gfm_agg_bwd(const void* dagg, const void* agg, const void* stat_mean, const int* argmax,
+                const void* h_in, const int* rowptr, const int* csc_ptr, const int* csc_eid,
+                const int* csc_dst, const void* edge_w, int n_nodes, int H, int parts, void* dh,
+                const void* gate, void* out, void* workspace, int dtype, int flags, void* stream);
+
+/* ---- K5/K9: dense layers (model.py:357-358, 365-372, 520-533, 549-558) */
+/* Y = act([X1 | X2] [W1 | W2]^T + bias), act 0 = identity, 1 = tanh */
+GFM_API int gfm_linear_fwd(const void* X1, int ld1, int K1, const void* X2, int ld2, int K2,
+                   const void* W1, int ldw1, const void* W2, int ldw2, const void* bias, int M,
+                   const int* M_dev, int N, int act, void* Y, int ldy, int dtype, void* stream);
+/* [out1 | out2] = dY [W1 | W2]; with gate: out1 *= (1 - gate^2) */
+GFM_API int gfm_linear_bwd_data(const void* dY, int ldd, int M, const int* M_dev, int N, const void* W1,
+                        int ldw1, int K1, const void* W2, int ldw2, int K2, void* out1, int ldo1,
+                        void* out2, int ldo2, const void* gate, int ldg, int dtype, void* stream);
+/* g1 = dY^T X1, g2 = dY^T X2, gb = colsum(dY): deterministic split-K */
+GFM_API size_t gfm_linear_bwd_weight_workspace_bytes(int M, int N, int K1, int K2, int with_bias,
+                                             int dtype);
+GFM_API int gfm_linear_bwd_weight(const void* dY, int ldd, int M, const int* M_dev, int N,
+                          const void* X1, int ld1, int K1, const void* X2, int ld2, int K2,
+                          int with_bias, void* g1, void* g2, void* gb, void* workspace, int dtype,
+                          void* stream);
+
+/* ---- K7/K10: force head (model.py:377-389, 535-547) ------------------- */
+/* pair = h[dst] + h[src]; t = tanh(pair V^T + c); m = t.u; f[dst] += m dx */
+GFM_API size_t gfm_force_fwd_workspace_bytes(int H, int e_cap, int dtype);
+GFM_API int gfm_force_fwd(const void* h, int H, int n_nodes, const int* rowptr, const int* col_src,
+                  const int* edge_dst, const void* edge_dx, int e_cap, const void* V,
+                  const void* c, const void* u, void* f_pred, void* m_out, void* workspace,
+                  int dtype, void* stream);
+/* grads of V, c, u and dh_final = dh_energy + scatter_dst(dpair) +
+ * scatter_src(dpair); dz_out = dh_final * (1 - h^2) when non-NULL. */
+GFM_API size_t gfm_force_bwd_workspace_bytes(int H, int e_cap, int dtype);
+GFM_API int gfm_force_bwd(const void* h, int H, int n_nodes, const int* rowptr, const int* col_src,
+                  const int* edge_dst, const void* edge_dx, int e_cap, const int* csc_ptr,
+                  const int* csc_eid, const void* V, const void* c, const void* u,
+                  const void* df, const void* dh_energy, void* grad_v, void* grad_c,
+                  void* grad_u, void* dh_out, void* dz_out, void* workspace, int dtype,
+                  void* stream);
+
+/* ---- K6/K8: energy readout, loss, seeds (model.py:365-373, 437-462, 510-533) */
+/* node_e = y a + c; e_pred = add.reduceat(node_e, node_offsets[:-1]) */
+GFM_API int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const void* c,
+                       const int* node_offsets, int n_graphs, void* node_e, void* e_pred,
+                       int dtype, void* stream);
+/* loss = [total, energy_term, force_term]; de, df = backward seeds;
+ * contrib (float32, optional) receives [total, 1.0] (train.py:257) */
+GFM_API int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_per, int n_graphs,
+                   const void* f_pred, const void* f_true, int n_nodes, double alpha_e,
+                   double alpha_f, void* loss, void* de, void* df, float* contrib, int dtype,
+                   void* stream);
+/* ds_i = de[g(i)]; dz = (ds_i a) * (1 - y^2)  (model.py:521-529) */
+GFM_API int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const void* a,
+                    const void* y, void* ds, void* dz, int dtype, void* stream);
+
+/* ---- K12: embedding gradient (model.py:564) --------------------------- */
+GFM_API size_t gfm_embedding_grad_workspace_bytes(int n_nodes, int H, int chunk, int dtype);
+GFM_API int gfm_embedding_grad(const int* z, int n_nodes, const void* dh, int H, int chunk, void* grad,
+                       void* workspace, int dtype, void* stream);
+
+/* ---- K13: optimiser and guard (train.py:96-108, 262-274) -------------- */
+/* *flag |= any(!isfinite(v)) */
+GFM_API int gfm_nonfinite_flag(const void* v, long long n, int dtype, int* flag, void* stream);
+/* Adam on float64 master weights: grad = grad_sum / world; bias_corr (device)
+ * = [1 - b1^t, 1 - b2^t]; skipped entirely when *skip_flag != 0; params32
+ * (optional) receives the float32 working copy. */
+GFM_API int gfm_adam_step(const void* grad_sum, int grad_dtype, long long n, double world, double* master,
+                  double* m, double* v, const double* bias_corr, double lr, double beta1,
+                  double beta2, double eps, const int* skip_flag, float* params32, void* stream);
+/* device step counter: *step += 1, bias_corr = [1 - b1^step, 1 - b2^step]
+ * (skipped when *skip_flag != 0) -- lets a CUDA-graph-captured step advance
+ * Adam without host involvement */
+GFM_API int gfm_adam_advance(long long* step, double beta1, double beta2, double* bias_corr,
+                             const int* skip_flag, void* stream);
+GFM_API int gfm_sgd_step(const void* grad_sum, int grad_dtype, long long n, double world, double* master,
+                 double lr, const int* skip_flag, float* params32, void* stream);
+GFM_API int gfm_cast_f64_to_f32(const double* in, long long n, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GFM_B200_H */

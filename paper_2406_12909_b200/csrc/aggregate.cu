@@ -1,0 +1,527 @@
+// Deterministic segmented aggregation over the dst-sorted CSR (forward) and
+// its backward as a src-sorted CSC gather -- no atomics anywhere.
+//
+// Reference: _aggregate / _aggregate_backward (model.py:293-341), the message
+// msg = h[src] * w (model.py:354) and the scatter dh_in[src] += dmsg * w
+// (model.py:561).  Extensions (parity unpinned): std (PyG convention) and
+// PNA = concat[sum, mean, max, std].
+//
+// Output row layout for the parts mask (bit order sum, mean, max, std): the
+// present parts are concatenated, each H wide.  argmax holds the CSR position
+// of the FIRST edge attaining the max per (node, column) (model.py:304-316),
+// -1 for an empty neighbourhood.
+//
+// Two instantiations:
+//  * vectorised float32 (H % 4 == 0, H/4 lanes per node up to 32 lanes with
+//    1, 2 or 4 float4 per lane): lanes of a node group read the neighbour's
+//    row slice with 16-byte coalesced loads, edges unrolled 4 deep for
+//    memory-level parallelism.  Accumulation is sequential in CSR order.
+//  * scalar (float64, or float32 with odd H): one thread per (node, column);
+//    sums follow numpy's reduceat order (x0 + pairwise(x1..)) with separately
+//    rounded operations, which makes the float64 result bit-identical to
+//    np.add.reduceat / np.maximum.reduceat.
+#include "common.cuh"
+
+namespace gfm {
+
+struct AggLayout {
+  int K;                          // number of parts
+  int o_sum, o_mean, o_max, o_std;  // column offset of each part (-1 absent)
+};
+
+__host__ __device__ inline AggLayout agg_layout(int parts, int H) {
+  AggLayout L;
+  int k = 0;
+  L.o_sum = (parts & GFM_PART_SUM) ? (k++) * H : -1;
+  L.o_mean = (parts & GFM_PART_MEAN) ? (k++) * H : -1;
+  L.o_max = (parts & GFM_PART_MAX) ? (k++) * H : -1;
+  L.o_std = (parts & GFM_PART_STD) ? (k++) * H : -1;
+  L.K = k;
+  return L;
+}
+
+// ------------------------------------------------------------ embedding
+template <typename T>
+__global__ void k_embed(const int* __restrict__ z, int n, const T* __restrict__ emb, int H,
+                        T* __restrict__ h) {
+  long long total = (long long)n * H;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx / H), c = (int)(idx % H);
+    h[idx] = emb[(long long)(z[i] - 1) * H + c];  // model.py:351
+  }
+}
+
+// ------------------------------------------------------------ forward, scalar
+template <typename T>
+__global__ void k_agg_fwd_scalar(const T* __restrict__ h, int n_nodes, int H,
+                                 const int* __restrict__ rowptr, const int* __restrict__ col_src,
+                                 const T* __restrict__ w, int parts, T* __restrict__ agg,
+                                 int* __restrict__ argmax, T* __restrict__ stat_mean) {
+  const AggLayout L = agg_layout(parts, H);
+  const int ld = L.K * H;
+  const long long total = (long long)n_nodes * H;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / H), c = (int)(idx % H);
+    const int beg = rowptr[i], end = rowptr[i + 1];
+    const int deg = end - beg;
+    T* out = agg + (long long)i * ld;
+    if (deg == 0) {
+      if (L.o_sum >= 0) out[L.o_sum + c] = T(0);
+      if (L.o_mean >= 0) out[L.o_mean + c] = T(0);
+      if (L.o_max >= 0) out[L.o_max + c] = T(0);
+      if (L.o_std >= 0) out[L.o_std + c] = T(0);
+      if (argmax && L.o_max >= 0) argmax[idx] = -1;
+      if (stat_mean) stat_mean[idx] = T(0);
+      continue;
+    }
+    auto msg = [&](long long p) -> T {
+      return mul_rn(h[(long long)col_src[p] * H + c], w[p]);
+    };
+    if (L.o_sum >= 0 || L.o_mean >= 0 || L.o_std >= 0) {
+      const T s1 = add_rn(msg(beg), np_pairwise<T>(msg, beg + 1, deg - 1));
+      const T dg = (T)deg;
+      const T mean = div_rn(s1, dg);
+      if (L.o_sum >= 0) out[L.o_sum + c] = s1;
+      if (L.o_mean >= 0) out[L.o_mean + c] = mean;
+      if (L.o_std >= 0) {  // moments in float64 (same ops as before for T = double)
+        auto md = [&](long long p) -> double { return (double)msg(p); };
+        auto sq = [&](long long p) -> double {
+          const double m = md(p);
+          return __dmul_rn(m, m);
+        };
+        const double s1d = __dadd_rn(md(beg), np_pairwise<double>(md, beg + 1, deg - 1));
+        const double s2d = __dadd_rn(sq(beg), np_pairwise<double>(sq, beg + 1, deg - 1));
+        const double mu = __ddiv_rn(s1d, (double)deg);
+        const double var = __dsub_rn(__ddiv_rn(s2d, (double)deg), __dmul_rn(mu, mu));
+        out[L.o_std + c] = var > 1e-5 ? (T)__dsqrt_rn(var) : T(0);
+        if (stat_mean) stat_mean[idx] = (T)mu;
+      }
+    }
+    if (L.o_max >= 0) {
+      T best = msg(beg);
+      int arg = beg;
+      for (int p = beg + 1; p < end; ++p) {
+        T m = msg(p);
+        if (m > best) {
+          best = m;
+          arg = p;
+        }
+      }
+      out[L.o_max + c] = best;
+      if (argmax) argmax[idx] = arg;
+    }
+  }
+}
+
+// ------------------------------------------------------------ forward, float4
+template <int NV, int LPN>
+__global__ void __launch_bounds__(256)
+    k_agg_fwd_vec(const float* __restrict__ h, int n_nodes, int H, const int* __restrict__ rowptr,
+                  const int* __restrict__ col_src, const float* __restrict__ w, int parts,
+                  float* __restrict__ agg, int* __restrict__ argmax, float* __restrict__ stat_mean) {
+  constexpr int NPW = 32 / LPN;  // nodes per warp
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % LPN;
+  const int node = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
+  if (node >= n_nodes) return;
+  const AggLayout L = agg_layout(parts, H);
+  const bool need_s = L.o_sum >= 0 || L.o_mean >= 0 || L.o_std >= 0;
+  const bool need_q = L.o_std >= 0;
+  const bool need_m = L.o_max >= 0;
+  const int beg = rowptr[node], end = rowptr[node + 1];
+  // std accumulates around the first message (x - x0) to avoid the
+  // E[x^2] - E[x]^2 cancellation in float32
+  float4 s[NV], d1[NV], q[NV], x0[NV], mx[NV];
+  int4 am[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    s[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    q[v] = s[v];
+    d1[v] = s[v];
+    x0[v] = s[v];
+    mx[v] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    am[v] = make_int4(-1, -1, -1, -1);
+  }
+  const float4* __restrict__ h4 = reinterpret_cast<const float4*>(h);
+  const int H4 = H >> 2;
+  auto consume = [&](const float4 (&r)[NV], float ww, int p) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      float4 m = make_float4(r[v].x * ww, r[v].y * ww, r[v].z * ww, r[v].w * ww);
+      if (need_s) {
+        s[v].x += m.x; s[v].y += m.y; s[v].z += m.z; s[v].w += m.w;
+      }
+      if (need_q) {
+        if (p == beg) x0[v] = m;
+        const float4 d = make_float4(m.x - x0[v].x, m.y - x0[v].y, m.z - x0[v].z, m.w - x0[v].w);
+        d1[v].x += d.x; d1[v].y += d.y; d1[v].z += d.z; d1[v].w += d.w;
+        q[v].x += d.x * d.x; q[v].y += d.y * d.y; q[v].z += d.z * d.z; q[v].w += d.w * d.w;
+      }
+      if (need_m) {
+        if (m.x > mx[v].x) { mx[v].x = m.x; am[v].x = p; }
+        if (m.y > mx[v].y) { mx[v].y = m.y; am[v].y = p; }
+        if (m.z > mx[v].z) { mx[v].z = m.z; am[v].z = p; }
+        if (m.w > mx[v].w) { mx[v].w = m.w; am[v].w = p; }
+      }
+    }
+  };
+  int p = beg;
+  for (; p + 4 <= end; p += 4) {
+    int sj[4];
+    float ww[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      sj[u] = __ldg(col_src + p + u);
+      ww[u] = __ldg(w + p + u);
+    }
+    float4 r[4][NV];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) r[u][v] = __ldg(h4 + (long long)sj[u] * H4 + v * LPN + sub);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) consume(r[u], ww[u], p + u);
+  }
+  for (; p < end; ++p) {
+    const int sj = __ldg(col_src + p);
+    const float ww = __ldg(w + p);
+    float4 r[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) r[v] = __ldg(h4 + (long long)sj * H4 + v * LPN + sub);
+    consume(r, ww, p);
+  }
+  const int deg = end - beg;
+  const float inv = deg > 0 ? 1.f / (float)deg : 0.f;
+  float4* out4 = reinterpret_cast<float4*>(agg + (long long)node * L.K * H);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int c4 = v * LPN + sub;
+    float4 mean = make_float4(s[v].x * inv, s[v].y * inv, s[v].z * inv, s[v].w * inv);
+    if (L.o_sum >= 0) out4[(L.o_sum >> 2) + c4] = s[v];
+    if (L.o_mean >= 0) out4[(L.o_mean >> 2) + c4] = mean;
+    if (need_m) {
+      float4 o = deg > 0 ? mx[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+      out4[(L.o_max >> 2) + c4] = o;
+      if (argmax) reinterpret_cast<int4*>(argmax + (long long)node * H)[c4] = am[v];
+    }
+    if (need_q) {
+      auto sd = [&](float sq, float sd1) {
+        const float mu = sd1 * inv;
+        float var = sq * inv - mu * mu;
+        return var > 1e-5f ? sqrtf(var) : 0.f;
+      };
+      float4 o = make_float4(sd(q[v].x, d1[v].x), sd(q[v].y, d1[v].y), sd(q[v].z, d1[v].z),
+                             sd(q[v].w, d1[v].w));
+      out4[(L.o_std >> 2) + c4] = o;
+      if (stat_mean) reinterpret_cast<float4*>(stat_mean + (long long)node * H)[c4] = mean;
+    }
+  }
+}
+
+// ------------------------------------------------------------ backward prep
+// G = dsum + dmean/deg - coef*mean,  coef = dstd / (deg*std)  (std > 0)
+template <typename T>
+__global__ void k_agg_bwd_prep(const T* __restrict__ dagg, const int* __restrict__ rowptr,
+                               int n_nodes, int H, int parts, const T* __restrict__ agg,
+                               const T* __restrict__ stat_mean, T* __restrict__ G,
+                               T* __restrict__ coef) {
+  const AggLayout L = agg_layout(parts, H);
+  const int ld = L.K * H;
+  const long long total = (long long)n_nodes * H;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / H), c = (int)(idx % H);
+    const int deg = rowptr[i + 1] - rowptr[i];
+    const T* d = dagg + (long long)i * ld;
+    T g = T(0);
+    if (L.o_sum >= 0) g = d[L.o_sum + c];
+    if (L.o_mean >= 0 && deg > 0) {
+      T m = div_rn(d[L.o_mean + c], (T)deg);  // model.py:333
+      g = (L.o_sum >= 0) ? add_rn(g, m) : m;
+    }
+    T cf = T(0);
+    if (L.o_std >= 0 && deg > 0) {
+      const T sd = agg[(long long)i * ld + L.o_std + c];
+      if (sd > T(0)) {
+        cf = d[L.o_std + c] / ((T)deg * sd);
+        g = g - cf * stat_mean[idx];
+      }
+    }
+    G[idx] = g;
+    if (coef) coef[idx] = cf;
+  }
+}
+
+// ------------------------------------------------------------ backward gather
+// dh[j] (= dz W on entry) += sum over CSC slots of w * dmsg, in CSC order
+// (np.add.at order).  dmsg = G[dst] + coef[dst]*msg + [argmax==p]*dmax[dst].
+// Optional epilogue: out = acc * (1 - gate^2) (the previous layer's tanh').
+template <typename T>
+__global__ void k_agg_bwd_scalar(const T* __restrict__ G, int ldg, const T* __restrict__ coef,
+                                 const T* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
+                                 const T* __restrict__ h_in, const int* __restrict__ csc_ptr,
+                                 const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
+                                 const T* __restrict__ w, int n_nodes, int H, T* __restrict__ dh,
+                                 const T* __restrict__ gate, T* __restrict__ out) {
+  const long long total = (long long)n_nodes * H;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / H), c = (int)(idx % H);
+    T acc = dh[idx];
+    const T hj = coef ? h_in[idx] : T(0);
+    for (int q = csc_ptr[j]; q < csc_ptr[j + 1]; ++q) {
+      const int p = csc_eid[q], i = csc_dst[q];
+      const T ww = w[p];
+      T dm = G ? G[(long long)i * ldg + c] : T(0);
+      if (coef) dm = dm + coef[(long long)i * H + c] * (hj * ww);
+      if (argmax) {
+        if (argmax[(long long)i * H + c] == p) dm = G || coef ? dm + dmax[(long long)i * ldm + c]
+                                                              : dmax[(long long)i * ldm + c];
+      }
+      acc = add_rn(acc, mul_rn(dm, ww));
+    }
+    if (gate) {
+      const T g = gate[idx];
+      out[idx] = mul_rn(acc, sub_rn(T(1), mul_rn(g, g)));  // model.py:553
+    } else {
+      out[idx] = acc;
+    }
+  }
+}
+
+template <int NV, int LPN>
+__global__ void __launch_bounds__(256)
+    k_agg_bwd_vec(const float* __restrict__ G, int ldg, const float* __restrict__ coef,
+                  const float* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
+                  const float* __restrict__ h_in, const int* __restrict__ csc_ptr,
+                  const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
+                  const float* __restrict__ w, int n_nodes, int H, float* __restrict__ dh,
+                  const float* __restrict__ gate, float* __restrict__ out) {
+  constexpr int NPW = 32 / LPN;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % LPN;
+  const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
+  if (j >= n_nodes) return;
+  const int H4 = H >> 2;
+  float4 acc[NV], hj[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const long long o = (long long)j * H4 + v * LPN + sub;
+    acc[v] = reinterpret_cast<const float4*>(dh)[o];
+    hj[v] = coef ? reinterpret_cast<const float4*>(h_in)[o] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int qb = csc_ptr[j], qe = csc_ptr[j + 1];
+  for (int q = qb; q < qe; ++q) {
+    const int p = __ldg(csc_eid + q), i = __ldg(csc_dst + q);
+    const float ww = __ldg(w + p);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c4 = v * LPN + sub;
+      float4 dm = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (G) dm = __ldg(reinterpret_cast<const float4*>(G + (long long)i * ldg) + c4);
+      if (coef) {
+        const float4 cf = __ldg(reinterpret_cast<const float4*>(coef + (long long)i * H) + c4);
+        dm.x += cf.x * (hj[v].x * ww); dm.y += cf.y * (hj[v].y * ww);
+        dm.z += cf.z * (hj[v].z * ww); dm.w += cf.w * (hj[v].w * ww);
+      }
+      if (argmax) {
+        const int4 a = __ldg(reinterpret_cast<const int4*>(argmax + (long long)i * H) + c4);
+        if (a.x == p || a.y == p || a.z == p || a.w == p) {
+          const float4 d = __ldg(reinterpret_cast<const float4*>(dmax + (long long)i * ldm) + c4);
+          if (a.x == p) dm.x += d.x;
+          if (a.y == p) dm.y += d.y;
+          if (a.z == p) dm.z += d.z;
+          if (a.w == p) dm.w += d.w;
+        }
+      }
+      acc[v].x += dm.x * ww; acc[v].y += dm.y * ww; acc[v].z += dm.z * ww; acc[v].w += dm.w * ww;
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const long long o = (long long)j * H4 + v * LPN + sub;
+    float4 r = acc[v];
+    if (gate) {
+      const float4 g = reinterpret_cast<const float4*>(gate)[o];
+      r.x *= 1.f - g.x * g.x; r.y *= 1.f - g.y * g.y; r.z *= 1.f - g.z * g.z; r.w *= 1.f - g.w * g.w;
+    }
+    reinterpret_cast<float4*>(out)[o] = r;
+  }
+}
+
+// ------------------------------------------------------------ dispatch
+static inline int grid_1d(long long n, int threads = 256) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 32) b = 148 * 32;
+  return (int)b;
+}
+
+// choose (NV, LPN) for the float4 path; returns false if H does not fit
+static bool vec_shape(int H, int& nv, int& lpn) {
+  if (H % 4) return false;
+  const int h4 = H / 4;
+  for (int v : {1, 2, 4}) {
+    if (h4 % v) continue;
+    int l = h4 / v;
+    if (l <= 32 && (l & (l - 1)) == 0) {
+      nv = v;
+      lpn = l;
+      return true;
+    }
+  }
+  return false;
+}
+
+#define GFM_VEC_CASES(MACRO) \
+  MACRO(1, 1) MACRO(1, 2) MACRO(1, 4) MACRO(1, 8) MACRO(1, 16) MACRO(1, 32) MACRO(2, 32) MACRO(4, 32)
+
+cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, const int* col_src,
+                    const void* w, int parts, void* agg, int* argmax, void* stat_mean,
+                    int force_scalar, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int nv = 0, lpn = 0;
+  if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn)) {
+    const int nodes_per_block = 8 * (32 / lpn);
+    const int grid = ceil_div(n, nodes_per_block);
+#define GFM_FWD_CASE(NV_, LPN_)                                                                \
+  if (nv == NV_ && lpn == LPN_) {                                                              \
+    k_agg_fwd_vec<NV_, LPN_><<<grid, 256, 0, s>>>((const float*)h, n, H, rowptr, col_src,      \
+                                                  (const float*)w, parts, (float*)agg, argmax, \
+                                                  (float*)stat_mean);                          \
+    return cudaGetLastError();                                                                 \
+  }
+    GFM_VEC_CASES(GFM_FWD_CASE)
+#undef GFM_FWD_CASE
+  }
+  if (dtype == GFM_F32)
+    k_agg_fwd_scalar<float><<<grid_1d((long long)n * H), 256, 0, s>>>(
+        (const float*)h, n, H, rowptr, col_src, (const float*)w, parts, (float*)agg, argmax,
+        (float*)stat_mean);
+  else
+    k_agg_fwd_scalar<double><<<grid_1d((long long)n * H), 256, 0, s>>>(
+        (const double*)h, n, H, rowptr, col_src, (const double*)w, parts, (double*)agg, argmax,
+        (double*)stat_mean);
+  return cudaGetLastError();
+}
+
+cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* stat_mean,
+                    const int* argmax, const void* h_in, const int* rowptr, const int* csc_ptr,
+                    const int* csc_eid, const int* csc_dst, const void* w, int n, int H, int parts,
+                    void* dh, const void* gate, void* out, void* ws, int force_scalar,
+                    cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const AggLayout L = agg_layout(parts, H);
+  const int ld = L.K * H;
+  const size_t esz = dtype == GFM_F32 ? 4 : 8;
+  // G: dsum alone needs no prep (read dagg in place); mean/std need G/coef
+  const void* G = nullptr;
+  int ldg = ld;
+  const void* coef = nullptr;
+  if (L.o_mean >= 0 || L.o_std >= 0) {
+    void* Gw = ws;
+    void* Cw = L.o_std >= 0 ? (void*)((char*)ws + esz * (size_t)n * H) : nullptr;
+    if (dtype == GFM_F32)
+      k_agg_bwd_prep<float><<<grid_1d((long long)n * H), 256, 0, s>>>(
+          (const float*)dagg, rowptr, n, H, parts, (const float*)agg, (const float*)stat_mean,
+          (float*)Gw, (float*)Cw);
+    else
+      k_agg_bwd_prep<double><<<grid_1d((long long)n * H), 256, 0, s>>>(
+          (const double*)dagg, rowptr, n, H, parts, (const double*)agg, (const double*)stat_mean,
+          (double*)Gw, (double*)Cw);
+    G = Gw;
+    ldg = H;
+    coef = Cw;
+  } else if (L.o_sum >= 0) {
+    G = (const char*)dagg + esz * L.o_sum;
+  }
+  const void* dmax = L.o_max >= 0 ? (const char*)dagg + esz * L.o_max : nullptr;
+  const int* am = L.o_max >= 0 ? argmax : nullptr;
+  int nv = 0, lpn = 0;
+  if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn)) {
+    const int nodes_per_block = 8 * (32 / lpn);
+    const int grid = ceil_div(n, nodes_per_block);
+#define GFM_BWD_CASE(NV_, LPN_)                                                              \
+  if (nv == NV_ && lpn == LPN_) {                                                            \
+    k_agg_bwd_vec<NV_, LPN_><<<grid, 256, 0, s>>>(                                           \
+        (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am,                \
+        (const float*)h_in, csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh,    \
+        (const float*)gate, (float*)out);                                                    \
+    return cudaGetLastError();                                                               \
+  }
+    GFM_VEC_CASES(GFM_BWD_CASE)
+#undef GFM_BWD_CASE
+  }
+  if (dtype == GFM_F32)
+    k_agg_bwd_scalar<float><<<grid_1d((long long)n * H), 256, 0, s>>>(
+        (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in,
+        csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,
+        (float*)out);
+  else
+    k_agg_bwd_scalar<double><<<grid_1d((long long)n * H), 256, 0, s>>>(
+        (const double*)G, ldg, (const double*)coef, (const double*)dmax, ld, am,
+        (const double*)h_in, csc_ptr, csc_eid, csc_dst, (const double*)w, n, H, (double*)dh,
+        (const double*)gate, (double*)out);
+  return cudaGetLastError();
+}
+
+}  // namespace gfm
+
+using namespace gfm;
+
+extern "C" {
+
+int gfm_agg_parts_count(int parts) { return agg_layout(parts, 1).K; }
+
+size_t gfm_agg_bwd_workspace_bytes(int n_nodes, int H, int parts, int dtype) {
+  const size_t esz = dtype == GFM_F32 ? 4 : 8;
+  return esz * (size_t)n_nodes * H * 2 + 256;
+}
+
+int gfm_embed(const int* z, int n, const void* emb, int H, void* h, int dtype, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GFM_F32)
+    k_embed<float><<<grid_1d((long long)n * H), 256, 0, s>>>(z, n, (const float*)emb, H, (float*)h);
+  else if (dtype == GFM_F64)
+    k_embed<double><<<grid_1d((long long)n * H), 256, 0, s>>>(z, n, (const double*)emb, H, (double*)h);
+  else {
+    set_error("gfm_embed: bad dtype %d", dtype);
+    return GFM_EINVAL;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) set_error("gfm_embed: %s", cudaGetErrorString(e));
+  return (int)e;
+}
+
+int gfm_agg_fwd(const void* h, int n_nodes, int H, const int* rowptr, const int* col_src,
+                const void* edge_w, int parts, void* agg, int* argmax, void* stat_mean, int dtype,
+                int flags, void* stream) {
+  if ((dtype != GFM_F32 && dtype != GFM_F64) || parts <= 0 || parts > 15 || H <= 0) {
+    set_error("gfm_agg_fwd: bad arguments (dtype %d parts %d H %d)", dtype, parts, H);
+    return GFM_EINVAL;
+  }
+  cudaError_t e = agg_fwd(dtype, h, n_nodes, H, rowptr, col_src, edge_w, parts, agg, argmax,
+                          stat_mean, flags & GFM_FLAG_SCALAR, (cudaStream_t)stream);
+  if (e != cudaSuccess) set_error("gfm_agg_fwd: %s", cudaGetErrorString(e));
+  return (int)e;
+}
+
+int gfm_agg_bwd(const void* dagg, const void* agg, const void* stat_mean, const int* argmax,
+                const void* h_in, const int* rowptr, const int* csc_ptr, const int* csc_eid,
+                const int* csc_dst, const void* edge_w, int n_nodes, int H, int parts, void* dh,
+                const void* gate, void* out, void* workspace, int dtype, int flags, void* stream) {
+  if ((dtype != GFM_F32 && dtype != GFM_F64) || parts <= 0 || parts > 15 || H <= 0) {
+    set_error("gfm_agg_bwd: bad arguments (dtype %d parts %d H %d)", dtype, parts, H);
+    return GFM_EINVAL;
+  }
+  cudaError_t e = agg_bwd(dtype, dagg, agg, stat_mean, argmax, h_in, rowptr, csc_ptr, csc_eid,
+                          csc_dst, edge_w, n_nodes, H, parts, dh, gate, out, workspace,
+                          flags & GFM_FLAG_SCALAR, (cudaStream_t)stream);
+  if (e != cudaSuccess) set_error("gfm_agg_bwd: %s", cudaGetErrorString(e));
+  return (int)e;
+}
+
+}  // extern "C"

@@ -1,0 +1,32 @@
+// C-ABI housekeeping: version, thread-local error text, device sync helper.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace gfm {
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+}  // namespace gfm
+
+extern "C" {
+
+int gfm_abi_version(void) { return GFM_ABI_VERSION; }
+
+const char* gfm_last_error(void) { return gfm::g_err; }
+
+int gfm_device_sm_count(void) { return gfm::num_sms(); }
+
+int gfm_stream_sync(void* stream) {
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) gfm::set_error("gfm_stream_sync: %s", cudaGetErrorString(e));
+  return (int)e;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// Shared device helpers for the gfm_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gfm_b200.h"
+
+#define GFM_WARP 32
+
+namespace gfm {
+
+// Thread-local last error (set by the C-ABI layer).
+void set_error(const char* fmt, ...);
+
+// ---------------------------------------------------------------------------
+// Exactly-rounded arithmetic.  nvcc contracts a*b+c into FMA by default; the
+// float64 parity paths (neighbour predicate, aggregation, Adam) must match
+// numpy's separately rounded operations, so they go through these.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+
+__device__ __forceinline__ float tanh_t(float x) { return tanhf(x); }
+__device__ __forceinline__ double tanh_t(double x) { return tanh(x); }
+
+template <typename T>
+__device__ __forceinline__ T sign_t(T x) {
+  return x > T(0) ? T(1) : (x < T(0) ? T(-1) : T(0));
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v, unsigned mask = 0xffffffffu) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// numpy's pairwise_sum (loops_utils.h.src) over a run of n values produced
+// by `get(i)`; used by the float64 instantiations so that add.reduceat
+// segments come out bit-identical: seg = x0 + pairwise(x1 .. x_{n}).
+template <typename T, typename Get>
+__device__ __forceinline__ T np_pairwise_leaf(const Get& get, long long b, long long m) {
+  if (m < 8) {
+    T r = T(0);
+    for (long long i = 0; i < m; ++i) r = add_rn(r, get(b + i));
+    return r;
+  }
+  T r0 = get(b + 0), r1 = get(b + 1), r2 = get(b + 2), r3 = get(b + 3);
+  T r4 = get(b + 4), r5 = get(b + 5), r6 = get(b + 6), r7 = get(b + 7);
+  long long i = 8;
+  for (; i < m - (m % 8); i += 8) {
+    r0 = add_rn(r0, get(b + i + 0)); r1 = add_rn(r1, get(b + i + 1));
+    r2 = add_rn(r2, get(b + i + 2)); r3 = add_rn(r3, get(b + i + 3));
+    r4 = add_rn(r4, get(b + i + 4)); r5 = add_rn(r5, get(b + i + 5));
+    r6 = add_rn(r6, get(b + i + 6)); r7 = add_rn(r7, get(b + i + 7));
+  }
+  T res = add_rn(add_rn(add_rn(r0, r1), add_rn(r2, r3)),
+                 add_rn(add_rn(r4, r5), add_rn(r6, r7)));
+  for (; i < m; ++i) res = add_rn(res, get(b + i));
+  return res;
+}
+
+template <typename T, typename Get>
+__device__ __noinline__ T np_pairwise_deep(const Get& get, long long base, long long n) {
+  // post-order walk of numpy's halving recursion with explicit stacks
+  long long sb[64], sn[64];
+  int st[64];
+  T vals[64];
+  int sp = 0, vp = 0;
+  sb[0] = base; sn[0] = n; st[0] = 0; sp = 1;
+  while (sp > 0) {
+    --sp;
+    long long b = sb[sp], m = sn[sp];
+    if (st[sp] == 1) {
+      T r = vals[--vp];
+      T l = vals[--vp];
+      vals[vp++] = add_rn(l, r);
+    } else if (m <= 128) {
+      vals[vp++] = np_pairwise_leaf<T>(get, b, m);
+    } else {
+      long long n2 = m / 2;
+      n2 -= n2 % 8;
+      st[sp] = 1; ++sp;                                   // combine after both
+      sb[sp] = b + n2; sn[sp] = m - n2; st[sp] = 0; ++sp; // right
+      sb[sp] = b; sn[sp] = n2; st[sp] = 0; ++sp;          // left first
+    }
+  }
+  return vals[0];
+}
+
+template <typename T, typename Get>
+__device__ __forceinline__ T np_pairwise(const Get& get, long long base, long long n) {
+  if (n <= 128) return np_pairwise_leaf<T>(get, base, n);
+  return np_pairwise_deep<T>(get, base, n);
+}
+
+}  // namespace gfm

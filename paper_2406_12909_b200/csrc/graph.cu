@@ -1,0 +1,520 @@
+// Batch geometry on device: radius graph -> dst-sorted CSR, stable CSR/CSC
+// construction for arbitrary record edge lists, scans and per-graph maps.
+//
+// Reference: build_cutoff_edges (preprocess.py:90-104) and make_batch
+// (model.py:234-285).  Layout produced for a batch of N nodes / E edges:
+//   rowptr[N+1], col_src[E], edge_dst[E], edge_w[E], edge_dx[E][3]
+//     -- CSR in (dst, src) order == the reference's stable dst sort
+//   csc_ptr[N+1], csc_eid[E] (CSR position of each src-sorted edge),
+//   csc_dst[E]   -- the stable src sort used by the backward gathers.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace gfm {
+
+// ---------------------------------------------------------------- helpers
+__global__ void k_graph_of_node(const int* __restrict__ off, int n_graphs, int* __restrict__ gnode) {
+  for (int g = blockIdx.x; g < n_graphs; g += gridDim.x)
+    for (int i = off[g] + threadIdx.x; i < off[g + 1]; i += blockDim.x) gnode[i] = g;
+}
+
+__global__ void k_iota(int* __restrict__ out, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
+}
+
+__global__ void k_zero_i32(int* __restrict__ out, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 0;
+}
+
+// count[key]++ over keys[0 .. n) where n = n_dev ? *n_dev : n_cap (int atomics:
+// the result is order independent, hence deterministic).
+__global__ void k_histogram(const int* __restrict__ keys, int n_cap, const int* __restrict__ n_dev,
+                            int* __restrict__ count) {
+  const int n = n_dev ? *n_dev : n_cap;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&count[keys[i]], 1);
+}
+
+// ------------------------------------------------------------ exclusive scan
+// out[0..n] = exclusive prefix of in[0..n), out[n] = total.  Three passes:
+// per-block totals, a single-block scan of the totals, per-block rescans.
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* tmp, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < (blockDim.x >> 5) ? tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    tmp[lane] = s;
+  }
+  __syncthreads();
+  total = tmp[(blockDim.x >> 5) - 1];
+  int before = wid ? tmp[wid - 1] : 0;
+  __syncthreads();
+  return before + x - v;
+}
+
+__global__ void k_scan_partials(const int* __restrict__ in, int n, int* __restrict__ partial) {
+  __shared__ int tmp[32];
+  const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (base + k < n) s += in[base + k];
+  int total;
+  block_excl_scan(s, tmp, total);
+  if (threadIdx.x == 0) partial[blockIdx.x] = total;
+}
+
+__global__ void k_scan_totals(int* __restrict__ partial, int nb) {
+  __shared__ int tmp[32];
+  int carry = 0;
+  for (int c = 0; c < nb; c += kScanThreads) {
+    int i = c + threadIdx.x;
+    int v = i < nb ? partial[i] : 0;
+    int total;
+    int ex = block_excl_scan(v, tmp, total);
+    if (i < nb) partial[i] = carry + ex;
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[nb] = carry;
+}
+
+__global__ void k_scan_final(const int* __restrict__ in, int n, const int* __restrict__ partial,
+                             int* __restrict__ out) {
+  __shared__ int tmp[32];
+  const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  int v[kScanItems];
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = base + k < n ? in[base + k] : 0;
+    s += v[k];
+  }
+  int total;
+  int ex = block_excl_scan(s, tmp, total) + partial[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) out[base + k] = ex;
+    ex += v[k];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = partial[gridDim.x];
+}
+
+size_t scan_ws_bytes(int n) { return sizeof(int) * ((size_t)ceil_div(n > 0 ? n : 1, kScanTile) + 1); }
+
+cudaError_t exclusive_scan(const int* in, int n, int* out, int* ws, cudaStream_t s) {
+  if (n <= 0) return cudaMemsetAsync(out, 0, sizeof(int), s);
+  int nb = ceil_div(n, kScanTile);
+  k_scan_partials<<<nb, kScanThreads, 0, s>>>(in, n, ws);
+  k_scan_totals<<<1, kScanThreads, 0, s>>>(ws, nb);
+  k_scan_final<<<nb, kScanThreads, 0, s>>>(in, n, ws, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ radius graph
+// One warp per destination atom i scans the atoms j of its graph in index
+// order; pairs with d(i, j) <= rc (j != i) become edges j -> i.  The float64
+// predicate reproduces numpy exactly: d = sqrt((dx*dx + dy*dy) + dz*dz), each
+// operation separately rounded (no FMA), so the neighbour list is bit-exact
+// against build_cutoff_edges.  Optional minimum image over an orthorhombic
+// cell (shift = -L * rint(delta / L)) and a per-destination cap keeping the
+// max_nbr nearest sources by (distance, source index).
+constexpr int kRadiusWarps = 4, kCapBuf = 256;
+
+struct PairGeom {
+  double dx, dy, dz, d;
+};
+
+__device__ __forceinline__ PairGeom pair_geom(const double* __restrict__ pos, int src, int dst,
+                                              const double* cell) {
+  PairGeom g;
+  g.dx = __dsub_rn(pos[3 * src + 0], pos[3 * dst + 0]);
+  g.dy = __dsub_rn(pos[3 * src + 1], pos[3 * dst + 1]);
+  g.dz = __dsub_rn(pos[3 * src + 2], pos[3 * dst + 2]);
+  if (cell) {
+    g.dx = __dadd_rn(g.dx, __dmul_rn(-cell[0], rint(__ddiv_rn(g.dx, cell[0]))));
+    g.dy = __dadd_rn(g.dy, __dmul_rn(-cell[1], rint(__ddiv_rn(g.dy, cell[1]))));
+    g.dz = __dadd_rn(g.dz, __dmul_rn(-cell[2], rint(__ddiv_rn(g.dz, cell[2]))));
+  }
+  g.d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(g.dx, g.dx), __dmul_rn(g.dy, g.dy)),
+                             __dmul_rn(g.dz, g.dz)));
+  return g;
+}
+
+__device__ __forceinline__ bool key_less(double da, int ja, double db, int jb) {
+  return da < db || (da == db && ja < jb);
+}
+
+template <typename T, bool kFill>
+__global__ void __launch_bounds__(kRadiusWarps * 32)
+    k_radius(const double* __restrict__ pos, const int* __restrict__ node_off,
+             const int* __restrict__ gnode, int n_nodes, const double* __restrict__ cells, double rc,
+             int max_nbr, int* __restrict__ deg, const int* __restrict__ rowptr,
+             int* __restrict__ col_src, int* __restrict__ edge_dst, T* __restrict__ edge_w,
+             T* __restrict__ edge_dx) {
+  __shared__ double s_d[kRadiusWarps][kCapBuf];
+  __shared__ int s_j[kRadiusWarps][kCapBuf];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int i = blockIdx.x * kRadiusWarps + wib;
+  if (i >= n_nodes) return;
+  const int g = gnode[i];
+  const int lo = node_off[g], hi = node_off[g + 1];
+  const double* cell = cells ? cells + 3 * g : nullptr;
+  const unsigned lt = (1u << lane) - 1u;
+
+  // pass 1: candidate count (and, when a cap binds, candidate list)
+  int c = 0;
+  for (int j0 = lo; j0 < hi; j0 += 32) {
+    const int j = j0 + lane;
+    bool hit = false;
+    double d = 0.0;
+    if (j < hi && j != i) {
+      PairGeom pg = pair_geom(pos, j, i, cell);
+      d = pg.d;
+      hit = d <= rc;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, hit);
+    if (kFill && max_nbr > 0 && hit) {
+      const int k = c + __popc(b & lt);
+      if (k < kCapBuf) {
+        s_d[wib][k] = d;
+        s_j[wib][k] = j;
+      }
+    }
+    c += __popc(b);
+  }
+  const bool capped = max_nbr > 0 && c > max_nbr;
+  if (!kFill) {
+    if (lane == 0) deg[i] = capped ? max_nbr : c;
+    return;
+  }
+  __syncwarp();
+  int out = rowptr[i];
+  auto emit = [&](int j, int slot) {
+    PairGeom pg = pair_geom(pos, j, i, cell);
+    const int p = out + slot;
+    col_src[p] = j;
+    edge_dst[p] = i;
+    edge_dx[3LL * p + 0] = (T)pg.dx;
+    edge_dx[3LL * p + 1] = (T)pg.dy;
+    edge_dx[3LL * p + 2] = (T)pg.dz;
+    // make_batch (model.py:256-258): w = 1 / (1 + |pos[src] - pos[dst]|)
+    edge_w[p] = (T)__ddiv_rn(1.0, __dadd_rn(1.0, pg.d));
+  };
+  if (!capped) {
+    int k = 0;
+    for (int j0 = lo; j0 < hi; j0 += 32) {
+      const int j = j0 + lane;
+      bool hit = false;
+      if (j < hi && j != i) hit = pair_geom(pos, j, i, cell).d <= rc;
+      const unsigned b = __ballot_sync(0xffffffffu, hit);
+      if (hit) emit(j, k + __popc(b & lt));
+      k += __popc(b);
+    }
+    return;
+  }
+  if (c <= kCapBuf) {
+    // rank every candidate by (d, j); keep rank < max_nbr, emit in j order
+    int k = 0;
+    for (int a0 = 0; a0 < c; a0 += 32) {
+      const int a = a0 + lane;
+      bool keep = false;
+      int ja = 0;
+      if (a < c) {
+        const double da = s_d[wib][a];
+        ja = s_j[wib][a];
+        int rank = 0;
+        for (int q = 0; q < c; ++q) rank += key_less(s_d[wib][q], s_j[wib][q], da, ja);
+        keep = rank < max_nbr;
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, keep);
+      if (keep) emit(ja, k + __popc(b & lt));
+      k += __popc(b);
+    }
+    return;
+  }
+  // large candidate sets: recompute ranks from global memory (O(n * c))
+  int k = 0;
+  for (int j0 = lo; j0 < hi; j0 += 32) {
+    const int j = j0 + lane;
+    bool keep = false;
+    if (j < hi && j != i) {
+      const double dj = pair_geom(pos, j, i, cell).d;
+      if (dj <= rc) {
+        int rank = 0;
+        for (int q = lo; q < hi; ++q) {
+          if (q == i) continue;
+          const double dq = pair_geom(pos, q, i, cell).d;
+          if (dq <= rc && key_less(dq, q, dj, j)) ++rank;
+        }
+        keep = rank < max_nbr;
+      }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    if (keep) emit(j, k + __popc(b & lt));
+    k += __popc(b);
+  }
+}
+
+// ------------------------------------------------- stable bucket placement
+// For each segment s (one graph's edges [seg[s], seg[s+1])) a warp walks the
+// edges in order, 32 at a time; lanes with equal keys are ranked with
+// __match_any_sync so the placement is stable.  cursor[] starts as a copy of
+// the bucket pointers.  Graphs own disjoint node ranges, so warps never share
+// a cursor.  Output perm[position] = input edge index.
+__global__ void k_stable_bucket(const int* __restrict__ keys, const int* __restrict__ seg,
+                                int n_segs, int* __restrict__ cursor, int* __restrict__ perm) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= n_segs) return;
+  const int lo = seg[s], hi = seg[s + 1];
+  const unsigned lt = (1u << lane) - 1u;
+  for (int e0 = lo; e0 < hi; e0 += 32) {
+    const int e = e0 + lane;
+    const bool act = e < hi;
+    const int key = act ? keys[e] : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    int base = 0;
+    if (act) base = cursor[key];
+    __syncwarp();
+    if (act) {
+      perm[base + __popc(peers & lt)] = e;
+      if ((peers & lt) == 0) cursor[key] = base + __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_copy_i32(const int* __restrict__ in, int n, int* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i];
+}
+
+__global__ void k_edge_offsets(const int* __restrict__ rowptr, const int* __restrict__ node_off,
+                               int n_graphs, int* __restrict__ eoff) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g <= n_graphs; g += gridDim.x * blockDim.x)
+    eoff[g] = rowptr[node_off[g]];
+}
+
+// CSR arrays from record edges through the dst permutation; geometry in
+// float64 exactly as make_batch (model.py:256-258), cast to T on store.
+template <typename T>
+__global__ void k_csr_gather(const int* __restrict__ perm, int n_edges, const int* __restrict__ src,
+                             const int* __restrict__ dst, const double* __restrict__ pos,
+                             const double* __restrict__ shift, int* __restrict__ col_src,
+                             int* __restrict__ edge_dst, T* __restrict__ edge_w,
+                             T* __restrict__ edge_dx, int* __restrict__ inv) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_edges; p += gridDim.x * blockDim.x) {
+    const int e = perm[p];
+    const int s = src[e], d = dst[e];
+    double dx = __dsub_rn(pos[3 * s + 0], pos[3 * d + 0]);
+    double dy = __dsub_rn(pos[3 * s + 1], pos[3 * d + 1]);
+    double dz = __dsub_rn(pos[3 * s + 2], pos[3 * d + 2]);
+    if (shift) {
+      dx = __dadd_rn(dx, shift[3LL * e + 0]);
+      dy = __dadd_rn(dy, shift[3LL * e + 1]);
+      dz = __dadd_rn(dz, shift[3LL * e + 2]);
+    }
+    const double dist =
+        __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    col_src[p] = s;
+    edge_dst[p] = d;
+    edge_w[p] = (T)__ddiv_rn(1.0, __dadd_rn(1.0, dist));
+    edge_dx[3LL * p + 0] = (T)dx;
+    edge_dx[3LL * p + 1] = (T)dy;
+    edge_dx[3LL * p + 2] = (T)dz;
+    if (inv) inv[e] = p;
+  }
+}
+
+__global__ void k_csc_finish(const int* __restrict__ perm_csc, int n_cap, const int* __restrict__ n_dev,
+                             const int* __restrict__ inv, const int* __restrict__ dst,
+                             int* __restrict__ csc_eid, int* __restrict__ csc_dst) {
+  const int n = n_dev ? *n_dev : n_cap;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int e = perm_csc[q];
+    csc_eid[q] = inv ? inv[e] : e;
+    csc_dst[q] = dst[e];
+  }
+}
+
+// ------------------------------------------------------------ entry points
+template <typename T>
+cudaError_t radius_fill_t(const double* pos, const int* node_off, const int* gnode, int n_nodes,
+                          const double* cells, double rc, int max_nbr, const int* rowptr,
+                          int* col_src, int* edge_dst, void* w, void* dx, cudaStream_t s) {
+  if (n_nodes <= 0) return cudaSuccess;
+  k_radius<T, true><<<ceil_div(n_nodes, kRadiusWarps), kRadiusWarps * 32, 0, s>>>(
+      pos, node_off, gnode, n_nodes, cells, rc, max_nbr, nullptr, rowptr, col_src, edge_dst,
+      (T*)w, (T*)dx);
+  return cudaGetLastError();
+}
+
+}  // namespace gfm
+
+using namespace gfm;
+
+static inline int grid_for(long long n, int threads = 256) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)b;
+}
+
+#define GFM_TRY(expr)                                                   \
+  do {                                                                  \
+    cudaError_t _e = (expr);                                            \
+    if (_e != cudaSuccess) {                                            \
+      gfm::set_error("%s: %s", #expr, cudaGetErrorString(_e));          \
+      return (int)_e;                                                   \
+    }                                                                   \
+  } while (0)
+
+extern "C" {
+
+int gfm_graph_of_node(const int* node_offsets, int n_graphs, int* gnode, void* stream) {
+  if (n_graphs <= 0) return 0;
+  k_graph_of_node<<<grid_for(n_graphs, 1), 128, 0, (cudaStream_t)stream>>>(node_offsets, n_graphs, gnode);
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+size_t gfm_scan_workspace_bytes(int n) { return scan_ws_bytes(n); }
+
+int gfm_exclusive_scan(const int* in, int n, int* out, void* workspace, void* stream) {
+  GFM_TRY(exclusive_scan(in, n, out, (int*)workspace, (cudaStream_t)stream));
+  return 0;
+}
+
+int gfm_radius_count(const double* pos, const int* node_offsets, const int* gnode, int n_nodes,
+                     const double* cells, double rc, int max_nbr, int* deg, void* stream) {
+  if (n_nodes <= 0) return 0;
+  k_radius<float, false><<<ceil_div(n_nodes, kRadiusWarps), kRadiusWarps * 32, 0,
+                           (cudaStream_t)stream>>>(pos, node_offsets, gnode, n_nodes, cells, rc,
+                                                   max_nbr, deg, nullptr, nullptr, nullptr, nullptr,
+                                                   nullptr);
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gfm_radius_fill(const double* pos, const int* node_offsets, const int* gnode, int n_nodes,
+                    const double* cells, double rc, int max_nbr, const int* rowptr, int* col_src,
+                    int* edge_dst, void* edge_w, void* edge_dx, int dtype, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GFM_F32)
+    GFM_TRY(radius_fill_t<float>(pos, node_offsets, gnode, n_nodes, cells, rc, max_nbr, rowptr,
+                                 col_src, edge_dst, edge_w, edge_dx, s));
+  else if (dtype == GFM_F64)
+    GFM_TRY(radius_fill_t<double>(pos, node_offsets, gnode, n_nodes, cells, rc, max_nbr, rowptr,
+                                  col_src, edge_dst, edge_w, edge_dx, s));
+  else {
+    set_error("gfm_radius_fill: bad dtype %d", dtype);
+    return GFM_EINVAL;
+  }
+  return 0;
+}
+
+size_t gfm_csr_workspace_bytes(int n_nodes, int n_edges, int n_graphs) {
+  (void)n_graphs;
+  size_t b = scan_ws_bytes(n_nodes + 1);
+  b += sizeof(int) * (size_t)(n_nodes + 1) * 2;  // degree + cursor
+  b += sizeof(int) * (size_t)(n_edges + 1) * 2;  // inv + perm_csc
+  b += sizeof(int) * (size_t)(n_graphs + 1);     // per-graph edge offsets
+  return b + 256 * 6;
+}
+
+static char* carve(char*& p, size_t bytes) {
+  char* r = p;
+  p += (bytes + 255) & ~(size_t)255;
+  return r;
+}
+
+int gfm_csr_build(const int* src, const int* dst, const int* edge_offsets, int n_graphs,
+                  const double* pos, const double* shift, int n_nodes, int n_edges, int* rowptr,
+                  int* col_src, int* edge_dst, void* edge_w, void* edge_dx, int* order, int* csc_ptr,
+                  int* csc_eid, int* csc_dst, int dtype, void* workspace, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype != GFM_F32 && dtype != GFM_F64) {
+    set_error("gfm_csr_build: bad dtype %d", dtype);
+    return GFM_EINVAL;
+  }
+  char* p = (char*)workspace;
+  int* scan_ws = (int*)carve(p, scan_ws_bytes(n_nodes + 1));
+  int* count = (int*)carve(p, sizeof(int) * (n_nodes + 1));
+  int* cursor = (int*)carve(p, sizeof(int) * (n_nodes + 1));
+  int* inv = (int*)carve(p, sizeof(int) * (n_edges + 1));
+  int* perm_csc = (int*)carve(p, sizeof(int) * (n_edges + 1));
+  const int nt = 256;
+  // dst-sorted CSR (stable): order[p] = original edge index (model.py:260)
+  k_zero_i32<<<grid_for(n_nodes), nt, 0, s>>>(count, n_nodes);
+  if (n_edges > 0) k_histogram<<<grid_for(n_edges), nt, 0, s>>>(dst, n_edges, nullptr, count);
+  GFM_TRY(exclusive_scan(count, n_nodes, rowptr, scan_ws, s));
+  k_copy_i32<<<grid_for(n_nodes), nt, 0, s>>>(rowptr, n_nodes, cursor);
+  if (n_edges > 0 && n_graphs > 0)
+    k_stable_bucket<<<ceil_div(n_graphs, 4), 128, 0, s>>>(dst, edge_offsets, n_graphs, cursor, order);
+  if (n_edges > 0) {
+    if (dtype == GFM_F32)
+      k_csr_gather<float><<<grid_for(n_edges), nt, 0, s>>>(order, n_edges, src, dst, pos, shift,
+                                                           col_src, edge_dst, (float*)edge_w,
+                                                           (float*)edge_dx, inv);
+    else
+      k_csr_gather<double><<<grid_for(n_edges), nt, 0, s>>>(order, n_edges, src, dst, pos, shift,
+                                                            col_src, edge_dst, (double*)edge_w,
+                                                            (double*)edge_dx, inv);
+  }
+  // src-sorted CSC (stable over original order)
+  k_zero_i32<<<grid_for(n_nodes), nt, 0, s>>>(count, n_nodes);
+  if (n_edges > 0) k_histogram<<<grid_for(n_edges), nt, 0, s>>>(src, n_edges, nullptr, count);
+  GFM_TRY(exclusive_scan(count, n_nodes, csc_ptr, scan_ws, s));
+  k_copy_i32<<<grid_for(n_nodes), nt, 0, s>>>(csc_ptr, n_nodes, cursor);
+  if (n_edges > 0 && n_graphs > 0) {
+    k_stable_bucket<<<ceil_div(n_graphs, 4), 128, 0, s>>>(src, edge_offsets, n_graphs, cursor, perm_csc);
+    k_csc_finish<<<grid_for(n_edges), nt, 0, s>>>(perm_csc, n_edges, nullptr, inv, dst, csc_eid, csc_dst);
+  }
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* edge_dst,
+                     const int* node_offsets, int n_graphs, int n_nodes, int e_cap, int* csc_ptr,
+                     int* csc_eid, int* csc_dst, void* workspace, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  char* p = (char*)workspace;
+  int* scan_ws = (int*)carve(p, scan_ws_bytes(n_nodes + 1));
+  int* count = (int*)carve(p, sizeof(int) * (n_nodes + 1));
+  int* cursor = (int*)carve(p, sizeof(int) * (n_nodes + 1));
+  carve(p, sizeof(int) * (e_cap + 1));
+  int* perm_csc = (int*)carve(p, sizeof(int) * (e_cap + 1));
+  int* eoff = (int*)carve(p, sizeof(int) * (n_graphs + 1));
+  const int nt = 256;
+  const int* n_dev = rowptr + n_nodes;
+  k_zero_i32<<<grid_for(n_nodes), nt, 0, s>>>(count, n_nodes);
+  if (e_cap > 0) k_histogram<<<grid_for(e_cap), nt, 0, s>>>(col_src, e_cap, n_dev, count);
+  GFM_TRY(exclusive_scan(count, n_nodes, csc_ptr, scan_ws, s));
+  k_copy_i32<<<grid_for(n_nodes), nt, 0, s>>>(csc_ptr, n_nodes, cursor);
+  if (n_graphs > 0) {
+    k_edge_offsets<<<grid_for(n_graphs + 1), nt, 0, s>>>(rowptr, node_offsets, n_graphs, eoff);
+    k_stable_bucket<<<ceil_div(n_graphs, 4), 128, 0, s>>>(col_src, eoff, n_graphs, cursor, perm_csc);
+  }
+  if (e_cap > 0)
+    k_csc_finish<<<grid_for(e_cap), nt, 0, s>>>(perm_csc, e_cap, n_dev, nullptr, edge_dst, csc_eid, csc_dst);
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,352 @@
+"""Data-parallel MTL training step and loop (drop-in for ``gfmkit.train``).
+
+Reference: train.py:59-338.  One process per GPU; each step a rank runs
+forward + backward on its own batch into a float32 ``[grad | loss | 1]``
+vector, the vector is summed across ranks by the ``Comm`` (NCCL over
+NVLink), a device-side non-finite guard is raised if any entry is bad, and
+the Adam / SGD kernel divides by the world size and updates float64 master
+weights plus the float32 working copy -- identical bytes on every rank, so
+parameters stay bitwise equal across ranks (train.py:1-10).
+
+The guard is sticky on the device: once set, every later update is skipped,
+which is exactly the reference's "update discarded, training aborted"
+(train.py:264-274) without a host round trip per step.
+"""
+
+from __future__ import annotations
+
+import logging
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream_handle
+from .comm import Comm, LocalComm
+from .errors import ConfigError, ValidationError
+from .model import (ModelConfig, ModelParams, _Scratch, count_params, forward_batch,
+                    init_params_flat, loss_and_grad, make_batch)
+from .schedule import epoch_schedule
+from .telemetry import PhaseClock
+
+log = logging.getLogger(__name__)
+
+OPTIMIZERS = ("adam", "sgd")
+
+
+@dataclass
+class TrainConfig:
+    """train.py:59-82."""
+
+    max_epochs: int = 30
+    patience: int = 10
+    base_seed: int = 0
+    optimizer: str = "adam"
+    learning_rate: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    wall_clock_budget_s: float | None = None
+    checkpoint_path: str | None = None
+
+    def __post_init__(self):
+        if self.optimizer not in OPTIMIZERS:
+            raise ConfigError(f"optimizer must be one of {OPTIMIZERS}, got {self.optimizer!r}")
+        if self.max_epochs < 0:
+            raise ConfigError(f"max_epochs must be >= 0, got {self.max_epochs}")
+        if self.patience < 1:
+            raise ConfigError(f"patience must be >= 1, got {self.patience}")
+        if self.learning_rate <= 0:
+            raise ConfigError(f"learning_rate must be > 0, got {self.learning_rate}")
+
+
+class OptimizerState:
+    """Adam moments (float64, on the device) and step counter (train.py:85-93)."""
+
+    def __init__(self, m, v, t: int = 0):
+        self.m = m
+        self.v = v
+        self.t = t
+
+    @classmethod
+    def zeros(cls, n: int, device=None) -> "OptimizerState":
+        dev = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        return cls(torch.zeros(n, dtype=torch.float64, device=dev),
+                   torch.zeros(n, dtype=torch.float64, device=dev), 0)
+
+
+def _dev_f64(x, device):
+    if isinstance(x, torch.Tensor):
+        return x.detach().to(device=device, dtype=torch.float64).contiguous()
+    return torch.as_tensor(np.asarray(x, dtype=np.float64), device=device)
+
+
+def apply_update(flat, grad, cfg: TrainConfig, state: OptimizerState):
+    """One optimiser step (train.py:96-108) on the device; returns a NEW
+    float64 vector (numpy in -> numpy out) and mutates ``state``.  Bit-identical
+    to the reference for identical float64 inputs."""
+    _lib.load(require_device=True)
+    dev = state.m.device if isinstance(state.m, torch.Tensor) else torch.device("cuda")
+    if not isinstance(state.m, torch.Tensor):
+        state.m = _dev_f64(state.m, dev)
+        state.v = _dev_f64(state.v, dev)
+    as_numpy = not isinstance(flat, torch.Tensor)
+    master = _dev_f64(flat, dev).clone()
+    g = grad.detach() if isinstance(grad, torch.Tensor) else torch.as_tensor(
+        np.asarray(grad, np.float64))
+    g = g.to(dev).contiguous()
+    if g.dtype not in (torch.float32, torch.float64):
+        g = g.to(torch.float64)
+    n = master.shape[0]
+    if g.shape[0] != n:
+        raise ValidationError(f"grad has {g.shape[0]} entries, params {n}")
+    state.t += 1
+    s = stream_handle()
+    code = _lib.dtype_code(g.dtype)
+    if cfg.optimizer == "sgd":
+        call("gfm_sgd_step", ptr(g), code, n, 1.0, ptr(master), float(cfg.learning_rate), None,
+             None, s)
+    else:
+        bc = torch.tensor([1.0 - cfg.beta1 ** state.t, 1.0 - cfg.beta2 ** state.t],
+                          dtype=torch.float64, device=dev)
+        call("gfm_adam_step", ptr(g), code, n, 1.0, ptr(master), ptr(state.m), ptr(state.v),
+             ptr(bc), float(cfg.learning_rate), float(cfg.beta1), float(cfg.beta2),
+             float(cfg.eps), None, None, s)
+    return master.cpu().numpy() if as_numpy else master
+
+
+class EarlyStopper:
+    """Stop when the metric has not decreased for ``patience`` epochs (train.py:111-126)."""
+
+    def __init__(self, patience: int):
+        self.patience = patience
+        self.best = np.inf
+        self.since_improvement = 0
+
+    def update(self, value: float) -> bool:
+        if value < self.best:
+            self.best = value
+            self.since_improvement = 0
+        else:
+            self.since_improvement += 1
+        return self.since_improvement >= self.patience
+
+
+@dataclass
+class EpochMetrics:
+    epoch: int
+    train_loss: float
+    val_mae: float
+    val_energy_mae: float
+    val_force_mae: float
+    epoch_time_s: float
+    phase_seconds: dict = field(default_factory=dict)
+
+    def to_dict(self) -> dict:
+        return dict(epoch=self.epoch, train_loss=self.train_loss, val_mae=self.val_mae,
+                    val_energy_mae=self.val_energy_mae, val_force_mae=self.val_force_mae,
+                    epoch_time_s=self.epoch_time_s, phase_seconds=dict(self.phase_seconds))
+
+
+@dataclass
+class TrainResult:
+    params: ModelParams
+    metrics: list
+    stop_reason: str
+    nan_event: bool
+    epochs_run: int
+
+
+class DataParallelTrainer:
+    """The hot path: device-resident parameters, optimiser state and
+    scratch; ``step(batch)`` = forward + backward + allreduce + guard + update
+    with no host synchronisation.  Float32 compute by default (float64 for
+    exact-parity runs)."""
+
+    def __init__(self, model_config: ModelConfig, train_config: TrainConfig | None = None,
+                 comm: Comm | None = None, device=None, initial=None,
+                 dtype=torch.float32, flags: int = 0):
+        _lib.load(require_device=True)
+        self.cfg = model_config
+        self.tcfg = train_config or TrainConfig()
+        self.comm = comm or LocalComm()
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.dtype = dtype
+        self.flags = flags
+        P = count_params(model_config)
+        self.P = P
+        if initial is None:
+            flat = init_params_flat(model_config, self.tcfg.base_seed)
+        elif isinstance(initial, ModelParams):
+            flat = initial.flatten()
+        else:
+            flat = np.asarray(initial, np.float64)
+        self.master = torch.as_tensor(flat, dtype=torch.float64, device=self.device).clone()
+        self.m = torch.zeros_like(self.master)
+        self.v = torch.zeros_like(self.master)
+        self.t_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.bc = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.contrib = torch.zeros(P + 2, dtype=dtype, device=self.device)
+        if dtype == torch.float32:
+            self.work = torch.empty(P, dtype=torch.float32, device=self.device)
+            call("gfm_cast_f64_to_f32", ptr(self.master), P, ptr(self.work), stream_handle())
+        else:
+            self.work = self.master
+        self.params = ModelParams(model_config, self.work)
+        self.scratch = _Scratch(self.device)
+        self.steps = 0
+
+    def compute(self, batch):
+        """forward + backward into ``contrib`` (or zeros when no batch)."""
+        P = self.P
+        if batch is None:
+            self.contrib.zero_()
+            return
+        if self.dtype == torch.float32:
+            loss_and_grad(self.params, batch, scratch=self.scratch, grad_out=self.contrib[:P],
+                          contrib=self.contrib[P:], flags=self.flags)
+        else:
+            lb, _ = loss_and_grad(self.params, batch, scratch=self.scratch,
+                                  grad_out=self.contrib[:P], flags=self.flags)
+            self.contrib[P:P + 1].copy_(lb.values[:1])
+            self.contrib[P + 1].fill_(1.0)
+
+    def reduce_and_update(self):
+        P = self.P
+        s = stream_handle()
+        self.comm.allreduce_sum_(self.contrib)
+        code = _lib.dtype_code(self.dtype)
+        call("gfm_nonfinite_flag", ptr(self.contrib), P + 1, code, ptr(self.flag), s)
+        out32 = self.work if self.dtype == torch.float32 else None
+        world = float(self.comm.size)
+        if self.tcfg.optimizer == "adam":
+            call("gfm_adam_advance", ptr(self.t_dev), float(self.tcfg.beta1),
+                 float(self.tcfg.beta2), ptr(self.bc), ptr(self.flag), s)
+            call("gfm_adam_step", ptr(self.contrib), code, P, world, ptr(self.master), ptr(self.m),
+                 ptr(self.v), ptr(self.bc), float(self.tcfg.learning_rate),
+                 float(self.tcfg.beta1), float(self.tcfg.beta2), float(self.tcfg.eps),
+                 ptr(self.flag), ptr(out32), s)
+        else:
+            call("gfm_sgd_step", ptr(self.contrib), code, P, world, ptr(self.master),
+                 float(self.tcfg.learning_rate), ptr(self.flag), ptr(out32), s)
+        self.steps += 1
+
+    def step(self, batch):
+        self.compute(batch)
+        self.reduce_and_update()
+        return self.contrib[self.P:self.P + 2]
+
+    @property
+    def nan_event(self) -> bool:
+        return bool(self.flag.item())
+
+    def current_params(self) -> ModelParams:
+        return ModelParams(self.cfg, self.master.clone())
+
+
+def evaluate(params: ModelParams, store, comm: Comm, group: str = "valset",
+             batch_size: int = 64) -> tuple[float, float]:
+    """Per-atom energy MAE and force-component MAE over a group
+    (train.py:160-189): rank r scores ``r::P``; sums are allreduced."""
+    ownership = store.ownership.get(group)
+    if ownership is None:
+        raise ValidationError(f"group {group!r} not loaded on rank {comm.rank}")
+    n = ownership.n_samples
+    dev = params.flat.device
+    acc = torch.zeros(4, dtype=torch.float64, device=dev)
+    mine = np.arange(comm.rank, n, comm.size)
+    for lo in range(0, mine.shape[0], batch_size):
+        records = store.fetch_batch(group, mine[lo:lo + batch_size])
+        batch = make_batch(records, device=dev, dtype=params.dtype)
+        e_pred, f_pred = forward_batch(params, batch)
+        acc[0] += ((e_pred - batch.energy_true) / batch.n_per_graph.to(e_pred.dtype)).abs().sum()
+        acc[1] += batch.n_graphs
+        acc[2] += (f_pred - batch.forces_true).abs().sum()
+        acc[3] += 3.0 * batch.n_nodes
+    totals = comm.allreduce_sum(acc.cpu().numpy())
+    energy_mae = totals[0] / totals[1] if totals[1] else 0.0
+    force_mae = totals[2] / totals[3] if totals[3] else 0.0
+    return float(energy_mae), float(force_mae)
+
+
+def train(model_config: ModelConfig, store, comm: Comm | None = None,
+          config: TrainConfig | None = None, clock: PhaseClock | None = None,
+          initial: ModelParams | None = None, schedule_fn=None, device=None,
+          dtype=torch.float32) -> TrainResult:
+    """The data-parallel training loop on this rank (train.py:192-338)."""
+    comm = comm or LocalComm()
+    config = config or TrainConfig()
+    clock = clock or PhaseClock()
+    if config.checkpoint_path:
+        raise ConfigError("GFMP checkpoint I/O is not part of the GPU hot path (see DESIGN.md)")
+    trainer = DataParallelTrainer(model_config, config, comm, device=device, initial=initial,
+                                  dtype=dtype)
+    ownership = store.ownership.get("trainset")
+    if ownership is None:
+        raise ValidationError(f"trainset not loaded on rank {comm.rank}")
+    n_train = ownership.n_samples
+    start = time.monotonic()
+    stopper = EarlyStopper(config.patience)
+    metrics = []
+    stop_reason = "max_epochs"
+    nan_event = False
+    P = trainer.P
+    for epoch in range(1, config.max_epochs + 1):
+        t0 = time.perf_counter()
+        before = clock.totals()
+        if schedule_fn is not None:
+            per_rank = schedule_fn(epoch)
+            mine = per_rank[comm.rank]
+            steps = max(len(b) for b in per_rank)
+        else:
+            sched = epoch_schedule(n_train, comm.size, model_config.batch_size, config.base_seed,
+                                   epoch)
+            mine = sched.for_rank(comm.rank)
+            steps = sched.max_batches()
+        acc = torch.zeros(2, dtype=torch.float64, device=trainer.device)
+        for step in range(steps):
+            batch = None
+            if step < len(mine) and len(mine[step]):
+                with clock.phase("dataload"):
+                    batch = make_batch(store.fetch_batch("trainset", mine[step]),
+                                       device=trainer.device, dtype=dtype)
+                with clock.phase("forward"):
+                    trainer.compute(batch)
+            else:
+                trainer.contrib.zero_()
+            with clock.phase("sync"):
+                trainer.reduce_and_update()
+            if trainer.nan_event:  # train.py:264-274
+                log.warning("rank %d: non-finite loss at epoch %d step %d; update discarded, "
+                            "training aborted", comm.rank, epoch, step)
+                nan_event = True
+                stop_reason = "nan"
+                break
+            acc += trainer.contrib[P:P + 2].to(torch.float64)
+        if nan_event:
+            break
+        params = ModelParams(model_config, trainer.work)
+        ve, vf = evaluate(params, store, comm)
+        after = clock.totals()
+        loss_sum, loss_count = acc.cpu().numpy()
+        metrics.append(EpochMetrics(
+            epoch=epoch, train_loss=loss_sum / loss_count if loss_count else float("nan"),
+            val_mae=ve + vf, val_energy_mae=ve, val_force_mae=vf,
+            epoch_time_s=time.perf_counter() - t0,
+            phase_seconds={k: after[k] - before.get(k, 0.0) for k in after}))
+        if stopper.update(ve + vf):
+            stop_reason = "early_stop"
+            break
+        over = (config.wall_clock_budget_s is not None
+                and time.monotonic() - start >= config.wall_clock_budget_s)
+        if comm.broadcast_obj("budget" if over else None) is not None:
+            stop_reason = "budget"
+            break
+    return TrainResult(params=trainer.current_params(), metrics=metrics,
+                       stop_reason=stop_reason, nan_event=nan_event,
+                       epochs_run=len(metrics) + (1 if nan_event else 0))
