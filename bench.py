@@ -1,0 +1,378 @@
+"""Benchmark: training graphs/s of the data-parallel energy+force MTL step.
+
+Workload (BASELINE.json configs[1], "C2"): HydraGNN-PNA stand-in -- pna-agg
+(sum|mean|max|std), 3 message-passing layers, hidden 64, fc 2 x 64 -- on
+synthetic 32-atom molecular graphs (8 A box, radius 5 A, max 20
+neighbours), 1024 graphs per GPU per step.  A step = device batch assembly
+(radius graph -> CSR/CSC) from device-resident raw structures + forward +
+backward + gradient allreduce (NCCL) + Adam.  N > 1: one process per GPU
+(torchrun), per-GPU batch fixed (weak scaling).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the CPU oracle
+port (numpy float64, the reference's algorithm) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(kind="pna-agg", layers=3, hidden=64, fc_layers=2, fc_width=64,
+                atoms=32, box=8.0, rc=5.0, max_nbr=20, batch=1024)
+METRIC = "training graphs/sec (energy+forces MTL) at 1/2/4/8 B200; aggregation HBM GB/s"
+UNIT = "graphs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--batch", type=int, default=WORKLOAD["batch"])
+    ap.add_argument("--no-graph", action="store_true", help="disable CUDA-graph capture")
+    ap.add_argument("--cpu-sample-s", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- synthetic data
+def make_structures(n_graphs, seed):
+    """Positions / species / labels of n_graphs 32-atom structures (host)."""
+    rng = np.random.default_rng(seed)
+    n = WORKLOAD["atoms"]
+    z = rng.choice(np.array([1, 6, 8]), size=(n_graphs, n)).astype(np.int32)
+    pos = rng.uniform(0.0, WORKLOAD["box"], size=(n_graphs, n, 3))
+    energy = rng.normal(size=n_graphs) * 5.0 - 0.1 * z.sum(axis=1)
+    forces = rng.normal(size=(n_graphs, n, 3))
+    return z, pos, energy, forces
+
+
+# ---------------------------------------------------------------- CPU oracle leg
+def _cpu_worker(args):
+    seed, n_graphs, budget_s = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import gfm_oracle as O
+
+    cfg = O.config(WORKLOAD["kind"], WORKLOAD["layers"], WORKLOAD["hidden"],
+                   WORKLOAD["fc_layers"], WORKLOAD["fc_width"])
+    flat = O.init_flat(cfg, 0)
+    m = np.zeros_like(flat)
+    v = np.zeros_like(flat)
+    z, pos, energy, forces = make_structures(n_graphs, seed)
+    recs = []
+    for g in range(n_graphs):
+        edges, shift = O.cutoff_edges(pos[g], WORKLOAD["rc"], max_nbr=WORKLOAD["max_nbr"])
+        recs.append(dict(z=z[g], pos=pos[g], edges=edges, shift=shift, energy=energy[g],
+                         forces=forces[g]))
+    steps, t = 0, 0
+    t0 = time.perf_counter()
+    while True:
+        b = O.pack(recs)
+        _, grad, _ = O.loss_and_grad(cfg, flat, b)
+        flat, m, v, t = O.adam(flat, grad, m, v, t)
+        steps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    return steps * n_graphs, time.perf_counter() - t0
+
+
+def cpu_oracle_rate(budget_s, procs=None, sample_graphs=32):
+    """graphs/s of the numpy oracle step (make_batch + fwd + bwd + Adam, the
+    reference's train.py:247-277 minus the fetch) over all host cores: one
+    single-threaded process per core, each on its own 32-graph sample."""
+    import multiprocessing as mp
+
+    procs = procs or len(os.sched_getaffinity(0))
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_cpu_worker, [(1000 + k, sample_graphs, budget_s) for k in range(procs)])
+    graphs = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return graphs / wall, procs, (f"{procs} processes x {sample_graphs}-graph C2 samples "
+                                  f"(numpy float64 oracle port, OPENBLAS_NUM_THREADS=1), "
+                                  f"~{budget_s:.0f} s each")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s)
+    line = dict(metric=METRIC, value=rate, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, higher_is_better=True, scaling="weak", vs_baseline=None,
+                dtype="f64", data="synthetic", impl="reference",
+                config=dict(workload="C2: pna-agg L3 H64, 32-atom graphs, rc 5 A, cap 20",
+                            global_batch=WORKLOAD["batch"] * args.gpus),
+                cpu_baseline=dict(value=rate, unit=UNIT, cores=cores, kind="port", sample=sample),
+                e2e=dict(value=rate, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(10)
+
+    def summary(self):
+        if not self.rows:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
+        return dict(sm_mhz=float(np.median(sm)) if sm else None,
+                    sm_max_mhz=max(mx) if mx else None, reasons=reasons, samples=len(self.rows))
+
+
+# ---------------------------------------------------------------- native leg
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_12909_b200 import _lib
+    from paper_2406_12909_b200 import model as M
+    from paper_2406_12909_b200 import train as T
+    from paper_2406_12909_b200.comm import LocalComm, TorchComm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = TorchComm()
+    else:
+        comm = LocalComm()
+    _lib.load(require_device=True)
+
+    B, n = args.batch, WORKLOAD["atoms"]
+    N = B * n
+    cfg = M.ModelConfig(mpnn_kind=WORKLOAD["kind"], mpnn_layers=WORKLOAD["layers"],
+                        mpnn_width=WORKLOAD["hidden"], fc_layers=WORKLOAD["fc_layers"],
+                        fc_width=WORKLOAD["fc_width"], batch_size=B)
+    tr = T.DataParallelTrainer(cfg, T.TrainConfig(optimizer="adam", learning_rate=1e-3),
+                               comm=comm, device=dev)
+    host_off = (np.arange(B + 1) * n).astype(np.int32)
+    runner = T.StructureStepRunner(tr, host_off, WORKLOAD["rc"], WORKLOAD["max_nbr"],
+                                   use_graph=not args.no_graph)
+
+    # pool of distinct device-resident batches (raw structures + labels)
+    pool = []
+    for k in range(8):
+        z, pos, energy, forces = make_structures(B, 1000 * rank + k)
+        pool.append(dict(
+            z=torch.as_tensor(z.reshape(-1), device=dev),
+            pos=torch.as_tensor(pos.reshape(-1, 3), device=dev),
+            e=torch.as_tensor(energy, dtype=torch.float32, device=dev),
+            f=torch.as_tensor(forces.reshape(-1, 3), dtype=torch.float32, device=dev)))
+
+    def load_slot(k):
+        d = pool[k % len(pool)]
+        runner.load(d["pos"], d["z"], d["e"], d["f"])
+
+    s = torch.cuda.current_stream()
+    load_slot(0)
+    try:
+        runner.capture(warmup=max(args.warmup, 3))
+    except Exception as exc:  # e.g. a collective that refuses capture: run eagerly
+        print(f"[bench] CUDA-graph capture failed ({exc}); eager launches", file=sys.stderr)
+        runner.graph = None
+        runner.use_graph = False
+    for i in range(3):
+        load_slot(i)
+        runner.run()
+    torch.cuda.synchronize()
+
+    def one(i):
+        load_slot(i)
+        runner.run()
+
+    # ---- timed region: K steps, inputs already in HBM
+    if world > 1:
+        comm.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(s)
+        for i in range(args.steps):
+            one(i)
+        ev1.record(s)
+        torch.cuda.synchronize()
+    if world > 1:
+        comm.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * B * args.steps / (ms / 1e3)
+
+    # ---- e2e: the public call (StructureStepRunner.step) from pinned host
+    # buffers, with the loss read back to the host every step
+    host = []
+    for k in range(4):
+        z, pos, energy, forces = make_structures(B, 5000 + 1000 * rank + k)
+        host.append(dict(z=torch.as_tensor(z.reshape(-1)).pin_memory(),
+                         pos=torch.as_tensor(pos.reshape(-1, 3)).pin_memory(),
+                         e=torch.as_tensor(energy, dtype=torch.float32).pin_memory(),
+                         f=torch.as_tensor(forces.reshape(-1, 3), dtype=torch.float32).pin_memory()))
+    h2d = sum(v.numel() * v.element_size() for v in host[0].values())
+    d2h = runner.loss_host.numel() * runner.loss_host.element_size()
+
+    def e2e_step(i):
+        hb = host[i % len(host)]
+        return runner.step(hb["pos"], hb["z"], hb["e"], hb["f"])
+
+    for i in range(2):
+        e2e_step(i)
+    if world > 1:
+        comm.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * args.steps / float(e2e_s.item())
+    graph = runner.graph
+
+    # ---- roofline of the aggregation kernel (CUDA events on the launch stream)
+    load_slot(0)
+    runner._eager()
+    b = runner.batch
+    torch.cuda.synchronize()
+    E = b.n_edges
+    H, K = cfg.mpnn_width, cfg.n_parts
+    h_in = torch.randn(N, H, device=dev)
+    agg = torch.empty(N, K * H, device=dev)
+    am = torch.empty(N, H, dtype=torch.int32, device=dev)
+    sm_ = torch.empty(N, H, device=dev)
+    sh = _lib.stream_handle()
+
+    def agg_call():
+        _lib.call("gfm_agg_fwd", _lib.ptr(h_in), N, H, _lib.ptr(b.rowptr), _lib.ptr(b.col_src),
+                  _lib.ptr(b.edge_w), M.KIND_PARTS[cfg.mpnn_kind], _lib.ptr(agg), _lib.ptr(am),
+                  _lib.ptr(sm_), _lib.F32, 0, sh)
+
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        agg_call()
+    reps, tot = 20, 0.0
+    for _ in range(reps):
+        flush.zero_()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s)
+        agg_call()
+        a1.record(s)
+        torch.cuda.synchronize()
+        tot += a0.elapsed_time(a1)
+    agg_ms = tot / reps
+    # SURVEY 8(d) C5 forward formula (fused h + src + w mode), s = 4 bytes:
+    # E*H*s (gathered rows) + 4E src + 4E w + 4(N+1) rowptr + K*N*H*s out
+    # + 4*N*H argmax + 4*N*H std mean
+    agg_bytes = E * H * 4 + 8 * E + 4 * (N + 1) + K * N * H * 4 + 4 * N * H + 4 * N * H
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = agg_bytes / (agg_ms / 1e3) / 1e9
+
+    # ---- launches per step (one extra untimed step under the profiler)
+    launches = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        load_slot(1)
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            one(1)
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+        ours = [nm for nm in names if nm.startswith(("gfm::", "void gfm::")) or "gfm::" in nm]
+        launches = len(ours) * args.steps
+    except Exception:
+        launches = None
+
+    if rank == 0:
+        clocks = clk.summary()
+        cpu = None
+        if world == 1:
+            rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s)
+            cpu = dict(value=rate, unit=UNIT, cores=cores, kind="port", sample=sample)
+        line = dict(
+            metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
+            warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True,
+            scaling="weak", vs_baseline=None, dtype="f32", data="synthetic",
+            config=dict(workload="C2: pna-agg L3 H64 fc2x64, 32-atom graphs, box 8 A, rc 5 A, "
+                                 "max 20 neighbours, 1024 graphs/GPU",
+                        global_batch=B * world, per_gpu_batch=B, nodes_per_gpu=N,
+                        edges_per_gpu=E, parallelism=f"dp{world}",
+                        cuda_graph=graph is not None,
+                        l2=("step working set (activations, E x H workspaces) > 126 MB L2; "
+                            "8-batch input pool cycled")),
+            e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
+            roofline=dict(kernel="gfm_agg_fwd (pna: sum|mean|max|std)", bound="hbm",
+                          achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
+                          traffic=None, launch_ms=agg_ms, algorithmic_bytes=agg_bytes,
+                          peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"),
+            cpu_baseline=cpu, clocks=clocks, gpu_launches=launches)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_native(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -249,6 +249,89 @@ class DataParallelTrainer:
         return ModelParams(self.cfg, self.master.clone())
 
 
+class StructureStepRunner:
+    """Fixed-shape training step on raw structures: device batch assembly
+    (radius graph -> CSR/CSC) + forward + backward + allreduce + update,
+    optionally captured once into a CUDA graph and replayed.
+
+    ``load(...)`` copies a batch's raw inputs (host pinned or device tensors)
+    into stable device slots; ``run()`` executes one step; ``step(...)`` =
+    load + run + loss read-back (the end-to-end public call)."""
+
+    def __init__(self, trainer: DataParallelTrainer, host_offsets, rc: float, max_nbr: int = 0,
+                 cells=None, use_graph: bool = True, e_cap: int | None = None):
+        from .model import radius_batch  # noqa: F401  (kept local: avoids import cycle)
+
+        self.tr = trainer
+        dev = trainer.device
+        self.host_off = np.asarray(host_offsets, np.int32)
+        self.N = int(self.host_off[-1])
+        self.B = int(self.host_off.shape[0] - 1)
+        self.off = torch.as_tensor(self.host_off, device=dev)
+        self.rc = float(rc)
+        self.max_nbr = int(max_nbr or 0)
+        self.cells = None if cells is None else torch.as_tensor(
+            np.asarray(cells, np.float64).reshape(self.B, 3), device=dev)
+        if e_cap is None:
+            if not self.max_nbr:
+                n = np.diff(self.host_off).astype(np.int64)
+                e_cap = int((n * (n - 1)).sum())
+            else:
+                e_cap = self.N * self.max_nbr
+        self.e_cap = int(e_cap)
+        dt = trainer.dtype
+        self.slot = dict(pos=torch.empty(self.N, 3, dtype=torch.float64, device=dev),
+                         z=torch.empty(self.N, dtype=torch.int32, device=dev),
+                         e=torch.empty(self.B, dtype=dt, device=dev),
+                         f=torch.empty(self.N, 3, dtype=dt, device=dev))
+        self.bufs = {}
+        self.use_graph = use_graph
+        self.graph = None
+        self.batch = None
+        self.loss_host = torch.empty(2, dtype=torch.float32).pin_memory()
+
+    def load(self, pos, z, energy, forces):
+        for key, v in (("pos", pos), ("z", z), ("e", energy), ("f", forces)):
+            dst = self.slot[key]
+            dst.copy_(v.reshape(dst.shape), non_blocking=True)
+
+    def _eager(self):
+        from .model import radius_batch
+
+        self.batch = radius_batch(self.slot["pos"], self.slot["z"], self.off, self.host_off,
+                                  self.rc, self.max_nbr, self.cells, self.slot["e"],
+                                  self.slot["f"], self.tr.dtype, e_cap=self.e_cap, out=self.bufs)
+        self.tr.step(self.batch)
+
+    def capture(self, warmup: int = 2):
+        """Warm up eagerly (allocates every buffer), then record one step."""
+        for _ in range(warmup):
+            self._eager()
+        torch.cuda.synchronize()
+        if self.use_graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._eager()
+            self.graph = g
+        return self
+
+    def run(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._eager()
+
+    def step(self, pos, z, energy, forces) -> float:
+        """End to end: inputs (host or device) -> step -> mean loss on host."""
+        self.load(pos, z, energy, forces)
+        self.run()
+        P = self.tr.P
+        self.loss_host.copy_(self.tr.contrib[P:P + 2].float(), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        tot, cnt = float(self.loss_host[0]), float(self.loss_host[1])
+        return tot / cnt if cnt else float("nan")
+
+
 def evaluate(params: ModelParams, store, comm: Comm, group: str = "valset",
              batch_size: int = 64) -> tuple[float, float]:
     """Per-atom energy MAE and force-component MAE over a group

@@ -1,0 +1,38 @@
+"""Run the bench workload's training step eagerly a few times (for ncu launch
+lists / full captures).  Usage: python tools/step_once.py [--steps 3] [--batch 1024]"""
+
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from bench import WORKLOAD, make_structures  # noqa: E402
+from paper_2406_12909_b200 import model as M, train as T  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--batch", type=int, default=WORKLOAD["batch"])
+ap.add_argument("--kind", default=WORKLOAD["kind"])
+ap.add_argument("--hidden", type=int, default=WORKLOAD["hidden"])
+ap.add_argument("--layers", type=int, default=WORKLOAD["layers"])
+a = ap.parse_args()
+B, n = a.batch, WORKLOAD["atoms"]
+cfg = M.ModelConfig(mpnn_kind=a.kind, mpnn_layers=a.layers, mpnn_width=a.hidden,
+                    fc_layers=2, fc_width=a.hidden, batch_size=B)
+tr = T.DataParallelTrainer(cfg, T.TrainConfig())
+runner = T.StructureStepRunner(tr, (np.arange(B + 1) * n).astype(np.int32), WORKLOAD["rc"],
+                               WORKLOAD["max_nbr"], use_graph=False)
+z, pos, e, f = make_structures(B, 0)
+dev = tr.device
+runner.load(torch.as_tensor(pos.reshape(-1, 3), device=dev), torch.as_tensor(z.reshape(-1), device=dev),
+            torch.as_tensor(e, dtype=torch.float32, device=dev),
+            torch.as_tensor(f.reshape(-1, 3), dtype=torch.float32, device=dev))
+for _ in range(a.steps):
+    runner.run()
+torch.cuda.synchronize()
+print("ok", float(tr.contrib[tr.P]))
