@@ -45,12 +45,17 @@ enum { GFM_EINVAL = -1 };
 /* aggregation parts (bit order = column-block order of the output) */
 enum { GFM_PART_SUM = 1, GFM_PART_MEAN = 2, GFM_PART_MAX = 4, GFM_PART_STD = 8 };
 enum { GFM_FLAG_SCALAR = 1 }; /* force the scalar (numpy-order) kernels */
+/* float32 GEMM engine: tcgen05 3xTF32 (default, fp32-level accuracy),
+ * tcgen05 1xTF32 (faster, ~1e-3 relative), or the SIMT fp32 engine */
+enum { GFM_GEMM_SIMT = 0, GFM_GEMM_TC3 = 1, GFM_GEMM_TC1 = 2 };
 
 /* ---- housekeeping ---------------------------------------------------- */
 GFM_API int gfm_abi_version(void);
 GFM_API const char* gfm_last_error(void);
 GFM_API int gfm_device_sm_count(void);
 GFM_API int gfm_stream_sync(void* stream);
+GFM_API int gfm_set_gemm_mode(int mode);
+GFM_API int gfm_get_gemm_mode(void);
 
 /* ---- K1/K2: batch geometry (preprocess.py:90-104, model.py:234-285) --- */
 /* gnode[i] = graph of node i (model.py:243) */
@@ -126,21 +131,24 @@ GFM_API int gfm_linear_bwd_weight(const void* dY, int ldd, int M, const int* M_d
                           void* stream);
 
 /* ---- K7/K10: force head (model.py:377-389, 535-547) ------------------- */
-/* pair = h[dst] + h[src]; t = tanh(pair V^T + c); m = t.u; f[dst] += m dx */
-GFM_API size_t gfm_force_fwd_workspace_bytes(int H, int e_cap, int dtype);
-GFM_API int gfm_force_fwd(const void* h, int H, int n_nodes, const int* rowptr, const int* col_src,
-                  const int* edge_dst, const void* edge_dx, int e_cap, const void* V,
-                  const void* c, const void* u, void* f_pred, void* m_out, void* workspace,
-                  int dtype, void* stream);
-/* grads of V, c, u and dh_final = dh_energy + scatter_dst(dpair) +
- * scatter_src(dpair); dz_out = dh_final * (1 - h^2) when non-NULL. */
-GFM_API size_t gfm_force_bwd_workspace_bytes(int H, int e_cap, int dtype);
-GFM_API int gfm_force_bwd(const void* h, int H, int n_nodes, const int* rowptr, const int* col_src,
-                  const int* edge_dst, const void* edge_dx, int e_cap, const int* csc_ptr,
-                  const int* csc_eid, const void* V, const void* c, const void* u,
-                  const void* df, const void* dh_energy, void* grad_v, void* grad_c,
-                  void* grad_u, void* dh_out, void* dz_out, void* workspace, int dtype,
-                  void* stream);
+/* Node-factored: the pair pre-activation (h[dst] + h[src]) V^T + c equals
+ * P[dst] + P[src] + c with P = h V^T (written to caller-owned P [N][H] and
+ * reused by the backward); then t = tanh(.), m = t.u and f[dst] += m dx over
+ * the dst-CSR in one gather pass. */
+GFM_API int gfm_force_fwd(const void* h, int H, int n_nodes, const int* rowptr,
+                          const int* col_src, const void* edge_dx, const void* V, const void* c,
+                          const void* u, void* P, void* f_pred, int dtype, int flags,
+                          void* stream);
+/* grads of V, c, u: with S[i] = sum of dpre over edges with dst i plus those
+ * with src i, grad_V = S^T h and dh_final = dh_energy + S V; dz_out =
+ * dh_final * (1 - h^2) (model.py:553) feeds the last message-passing layer. */
+GFM_API size_t gfm_force_bwd_workspace_bytes(int H, int n_nodes, int dtype);
+GFM_API int gfm_force_bwd(const void* h, const void* P, int H, int n_nodes, const int* rowptr,
+                          const int* col_src, const void* edge_dx, const int* csc_ptr,
+                          const int* csc_eid, const int* csc_dst, const void* V, const void* c,
+                          const void* u, const void* df, const void* dh_energy, void* grad_v,
+                          void* grad_c, void* grad_u, void* dz_out, void* workspace, int dtype,
+                          int flags, void* stream);
 
 /* ---- K6/K8: energy readout, loss, seeds (model.py:365-373, 437-462, 510-533) */
 /* node_e = y a + c; e_pred = add.reduceat(node_e, node_offsets[:-1]) */

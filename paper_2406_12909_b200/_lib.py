@@ -34,6 +34,8 @@ SIGNATURES = {
     "gfm_last_error": (ctypes.c_char_p, []),
     "gfm_device_sm_count": (_I, []),
     "gfm_stream_sync": (_I, [_P]),
+    "gfm_set_gemm_mode": (_I, [_I]),
+    "gfm_get_gemm_mode": (_I, []),
     "gfm_graph_of_node": (_I, [_P, _I, _P, _P]),
     "gfm_scan_workspace_bytes": (_S, [_I]),
     "gfm_exclusive_scan": (_I, [_P, _I, _P, _P, _P]),
@@ -56,11 +58,10 @@ SIGNATURES = {
     "gfm_linear_bwd_weight_workspace_bytes": (_S, [_I, _I, _I, _I, _I, _I]),
     "gfm_linear_bwd_weight": (_I, [_P, _I, _I, _P, _I, _P, _I, _I, _P, _I, _I, _I, _P, _P, _P,
                                    _P, _I, _P]),
-    "gfm_force_fwd_workspace_bytes": (_S, [_I, _I, _I]),
-    "gfm_force_fwd": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _I, _P]),
+    "gfm_force_fwd": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "gfm_force_bwd_workspace_bytes": (_S, [_I, _I, _I]),
-    "gfm_force_bwd": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                           _P, _P, _P, _P, _I, _P]),
+    "gfm_force_bwd": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                           _P, _P, _P, _I, _I, _P]),
     "gfm_energy_readout": (_I, [_P, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P]),
     "gfm_loss_seeds": (_I, [_P, _P, _P, _I, _P, _P, _I, _D, _D, _P, _P, _P, _P, _I, _P]),
     "gfm_energy_seed": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _I, _P]),

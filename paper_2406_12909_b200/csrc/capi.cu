@@ -6,6 +6,9 @@
 
 namespace gfm {
 static thread_local char g_err[512] = "";
+static int g_gemm_mode = GFM_GEMM_TC3;
+
+int gemm_mode() { return g_gemm_mode; }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -22,6 +25,17 @@ int gfm_abi_version(void) { return GFM_ABI_VERSION; }
 const char* gfm_last_error(void) { return gfm::g_err; }
 
 int gfm_device_sm_count(void) { return gfm::num_sms(); }
+
+int gfm_set_gemm_mode(int mode) {
+  if (mode != GFM_GEMM_SIMT && mode != GFM_GEMM_TC3 && mode != GFM_GEMM_TC1) {
+    gfm::set_error("gfm_set_gemm_mode: unknown mode %d", mode);
+    return GFM_EINVAL;
+  }
+  gfm::g_gemm_mode = mode;
+  return 0;
+}
+
+int gfm_get_gemm_mode(void) { return gfm::g_gemm_mode; }
 
 int gfm_stream_sync(void* stream) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);

@@ -13,6 +13,9 @@ namespace gfm {
 // Thread-local last error (set by the C-ABI layer).
 void set_error(const char* fmt, ...);
 
+// Process-wide GEMM engine selection for float32 (GFM_GEMM_*).
+int gemm_mode();
+
 // ---------------------------------------------------------------------------
 // Exactly-rounded arithmetic.  nvcc contracts a*b+c into FMA by default; the
 // float64 parity paths (neighbour predicate, aggregation, Adam) must match

@@ -1,0 +1,382 @@
+// Force head, node-factored (forward + backward).
+//
+// Reference (model.py:377-389, 535-547):
+//   pair_e = h[dst] + h[src];  t_e = tanh(pair_e V^T + c);  m_e = t_e . u
+//   f[dst] += m_e * dx_e
+// The pre-activation is linear in the pair, so with P = h V^T (one N x H x H
+// GEMM per step instead of an E x H x H one):
+//   pre_e = P[dst] + P[src] + c
+// and the edge work becomes a memory-bound gather over the dst-CSR (P[dst]
+// held in registers, P[src] gathered from L2), fused with the u-dot and the
+// segmented force reduction -- the same kernel shape as the aggregation.
+// Backward: dpre_e = dm_e u (1 - t_e^2) with dm_e = df[dst] . dx_e;
+//   D_dst[i] = sum_{e in CSR row i} dpre_e,  D_src[j] = sum_{e in CSC row j} dpre_e
+//   S = D_dst + D_src      (N x H)
+//   grad_V = sum_e dpre_e pair_e^T = S^T h          (node GEMM)
+//   dh    += sum_e (dpre_e V) at dst and src = S V  (node GEMM)
+//   grad_c = colsum(D_dst),  grad_u = colsum(sum_{e in row i} t_e dm_e)
+// Two gather passes (dst-CSR then src-CSC, recomputing t instead of storing
+// E x H intermediates); no atomics, fixed summation orders.
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace gfm {
+
+// choose (NV float4 per lane, LPN lanes per node) for the float32 path
+static bool force_vec_shape(int H, int& nv, int& lpn) {
+  if (H % 4) return false;
+  const int h4 = H / 4;
+  for (int v : {1, 2, 4}) {
+    if (h4 % v) continue;
+    const int l = h4 / v;
+    if (l <= 32 && (l & (l - 1)) == 0) {
+      nv = v;
+      lpn = l;
+      return true;
+    }
+  }
+  return false;
+}
+
+// sum over the LPN lanes of this node's group (only the group's lanes named,
+// so groups of one warp may diverge / exit independently)
+template <int LPN>
+__device__ __forceinline__ float group_sum(float v) {
+  const int lane = threadIdx.x & 31;
+  const unsigned mask = LPN == 32 ? 0xffffffffu : (((1u << LPN) - 1u) << (lane / LPN * LPN));
+#pragma unroll
+  for (int o = LPN / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, LPN);
+  return v;
+}
+
+__device__ __forceinline__ float4 f4add3(float4 a, float4 b, float4 c) {
+  return make_float4(a.x + b.x + c.x, a.y + b.y + c.y, a.z + b.z + c.z, a.w + b.w + c.w);
+}
+
+// ------------------------------------------------------------------ forward
+template <int NV, int LPN>
+__global__ void __launch_bounds__(256)
+    k_force_fwd_vec(const float* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
+                    const int* __restrict__ col_src, const float* __restrict__ dx,
+                    const float* __restrict__ c, const float* __restrict__ u,
+                    float* __restrict__ f) {
+  constexpr int NPW = 32 / LPN;
+  const int lane = threadIdx.x & 31, sub = lane % LPN;
+  const int i = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
+  if (i >= n) return;  // whole LPN groups exit together
+  const int H4 = H >> 2;
+  const float4* P4 = reinterpret_cast<const float4*>(P);
+  float4 pi[NV], cu[NV], uu[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int c4 = v * LPN + sub;
+    pi[v] = __ldg(P4 + (long long)i * H4 + c4);
+    cu[v] = __ldg(reinterpret_cast<const float4*>(c) + c4);
+    uu[v] = __ldg(reinterpret_cast<const float4*>(u) + c4);
+  }
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  const int beg = rowptr[i], end = rowptr[i + 1];
+  int p = beg;
+  for (; p + 2 <= end; p += 2) {  // two edges in flight
+    const int s0 = __ldg(col_src + p), s1 = __ldg(col_src + p + 1);
+    float4 r0[NV], r1[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      r0[v] = __ldg(P4 + (long long)s0 * H4 + v * LPN + sub);
+      r1[v] = __ldg(P4 + (long long)s1 * H4 + v * LPN + sub);
+    }
+    float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float4 x0 = f4add3(pi[v], r0[v], cu[v]), x1 = f4add3(pi[v], r1[v], cu[v]);
+      d0 += tanhf(x0.x) * uu[v].x + tanhf(x0.y) * uu[v].y + tanhf(x0.z) * uu[v].z + tanhf(x0.w) * uu[v].w;
+      d1 += tanhf(x1.x) * uu[v].x + tanhf(x1.y) * uu[v].y + tanhf(x1.z) * uu[v].z + tanhf(x1.w) * uu[v].w;
+    }
+    const float m0 = group_sum<LPN>(d0), m1 = group_sum<LPN>(d1);
+    fx += (double)m0 * dx[3LL * p + 0]; fy += (double)m0 * dx[3LL * p + 1]; fz += (double)m0 * dx[3LL * p + 2];
+    fx += (double)m1 * dx[3LL * p + 3]; fy += (double)m1 * dx[3LL * p + 4]; fz += (double)m1 * dx[3LL * p + 5];
+  }
+  for (; p < end; ++p) {
+    const int s0 = __ldg(col_src + p);
+    float d0 = 0.f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float4 x0 = f4add3(pi[v], __ldg(P4 + (long long)s0 * H4 + v * LPN + sub), cu[v]);
+      d0 += tanhf(x0.x) * uu[v].x + tanhf(x0.y) * uu[v].y + tanhf(x0.z) * uu[v].z + tanhf(x0.w) * uu[v].w;
+    }
+    const float m0 = group_sum<LPN>(d0);
+    fx += (double)m0 * dx[3LL * p + 0]; fy += (double)m0 * dx[3LL * p + 1]; fz += (double)m0 * dx[3LL * p + 2];
+  }
+  if (sub == 0) {
+    f[3LL * i + 0] = (float)fx;
+    f[3LL * i + 1] = (float)fy;
+    f[3LL * i + 2] = (float)fz;
+  }
+}
+
+// generic: one warp per node, lanes over columns (any H, float or double)
+template <typename T>
+__global__ void k_force_fwd_warp(const T* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
+                                 const int* __restrict__ col_src, const T* __restrict__ dx,
+                                 const T* __restrict__ c, const T* __restrict__ u,
+                                 T* __restrict__ f) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+    const int s = col_src[p];
+    T d = T(0);
+    for (int k = lane; k < H; k += 32)
+      d += tanh_t(P[(long long)i * H + k] + P[(long long)s * H + k] + c[k]) * u[k];
+    d = warp_sum(d);
+    fx = __dadd_rn(fx, __dmul_rn((double)d, (double)dx[3LL * p + 0]));
+    fy = __dadd_rn(fy, __dmul_rn((double)d, (double)dx[3LL * p + 1]));
+    fz = __dadd_rn(fz, __dmul_rn((double)d, (double)dx[3LL * p + 2]));
+  }
+  if (lane == 0) {
+    f[3LL * i + 0] = (T)fx;
+    f[3LL * i + 1] = (T)fy;
+    f[3LL * i + 2] = (T)fz;
+  }
+}
+
+// ------------------------------------------------------------------ backward
+// pass 1 (dst rows): D_dst[i] = sum dpre_e, TU[i] = sum t_e dm_e
+template <int NV, int LPN>
+__global__ void __launch_bounds__(256)
+    k_force_bwd_dst_vec(const float* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
+                        const int* __restrict__ col_src, const float* __restrict__ dx,
+                        const float* __restrict__ df, const float* __restrict__ c,
+                        const float* __restrict__ u, float* __restrict__ Ddst,
+                        float* __restrict__ TU) {
+  constexpr int NPW = 32 / LPN;
+  const int lane = threadIdx.x & 31, sub = lane % LPN;
+  const int i = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
+  if (i >= n) return;
+  const int H4 = H >> 2;
+  const float4* P4 = reinterpret_cast<const float4*>(P);
+  float4 pi[NV], cu[NV], uu[NV], dd[NV], tu[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int c4 = v * LPN + sub;
+    pi[v] = __ldg(P4 + (long long)i * H4 + c4);
+    cu[v] = __ldg(reinterpret_cast<const float4*>(c) + c4);
+    uu[v] = __ldg(reinterpret_cast<const float4*>(u) + c4);
+    dd[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    tu[v] = dd[v];
+  }
+  const float fx = df[3LL * i + 0], fy = df[3LL * i + 1], fz = df[3LL * i + 2];
+  for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+    const int s = __ldg(col_src + p);
+    // model.py:537-538 (sum over xyz left to right)
+    const float dm = __fadd_rn(__fadd_rn(__fmul_rn(fx, dx[3LL * p]), __fmul_rn(fy, dx[3LL * p + 1])),
+                               __fmul_rn(fz, dx[3LL * p + 2]));
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float4 x = f4add3(pi[v], __ldg(P4 + (long long)s * H4 + v * LPN + sub), cu[v]);
+      const float4 t = make_float4(tanhf(x.x), tanhf(x.y), tanhf(x.z), tanhf(x.w));
+      dd[v].x += dm * uu[v].x * (1.f - t.x * t.x); dd[v].y += dm * uu[v].y * (1.f - t.y * t.y);
+      dd[v].z += dm * uu[v].z * (1.f - t.z * t.z); dd[v].w += dm * uu[v].w * (1.f - t.w * t.w);
+      tu[v].x += t.x * dm; tu[v].y += t.y * dm; tu[v].z += t.z * dm; tu[v].w += t.w * dm;
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const long long o = (long long)i * H4 + v * LPN + sub;
+    reinterpret_cast<float4*>(Ddst)[o] = dd[v];
+    reinterpret_cast<float4*>(TU)[o] = tu[v];
+  }
+}
+
+// pass 2 (src rows): S[j] = D_dst[j] + sum over CSC slots of dpre_e
+template <int NV, int LPN>
+__global__ void __launch_bounds__(256)
+    k_force_bwd_src_vec(const float* __restrict__ P, int n, int H, const int* __restrict__ csc_ptr,
+                        const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
+                        const float* __restrict__ dx, const float* __restrict__ df,
+                        const float* __restrict__ c, const float* __restrict__ u,
+                        const float* __restrict__ Ddst, float* __restrict__ S) {
+  constexpr int NPW = 32 / LPN;
+  const int lane = threadIdx.x & 31, sub = lane % LPN;
+  const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
+  if (j >= n) return;
+  const int H4 = H >> 2;
+  const float4* P4 = reinterpret_cast<const float4*>(P);
+  float4 pj[NV], cu[NV], uu[NV], acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int c4 = v * LPN + sub;
+    pj[v] = __ldg(P4 + (long long)j * H4 + c4);
+    cu[v] = __ldg(reinterpret_cast<const float4*>(c) + c4);
+    uu[v] = __ldg(reinterpret_cast<const float4*>(u) + c4);
+    acc[v] = reinterpret_cast<const float4*>(Ddst)[(long long)j * H4 + c4];
+  }
+  for (int q = csc_ptr[j]; q < csc_ptr[j + 1]; ++q) {
+    const int p = __ldg(csc_eid + q), i = __ldg(csc_dst + q);
+    const float dm = __fadd_rn(__fadd_rn(__fmul_rn(df[3LL * i], dx[3LL * p]), __fmul_rn(df[3LL * i + 1], dx[3LL * p + 1])),
+                               __fmul_rn(df[3LL * i + 2], dx[3LL * p + 2]));
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float4 x = f4add3(__ldg(P4 + (long long)i * H4 + v * LPN + sub), pj[v], cu[v]);
+      const float4 t = make_float4(tanhf(x.x), tanhf(x.y), tanhf(x.z), tanhf(x.w));
+      acc[v].x += dm * uu[v].x * (1.f - t.x * t.x); acc[v].y += dm * uu[v].y * (1.f - t.y * t.y);
+      acc[v].z += dm * uu[v].z * (1.f - t.z * t.z); acc[v].w += dm * uu[v].w * (1.f - t.w * t.w);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+    reinterpret_cast<float4*>(S)[(long long)j * H4 + v * LPN + sub] = acc[v];
+}
+
+// generic (any H, float / double): thread per (node, column)
+template <typename T>
+__global__ void k_force_bwd_dst_scalar(const T* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
+                                       const int* __restrict__ col_src, const T* __restrict__ dx,
+                                       const T* __restrict__ df, const T* __restrict__ c,
+                                       const T* __restrict__ u, T* __restrict__ Ddst,
+                                       T* __restrict__ TU) {
+  const long long total = (long long)n * H;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / H), k = (int)(idx % H);
+    T dd = T(0), tu = T(0);
+    for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+      const int s = col_src[p];
+      const T dm = add_rn(add_rn(mul_rn(df[3LL * i], dx[3LL * p]), mul_rn(df[3LL * i + 1], dx[3LL * p + 1])),
+                          mul_rn(df[3LL * i + 2], dx[3LL * p + 2]));
+      const T t = tanh_t(P[(long long)i * H + k] + P[(long long)s * H + k] + c[k]);
+      dd += mul_rn(mul_rn(dm, u[k]), sub_rn(T(1), mul_rn(t, t)));
+      tu += t * dm;
+    }
+    Ddst[idx] = dd;
+    TU[idx] = tu;
+  }
+}
+
+template <typename T>
+__global__ void k_force_bwd_src_scalar(const T* __restrict__ P, int n, int H, const int* __restrict__ csc_ptr,
+                                       const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
+                                       const T* __restrict__ dx, const T* __restrict__ df,
+                                       const T* __restrict__ c, const T* __restrict__ u,
+                                       const T* __restrict__ Ddst, T* __restrict__ S) {
+  const long long total = (long long)n * H;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / H), k = (int)(idx % H);
+    T acc = Ddst[idx];
+    for (int q = csc_ptr[j]; q < csc_ptr[j + 1]; ++q) {
+      const int p = csc_eid[q], i = csc_dst[q];
+      const T dm = add_rn(add_rn(mul_rn(df[3LL * i], dx[3LL * p]), mul_rn(df[3LL * i + 1], dx[3LL * p + 1])),
+                          mul_rn(df[3LL * i + 2], dx[3LL * p + 2]));
+      const T t = tanh_t(P[(long long)i * H + k] + P[(long long)j * H + k] + c[k]);
+      acc += mul_rn(mul_rn(dm, u[k]), sub_rn(T(1), mul_rn(t, t)));
+    }
+    S[idx] = acc;
+  }
+}
+
+// deterministic column sums of X [n][H] (+ optional second matrix Y):
+// pass 1 -- fixed row chunks -> partials; pass 2 -- ordered sum of partials
+constexpr int kColChunk = 512;
+template <typename T>
+__global__ void k_colsum_partial(const T* __restrict__ X, int n, int H, T* __restrict__ part) {
+  const int ch = blockIdx.x;
+  const int lo = ch * kColChunk, hi = min(n, lo + kColChunk);
+  for (int k = threadIdx.x + blockIdx.y * blockDim.x; k < H; k += blockDim.x * gridDim.y) {
+    double s = 0.0;
+    for (int i = lo; i < hi; ++i) s += (double)X[(long long)i * H + k];
+    part[(long long)ch * H + k] = (T)s;
+  }
+}
+
+template <typename T>
+__global__ void k_colsum_final(const T* __restrict__ part, int nch, int H, T* __restrict__ out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < H; k += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int ch = 0; ch < nch; ++ch) s += (double)part[(long long)ch * H + k];
+    out[k] = (T)s;
+  }
+}
+
+template <typename T>
+cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s) {
+  const int nch = ceil_div(n > 0 ? n : 1, kColChunk);
+  dim3 g1(nch, ceil_div(H, 256));
+  if (n > 0) k_colsum_partial<T><<<g1, 256, 0, s>>>(X, n, H, part);
+  k_colsum_final<T><<<ceil_div(H, 256), 256, 0, s>>>(part, n > 0 ? nch : 0, H, out);
+  return cudaGetLastError();
+}
+
+#define GFM_FVEC_CASES(M) M(1, 1) M(1, 2) M(1, 4) M(1, 8) M(1, 16) M(1, 32) M(2, 32) M(4, 32)
+
+template <typename T>
+cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const int* col_src,
+                            const T* dx, const T* c, const T* u, T* f, int flags, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int nv = 0, lpn = 0;
+  if constexpr (std::is_same<T, float>::value) {
+    if (!(flags & GFM_FLAG_SCALAR) && force_vec_shape(H, nv, lpn)) {
+      const int grid = ceil_div(n, 8 * (32 / lpn));
+#define GFM_FF(NV_, LPN_)                                                                    \
+  if (nv == NV_ && lpn == LPN_) {                                                            \
+    k_force_fwd_vec<NV_, LPN_><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);  \
+    return cudaGetLastError();                                                               \
+  }
+      GFM_FVEC_CASES(GFM_FF)
+#undef GFM_FF
+    }
+  }
+  k_force_fwd_warp<T><<<ceil_div(n, 8), 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t force_bwd_edges(const T* P, int n, int H, const int* rowptr, const int* col_src,
+                            const int* csc_ptr, const int* csc_eid, const int* csc_dst,
+                            const T* dx, const T* df, const T* c, const T* u, T* Ddst, T* TU,
+                            T* S, int flags, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int nv = 0, lpn = 0;
+  if constexpr (std::is_same<T, float>::value) {
+    if (!(flags & GFM_FLAG_SCALAR) && force_vec_shape(H, nv, lpn)) {
+      const int grid = ceil_div(n, 8 * (32 / lpn));
+#define GFM_FB(NV_, LPN_)                                                                         \
+  if (nv == NV_ && lpn == LPN_) {                                                                 \
+    k_force_bwd_dst_vec<NV_, LPN_><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df, c, u,   \
+                                                        Ddst, TU);                                \
+    k_force_bwd_src_vec<NV_, LPN_><<<grid, 256, 0, s>>>(P, n, H, csc_ptr, csc_eid, csc_dst, dx,   \
+                                                        df, c, u, Ddst, S);                       \
+    return cudaGetLastError();                                                                    \
+  }
+      GFM_FVEC_CASES(GFM_FB)
+#undef GFM_FB
+    }
+  }
+  const long long total = (long long)n * H;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+  k_force_bwd_dst_scalar<T><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df, c, u, Ddst, TU);
+  k_force_bwd_src_scalar<T><<<grid, 256, 0, s>>>(P, n, H, csc_ptr, csc_eid, csc_dst, dx, df, c, u,
+                                                 Ddst, S);
+  return cudaGetLastError();
+}
+
+template cudaError_t force_fwd_edges<float>(const float*, int, int, const int*, const int*,
+                                            const float*, const float*, const float*, float*, int,
+                                            cudaStream_t);
+template cudaError_t force_fwd_edges<double>(const double*, int, int, const int*, const int*,
+                                             const double*, const double*, const double*, double*,
+                                             int, cudaStream_t);
+template cudaError_t force_bwd_edges<float>(const float*, int, int, const int*, const int*,
+                                            const int*, const int*, const int*, const float*,
+                                            const float*, const float*, const float*, float*,
+                                            float*, float*, int, cudaStream_t);
+template cudaError_t force_bwd_edges<double>(const double*, int, int, const int*, const int*,
+                                             const int*, const int*, const int*, const double*,
+                                             const double*, const double*, const double*, double*,
+                                             double*, double*, int, cudaStream_t);
+template cudaError_t colsum<float>(const float*, int, int, float*, float*, cudaStream_t);
+template cudaError_t colsum<double>(const double*, int, int, double*, double*, cudaStream_t);
+
+}  // namespace gfm

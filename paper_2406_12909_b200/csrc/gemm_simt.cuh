@@ -130,6 +130,7 @@ struct EpiSplitCols {  // columns [0, n1) -> o1, [n1, N) -> o2; optional *(1 - g
   int ld2;
   const T* gate;  // if set: out *= (1 - gate[m][n]^2), gate row stride ldg
   int ldg;
+  const T* add;   // if set: o1 columns get + add[m][n] (row stride ld1) before the gate
   __device__ void operator()(T (&acc)[kTM][kTN], int m0, int n0, int M, int N, int, int, int, int,
                              int) const {
 #pragma unroll
@@ -141,6 +142,7 @@ struct EpiSplitCols {  // columns [0, n1) -> o1, [n1, N) -> o2; optional *(1 - g
         int n = n0 + j;
         if (n >= N) continue;
         T v = acc[i][j];
+        if (add && n < n1) v = add[(long long)m * ld1 + n] + v;
         if (gate) {
           T g = gate[(long long)m * ldg + n];
           v = v * (T(1) - g * g);

@@ -1,12 +1,16 @@
-// Dense model pieces on the SIMT engine: node update / head linear layers
-// (forward, data-grad, deterministic split-K weight-grad), the fused force
-// head (gather-fed GEMM + tanh + u-dot + dst-CSR reduction, and its
-// backward with recompute), energy readout + graph pooling, the L1 MTL loss
-// with its seeds, and the embedding gradient.
+// Dense model pieces: node update / head linear layers (forward, data-grad,
+// deterministic split-K weight-grad) on the tcgen05 engine (float32) or the
+// SIMT engine (float64), the node-factored force head drivers (force.cu has
+// the edge kernels), energy readout + graph pooling, the L1 MTL loss with its
+// seeds, and the embedding gradient.
 //
 // Reference: forward_batch (model.py:344-400), mtl_loss (model.py:437-462),
 // loss_and_grad (model.py:483-565).
+#include <algorithm>
+#include <type_traits>
+
 #include "gemm_simt.cuh"
+#include "tc_gemm.cuh"
 
 namespace gfm {
 
@@ -16,89 +20,6 @@ static inline int grid_1d(long long n, int threads = 256) {
   if (b > 148 * 32) b = 148 * 32;
   return (int)b;
 }
-
-// ------------------------------------------------------------ force epilogues
-template <typename T>
-struct EpiForceFwd {  // t = tanh(pre + c); partial m = sum_n t*u over this N tile
-  const T* c;
-  const T* u;
-  T* m_part;
-  int ntiles;
-  __device__ void operator()(T (&acc)[kTM][kTN], int m0, int n0, int M, int N, int, int, int bn,
-                             int tx, int) const {
-    T part[kTM];
-#pragma unroll
-    for (int i = 0; i < kTM; ++i) {
-      part[i] = T(0);
-#pragma unroll
-      for (int j = 0; j < kTN; ++j) {
-        const int n = n0 + j;
-        if (n < N) part[i] += tanh_t(acc[i][j] + c[n]) * u[n];
-      }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) part[i] += __shfl_xor_sync(0xffffffffu, part[i], o);
-    }
-    if (tx == 0) {
-#pragma unroll
-      for (int i = 0; i < kTM; ++i)
-        if (m0 + i < M) m_part[(long long)(m0 + i) * ntiles + bn] = part[i];
-    }
-  }
-};
-
-template <typename T>
-struct EpiForceBwd {  // dm = df[dst].dx; dpre = dm*u*(1-t^2); column partials of t*dm
-  const T* c;
-  const T* u;
-  const T* df;
-  const int* edge_dst;
-  const T* dx;
-  T* dpre;
-  int H;
-  T* ws_u;
-  __device__ void operator()(T (&acc)[kTM][kTN], int m0, int n0, int M, int N, int, int bm, int,
-                             int tx, int ty) const {
-    __shared__ T red[16][kBN];
-    T dm[kTM];
-#pragma unroll
-    for (int i = 0; i < kTM; ++i) {
-      const int m = m0 + i;
-      dm[i] = T(0);
-      if (m < M) {  // model.py:537-538, sum over xyz left to right
-        const T* f = df + 3LL * edge_dst[m];
-        const T* d = dx + 3LL * m;
-        dm[i] = add_rn(add_rn(mul_rn(f[0], d[0]), mul_rn(f[1], d[1])), mul_rn(f[2], d[2]));
-      }
-    }
-    T colpart[kTN];
-#pragma unroll
-    for (int j = 0; j < kTN; ++j) {
-      colpart[j] = T(0);
-      const int n = n0 + j;
-      if (n >= N) continue;
-#pragma unroll
-      for (int i = 0; i < kTM; ++i) {
-        const int m = m0 + i;
-        if (m >= M) continue;
-        const T t = tanh_t(acc[i][j] + c[n]);
-        dpre[(long long)m * H + n] = mul_rn(mul_rn(dm[i], u[n]), sub_rn(T(1), mul_rn(t, t)));
-        colpart[j] += t * dm[i];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kTN; ++j) red[ty][tx * kTN + j] = colpart[j];
-    __syncthreads();
-    if (ty == 0) {
-#pragma unroll
-      for (int j = 0; j < kTN; ++j) {
-        const int n = n0 + j;
-        T s = T(0);
-        for (int y = 0; y < 16; ++y) s += red[y][tx * kTN + j];
-        if (n < N) ws_u[(long long)bm * H + n] = s;
-      }
-    }
-  }
-};
 
 // ------------------------------------------------------------ reductions
 // out segment mapping for split-K weight grads: result matrix R[N][Kt] with
@@ -111,8 +32,9 @@ __global__ void k_splitk_reduce(const T* __restrict__ ws, int splits, int N, int
   const long long total = (long long)N * Kt;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    T s = ws[idx];
-    for (int k = 1; k < splits; ++k) s += ws[(long long)k * total + idx];
+    double acc = (double)ws[idx];  // float64 sum of the partials (same order for every run)
+    for (int k = 1; k < splits; ++k) acc += (double)ws[(long long)k * total + idx];
+    const T s = (T)acc;
     const int n = (int)(idx / Kt), k = (int)(idx % Kt);
     if (k < K1)
       g1[(long long)n * K1 + k] = s;
@@ -120,68 +42,6 @@ __global__ void k_splitk_reduce(const T* __restrict__ ws, int splits, int N, int
       g2[(long long)n * K2 + (k - K1)] = s;
     else
       gb[n] = s;
-  }
-}
-
-template <typename T>
-__global__ void k_rows_reduce(const T* __restrict__ ws, const int* __restrict__ n_rows_dev,
-                              int rows_per_item, int cols, T* __restrict__ out) {
-  // out[c] = sum over tiles r < ceil(E / rows_per_item) of ws[r][c]
-  const int E = *n_rows_dev;
-  const int tiles = (E + rows_per_item - 1) / rows_per_item;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
-    T s = T(0);
-    for (int r = 0; r < tiles; ++r) s += ws[(long long)r * cols + c];
-    out[c] = s;
-  }
-}
-
-// f[i] = sum over CSR row i of m_e * dx_e, m_e = sum of the N-tile partials
-// (np.add.at over edge_dst in edge order, model.py:382-384).
-template <typename T>
-__global__ void k_force_combine(const T* __restrict__ m_part, int ntiles,
-                                const int* __restrict__ rowptr, const T* __restrict__ dx, int n,
-                                T* __restrict__ f, T* __restrict__ m_out) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    // float64 accumulation (identical ops for T = double; for float32 the
-    // cancelling pair sum keeps full precision)
-    double fx = 0.0, fy = 0.0, fz = 0.0;
-    for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
-      T m = m_part[(long long)p * ntiles];
-      for (int t = 1; t < ntiles; ++t) m += m_part[(long long)p * ntiles + t];
-      if (m_out) m_out[p] = m;
-      fx = __dadd_rn(fx, __dmul_rn((double)m, (double)dx[3LL * p + 0]));
-      fy = __dadd_rn(fy, __dmul_rn((double)m, (double)dx[3LL * p + 1]));
-      fz = __dadd_rn(fz, __dmul_rn((double)m, (double)dx[3LL * p + 2]));
-    }
-    f[3LL * i + 0] = (T)fx;
-    f[3LL * i + 1] = (T)fy;
-    f[3LL * i + 2] = (T)fz;
-  }
-}
-
-// dh_final[i] = dh_energy[i] + sum_{CSR row i} dpair + sum_{CSC row i} dpair
-// (model.py:533, 546-547, in that order); optional gate -> dz of last layer.
-template <typename T>
-__global__ void k_node_combine(const T* __restrict__ dh_e, const T* __restrict__ dpair,
-                               const int* __restrict__ rowptr, const int* __restrict__ csc_ptr,
-                               const int* __restrict__ csc_eid, int n, int H,
-                               const T* __restrict__ gate, T* __restrict__ dh_out,
-                               T* __restrict__ dz_out) {
-  const long long total = (long long)n * H;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx / H), c = (int)(idx % H);
-    double acc = (double)dh_e[idx];
-    for (int p = rowptr[i]; p < rowptr[i + 1]; ++p)
-      acc = __dadd_rn(acc, (double)dpair[(long long)p * H + c]);
-    for (int q = csc_ptr[i]; q < csc_ptr[i + 1]; ++q)
-      acc = __dadd_rn(acc, (double)dpair[(long long)csc_eid[q] * H + c]);
-    if (dh_out) dh_out[idx] = (T)acc;
-    if (dz_out) {
-      const T g = gate[idx];
-      dz_out[idx] = mul_rn((T)acc, sub_rn(T(1), mul_rn(g, g)));
-    }
   }
 }
 
@@ -324,12 +184,27 @@ __global__ void k_emb_reduce(const T* __restrict__ ws, const unsigned char* __re
 }
 
 // ------------------------------------------------------------ typed drivers
+// float32 GEMMs run on the tcgen05 tensor cores (3xTF32 by default,
+// gemm_mode() == GFM_GEMM_TC3); float64 and GFM_GEMM_SIMT use the SIMT engine.
+template <typename T>
+inline bool use_tc() {
+  return std::is_same<T, float>::value && gemm_mode() != GFM_GEMM_SIMT;
+}
+inline int tc_split3() { return gemm_mode() == GFM_GEMM_TC1 ? 0 : 1; }
+inline int tc_bn(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+
 template <typename T>
 cudaError_t linear_fwd_t(const T* X1, int ld1, int K1, const T* X2, int ld2, int K2, const T* W1,
                          int ldw1, const T* W2, int ldw2, const T* bias, int M, const int* M_dev,
                          int N, int act, T* Y, int ldy, cudaStream_t s) {
   Rows2Ld<T> a{X1, ld1, K1, X2, ld2, K2};
   Rows2Ld<T> b{W1, ldw1, K1, W2, ldw2, K2};
+  if constexpr (std::is_same<T, float>::value) {
+    if (use_tc<T>()) {
+      tc::TcEpiBiasAct epi{Y, ldy, bias, act};
+      return tc::launch(M, M_dev, N, K1 + K2, nullptr, 1, tc_split3(), a, b, epi, s);
+    }
+  }
   EpiBiasAct<T> epi{Y, ldy, bias, act};
   return launch_simt_gemm<T>(M, M_dev, N, K1 + K2, nullptr, 1, a, b, epi, s);
 }
@@ -337,18 +212,36 @@ cudaError_t linear_fwd_t(const T* X1, int ld1, int K1, const T* X2, int ld2, int
 template <typename T>
 cudaError_t linear_bwd_data_t(const T* dY, int ldd, int M, const int* M_dev, int N, const T* W1,
                               int ldw1, int K1, const T* W2, int ldw2, int K2, T* o1, int ldo1,
-                              T* o2, int ldo2, const T* gate, int ldg, cudaStream_t s) {
+                              T* o2, int ldo2, const T* gate, int ldg, cudaStream_t s,
+                              const T* add = nullptr) {
   RowsLd<T> a{dY, ldd};
   Cols2Ld<T> b{W1, ldw1, K1, W2, ldw2, K2};
-  EpiSplitCols<T> epi{o1, ldo1, K1, o2, ldo2, gate, ldg};
+  if constexpr (std::is_same<T, float>::value) {
+    if (use_tc<T>()) {
+      tc::TcEpiSplitCols epi{o1, ldo1, K1, o2, ldo2, gate, ldg, add};
+      return tc::launch(M, M_dev, K1 + K2, N, nullptr, 1, tc_split3(), a, b, epi, s);
+    }
+  }
+  EpiSplitCols<T> epi{o1, ldo1, K1, o2, ldo2, gate, ldg, add};
   return launch_simt_gemm<T>(M, M_dev, K1 + K2, N, nullptr, 1, a, b, epi, s);
+}
+
+template <typename T>
+int wgrad_splits(int M, int N, int Kt) {
+  return use_tc<T>() ? tc::splits_for(N, Kt, M, tc_bn(Kt)) : choose_splits(N, Kt, M);
 }
 
 template <typename T>
 size_t linear_bwd_weight_ws(int M, int N, int K1, int K2, int with_bias) {
   const int Kt = K1 + K2 + with_bias;
-  const int splits = choose_splits(N, Kt, M);
+  const int splits = std::max(choose_splits(N, Kt, M), tc::splits_for(N, Kt, M, tc_bn(Kt)));
   return sizeof(T) * (size_t)splits * N * Kt;
+}
+
+// actual number of K splits after rounding the chunk to the engine's K step
+inline int real_splits(int K, int splits, int kstep) {
+  int k_chunk = ceil_div(ceil_div(K > 0 ? K : 1, splits), kstep) * kstep;
+  return ceil_div(K > 0 ? K : 1, k_chunk);
 }
 
 template <typename T>
@@ -356,85 +249,88 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
                                 int ld1, int K1, const T* X2, int ld2, int K2, int with_bias,
                                 T* g1, T* g2, T* gb, T* ws, cudaStream_t s) {
   const int Kt = K1 + K2 + with_bias;
-  const int splits = choose_splits(N, Kt, M);
+  const int splits = wgrad_splits<T>(M, N, Kt);
   ColsLd<T> a{dY, ldd};
   Cols2Ld<T> b{X1, ld1, K1, X2, ld2, K2};
-  EpiPartial<T> epi{ws, (long long)N * Kt};
+  cudaError_t e;
+  int real;
   // rows = output features N, cols = Kt, reduction over the M batch rows
-  cudaError_t e = launch_simt_gemm<T>(N, nullptr, Kt, M, M_dev, splits, a, b, epi, s);
+  if constexpr (std::is_same<T, float>::value) {
+    if (use_tc<T>()) {
+      tc::TcEpiPartial epi{ws, (long long)N * Kt, N, Kt, 0};
+      e = tc::launch(N, nullptr, Kt, M, M_dev, splits, tc_split3(), a, b, epi, s);
+      real = real_splits(M, splits, tc::kBK);
+      goto reduce;
+    }
+  }
+  {
+    EpiPartial<T> epi{ws, (long long)N * Kt};
+    e = launch_simt_gemm<T>(N, nullptr, Kt, M, M_dev, splits, a, b, epi, s);
+    real = real_splits(M, splits, kBK);
+  }
+reduce:
   if (e != cudaSuccess) return e;
-  int k_chunk = ceil_div(ceil_div(M > 0 ? M : 1, splits), kBK) * kBK;
-  int real_splits = ceil_div(M > 0 ? M : 1, k_chunk);
-  k_splitk_reduce<T><<<grid_1d((long long)N * Kt), 256, 0, s>>>(ws, real_splits, N, K1, K2,
-                                                                 with_bias, g1, g2, gb);
+  k_splitk_reduce<T><<<grid_1d((long long)N * Kt), 256, 0, s>>>(ws, real, N, K1, K2, with_bias,
+                                                                 g1, g2, gb);
   return cudaGetLastError();
 }
+
+// ------------------------------------------------------------ force head
+// node-factored (see force.cu): P = h V^T, then edge gathers
+template <typename T>
+cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const int* col_src,
+                            const T* dx, const T* c, const T* u, T* f, int flags, cudaStream_t s);
+template <typename T>
+cudaError_t force_bwd_edges(const T* P, int n, int H, const int* rowptr, const int* col_src,
+                            const int* csc_ptr, const int* csc_eid, const int* csc_dst,
+                            const T* dx, const T* df, const T* c, const T* u, T* Ddst, T* TU,
+                            T* S, int flags, cudaStream_t s);
+template <typename T>
+cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s);
 
 template <typename T>
 cudaError_t force_fwd_t(const T* h, int H, int n, const int* rowptr, const int* col_src,
-                        const int* edge_dst, const T* dx, int e_cap, const T* V, const T* c,
-                        const T* u, T* m_part, T* f, T* m_out, cudaStream_t s) {
-  const int ntiles = ceil_div(H, kBN);
-  PairLd<T> a{h, H, edge_dst, col_src};
-  RowsLd<T> b{V, H};
-  EpiForceFwd<T> epi{c, u, m_part, ntiles};
-  cudaError_t e = launch_simt_gemm<T>(e_cap, rowptr + n, H, H, nullptr, 1, a, b, epi, s);
-  if (e != cudaSuccess) return e;
-  k_force_combine<T><<<grid_1d(n), 256, 0, s>>>(m_part, ntiles, rowptr, dx, n, f, m_out);
-  return cudaGetLastError();
-}
-
-template <typename T>
-size_t force_bwd_ws(int H, int e_cap) {
-  // dpre (E x H) + dpair (E x H) + u partials + split-K partials of [V | c]
-  const int splits = choose_splits(H, H + 1, e_cap);
-  return sizeof(T) * ((size_t)e_cap * H * 2 + (size_t)(ceil_div(e_cap, kBM) + 1) * H +
-                      (size_t)splits * H * (H + 1)) + 1024;
-}
-
-template <typename T>
-cudaError_t force_bwd_t(const T* h, int H, int n, const int* rowptr, const int* col_src,
-                        const int* edge_dst, const T* dx, int e_cap, const int* csc_ptr,
-                        const int* csc_eid, const T* V, const T* c, const T* u, const T* df,
-                        const T* dh_e, T* gV, T* gc, T* gu, T* dh_out, T* dz_out, void* ws,
+                        const T* dx, const T* V, const T* c, const T* u, T* P, T* f, int flags,
                         cudaStream_t s) {
-  const int* E_dev = rowptr + n;
-  T* dpre = (T*)ws;
-  T* dpair = dpre + (size_t)e_cap * H;
-  T* wsu = dpair + (size_t)e_cap * H;
-  T* wsk = wsu + (size_t)(ceil_div(e_cap, kBM) + 1) * H;
-  cudaError_t e;
-  {  // recompute t, produce dpre and grad_u partials (model.py:537-542)
-    PairLd<T> a{h, H, edge_dst, col_src};
-    RowsLd<T> b{V, H};
-    EpiForceBwd<T> epi{c, u, df, edge_dst, dx, dpre, H, wsu};
-    e = launch_simt_gemm<T>(e_cap, E_dev, H, H, nullptr, 1, a, b, epi, s);
-    if (e != cudaSuccess) return e;
-    k_rows_reduce<T><<<grid_1d(H), 256, 0, s>>>(wsu, E_dev, kBM, H, gu);
-  }
-  {  // [grad_V | grad_c] = dpre^T [pair | 1]   (model.py:543-544)
-    const int splits = choose_splits(H, H + 1, e_cap);
-    ColsLd<T> a{dpre, H};
-    PairColsLd<T> b{h, H, edge_dst, col_src};
-    EpiPartial<T> epi{wsk, (long long)H * (H + 1)};
-    e = launch_simt_gemm<T>(H, nullptr, H + 1, e_cap, E_dev, splits, a, b, epi, s);
-    if (e != cudaSuccess) return e;
-    int k_chunk = ceil_div(ceil_div(e_cap > 0 ? e_cap : 1, splits), kBK) * kBK;
-    int real = ceil_div(e_cap > 0 ? e_cap : 1, k_chunk);
-    k_splitk_reduce<T><<<grid_1d((long long)H * (H + 1)), 256, 0, s>>>(wsk, real, H, H, 0, 1, gV,
-                                                                         nullptr, gc);
-  }
-  {  // dpair = dpre V  (model.py:545)
-    RowsLd<T> a{dpre, H};
-    ColsLd<T> b{V, H};
-    EpiSplitCols<T> epi{dpair, H, H, nullptr, 0, nullptr, 0};
-    e = launch_simt_gemm<T>(e_cap, E_dev, H, H, nullptr, 1, a, b, epi, s);
-    if (e != cudaSuccess) return e;
-  }
-  k_node_combine<T><<<grid_1d((long long)n * H), 256, 0, s>>>(dh_e, dpair, rowptr, csc_ptr, csc_eid,
-                                                              n, H, dz_out ? h : nullptr, dh_out,
-                                                              dz_out);
-  return cudaGetLastError();
+  // P = h V^T  (the pair pre-activation is P[dst] + P[src] + c)
+  cudaError_t e = linear_fwd_t<T>(h, H, H, nullptr, 0, 0, V, H, nullptr, 0, nullptr, n, nullptr, H,
+                                  0, P, H, s);
+  if (e != cudaSuccess) return e;
+  return force_fwd_edges<T>(P, n, H, rowptr, col_src, dx, c, u, f, flags, s);
+}
+
+template <typename T>
+size_t force_bwd_ws(int H, int n) {
+  const size_t nh = (size_t)(n > 0 ? n : 1) * H;
+  const size_t parts = (size_t)ceil_div(n > 0 ? n : 1, 512) * H;
+  return sizeof(T) * (3 * nh + parts + 64) + linear_bwd_weight_ws<T>(n, H, H, 0, 0) + 4096;
+}
+
+template <typename T>
+cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
+                        const int* col_src, const T* dx, const int* csc_ptr, const int* csc_eid,
+                        const int* csc_dst, const T* V, const T* c, const T* u, const T* df,
+                        const T* dh_e, T* gV, T* gc, T* gu, T* dz_out, void* ws, int flags,
+                        cudaStream_t s) {
+  const size_t nh = (size_t)(n > 0 ? n : 1) * H;
+  T* Ddst = (T*)ws;
+  T* TU = Ddst + nh;
+  T* S = TU + nh;
+  T* part = S + nh;
+  T* wws = part + (size_t)ceil_div(n > 0 ? n : 1, 512) * H + 64;
+  wws = (T*)(((uintptr_t)wws + 255) & ~(uintptr_t)255);
+  cudaError_t e = force_bwd_edges<T>(P, n, H, rowptr, col_src, csc_ptr, csc_eid, csc_dst, dx, df,
+                                     c, u, Ddst, TU, S, flags, s);
+  if (e != cudaSuccess) return e;
+  // grad_V = S^T h   (= sum_e dpre_e pair_e^T, model.py:543)
+  e = linear_bwd_weight_t<T>(S, H, n, nullptr, H, h, H, H, nullptr, 0, 0, 0, gV, nullptr, nullptr,
+                             wws, s);
+  if (e != cudaSuccess) return e;
+  if ((e = colsum<T>(Ddst, n, H, gc, part, s)) != cudaSuccess) return e;  // model.py:544
+  if ((e = colsum<T>(TU, n, H, gu, part, s)) != cudaSuccess) return e;    // model.py:540
+  // dz_last = (dh_energy + S V) * (1 - h^2)   (model.py:545-547, 553)
+  return linear_bwd_data_t<T>(S, H, n, nullptr, H, V, H, H, nullptr, 0, 0, dz_out, H, nullptr, 0,
+                              h, H, s, dh_e);
 }
 
 template <typename T>
@@ -513,36 +409,30 @@ int gfm_linear_bwd_weight(const void* dY, int ldd, int M, const int* M_dev, int 
                                       (T*)workspace, (cudaStream_t)stream))
 }
 
-size_t gfm_force_fwd_workspace_bytes(int H, int e_cap, int dtype) {
-  const size_t esz = dtype == GFM_F64 ? 8 : 4;
-  return esz * (size_t)(e_cap > 0 ? e_cap : 1) * ceil_div(H, kBN) + 256;
-}
-
 int gfm_force_fwd(const void* h, int H, int n_nodes, const int* rowptr, const int* col_src,
-                  const int* edge_dst, const void* edge_dx, int e_cap, const void* V,
-                  const void* c, const void* u, void* f_pred, void* m_out, void* workspace,
-                  int dtype, void* stream) {
+                  const void* edge_dx, const void* V, const void* c, const void* u, void* P,
+                  void* f_pred, int dtype, int flags, void* stream) {
   GFM_DISPATCH(dtype, "gfm_force_fwd",
-               force_fwd_t<T>((const T*)h, H, n_nodes, rowptr, col_src, edge_dst,
-                              (const T*)edge_dx, e_cap, (const T*)V, (const T*)c, (const T*)u,
-                              (T*)workspace, (T*)f_pred, (T*)m_out, (cudaStream_t)stream))
+               force_fwd_t<T>((const T*)h, H, n_nodes, rowptr, col_src, (const T*)edge_dx,
+                              (const T*)V, (const T*)c, (const T*)u, (T*)P, (T*)f_pred, flags,
+                              (cudaStream_t)stream))
 }
 
-size_t gfm_force_bwd_workspace_bytes(int H, int e_cap, int dtype) {
-  return dtype == GFM_F64 ? force_bwd_ws<double>(H, e_cap) : force_bwd_ws<float>(H, e_cap);
+size_t gfm_force_bwd_workspace_bytes(int H, int n_nodes, int dtype) {
+  return dtype == GFM_F64 ? force_bwd_ws<double>(H, n_nodes) : force_bwd_ws<float>(H, n_nodes);
 }
 
-int gfm_force_bwd(const void* h, int H, int n_nodes, const int* rowptr, const int* col_src,
-                  const int* edge_dst, const void* edge_dx, int e_cap, const int* csc_ptr,
-                  const int* csc_eid, const void* V, const void* c, const void* u,
-                  const void* df, const void* dh_energy, void* grad_v, void* grad_c, void* grad_u,
-                  void* dh_out, void* dz_out, void* workspace, int dtype, void* stream) {
+int gfm_force_bwd(const void* h, const void* P, int H, int n_nodes, const int* rowptr,
+                  const int* col_src, const void* edge_dx, const int* csc_ptr, const int* csc_eid,
+                  const int* csc_dst, const void* V, const void* c, const void* u, const void* df,
+                  const void* dh_energy, void* grad_v, void* grad_c, void* grad_u, void* dz_out,
+                  void* workspace, int dtype, int flags, void* stream) {
   GFM_DISPATCH(dtype, "gfm_force_bwd",
-               force_bwd_t<T>((const T*)h, H, n_nodes, rowptr, col_src, edge_dst,
-                              (const T*)edge_dx, e_cap, csc_ptr, csc_eid, (const T*)V,
+               force_bwd_t<T>((const T*)h, (const T*)P, H, n_nodes, rowptr, col_src,
+                              (const T*)edge_dx, csc_ptr, csc_eid, csc_dst, (const T*)V,
                               (const T*)c, (const T*)u, (const T*)df, (const T*)dh_energy,
-                              (T*)grad_v, (T*)grad_c, (T*)grad_u, (T*)dh_out, (T*)dz_out,
-                              workspace, (cudaStream_t)stream))
+                              (T*)grad_v, (T*)grad_c, (T*)grad_u, (T*)dz_out, workspace, flags,
+                              (cudaStream_t)stream))
 }
 
 int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const void* c,

@@ -500,12 +500,12 @@ def forward_batch(params: ModelParams, batch: Batch, cache: dict | None = None,
          ptr(params.view(f"head_{F - 1}.b")), ptr(batch.node_offsets), B, ptr(node_e),
          ptr(e_pred), code, s)
     f_pred = sc.get("f_pred", (N, 3), dt)
-    ws = sc.bytes("force_fwd_ws", query("gfm_force_fwd_workspace_bytes", H, batch.e_cap, code))
-    call("gfm_force_fwd", ptr(h), H, N, ptr(batch.rowptr), ptr(batch.col_src), ptr(batch.edge_dst),
-         ptr(batch.edge_dx), batch.e_cap, ptr(params.force_v), ptr(params.force_c),
-         ptr(params.force_u), ptr(f_pred), None, ptr(ws), code, s)
+    P = sc.get("force_P", (N, H), dt)  # h V^T, reused by the backward
+    call("gfm_force_fwd", ptr(h), H, N, ptr(batch.rowptr), ptr(batch.col_src), ptr(batch.edge_dx),
+         ptr(params.force_v), ptr(params.force_c), ptr(params.force_u), ptr(P), ptr(f_pred), code,
+         flags, s)
     if cache is not None:
-        cache.update(layers=layers, h_final=h, head_inputs=ys)
+        cache.update(layers=layers, h_final=h, head_inputs=ys, force_P=P)
     if scratch is None:
         return e_pred.clone(), f_pred.clone()
     return e_pred, f_pred
@@ -674,12 +674,12 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
 
     # force head (model.py:535-547) -> dz of the last message-passing layer
     dzl = sc.get("dz_layer", (N, H), dt)
-    ws = sc.bytes("force_bwd_ws", query("gfm_force_bwd_workspace_bytes", H, batch.e_cap, code))
-    call("gfm_force_bwd", ptr(cache["h_final"]), H, N, ptr(batch.rowptr), ptr(batch.col_src),
-         ptr(batch.edge_dst), ptr(batch.edge_dx), batch.e_cap, ptr(batch.csc_ptr),
-         ptr(batch.csc_eid), ptr(params.force_v), ptr(params.force_c), ptr(params.force_u),
-         ptr(df), ptr(dh_e), ptr(gp.force_v), ptr(gp.force_c), ptr(gp.force_u), None, ptr(dzl),
-         ptr(ws), code, s)
+    ws = sc.bytes("force_bwd_ws", query("gfm_force_bwd_workspace_bytes", H, N, code))
+    call("gfm_force_bwd", ptr(cache["h_final"]), ptr(cache["force_P"]), H, N, ptr(batch.rowptr),
+         ptr(batch.col_src), ptr(batch.edge_dx), ptr(batch.csc_ptr), ptr(batch.csc_eid),
+         ptr(batch.csc_dst), ptr(params.force_v), ptr(params.force_c), ptr(params.force_u),
+         ptr(df), ptr(dh_e), ptr(gp.force_v), ptr(gp.force_c), ptr(gp.force_u), ptr(dzl),
+         ptr(ws), code, flags, s)
 
     # message-passing layers (model.py:549-562)
     dz = dzl
