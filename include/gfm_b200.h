@@ -156,18 +156,23 @@ GFM_API int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a,
                        const int* node_offsets, int n_graphs, void* node_e, void* e_pred,
                        int dtype, void* stream);
 /* loss = [total, energy_term, force_term]; de, df = backward seeds;
- * contrib (float32, optional) receives [total, 1.0] (train.py:257) */
+ * contrib (float32, optional) receives [total, 1.0] (train.py:257).
+ * workspace (gfm_loss_workspace_bytes) must be ZERO-initialised once; the
+ * kernel leaves it ready for the next call. */
+GFM_API size_t gfm_loss_workspace_bytes(void);
 GFM_API int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_per, int n_graphs,
                    const void* f_pred, const void* f_true, int n_nodes, double alpha_e,
-                   double alpha_f, void* loss, void* de, void* df, float* contrib, int dtype,
-                   void* stream);
+                   double alpha_f, void* loss, void* de, void* df, float* contrib,
+                   void* workspace, int dtype, void* stream);
 /* ds_i = de[g(i)]; dz = (ds_i a) * (1 - y^2)  (model.py:521-529) */
 GFM_API int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const void* a,
                     const void* y, void* ds, void* dz, int dtype, void* stream);
 
 /* ---- K12: embedding gradient (model.py:564) --------------------------- */
-GFM_API size_t gfm_embedding_grad_workspace_bytes(int n_nodes, int H, int chunk, int dtype);
-GFM_API int gfm_embedding_grad(const int* z, int n_nodes, const void* dh, int H, int chunk, void* grad,
+/* grad[118][H] = onehot(z - 1)^T dh as a split-K GEMM (one-hot generated on
+ * the fly, deterministic; absent elements exactly 0) */
+GFM_API size_t gfm_embedding_grad_workspace_bytes(int n_nodes, int H, int dtype);
+GFM_API int gfm_embedding_grad(const int* z, int n_nodes, const void* dh, int H, void* grad,
                        void* workspace, int dtype, void* stream);
 
 /* ---- K13: optimiser and guard (train.py:96-108, 262-274) -------------- */

@@ -50,6 +50,12 @@ __device__ __forceinline__ float group_sum(float v) {
   return v;
 }
 
+// c / u are views into the flat parameter vector: not 16-byte aligned
+__device__ __forceinline__ float4 ld4u(const float* p, int c4) {
+  return make_float4(__ldg(p + 4 * c4), __ldg(p + 4 * c4 + 1), __ldg(p + 4 * c4 + 2),
+                     __ldg(p + 4 * c4 + 3));
+}
+
 __device__ __forceinline__ float4 f4add3(float4 a, float4 b, float4 c) {
   return make_float4(a.x + b.x + c.x, a.y + b.y + c.y, a.z + b.z + c.z, a.w + b.w + c.w);
 }
@@ -72,8 +78,8 @@ __global__ void __launch_bounds__(256)
   for (int v = 0; v < NV; ++v) {
     const int c4 = v * LPN + sub;
     pi[v] = __ldg(P4 + (long long)i * H4 + c4);
-    cu[v] = __ldg(reinterpret_cast<const float4*>(c) + c4);
-    uu[v] = __ldg(reinterpret_cast<const float4*>(u) + c4);
+    cu[v] = ld4u(c, c4);
+    uu[v] = ld4u(u, c4);
   }
   double fx = 0.0, fy = 0.0, fz = 0.0;
   const int beg = rowptr[i], end = rowptr[i + 1];
@@ -162,8 +168,8 @@ __global__ void __launch_bounds__(256)
   for (int v = 0; v < NV; ++v) {
     const int c4 = v * LPN + sub;
     pi[v] = __ldg(P4 + (long long)i * H4 + c4);
-    cu[v] = __ldg(reinterpret_cast<const float4*>(c) + c4);
-    uu[v] = __ldg(reinterpret_cast<const float4*>(u) + c4);
+    cu[v] = ld4u(c, c4);
+    uu[v] = ld4u(u, c4);
     dd[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     tu[v] = dd[v];
   }
@@ -209,8 +215,8 @@ __global__ void __launch_bounds__(256)
   for (int v = 0; v < NV; ++v) {
     const int c4 = v * LPN + sub;
     pj[v] = __ldg(P4 + (long long)j * H4 + c4);
-    cu[v] = __ldg(reinterpret_cast<const float4*>(c) + c4);
-    uu[v] = __ldg(reinterpret_cast<const float4*>(u) + c4);
+    cu[v] = ld4u(c, c4);
+    uu[v] = ld4u(u, c4);
     acc[v] = reinterpret_cast<const float4*>(Ddst)[(long long)j * H4 + c4];
   }
   for (int q = csc_ptr[j]; q < csc_ptr[j + 1]; ++q) {
@@ -279,15 +285,30 @@ __global__ void k_force_bwd_src_scalar(const T* __restrict__ P, int n, int H, co
 
 // deterministic column sums of X [n][H] (+ optional second matrix Y):
 // pass 1 -- fixed row chunks -> partials; pass 2 -- ordered sum of partials
+// Block = 256 threads over a 512-row chunk: thread t owns column
+// (blockIdx.y * cw + t % cw) and rows r = t / cw, + 256 / cw, ... of the chunk
+// (coalesced row segments); the 256 / cw row-group sums are combined in a
+// fixed order in shared memory.
 constexpr int kColChunk = 512;
 template <typename T>
-__global__ void k_colsum_partial(const T* __restrict__ X, int n, int H, T* __restrict__ part) {
+__global__ void __launch_bounds__(256)
+    k_colsum_partial(const T* __restrict__ X, int n, int H, T* __restrict__ part) {
+  __shared__ double red[256];
+  const int cw = H < 64 ? H : 64;  // columns per block
+  const int groups = 256 / cw;
   const int ch = blockIdx.x;
   const int lo = ch * kColChunk, hi = min(n, lo + kColChunk);
-  for (int k = threadIdx.x + blockIdx.y * blockDim.x; k < H; k += blockDim.x * gridDim.y) {
-    double s = 0.0;
-    for (int i = lo; i < hi; ++i) s += (double)X[(long long)i * H + k];
-    part[(long long)ch * H + k] = (T)s;
+  const int c = blockIdx.y * cw + threadIdx.x % cw;
+  const int g = threadIdx.x / cw;
+  double s = 0.0;
+  if (g < groups && c < H)
+    for (int i = lo + g; i < hi; i += groups) s += (double)X[(long long)i * H + c];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < cw && c < H) {
+    double t = 0.0;
+    for (int q = 0; q < groups; ++q) t += red[q * cw + threadIdx.x];
+    part[(long long)ch * H + c] = (T)t;
   }
 }
 
@@ -303,7 +324,7 @@ __global__ void k_colsum_final(const T* __restrict__ part, int nch, int H, T* __
 template <typename T>
 cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s) {
   const int nch = ceil_div(n > 0 ? n : 1, kColChunk);
-  dim3 g1(nch, ceil_div(H, 256));
+  dim3 g1(nch, ceil_div(H, H < 64 ? H : 64));
   if (n > 0) k_colsum_partial<T><<<g1, 256, 0, s>>>(X, n, H, part);
   k_colsum_final<T><<<ceil_div(H, 256), 256, 0, s>>>(part, n > 0 ? nch : 0, H, out);
   return cudaGetLastError();

@@ -19,6 +19,14 @@ constexpr int kBM = 64, kBN = 64, kBK = 16, kTM = 4, kTN = 4, kGemmThreads = 256
 // ---------------------------------------------------------------- loaders
 // Each loader exposes  T operator()(int row, int k)  (row = m for A, n for
 // Bt) and kContigRow: true when consecutive rows are adjacent in memory.
+// For the tcgen05 engine's 16-byte cp.async staging they also expose
+// vec_ok(K) (host: alignment / divisibility check) and
+// src4(row, k, rows_left, &src, &imm): the global address of the 16-byte
+// chunk (k..k+3 of a row for k-contiguous loaders, rows row..row+3 at k for
+// row-contiguous ones) and its valid byte count, or -1 with an immediate.
+
+__host__ __device__ inline bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 
 template <typename T>
 struct RowsLd {  // X[row * ld + k]
@@ -26,6 +34,11 @@ struct RowsLd {  // X[row * ld + k]
   const T* p;
   int ld;
   __device__ T operator()(int r, int k) const { return p[(long long)r * ld + k]; }
+  bool vec_ok(int K) const { return sizeof(T) == 4 && al16(p) && ld % 4 == 0 && K % 4 == 0; }
+  __device__ int src4(int r, int k, int, const float** src, float4*) const {
+    *src = reinterpret_cast<const float*>(p + (long long)r * ld + k);
+    return 16;
+  }
 };
 
 template <typename T>
@@ -41,6 +54,15 @@ struct Rows2Ld {  // [X1 | X2 | 1] along k
     if (k < k2) return p2[(long long)r * ld2 + k];
     return T(1);
   }
+  bool vec_ok(int K) const {
+    return sizeof(T) == 4 && al16(p1) && ld1 % 4 == 0 && k1 % 4 == 0 && K % 4 == 0 &&
+           K <= k1 + k2 && (k2 == 0 || (al16(p2) && ld2 % 4 == 0 && k2 % 4 == 0));
+  }
+  __device__ int src4(int r, int k, int, const float** src, float4*) const {
+    *src = reinterpret_cast<const float*>(k < k1 ? p1 + (long long)r * ld1 + k
+                                                 : p2 + (long long)r * ld2 + (k - k1));
+    return 16;
+  }
 };
 
 template <typename T>
@@ -49,6 +71,11 @@ struct ColsLd {  // X[k * ld + row]  (transposed view)
   const T* p;
   int ld;
   __device__ T operator()(int r, int k) const { return p[(long long)k * ld + r]; }
+  bool vec_ok(int) const { return sizeof(T) == 4 && al16(p) && ld % 4 == 0; }
+  __device__ int src4(int r, int k, int rows_left, const float** src, float4*) const {
+    *src = reinterpret_cast<const float*>(p + (long long)k * ld + r);
+    return (rows_left < 4 ? rows_left : 4) * 4;
+  }
 };
 
 template <typename T>
@@ -64,6 +91,23 @@ struct Cols2Ld {  // rows split over [X1 | X2 | 1]: X1[k*ld1 + r], X2[k*ld2 + r 
     if (r < n2) return p2[(long long)k * ld2 + r];
     return T(1);
   }
+  bool vec_ok(int) const {
+    return sizeof(T) == 4 && al16(p1) && ld1 % 4 == 0 && n1 % 4 == 0 &&
+           (n2 == 0 || (al16(p2) && ld2 % 4 == 0 && n2 % 4 == 0));
+  }
+  __device__ int src4(int r, int k, int rows_left, const float** src, float4* imm) const {
+    const int nb = (rows_left < 4 ? rows_left : 4) * 4;
+    if (r < n1) {
+      *src = reinterpret_cast<const float*>(p1 + (long long)k * ld1 + r);
+      return nb;
+    }
+    if (r < n1 + n2) {
+      *src = reinterpret_cast<const float*>(p2 + (long long)k * ld2 + (r - n1));
+      return nb;
+    }
+    *imm = make_float4(1.f, 0.f, 0.f, 0.f);  // the virtual ones row (bias gradient)
+    return -1;
+  }
 };
 
 template <typename T>
@@ -76,6 +120,8 @@ struct PairLd {  // pair[e][k] = h[dst[e]][k] + h[src[e]][k]   (model.py:379)
   __device__ T operator()(int e, int k) const {
     return h[(long long)dst[e] * H + k] + h[(long long)src[e] * H + k];
   }
+  bool vec_ok(int) const { return false; }
+  __device__ int src4(int, int, int, const float**, float4*) const { return 0; }
 };
 
 template <typename T>
@@ -89,6 +135,8 @@ struct PairColsLd {  // Bt(n, e) = pair[e][n]; row n == H is a ones column
     if (n >= H) return T(1);
     return h[(long long)dst[e] * H + n] + h[(long long)src[e] * H + n];
   }
+  bool vec_ok(int) const { return false; }
+  __device__ int src4(int, int, int, const float**, float4*) const { return 0; }
 };
 
 // ---------------------------------------------------------------- epilogues

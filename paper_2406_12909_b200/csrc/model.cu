@@ -24,17 +24,30 @@ static inline int grid_1d(long long n, int threads = 256) {
 // ------------------------------------------------------------ reductions
 // out segment mapping for split-K weight grads: result matrix R[N][Kt] with
 // Kt = K1 + K2 (+1 bias column) is written to three destinations.
+// Block = 32 x 8 threads: x over 32 consecutive outputs, y over split groups
+// (split = y, y + 8, ...); the 8 group sums are combined in order in smem --
+// float64 accumulation, fixed order, 8x the parallelism of a serial walk.
 template <typename T>
-__global__ void k_splitk_reduce(const T* __restrict__ ws, int splits, int N, int K1, int K2,
-                                int with_bias, T* __restrict__ g1, T* __restrict__ g2,
-                                T* __restrict__ gb) {
+__global__ void __launch_bounds__(256)
+    k_splitk_reduce(const T* __restrict__ ws, int splits, int N, int K1, int K2, int with_bias,
+                    T* __restrict__ g1, T* __restrict__ g2, T* __restrict__ gb) {
+  __shared__ double red[8][33];
   const int Kt = K1 + K2 + with_bias;
   const long long total = (long long)N * Kt;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    double acc = (double)ws[idx];  // float64 sum of the partials (same order for every run)
-    for (int k = 1; k < splits; ++k) acc += (double)ws[(long long)k * total + idx];
-    const T s = (T)acc;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (long long base = (long long)blockIdx.x * 32; base < total; base += (long long)gridDim.x * 32) {
+    const long long idx = base + tx;
+    double acc = 0.0;
+    if (idx < total)
+      for (int k = ty; k < splits; k += 8) acc += (double)ws[(long long)k * total + idx];
+    red[ty][tx] = acc;
+    __syncthreads();
+    double a = 0.0;
+    if (ty == 0)
+      for (int q = 0; q < 8; ++q) a += red[q][tx];
+    __syncthreads();
+    if (ty != 0 || idx >= total) continue;
+    const T s = (T)a;
     const int n = (int)(idx / Kt), k = (int)(idx % Kt);
     if (k < K1)
       g1[(long long)n * K1 + k] = s;
@@ -70,43 +83,64 @@ __global__ void k_graph_pool(const T* __restrict__ node_e, const int* __restrict
   }
 }
 
-// L1 MTL loss + backward seeds (model.py:437-462, 510-516), one block.
+// L1 MTL loss + backward seeds (model.py:437-462, 510-516).  Grid-stride
+// seeds; per-block float64 partial sums; the last block to finish (ticket
+// counter) adds the partials in block order, so the result is deterministic.
+constexpr int kLossBlocks = 64;
 template <typename T>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(256)
     k_loss_seeds(const T* __restrict__ e_pred, const T* __restrict__ e_true,
                  const int* __restrict__ n_per, int B, const T* __restrict__ f_pred,
                  const T* __restrict__ f_true, int N, T aE, T aF, T* __restrict__ loss,
-                 T* __restrict__ de, T* __restrict__ df, float* __restrict__ contrib) {
-  __shared__ T red[32];
-  T se = T(0);
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+                 T* __restrict__ de, T* __restrict__ df, float* __restrict__ contrib,
+                 double* __restrict__ partial, unsigned* __restrict__ ticket) {
+  __shared__ double red[2][8];
+  __shared__ bool last;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  double se = 0.0, sf = 0.0;
+  for (int b = tid; b < B; b += nth) {
     const T r = div_rn(sub_rn(e_pred[b], e_true[b]), (T)n_per[b]);
-    se += fabs(r);
+    se += (double)fabs(r);
     de[b] = div_rn(mul_rn(aE, sign_t(r)), (T)n_per[b] * (T)B);
   }
-  T sf = T(0);
-  const T inv3n = T(3) * (T)N;
-  for (int k = threadIdx.x; k < 3 * N; k += blockDim.x) {
+  // aF * sign(d) / (3N) takes only the values {q, -q, 0}: q = aF / (3N)
+  const T q = div_rn(aF, T(3) * (T)N);
+#pragma unroll 4
+  for (int k = tid; k < 3 * N; k += nth) {
     const T d = sub_rn(f_pred[k], f_true[k]);
-    sf += fabs(d);
-    df[k] = div_rn(mul_rn(aF, sign_t(d)), inv3n);
+    sf += (double)fabs(d);
+    df[k] = d > T(0) ? q : (d < T(0) ? -q : T(0));
   }
-  auto block_sum = [&](T v) -> T {
-    v = warp_sum(v);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) red[wid] = v;
-    __syncthreads();
-    T s = T(0);
-    if (threadIdx.x == 0)
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    return s;
-  };
-  const T tot_e = block_sum(se);
-  const T tot_f = block_sum(sf);
+  se = warp_sum(se);
+  sf = warp_sum(sf);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = se;
+    red[1][wid] = sf;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const T et = B > 0 ? tot_e / (T)B : T(0);
-    const T ft = N > 0 ? tot_f / (T)(3LL * N) : T(0);
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    partial[2 * blockIdx.x] = a;
+    partial[2 * blockIdx.x + 1] = b;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double tot_e = 0.0, tot_f = 0.0;
+    for (int k = 0; k < (int)gridDim.x; ++k) {
+      tot_e += ((volatile double*)partial)[2 * k];
+      tot_f += ((volatile double*)partial)[2 * k + 1];
+    }
+    *ticket = 0u;  // ready for the next launch
+    const T et = B > 0 ? (T)(tot_e / (double)B) : T(0);
+    const T ft = N > 0 ? (T)(tot_f / (3.0 * (double)N)) : T(0);
     const T total = aE * et + aF * ft;
     loss[0] = total;
     loss[1] = et;
@@ -134,54 +168,22 @@ __global__ void k_energy_seed(const T* __restrict__ de, const int* __restrict__ 
   }
 }
 
-// embedding gradient (model.py:564): per (node chunk, 64-column block) a CTA
-// accumulates rows by element sequentially, then partials are summed over
-// chunks in order.  Absent elements stay exactly 0.
-constexpr int kEmbCols = 64;
+// embedding gradient (model.py:564): grad_emb = onehot(z - 1)^T dh, i.e. a
+// weight-gradient GEMM whose A operand is generated on the fly; absent
+// elements are sums of exact zeros (stay 0.0).
 template <typename T>
-__global__ void k_emb_partial(const int* __restrict__ z, int n, const T* __restrict__ dh, int H,
-                              int chunk, T* __restrict__ ws, unsigned char* __restrict__ present) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* acc = reinterpret_cast<T*>(smem_raw);                       // [118][kEmbCols]
-  unsigned char* seen = smem_raw + sizeof(T) * 118 * kEmbCols;   // [118]
-  const int ch = blockIdx.x, cb = blockIdx.y;
-  const int c = cb * kEmbCols + threadIdx.x;
-  for (int k = threadIdx.x; k < 118 * kEmbCols; k += blockDim.x) acc[k] = T(0);
-  for (int k = threadIdx.x; k < 118; k += blockDim.x) seen[k] = 0;
-  __syncthreads();
-  const int lo = ch * chunk, hi = min(n, lo + chunk);
-  for (int i = lo; i < hi; ++i) {
-    const int e = z[i] - 1;
-    if (c < H) acc[e * kEmbCols + threadIdx.x] = add_rn(acc[e * kEmbCols + threadIdx.x], dh[(long long)i * H + c]);
-    if (threadIdx.x == 0) seen[e] = 1;
+struct OneHotLd {  // A(row = element, k = node) = [z[node] - 1 == row]
+  static constexpr bool kContigRow = false;
+  const int* z;
+  __device__ T operator()(int r, int k) const { return z[k] - 1 == r ? T(1) : T(0); }
+  bool vec_ok(int K) const { return sizeof(T) == 4 && al16(z) && K % 4 == 0; }
+  __device__ int src4(int r, int k, int, const float**, float4* imm) const {
+    const int4 q = __ldg(reinterpret_cast<const int4*>(z + k));
+    *imm = make_float4(q.x - 1 == r ? 1.f : 0.f, q.y - 1 == r ? 1.f : 0.f,
+                       q.z - 1 == r ? 1.f : 0.f, q.w - 1 == r ? 1.f : 0.f);
+    return -1;
   }
-  __syncthreads();
-  for (int e = 0; e < 118; ++e) {
-    if (!seen[e]) continue;
-    if (c < H) ws[((long long)ch * 118 + e) * H + c] = acc[e * kEmbCols + threadIdx.x];
-  }
-  if (cb == 0)
-    for (int e = threadIdx.x; e < 118; e += blockDim.x) present[ch * 118 + e] = seen[e];
-}
-
-template <typename T>
-__global__ void k_emb_reduce(const T* __restrict__ ws, const unsigned char* __restrict__ present,
-                             int n_chunks, int H, T* __restrict__ grad) {
-  const long long total = 118LL * H;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int e = (int)(idx / H), c = (int)(idx % H);
-    T s = T(0);
-    bool any = false;
-    for (int ch = 0; ch < n_chunks; ++ch) {
-      if (!present[ch * 118 + e]) continue;
-      const T v = ws[((long long)ch * 118 + e) * H + c];
-      s = any ? add_rn(s, v) : add_rn(T(0), v);
-      any = true;
-    }
-    grad[idx] = s;
-  }
-}
+};
 
 // ------------------------------------------------------------ typed drivers
 // float32 GEMMs run on the tcgen05 tensor cores (3xTF32 by default,
@@ -191,7 +193,6 @@ inline bool use_tc() {
   return std::is_same<T, float>::value && gemm_mode() != GFM_GEMM_SIMT;
 }
 inline int tc_split3() { return gemm_mode() == GFM_GEMM_TC1 ? 0 : 1; }
-inline int tc_bn(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 
 template <typename T>
 cudaError_t linear_fwd_t(const T* X1, int ld1, int K1, const T* X2, int ld2, int K2, const T* W1,
@@ -228,13 +229,13 @@ cudaError_t linear_bwd_data_t(const T* dY, int ldd, int M, const int* M_dev, int
 
 template <typename T>
 int wgrad_splits(int M, int N, int Kt) {
-  return use_tc<T>() ? tc::splits_for(N, Kt, M, tc_bn(Kt)) : choose_splits(N, Kt, M);
+  return use_tc<T>() ? tc::splits_for(N, Kt, M) : choose_splits(N, Kt, M);
 }
 
 template <typename T>
 size_t linear_bwd_weight_ws(int M, int N, int K1, int K2, int with_bias) {
   const int Kt = K1 + K2 + with_bias;
-  const int splits = std::max(choose_splits(N, Kt, M), tc::splits_for(N, Kt, M, tc_bn(Kt)));
+  const int splits = std::max(choose_splits(N, Kt, M), tc::splits_for(N, Kt, M));
   return sizeof(T) * (size_t)splits * N * Kt;
 }
 
@@ -257,7 +258,7 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
   // rows = output features N, cols = Kt, reduction over the M batch rows
   if constexpr (std::is_same<T, float>::value) {
     if (use_tc<T>()) {
-      tc::TcEpiPartial epi{ws, (long long)N * Kt, N, Kt, 0};
+      tc::TcEpiPartial epi{ws, (long long)N * Kt, N, Kt};
       e = tc::launch(N, nullptr, Kt, M, M_dev, splits, tc_split3(), a, b, epi, s);
       real = real_splits(M, splits, tc::kBK);
       goto reduce;
@@ -270,7 +271,7 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
   }
 reduce:
   if (e != cudaSuccess) return e;
-  k_splitk_reduce<T><<<grid_1d((long long)N * Kt), 256, 0, s>>>(ws, real, N, K1, K2, with_bias,
+  k_splitk_reduce<T><<<grid_1d((long long)N * Kt, 32), 256, 0, s>>>(ws, real, N, K1, K2, with_bias,
                                                                  g1, g2, gb);
   return cudaGetLastError();
 }
@@ -334,22 +335,31 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
 }
 
 template <typename T>
-cudaError_t embedding_grad_t(const int* z, int n_nodes, const T* dh, int H, int chunk, T* grad,
-                             void* workspace, cudaStream_t s) {
-  if (chunk <= 0) chunk = n_nodes > 0 ? n_nodes : 1;
-  const int nch = ceil_div(n_nodes > 0 ? n_nodes : 1, chunk);
-  unsigned char* present =
-      (unsigned char*)workspace + ((sizeof(T) * (size_t)nch * 118 * H + 255) & ~(size_t)255);
-  const size_t smem = sizeof(T) * 118 * kEmbCols + 128;
-  cudaError_t e = cudaFuncSetAttribute(k_emb_partial<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  if (n_nodes > 0) {
-    dim3 grid(nch, ceil_div(H, kEmbCols));
-    k_emb_partial<T><<<grid, kEmbCols, smem, s>>>(z, n_nodes, dh, H, chunk, (T*)workspace, present);
+cudaError_t embedding_grad_t(const int* z, int n_nodes, const T* dh, int H, T* grad, T* ws,
+                             cudaStream_t s) {
+  constexpr int E = 118;
+  const int splits = wgrad_splits<T>(n_nodes, E, H);
+  OneHotLd<T> a{z};
+  ColsLd<T> b{dh, H};
+  cudaError_t e;
+  int real;
+  if constexpr (std::is_same<T, float>::value) {
+    if (use_tc<T>()) {
+      tc::TcEpiPartial epi{ws, (long long)E * H, E, H};
+      e = tc::launch(E, nullptr, H, n_nodes, nullptr, splits, tc_split3(), a, b, epi, s);
+      real = real_splits(n_nodes, splits, tc::kBK);
+      goto reduce;
+    }
   }
-  k_emb_reduce<T><<<grid_1d(118LL * H), 256, 0, s>>>((const T*)workspace, present,
-                                                      n_nodes > 0 ? nch : 0, H, grad);
+  {
+    EpiPartial<T> epi{ws, (long long)E * H};
+    e = launch_simt_gemm<T>(E, nullptr, H, n_nodes, nullptr, splits, a, b, epi, s);
+    real = real_splits(n_nodes, splits, kBK);
+  }
+reduce:
+  if (e != cudaSuccess) return e;
+  k_splitk_reduce<T><<<grid_1d((long long)E * H, 32), 256, 0, s>>>(ws, real, E, H, 0, 0, grad,
+                                                                    nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -447,16 +457,20 @@ int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const v
                 cudaGetLastError()))
 }
 
+size_t gfm_loss_workspace_bytes(void) { return sizeof(double) * 2 * kLossBlocks + 256; }
+
 int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_per, int n_graphs,
                    const void* f_pred, const void* f_true, int n_nodes, double alpha_e,
-                   double alpha_f, void* loss, void* de, void* df, float* contrib, int dtype,
-                   void* stream) {
+                   double alpha_f, void* loss, void* de, void* df, float* contrib,
+                   void* workspace, int dtype, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  double* partial = (double*)workspace;
+  unsigned* ticket = (unsigned*)(partial + 2 * kLossBlocks);
   GFM_DISPATCH(dtype, "gfm_loss_seeds",
-               (k_loss_seeds<T><<<1, 1024, 0, s>>>((const T*)e_pred, (const T*)e_true, n_per,
-                                                   n_graphs, (const T*)f_pred, (const T*)f_true,
-                                                   n_nodes, (T)alpha_e, (T)alpha_f, (T*)loss,
-                                                   (T*)de, (T*)df, contrib),
+               (k_loss_seeds<T><<<kLossBlocks, 256, 0, s>>>(
+                    (const T*)e_pred, (const T*)e_true, n_per, n_graphs, (const T*)f_pred,
+                    (const T*)f_true, n_nodes, (T)alpha_e, (T)alpha_f, (T*)loss, (T*)de, (T*)df,
+                    contrib, partial, ticket),
                 cudaGetLastError()))
 }
 
@@ -469,16 +483,15 @@ int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const 
                 cudaGetLastError()))
 }
 
-size_t gfm_embedding_grad_workspace_bytes(int n_nodes, int H, int chunk, int dtype) {
-  const size_t esz = dtype == GFM_F64 ? 8 : 4;
-  const int nch = ceil_div(n_nodes > 0 ? n_nodes : 1, chunk);
-  return esz * (size_t)nch * 118 * H + (size_t)nch * 118 + 512;
+size_t gfm_embedding_grad_workspace_bytes(int n_nodes, int H, int dtype) {
+  return dtype == GFM_F64 ? linear_bwd_weight_ws<double>(n_nodes, 118, H, 0, 0)
+                          : linear_bwd_weight_ws<float>(n_nodes, 118, H, 0, 0);
 }
 
-int gfm_embedding_grad(const int* z, int n_nodes, const void* dh, int H, int chunk, void* grad,
+int gfm_embedding_grad(const int* z, int n_nodes, const void* dh, int H, void* grad,
                        void* workspace, int dtype, void* stream) {
   GFM_DISPATCH(dtype, "gfm_embedding_grad",
-               embedding_grad_t<T>(z, n_nodes, (const T*)dh, H, chunk, (T*)grad, workspace,
+               embedding_grad_t<T>(z, n_nodes, (const T*)dh, H, (T*)grad, (T*)workspace,
                                    (cudaStream_t)stream))
 }
 

@@ -1,22 +1,31 @@
-// tcgen05 GEMM core for the model's skinny GEMMs (sm_100a).
+// tcgen05 GEMM core for the model's node-level GEMMs (sm_100a).
 //
-// C[m][n] = sum_k A(m, k) * Bt(n, k) with a 128 x BN CTA tile and the
-// accumulator in TMEM.  Operands are staged into shared memory by the CTA's
-// threads -- not TMA -- because the A operands are gathers (h[dst] + h[src]
-// pairs), concatenations ([h | agg]) or transposes that a tensor map cannot
-// express; the same loaders as the SIMT engine feed it.  Staging writes the
-// canonical K-major SWIZZLE_128B layout (8-row x 128-byte atoms, 16-byte
-// chunk index XOR row%8) that the UMMA shared-memory descriptors describe.
+// C[m][n] = sum_k A(m, k) * Bt(n, k) with a 128 x BN CTA tile (BN <= 128)
+// and the accumulator in TMEM.  Operands are staged into shared memory by the
+// CTA's threads -- not TMA -- because the A operands are concatenations
+// ([h | agg]), transposes (weight gradients: dY^T) or generated one-hot rows
+// that a tensor map cannot express; the same loaders as the SIMT engine feed
+// it.  k-contiguous operands are staged K-major SWIZZLE_128B (8-row x
+// 128-byte atoms, 16-byte chunk index XOR row % 8); row-contiguous operands
+// (transposes) are staged MN-major SWIZZLE_128B_BASE32B so 16-byte global
+// loads map to conflict-free 16-byte smem stores.
 //
-// Precision: "3xTF32".  Each fp32 operand is split hi = rna_tf32(x),
-// lo = x - hi, and the tile is accumulated as lo*hi + hi*lo + hi*hi with
-// kind::tf32 MMAs -> ~22 mantissa bits per product, fp32 accumulation, i.e.
-// float32-level results at tensor-core rate (1 x TF32 is selectable).
+// Precision: "3xTF32".  Each fp32 operand is split hi = trunc_tf32(x),
+// lo = x - hi (exact), and each tile is accumulated as lo*hi + hi*lo + hi*hi
+// with kind::tf32 MMAs -> ~21 mantissa bits per product with fp32
+// accumulation (measured max error ~3e-6 relative at K = 320, ~3x the SIMT
+// fp32 engine); 1xTF32 (GFM_GEMM_TC1) skips the corrections.
 //
-// Pipeline: 2 smem stages.  All 4 warps stage k-block kb+1 while the single
-// elected thread's MMAs for kb run; tcgen05.commit arrives on the stage's
-// mbarrier, which gates reuse of that stage.  Epilogue: each warp reads its
-// 32 TMEM lanes (one output row per thread) with tcgen05.ld.32x32b.x16.
+// Schedule: one persistent CTA of 8 warps per SM walks (m tile, n tile,
+// k split) work items as ONE flattened stream of 32-wide k-blocks.  Raw fp32
+// tiles land in an S-deep smem ring via cp.async (16-byte, zero-fill for
+// out-of-range chunks), L = S - 2 k-blocks ahead of the consumer, continuing
+// across tile boundaries.  The raw tile is itself the "hi" TF32 operand (the
+// tensor core ignores the low 13 mantissa bits); a light pass writes
+// lo = x - trunc_tf32(x) into one of two lo buffers.  One thread issues the
+// MMAs and tcgen05.commit arrives on the stage's mbarrier, which gates ring
+// reuse.  Epilogue: warp w reads TMEM lanes 32*(w%4).. (one output row per
+// thread) for column half w/4, 16 columns per tcgen05.ld.32x32b.x16.
 #pragma once
 
 #include <algorithm>
@@ -26,10 +35,9 @@
 namespace gfm {
 namespace tc {
 
-constexpr int kBM = 128;           // MMA M (cta_group::1)
-constexpr int kBK = 32;            // fp32 elements per 128-byte swizzle row
-constexpr int kThreads = 128;      // 4 warps: stage + epilogue; thread 0 issues MMAs
-constexpr int kStages = 2;
+constexpr int kBM = 128;       // MMA M (cta_group::1)
+constexpr int kBK = 32;        // fp32 elements per 128-byte swizzle row
+constexpr int kThreads = 256;  // 8 warps: staging + epilogue; thread 0 issues MMAs
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -47,20 +55,37 @@ __device__ __forceinline__ uint32_t swz(int row, int k) {
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B (8-row
-// group stride), LBO = 16 B (unused for swizzled K-major), version 1.
+// group stride), LBO = 16 B (ignored for swizzled K-major), version 1.
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)(16 >> 4) << 16;
   d |= (uint64_t)(1024 >> 4) << 32;
-  d |= (uint64_t)1 << 46;   // version (Blackwell)
-  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
 }
 
-// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = bn
-__host__ __device__ constexpr uint32_t make_idesc_tf32(int bn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+// MN-major SWIZZLE_128B_BASE32B descriptor (layout type 1): 128-byte rows
+// hold 32 consecutive M (or N) tf32 of one k; 4 k-rows form a 512 B atom;
+// LBO = byte stride between 32-element M/N atoms, SBO = stride between 4-k
+// groups (an 8-deep tf32 MMA spans two).
+__device__ __forceinline__ uint64_t make_desc_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, M = 128, N = bn; a_mn / b_mn
+// select MN-major operands (bits 15 / 16)
+__host__ __device__ constexpr uint32_t make_idesc_tf32(int bn, bool a_mn = false,
+                                                       bool b_mn = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -127,80 +152,159 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* gptr, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(saddr), "l"(gptr),
+               "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
+}
+
+constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : 128; }
+
+// ring depth by BN (192 KB of ring + lo buffers, one CTA per SM)
 template <int BN>
 struct Smem {
-  // per stage: A hi, A lo (128 x 128 B), B hi, B lo (BN x 128 B); 1024-aligned
-  static constexpr int kA = kBM * 128;
+  static constexpr int kA = kBM * 128;  // one k-block of A: 128 rows x 128 B
   static constexpr int kB = BN * 128;
-  static constexpr int kStage = 2 * kA + 2 * kB;
-  static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 64 /*barriers, tmem ptr*/;
+  static constexpr int kStage = kA + kB;
+  static constexpr int kS = BN >= 128 ? 4 : BN >= 64 ? 6 : 7;  // ring stages
+  static constexpr int kL = kS - 2;                              // lookahead
+  static constexpr int kBytes = kS * kStage + 2 * kStage + 1024 /*align*/ + 256;
 };
 
-constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256; }
+// MN-major tf32 tile of ROWS x 32 k in the SWIZZLE_128B_BASE32B layout (the
+// only MN-major smem layout tcgen05 accepts for tf32): atoms of 4 k-rows x
+// 128 B (32 rows) = 512 B; atom (k / 4, row / 32) at ((k/4) * ROWS/32 +
+// row/32) * 512; inside, k-row kr = k % 4 at kr * 128 and the 32-byte chunk
+// (row % 32) / 8 is XORed with kr.  A 16-byte row-quad is half a chunk.
+template <int ROWS>
+__device__ __forceinline__ uint32_t mn_off(int rq, int k) {
+  const int r = rq << 2;
+  const int kg = k >> 2, kr = k & 3, atom = r >> 5, c32 = (r & 31) >> 3, half = (r & 7) >> 2;
+  return (uint32_t)((kg * (ROWS / 32) + atom) * 512 + kr * 128 + ((c32 ^ kr) << 5) + (half << 4));
+}
 
-// Stage rows [r0, r0 + ROWS) x one 32-wide k-block of a loader into hi/lo
-// swizzled tiles.  All global loads of a thread are issued before any smem
-// store (register batch) so each thread keeps up to 32 loads in flight.
-// Mapping: k across lanes when k is contiguous in memory, rows otherwise.
-template <int ROWS, class L>
-__device__ __forceinline__ void stage(const L& ld, int r0, int rows_valid, int k0, int k_valid,
-                                      uint8_t* hi, uint8_t* lo, bool split) {
-  constexpr int kItems = ROWS * kBK / kThreads;  // elements per thread
-  constexpr int kBatch = kItems < 32 ? kItems : 32;
+// Issue one k-block of one operand into a raw tile.
+//  VEC: 16-byte chunks -- loaders expose src4(r, k, rows_left, &src, &imm):
+//       >= 0 -> cp.async from src with that many valid bytes (zero fill);
+//       < 0  -> immediate value imm (stored directly).  k-contiguous loaders
+//       give k..k+3 of row r (K-major chunk); row-contiguous ones give rows
+//       r..r+3 at k (MN-major chunk).
+//  scalar: synchronous register loads into the K-major layout.
+template <int ROWS, bool VEC, class L>
+__device__ __forceinline__ void issue_tile(const L& ld, int r0, int rows_valid, int k0, int k_valid,
+                                           uint8_t* dst) {
   const int tid = threadIdx.x;
+  if constexpr (VEC) {
+    constexpr int kChunks = ROWS * kBK / 4;
+    const uint32_t sbase = smem_u32(dst);
 #pragma unroll
-  for (int b0 = 0; b0 < kItems; b0 += kBatch) {
-    float v[kBatch];
-#pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-      const int it = b0 + j;
+    for (int j = 0; j < (kChunks + kThreads - 1) / kThreads; ++j) {
+      const int idx = tid + j * kThreads;
+      if (idx >= kChunks) break;
       int r, k;
+      uint32_t off;
       if (!L::kContigRow) {
-        r = (tid >> 5) + it * (kThreads / 32);
-        k = tid & 31;
+        r = idx >> 3;
+        k = (idx & 7) << 2;
+        off = (uint32_t)(r * 128 + (((idx & 7) ^ (r & 7)) << 4));
       } else {
-        const int idx = tid + it * kThreads;
-        r = idx % ROWS;
-        k = idx / ROWS;
+        const int rq = idx % (ROWS / 4);
+        r = rq << 2;
+        k = idx / (ROWS / 4);
+        off = mn_off<ROWS>(rq, k);
       }
-      v[j] = (r < rows_valid && k < k_valid) ? ld(r0 + r, k0 + k) : 0.f;
+      if (r < rows_valid && k < k_valid) {
+        const float* src = nullptr;
+        float4 imm;
+        const int nb = ld.src4(r0 + r, k0 + k, rows_valid - r, &src, &imm);
+        if (nb >= 0)
+          cp_async16(sbase + off, src, nb);
+        else
+          *reinterpret_cast<float4*>(dst + off) = imm;
+      } else {
+        *reinterpret_cast<uint4*>(dst + off) = make_uint4(0u, 0u, 0u, 0u);
+      }
     }
+  } else {
+    constexpr int kItems = ROWS * kBK / kThreads;
+    constexpr int kBatch = kItems < 16 ? kItems : 16;
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-      const int it = b0 + j;
-      int r, k;
-      if (!L::kContigRow) {
-        r = (tid >> 5) + it * (kThreads / 32);
-        k = tid & 31;
-      } else {
-        const int idx = tid + it * kThreads;
-        r = idx % ROWS;
-        k = idx / ROWS;
+    for (int b0 = 0; b0 < kItems; b0 += kBatch) {
+      float v[kBatch];
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        int r, k;
+        if (!L::kContigRow) {
+          r = (tid >> 5) + (b0 + j) * (kThreads / 32);
+          k = tid & 31;
+        } else {
+          const int idx = tid + (b0 + j) * kThreads;
+          r = idx % ROWS;
+          k = idx / ROWS;
+        }
+        v[j] = (r < rows_valid && k < k_valid) ? ld(r0 + r, k0 + k) : 0.f;
       }
-      const uint32_t off = swz(r, k);
-      const uint32_t h = split ? to_tf32(v[j]) : __float_as_uint(v[j]);
-      *reinterpret_cast<uint32_t*>(hi + off) = h;
-      if (split) *reinterpret_cast<float*>(lo + off) = v[j] - __uint_as_float(h);
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        int r, k;
+        if (!L::kContigRow) {
+          r = (tid >> 5) + (b0 + j) * (kThreads / 32);
+          k = tid & 31;
+        } else {
+          const int idx = tid + (b0 + j) * kThreads;
+          r = idx % ROWS;
+          k = idx / ROWS;
+        }
+        *reinterpret_cast<float*>(dst + swz(r, k)) = v[j];
+      }
     }
   }
 }
 
-// Persistent kernel: each CTA walks tiles t = blockIdx.x, += gridDim.x over
-// (m tiles x n tiles x k splits).  TMEM and barriers are set up once.
-// Epilogue concept (row owner; every thread calls every hook):
-//   set_tile(bm, bn, split); begin(m, valid);
-//   chunk(m, valid, n, v[16], ncols_valid) per 16-column chunk in order;
-//   end(m, valid, n0, bm, bn, split).
-template <int BN, class AL, class BL, class Epi>
-__global__ void __launch_bounds__(kThreads)
+// lo = x - trunc_tf32(x) for every 16-byte chunk of a raw stage
+template <int BYTES>
+__device__ __forceinline__ void make_lo(const uint8_t* raw, uint8_t* lo) {
+  constexpr int kChunks = BYTES / 16;
+#pragma unroll 4
+  for (int c = threadIdx.x; c < kChunks; c += kThreads) {
+    const uint4 x = reinterpret_cast<const uint4*>(raw)[c];
+    const uint32_t m = 0xFFFFE000u;
+    float4 l;
+    l.x = __uint_as_float(x.x) - __uint_as_float(x.x & m);
+    l.y = __uint_as_float(x.y) - __uint_as_float(x.y & m);
+    l.z = __uint_as_float(x.z) - __uint_as_float(x.z & m);
+    l.w = __uint_as_float(x.w) - __uint_as_float(x.w & m);
+    reinterpret_cast<float4*>(lo)[c] = l;
+  }
+}
+
+// Work item -> number of 32-wide k-blocks
+__device__ __forceinline__ int item_nkb(int w, int splits, int k_chunk, int k_total) {
+  const int split = w % splits;
+  const int kb0 = split * k_chunk, kb1 = min(k_total, kb0 + k_chunk);
+  return kb1 > kb0 ? (kb1 - kb0 + kBK - 1) / kBK : 0;
+}
+
+template <int BN, bool VA, bool VB, class AL, class BL, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(int M, const int* __restrict__ M_dev, int N, int K, const int* __restrict__ K_dev,
                    int k_chunk, int splits, int split3, AL a, BL b, Epi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = Smem<BN>;
   constexpr int NC = tmem_cols(BN);
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStages * S::kStage);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kStages + 1);
+  constexpr int kS = S::kS, kL = S::kL;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* ring = base;                          // kS x [A raw | B raw]
+  uint8_t* lobuf = base + kS * S::kStage;        // 2 x [A lo | B lo]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lobuf + 2 * S::kStage);  // kS stage bars + done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kS + 1);
 
   const int m_total = M_dev ? *M_dev : M;
   const int k_total = K_dev ? *K_dev : K;
@@ -211,8 +315,7 @@ __global__ void __launch_bounds__(kThreads)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    mbar_init(&bars[kStages], 1);
+    for (int q = 0; q < kS + 1; ++q) mbar_init(&bars[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc<NC>(tmem_slot);
@@ -220,54 +323,90 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = make_idesc_tf32(BN);
+  constexpr bool kAmn = VA && AL::kContigRow;  // operand staged MN-major
+  constexpr bool kBmn = VB && BL::kContigRow;
+  const uint32_t idesc = make_idesc_tf32(BN, kAmn, kBmn);
   const bool split_on = split3 != 0;
-  uint32_t phase[kStages] = {0, 0};
-  uint32_t done_phase = 0;
-  int g = 0;  // k-blocks issued by this CTA so far (stage ring position)
 
+  auto desc_a = [&](uint32_t addr, int ks) -> uint64_t {
+    if constexpr (kAmn)
+      return make_desc_mn(addr + ks * (kBM / 32) * 1024, 512, (kBM / 32) * 512);
+    else
+      return make_desc(addr + ks * 32);
+  };
+  auto desc_b = [&](uint32_t addr, int ks) -> uint64_t {
+    if constexpr (kBmn)
+      return make_desc_mn(addr + ks * (BN / 32) * 1024, 512, (BN / 32) * 512);
+    else
+      return make_desc(addr + ks * 32);
+  };
+
+  // ---- producer cursor over the flattened (work item, k-block) stream
+  int pw = blockIdx.x, pkb = 0;
+  while (pw < n_work && item_nkb(pw, splits, k_chunk, k_total) == 0) pw += gridDim.x;
+  int pstep = 0;
+  auto issue_next = [&]() {  // always commits one cp.async group (possibly empty)
+    if (pw < n_work) {
+      const int s = pstep % kS;
+      if (pstep >= kS) mbar_wait(&bars[s], ((pstep / kS) - 1) & 1);  // MMAs of pstep-kS done
+      const int split = pw % splits;
+      const int bn = (pw / splits) % n_tiles;
+      const int bm = pw / (splits * n_tiles);
+      const int k_begin = split * k_chunk;
+      const int k_end = min(k_total, k_begin + k_chunk);
+      const int k0 = k_begin + pkb * kBK;
+      const int kv = min(kBK, k_end - k0);
+      uint8_t* st = ring + s * S::kStage;
+      issue_tile<kBM, VA>(a, bm * kBM, min(kBM, m_total - bm * kBM), k0, kv, st);
+      issue_tile<BN, VB>(b, bn * BN, min(BN, N - bn * BN), k0, kv, st + S::kA);
+      ++pstep;
+      if (++pkb == item_nkb(pw, splits, k_chunk, k_total)) {
+        pkb = 0;
+        do {
+          pw += gridDim.x;
+        } while (pw < n_work && item_nkb(pw, splits, k_chunk, k_total) == 0);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int q = 0; q < kL; ++q) issue_next();
+
+  uint32_t done_phase = 0;
+  int g = 0;  // consumer step
   for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
     const int split = w % splits;
     const int bn = (w / splits) % n_tiles;
     const int bm = w / (splits * n_tiles);
     const int m0 = bm * kBM, n0 = bn * BN;
-    const int k_begin = split * k_chunk;
-    const int k_end = min(k_total, k_begin + k_chunk);
     const int rows_a = min(kBM, m_total - m0);
-    const int rows_b = min(BN, N - n0);
-    const int nkb = k_end > k_begin ? (k_end - k_begin + kBK - 1) / kBK : 0;
+    const int nkb = item_nkb(w, splits, k_chunk, k_total);
 
     for (int kb = 0; kb < nkb; ++kb, ++g) {
-      const int s = g % kStages;
-      if (g >= kStages) {  // the MMAs that read this stage must have completed
-        mbar_wait(&bars[s], phase[s]);
-        phase[s] ^= 1;
+      issue_next();                 // step g + kL
+      cp_async_wait<kL>();          // step g has landed (this thread's part)
+      __syncthreads();              // ... and everyone's
+      const int s = g % kS;
+      uint8_t* st = ring + s * S::kStage;
+      uint8_t* lo = lobuf + (g & 1) * S::kStage;
+      if (split_on) {
+        make_lo<S::kStage>(st, lo);
       }
-      uint8_t* st = base + s * S::kStage;
-      uint8_t* a_hi = st;
-      uint8_t* a_lo = st + S::kA;
-      uint8_t* b_hi = st + 2 * S::kA;
-      uint8_t* b_lo = st + 2 * S::kA + S::kB;
-      const int k0 = k_begin + kb * kBK;
-      const int kv = min(kBK, k_end - k0);
-      stage<kBM>(a, m0, rows_a, k0, kv, a_hi, a_lo, split_on);
-      stage<BN>(b, n0, rows_b, k0, kv, b_hi, b_lo, split_on);
       fence_async_smem();
       __syncthreads();
       if (threadIdx.x == 0) {
         tc_fence_after();
-        const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
-        const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+        const uint32_t ah = smem_u32(st), bh = smem_u32(st + S::kA);
+        const uint32_t al = smem_u32(lo), bl = smem_u32(lo + S::kA);
 #pragma unroll
-        for (int ks = 0; ks < kBK / 8; ++ks) {  // K = 8 tf32 per MMA = 32 bytes
-          const uint32_t o = ks * 32;
+        for (int ks = 0; ks < kBK / 8; ++ks) {  // K = 8 tf32 per MMA
           const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
           if (split_on) {
-            mma_tf32(tmem, make_desc(al + o), make_desc(bh + o), idesc, acc0);
-            mma_tf32(tmem, make_desc(ah + o), make_desc(bl + o), idesc, 1u);
-            mma_tf32(tmem, make_desc(ah + o), make_desc(bh + o), idesc, 1u);
+            mma_tf32(tmem, desc_a(al, ks), desc_b(bh, ks), idesc, acc0);
+            mma_tf32(tmem, desc_a(ah, ks), desc_b(bl, ks), idesc, 1u);
+            mma_tf32(tmem, desc_a(ah, ks), desc_b(bh, ks), idesc, 1u);
           } else {
-            mma_tf32(tmem, make_desc(ah + o), make_desc(bh + o), idesc, acc0);
+            mma_tf32(tmem, desc_a(ah, ks), desc_b(bh, ks), idesc, acc0);
           }
         }
         mma_commit(&bars[s]);
@@ -276,35 +415,36 @@ __global__ void __launch_bounds__(kThreads)
     // all MMAs of this tile done -> accumulator readable
     if (threadIdx.x == 0) {
       if (nkb > 0)
-        mma_commit(&bars[kStages]);
+        mma_commit(&bars[kS]);
       else
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&bars[kStages])) : "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&bars[kS]))
+                     : "memory");
     }
-    mbar_wait(&bars[kStages], done_phase);
+    mbar_wait(&bars[kS], done_phase);
     done_phase ^= 1;
     tc_fence_after();
 
-    const int row = warp * 32 + lane;
+    const int quarter = warp & 3, half = warp >> 2;
+    const int row = quarter * 32 + lane;
     const int m = m0 + row;
     const bool valid = row < rows_a;
-    epi.set_tile(bm, bn, split);
-    epi.begin(m, valid);
+    constexpr int kHalf = BN / 2;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
+    for (int c = half * kHalf; c < (half + 1) * kHalf; c += 16) {
       float v[16];
       if (nkb > 0) {
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c, v);
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = 0.f;
       }
-      epi.chunk(m, valid, n0 + c, v, min(16, N - (n0 + c)));
+      epi.chunk(m, valid, n0 + c, v, min(16, N - (n0 + c)), split);
     }
-    epi.end(m, valid, n0, bm, bn, split);
     tc_fence_before();
-    __syncthreads();  // TMEM reads (and epilogue smem) finished before the next tile
+    __syncthreads();  // TMEM reads finished before the next tile's MMAs
     tc_fence_after();
   }
+  cp_async_wait<0>();
   if (warp == 0) tmem_free<NC>(tmem);
 }
 
@@ -314,37 +454,43 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
   int k_chunk = ceil_div(ceil_div(K > 0 ? K : 1, splits), kBK) * kBK;
   splits = ceil_div(K > 0 ? K : 1, k_chunk);
   const int smem = Smem<BN>::kBytes;
-  auto kern = tc_gemm_kernel<BN, AL, BL, Epi>;
+  const bool va = a.vec_ok(K), vb = b.vec_ok(K);
+  auto kern = va ? (vb ? tc_gemm_kernel<BN, true, true, AL, BL, Epi>
+                       : tc_gemm_kernel<BN, true, false, AL, BL, Epi>)
+                 : (vb ? tc_gemm_kernel<BN, false, true, AL, BL, Epi>
+                       : tc_gemm_kernel<BN, false, false, AL, BL, Epi>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const long long work = (long long)ceil_div(M, kBM) * ceil_div(N, BN) * splits;
-  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
-  const int grid = (int)std::min<long long>(work, 148LL * per_sm);
+  const int grid = (int)std::min<long long>(work, 148LL);
   kern<<<grid, kThreads, smem, s>>>(M, M_dev, N, K, K_dev, k_chunk, splits, split3, a, b, epi);
   return cudaGetLastError();
 }
 
-// BN chosen from N: one N tile when N <= 256 (rounded up to 32/64/128/256)
+inline int pick_bn(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : 128; }
+
+// BN from N (32 / 64 / 128; N > 128 is tiled in 128-wide column tiles)
 template <class AL, class BL, class Epi>
 inline cudaError_t launch(int M, const int* M_dev, int N, int K, const int* K_dev, int splits,
-                          int split3, AL a, BL b, Epi epi, cudaStream_t s, int bn_hint = 0) {
+                          int split3, AL a, BL b, Epi epi, cudaStream_t s) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (splits < 1) splits = 1;
-  const int bn = bn_hint ? bn_hint : (N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256);
-  switch (bn) {
+  switch (pick_bn(N)) {
     case 32: return launch_bn<32>(M, M_dev, N, K, K_dev, splits, split3, a, b, epi, s);
     case 64: return launch_bn<64>(M, M_dev, N, K, K_dev, splits, split3, a, b, epi, s);
-    case 128: return launch_bn<128>(M, M_dev, N, K, K_dev, splits, split3, a, b, epi, s);
-    default: return launch_bn<256>(M, M_dev, N, K, K_dev, splits, split3, a, b, epi, s);
+    default: return launch_bn<128>(M, M_dev, N, K, K_dev, splits, split3, a, b, epi, s);
   }
 }
 
-// Number of K splits for weight-gradient GEMMs (shape-only -> deterministic)
-inline int splits_for(long long M, long long N, long long K, int bn) {
-  long long tiles = (long long)ceil_div(M, kBM) * ceil_div(N, bn);
-  long long want = (2LL * 148 + tiles - 1) / tiles;
+// Number of K splits for weight-gradient GEMMs (shape-only -> deterministic):
+// enough (tile x split) work items to give every SM one, chunks >= 256.
+inline int splits_for(long long M, long long N, long long K) {
+  long long tiles = (long long)ceil_div(M, kBM) * ceil_div(N, pick_bn((int)std::min<long long>(N, 128)));
+  long long want = (148LL + tiles - 1) / tiles;
   long long max_by_k = (K + 255) / 256;
+  long long min_by_k = (K + 2047) / 2048;  // <= 2048-deep TMEM accumulations (accuracy)
   long long s = want < max_by_k ? want : max_by_k;
+  if (s < min_by_k) s = min_by_k;
   if (s < 1) s = 1;
   if (s > 512) s = 512;
   return (int)s;
@@ -356,23 +502,20 @@ struct TcEpiBiasAct {  // out[m][n] = act(acc + bias[n])
   int ldo;
   const float* bias;
   int act;
-  __device__ void set_tile(int, int, int) {}
-  __device__ void begin(int, bool) {}
-  __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv) {
+  __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv, int) const {
     if (!valid) return;
     float* o = out + (long long)m * ldo + n;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (i < nv) {
-        float x = v[i] + (bias ? bias[n + i] : 0.f);
+        const float x = v[i] + (bias ? bias[n + i] : 0.f);
         o[i] = act ? tanhf(x) : x;
       }
     }
   }
-  __device__ void end(int, bool, int, int, int, int) {}
 };
 
-struct TcEpiSplitCols {  // cols [0, n1) -> o1, [n1, N) -> o2, optional *(1 - gate^2) on o1
+struct TcEpiSplitCols {  // cols [0, n1) -> o1 (+ add, * (1 - gate^2)), [n1, N) -> o2
   float* o1;
   int ld1, n1;
   float* o2;
@@ -380,9 +523,7 @@ struct TcEpiSplitCols {  // cols [0, n1) -> o1, [n1, N) -> o2, optional *(1 - ga
   const float* gate;
   int ldg;
   const float* add;  // optional addend on the o1 columns (row stride ld1), before the gate
-  __device__ void set_tile(int, int, int) {}
-  __device__ void begin(int, bool) {}
-  __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv) {
+  __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv, int) const {
     if (!valid) return;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -392,8 +533,8 @@ struct TcEpiSplitCols {  // cols [0, n1) -> o1, [n1, N) -> o2, optional *(1 - ga
       if (c < n1) {
         if (add) x = add[(long long)m * ld1 + c] + x;
         if (gate) {
-          const float g = gate[(long long)m * ldg + c];
-          x *= 1.f - g * g;
+          const float gg = gate[(long long)m * ldg + c];
+          x *= 1.f - gg * gg;
         }
         o1[(long long)m * ld1 + c] = x;
       } else {
@@ -401,24 +542,19 @@ struct TcEpiSplitCols {  // cols [0, n1) -> o1, [n1, N) -> o2, optional *(1 - ga
       }
     }
   }
-  __device__ void end(int, bool, int, int, int, int) {}
 };
 
 struct TcEpiPartial {  // split-K partial tile ws[split][m][n] (row-major, width N)
   float* ws;
   long long split_stride;
   int M, N;
-  int split;
-  __device__ void set_tile(int, int, int sp) { split = sp; }
-  __device__ void begin(int, bool) {}
-  __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv) {
+  __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv, int split) const {
     if (!valid) return;
     float* o = ws + split * split_stride + (long long)m * N + n;
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (i < nv) o[i] = v[i];
   }
-  __device__ void end(int, bool, int, int, int, int) {}
 };
 
 }  // namespace tc

@@ -577,8 +577,12 @@ def _loss_kernel(e_pred, f_pred, e_true, f_true, n_per, alpha_e, alpha_f, scratc
     vals = sc.get("loss", (3,), dt)
     de = sc.get("de", (max(B, 1),), dt)
     df = sc.get("df", (max(N, 1), 3), dt)
+    ws = sc.bufs.get("loss_ws")
+    if ws is None:  # zero once; the kernel re-arms its ticket after every call
+        ws = torch.zeros(query("gfm_loss_workspace_bytes"), dtype=torch.uint8, device=e_pred.device)
+        sc.bufs["loss_ws"] = ws
     call("gfm_loss_seeds", ptr(e_pred), ptr(e_true), ptr(n_per), B, ptr(f_pred), ptr(f_true), N,
-         float(alpha_e), float(alpha_f), ptr(vals), ptr(de), ptr(df), ptr(contrib), code,
+         float(alpha_e), float(alpha_f), ptr(vals), ptr(de), ptr(df), ptr(contrib), ptr(ws), code,
          stream_handle())
     return vals, de, df
 
@@ -699,10 +703,8 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
              ptr(batch.csc_dst), ptr(batch.edge_w), N, H, parts, ptr(dh_in),
              ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code, flags, s)
         dz = out
-    chunk = N if dt == torch.float64 else 256
-    ews = sc.bytes("emb_ws", query("gfm_embedding_grad_workspace_bytes", N, H, chunk, code))
-    call("gfm_embedding_grad", ptr(batch.z), N, ptr(dz), H, chunk, ptr(gp.embedding), ptr(ews),
-         code, s)
+    ews = sc.bytes("emb_ws", query("gfm_embedding_grad_workspace_bytes", N, H, code))
+    call("gfm_embedding_grad", ptr(batch.z), N, ptr(dz), H, ptr(gp.embedding), ptr(ews), code, s)
 
     e_true, n_per = batch.energy_true, batch.n_per_graph
     lb = LossBreakdown(vals if scratch is not None else vals.clone(),
