@@ -363,7 +363,13 @@ def run_native(args):
             cpu_baseline=cpu, clocks=clocks, gpu_launches=launches)
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        # A communicator captured inside a CUDA graph can block NCCL teardown;
+        # every rank is done and rank 0 has printed, so leave without it.
+        torch.cuda.synchronize()
+        comm.barrier()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
 
 
 def main():
