@@ -29,8 +29,19 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = dict(kind="pna-agg", layers=3, hidden=64, fc_layers=2, fc_width=64,
-                atoms=32, box=8.0, rc=5.0, max_nbr=20, batch=1024)
+CONFIGS = {
+    # BASELINE.json configs[1]: the single-GPU headline
+    "c2": dict(kind="pna-agg", layers=3, hidden=64, fc_layers=2, fc_width=64, atoms=32, box=8.0,
+               rc=5.0, max_nbr=20, batch=1024, periodic=False, cpu_sample=32,
+               desc="C2: pna-agg L3 H64 fc2x64, 32-atom graphs, box 8 A, rc 5 A, max 20 "
+                    "neighbours, 1024 graphs/GPU"),
+    # BASELINE.json configs[2]: GFM scale, data parallel
+    "c3": dict(kind="pna-agg", layers=6, hidden=512, fc_layers=2, fc_width=512, atoms=100,
+               box=12.0, rc=5.0, max_nbr=32, batch=512, periodic=True, cpu_sample=2,
+               desc="C3: pna-agg L6 H512 fc2x512, 100-atom periodic crystals, 12 A cell, "
+                    "rc 5 A, max 32 neighbours, 512 graphs/GPU"),
+}
+WORKLOAD = dict(CONFIGS["c2"])
 METRIC = "training graphs/sec (energy+forces MTL) at 1/2/4/8 B200; aggregation HBM GB/s"
 UNIT = "graphs/s"
 
@@ -41,7 +52,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--batch", type=int, default=WORKLOAD["batch"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-graph", action="store_true", help="disable CUDA-graph capture")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     return ap.parse_args()
@@ -61,7 +73,8 @@ def make_structures(n_graphs, seed):
 
 # ---------------------------------------------------------------- CPU oracle leg
 def _cpu_worker(args):
-    seed, n_graphs, budget_s = args
+    seed, n_graphs, budget_s, config = args
+    WORKLOAD.update(CONFIGS[config])
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import gfm_oracle as O
 
@@ -73,7 +86,9 @@ def _cpu_worker(args):
     z, pos, energy, forces = make_structures(n_graphs, seed)
     recs = []
     for g in range(n_graphs):
-        edges, shift = O.cutoff_edges(pos[g], WORKLOAD["rc"], max_nbr=WORKLOAD["max_nbr"])
+        cell = (WORKLOAD["box"],) * 3 if WORKLOAD["periodic"] else None
+        edges, shift = O.cutoff_edges(pos[g], WORKLOAD["rc"], max_nbr=WORKLOAD["max_nbr"],
+                                      cell=cell)
         recs.append(dict(z=z[g], pos=pos[g], edges=edges, shift=shift, energy=energy[g],
                          forces=forces[g]))
     steps, t = 0, 0
@@ -88,20 +103,23 @@ def _cpu_worker(args):
     return steps * n_graphs, time.perf_counter() - t0
 
 
-def cpu_oracle_rate(budget_s, procs=None, sample_graphs=32):
+def cpu_oracle_rate(budget_s, procs=None, sample_graphs=None, config="c2"):
     """graphs/s of the numpy oracle step (make_batch + fwd + bwd + Adam, the
     reference's train.py:247-277 minus the fetch) over all host cores: one
     single-threaded process per core, each on its own 32-graph sample."""
     import multiprocessing as mp
 
     procs = procs or len(os.sched_getaffinity(0))
+    sample_graphs = sample_graphs or CONFIGS[config]["cpu_sample"]
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
-        res = pool.map(_cpu_worker, [(1000 + k, sample_graphs, budget_s) for k in range(procs)])
+        res = pool.map(_cpu_worker, [(1000 + k, sample_graphs, budget_s, config)
+                                     for k in range(procs)])
     graphs = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
-    return graphs / wall, procs, (f"{procs} processes x {sample_graphs}-graph C2 samples "
+    return graphs / wall, procs, (f"{procs} processes x {sample_graphs}-graph "
+                                  f"{config.upper()} samples "
                                   f"(numpy float64 oracle port, OPENBLAS_NUM_THREADS=1), "
                                   f"~{budget_s:.0f} s each")
 
@@ -110,11 +128,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s)
+    rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s, config=args.config)
     line = dict(metric=METRIC, value=rate, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, higher_is_better=True, scaling="weak", vs_baseline=None,
                 dtype="f64", data="synthetic", impl="reference",
-                config=dict(workload="C2: pna-agg L3 H64, 32-atom graphs, rc 5 A, cap 20",
+                config=dict(workload=WORKLOAD["desc"],
                             global_batch=WORKLOAD["batch"] * args.gpus),
                 cpu_baseline=dict(value=rate, unit=UNIT, cores=cores, kind="port", sample=sample),
                 e2e=dict(value=rate, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
@@ -195,7 +213,8 @@ def run_native(args):
     tr = T.DataParallelTrainer(cfg, T.TrainConfig(optimizer="adam", learning_rate=1e-3),
                                comm=comm, device=dev)
     host_off = (np.arange(B + 1) * n).astype(np.int32)
-    runner = T.StructureStepRunner(tr, host_off, WORKLOAD["rc"], WORKLOAD["max_nbr"],
+    cells = [[WORKLOAD["box"]] * 3] * B if WORKLOAD["periodic"] else None
+    runner = T.StructureStepRunner(tr, host_off, WORKLOAD["rc"], WORKLOAD["max_nbr"], cells=cells,
                                    use_graph=not args.no_graph)
 
     # pool of distinct device-resident batches (raw structures + labels)
@@ -342,14 +361,13 @@ def run_native(args):
         clocks = clk.summary()
         cpu = None
         if world == 1:
-            rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s)
+            rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s, config=args.config)
             cpu = dict(value=rate, unit=UNIT, cores=cores, kind="port", sample=sample)
         line = dict(
             metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
             warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True,
             scaling="weak", vs_baseline=None, dtype="f32", data="synthetic",
-            config=dict(workload="C2: pna-agg L3 H64 fc2x64, 32-atom graphs, box 8 A, rc 5 A, "
-                                 "max 20 neighbours, 1024 graphs/GPU",
+            config=dict(workload=WORKLOAD["desc"],
                         global_batch=B * world, per_gpu_batch=B, nodes_per_gpu=N,
                         edges_per_gpu=E, parallelism=f"dp{world}",
                         cuda_graph=graph is not None,
@@ -374,6 +392,9 @@ def run_native(args):
 
 def main():
     args = parse()
+    WORKLOAD.update(CONFIGS[args.config])
+    if args.batch is None:
+        args.batch = WORKLOAD["batch"]
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -30,7 +30,7 @@ static inline int grid_1d(long long n, int threads = 256) {
 template <typename T>
 __global__ void __launch_bounds__(256)
     k_splitk_reduce(const T* __restrict__ ws, int splits, int N, int K1, int K2, int with_bias,
-                    T* __restrict__ g1, T* __restrict__ g2, T* __restrict__ gb) {
+                    T* __restrict__ g1, T* __restrict__ g2, T* __restrict__ gb, int trans) {
   __shared__ double red[8][33];
   const int Kt = K1 + K2 + with_bias;
   const long long total = (long long)N * Kt;
@@ -48,7 +48,9 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (ty != 0 || idx >= total) continue;
     const T s = (T)a;
-    const int n = (int)(idx / Kt), k = (int)(idx % Kt);
+    // partials are [N][Kt] (trans = 0) or [Kt][N] (trans = 1); idx walks them
+    const int n = trans ? (int)(idx % N) : (int)(idx / Kt);
+    const int k = trans ? (int)(idx / N) : (int)(idx % Kt);
     if (k < K1)
       g1[(long long)n * K1 + k] = s;
     else if (k < K1 + K2)
@@ -235,7 +237,7 @@ int wgrad_splits(int M, int N, int Kt) {
 template <typename T>
 size_t linear_bwd_weight_ws(int M, int N, int K1, int K2, int with_bias) {
   const int Kt = K1 + K2 + with_bias;
-  const int splits = std::max(choose_splits(N, Kt, M), tc::splits_for(N, Kt, M));
+  const int splits = std::max(choose_splits(N, Kt, M), tc::splits_for(Kt, N, M));
   return sizeof(T) * (size_t)splits * N * Kt;
 }
 
@@ -250,21 +252,27 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
                                 int ld1, int K1, const T* X2, int ld2, int K2, int with_bias,
                                 T* g1, T* g2, T* gb, T* ws, cudaStream_t s) {
   const int Kt = K1 + K2 + with_bias;
-  const int splits = wgrad_splits<T>(M, N, Kt);
-  ColsLd<T> a{dY, ldd};
-  Cols2Ld<T> b{X1, ld1, K1, X2, ld2, K2};
   cudaError_t e;
-  int real;
-  // rows = output features N, cols = Kt, reduction over the M batch rows
+  int real, trans = 0;
   if constexpr (std::is_same<T, float>::value) {
     if (use_tc<T>()) {
-      tc::TcEpiPartial epi{ws, (long long)N * Kt, N, Kt};
-      e = tc::launch(N, nullptr, Kt, M, M_dev, splits, tc_split3(), a, b, epi, s);
+      // tensor cores: C^T[Kt][N] = [X | 1]^T dY -- the wide operand X is read
+      // once (one column tile), no half-empty 128-row tiles for N = H
+      const int splits = tc::splits_for(Kt, N, M);
+      Cols2Ld<T> a{X1, ld1, K1, X2, ld2, K2};
+      ColsLd<T> b{dY, ldd};
+      tc::TcEpiPartial epi{ws, (long long)N * Kt, Kt, N};
+      e = tc::launch(Kt, nullptr, N, M, M_dev, splits, tc_split3(), a, b, epi, s);
       real = real_splits(M, splits, tc::kBK);
+      trans = 1;
       goto reduce;
     }
   }
   {
+    // rows = output features N, cols = Kt, reduction over the M batch rows
+    const int splits = choose_splits(N, Kt, M);
+    ColsLd<T> a{dY, ldd};
+    Cols2Ld<T> b{X1, ld1, K1, X2, ld2, K2};
     EpiPartial<T> epi{ws, (long long)N * Kt};
     e = launch_simt_gemm<T>(N, nullptr, Kt, M, M_dev, splits, a, b, epi, s);
     real = real_splits(M, splits, kBK);
@@ -272,12 +280,10 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
 reduce:
   if (e != cudaSuccess) return e;
   k_splitk_reduce<T><<<grid_1d((long long)N * Kt, 32), 256, 0, s>>>(ws, real, N, K1, K2, with_bias,
-                                                                 g1, g2, gb);
+                                                                 g1, g2, gb, trans);
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------ force head
-// node-factored (see force.cu): P = h V^T, then edge gathers
 template <typename T>
 cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const int* col_src,
                             const T* dx, const T* c, const T* u, T* f, int flags, cudaStream_t s);
@@ -359,7 +365,7 @@ cudaError_t embedding_grad_t(const int* z, int n_nodes, const T* dh, int H, T* g
 reduce:
   if (e != cudaSuccess) return e;
   k_splitk_reduce<T><<<grid_1d((long long)E * H, 32), 256, 0, s>>>(ws, real, E, H, 0, 0, grad,
-                                                                    nullptr, nullptr);
+                                                                    nullptr, nullptr, 0);
   return cudaGetLastError();
 }
 

@@ -164,7 +164,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
 }
 
-constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : 128; }
+constexpr int tmem_cols(int cols) { return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256; }
 
 // ring depth by BN (192 KB of ring + lo buffers, one CTA per SM)
 template <int BN>
@@ -174,7 +174,7 @@ struct Smem {
   static constexpr int kStage = kA + kB;
   static constexpr int kS = BN >= 128 ? 4 : BN >= 64 ? 6 : 7;  // ring stages
   static constexpr int kL = kS - 2;                              // lookahead
-  static constexpr int kBytes = kS * kStage + 2 * kStage + 1024 /*align*/ + 256;
+  static constexpr int kBytes = kS * kStage + 2 * kStage + 1024 /*align*/ + 512;
 };
 
 // MN-major tf32 tile of ROWS x 32 k in the SWIZZLE_128B_BASE32B layout (the
@@ -196,10 +196,9 @@ __device__ __forceinline__ uint32_t mn_off(int rq, int k) {
 //       give k..k+3 of row r (K-major chunk); row-contiguous ones give rows
 //       r..r+3 at k (MN-major chunk).
 //  scalar: synchronous register loads into the K-major layout.
-template <int ROWS, bool VEC, class L>
+template <int ROWS, bool VEC, int kThreads, class L>
 __device__ __forceinline__ void issue_tile(const L& ld, int r0, int rows_valid, int k0, int k_valid,
-                                           uint8_t* dst) {
-  const int tid = threadIdx.x;
+                                           uint8_t* dst, int tid) {
   if constexpr (VEC) {
     constexpr int kChunks = ROWS * kBK / 4;
     const uint32_t sbase = smem_u32(dst);
@@ -268,11 +267,11 @@ __device__ __forceinline__ void issue_tile(const L& ld, int r0, int rows_valid, 
 }
 
 // lo = x - trunc_tf32(x) for every 16-byte chunk of a raw stage
-template <int BYTES>
-__device__ __forceinline__ void make_lo(const uint8_t* raw, uint8_t* lo) {
+template <int BYTES, int kThreads>
+__device__ __forceinline__ void make_lo(const uint8_t* raw, uint8_t* lo, int tid) {
   constexpr int kChunks = BYTES / 16;
 #pragma unroll 4
-  for (int c = threadIdx.x; c < kChunks; c += kThreads) {
+  for (int c = tid; c < kChunks; c += kThreads) {
     const uint4 x = reinterpret_cast<const uint4*>(raw)[c];
     const uint32_t m = 0xFFFFE000u;
     float4 l;
@@ -291,20 +290,37 @@ __device__ __forceinline__ int item_nkb(int w, int splits, int k_chunk, int k_to
   return kb1 > kb0 ? (kb1 - kb0 + kBK - 1) / kBK : 0;
 }
 
+// Warp-specialised persistent kernel (one CTA per SM, 288 threads):
+//   warps 0-3  producers: cp.async k-block p into ring stage p % S (after the
+//              MMAs of p - S released it: empty[s]), and for k-block
+//              q = p - L: wait its copies, write lo = x - trunc(x), arrive
+//              full[q % S];
+//   warp 8     MMA issuer (one elected lane): waits full[s], issues the 4 (or
+//              12 with 3xTF32) tcgen05.mma of the k-block into TMEM
+//              accumulator t % 2, commits empty[s]; at a tile's last k-block
+//              commits tmem_full[t % 2] (waiting tmem_empty first for t >= 2);
+//   warps 4-7  epilogue: wait tmem_full, tcgen05.ld rows (warp w owns TMEM
+//              lanes 32*(w%4)), apply the epilogue, arrive tmem_empty.
+// Phases: the n-th completion of a barrier has parity n & 1.
+constexpr int kProducers = 128, kEpilogue = 128, kWSThreads = kProducers + kEpilogue + 32;
+
 template <int BN, bool VA, bool VB, class AL, class BL, class Epi>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kWSThreads, 1)
     tc_gemm_kernel(int M, const int* __restrict__ M_dev, int N, int K, const int* __restrict__ K_dev,
                    int k_chunk, int splits, int split3, AL a, BL b, Epi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = Smem<BN>;
-  constexpr int NC = tmem_cols(BN);
+  constexpr int NC = tmem_cols(2 * BN);  // two accumulators
   constexpr int kS = S::kS, kL = S::kL;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* ring = base;                          // kS x [A raw | B raw]
-  uint8_t* lobuf = base + kS * S::kStage;        // 2 x [A lo | B lo]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lobuf + 2 * S::kStage);  // kS stage bars + done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kS + 1);
+  uint8_t* ring = base;                    // kS x [A raw | B raw]
+  uint8_t* lobuf = base + kS * S::kStage;  // 2 x [A lo | B lo]
+  uint64_t* full = reinterpret_cast<uint64_t*>(lobuf + 2 * S::kStage);
+  uint64_t* empty = full + kS;
+  uint64_t* tfull = empty + kS;   // [2]
+  uint64_t* tempty = tfull + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int m_total = M_dev ? *M_dev : M;
   const int k_total = K_dev ? *K_dev : K;
@@ -315,7 +331,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kS + 1; ++q) mbar_init(&bars[q], 1);
+    for (int q = 0; q < kS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&tfull[q], 1);
+      mbar_init(&tempty[q], kEpilogue / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc<NC>(tmem_slot);
@@ -323,128 +346,154 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr bool kAmn = VA && AL::kContigRow;  // operand staged MN-major
-  constexpr bool kBmn = VB && BL::kContigRow;
-  const uint32_t idesc = make_idesc_tf32(BN, kAmn, kBmn);
   const bool split_on = split3 != 0;
 
-  auto desc_a = [&](uint32_t addr, int ks) -> uint64_t {
-    if constexpr (kAmn)
-      return make_desc_mn(addr + ks * (kBM / 32) * 1024, 512, (kBM / 32) * 512);
-    else
-      return make_desc(addr + ks * 32);
-  };
-  auto desc_b = [&](uint32_t addr, int ks) -> uint64_t {
-    if constexpr (kBmn)
-      return make_desc_mn(addr + ks * (BN / 32) * 1024, 512, (BN / 32) * 512);
-    else
-      return make_desc(addr + ks * 32);
+  auto tile_of = [&](int w, int& bm, int& bn, int& split) {
+    split = w % splits;
+    bn = (w / splits) % n_tiles;
+    bm = w / (splits * n_tiles);
   };
 
-  // ---- producer cursor over the flattened (work item, k-block) stream
-  int pw = blockIdx.x, pkb = 0;
-  while (pw < n_work && item_nkb(pw, splits, k_chunk, k_total) == 0) pw += gridDim.x;
-  int pstep = 0;
-  auto issue_next = [&]() {  // always commits one cp.async group (possibly empty)
-    if (pw < n_work) {
-      const int s = pstep % kS;
-      if (pstep >= kS) mbar_wait(&bars[s], ((pstep / kS) - 1) & 1);  // MMAs of pstep-kS done
-      const int split = pw % splits;
-      const int bn = (pw / splits) % n_tiles;
-      const int bm = pw / (splits * n_tiles);
-      const int k_begin = split * k_chunk;
-      const int k_end = min(k_total, k_begin + k_chunk);
-      const int k0 = k_begin + pkb * kBK;
-      const int kv = min(kBK, k_end - k0);
-      uint8_t* st = ring + s * S::kStage;
-      issue_tile<kBM, VA>(a, bm * kBM, min(kBM, m_total - bm * kBM), k0, kv, st);
-      issue_tile<BN, VB>(b, bn * BN, min(BN, N - bn * BN), k0, kv, st + S::kA);
-      ++pstep;
-      if (++pkb == item_nkb(pw, splits, k_chunk, k_total)) {
-        pkb = 0;
-        do {
+  if (warp < kProducers / 32) {
+    // ================================================================ producers
+    const int tid = threadIdx.x;
+    int pw = blockIdx.x, pkb = 0, p = 0;  // issue cursor
+    int cw = blockIdx.x, ckb = 0, q = 0;  // convert cursor
+    auto skip_empty = [&](int& w, int& kb) {
+      while (w < n_work && item_nkb(w, splits, k_chunk, k_total) == 0) w += gridDim.x;
+      kb = 0;
+    };
+    skip_empty(pw, pkb);
+    skip_empty(cw, ckb);
+    auto issue_one = [&]() {  // always commits one group (possibly empty)
+      if (pw < n_work) {
+        const int s = p % kS;
+        if (p >= kS) mbar_wait(&empty[s], ((p / kS) - 1) & 1);
+        int bm, bn, split;
+        tile_of(pw, bm, bn, split);
+        const int k_begin = split * k_chunk;
+        const int k_end = min(k_total, k_begin + k_chunk);
+        const int k0 = k_begin + pkb * kBK;
+        const int kv = min(kBK, k_end - k0);
+        uint8_t* st = ring + s * S::kStage;
+        issue_tile<kBM, VA, kProducers>(a, bm * kBM, min(kBM, m_total - bm * kBM), k0, kv, st, tid);
+        issue_tile<BN, VB, kProducers>(b, bn * BN, min(BN, N - bn * BN), k0, kv, st + S::kA, tid);
+        ++p;
+        if (++pkb == item_nkb(pw, splits, k_chunk, k_total)) {
           pw += gridDim.x;
-        } while (pw < n_work && item_nkb(pw, splits, k_chunk, k_total) == 0);
-      }
-    }
-    cp_async_commit();
-  };
-#pragma unroll 1
-  for (int q = 0; q < kL; ++q) issue_next();
-
-  uint32_t done_phase = 0;
-  int g = 0;  // consumer step
-  for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-    const int split = w % splits;
-    const int bn = (w / splits) % n_tiles;
-    const int bm = w / (splits * n_tiles);
-    const int m0 = bm * kBM, n0 = bn * BN;
-    const int rows_a = min(kBM, m_total - m0);
-    const int nkb = item_nkb(w, splits, k_chunk, k_total);
-
-    for (int kb = 0; kb < nkb; ++kb, ++g) {
-      issue_next();                 // step g + kL
-      cp_async_wait<kL>();          // step g has landed (this thread's part)
-      __syncthreads();              // ... and everyone's
-      const int s = g % kS;
-      uint8_t* st = ring + s * S::kStage;
-      uint8_t* lo = lobuf + (g & 1) * S::kStage;
-      if (split_on) {
-        make_lo<S::kStage>(st, lo);
-      }
-      fence_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tc_fence_after();
-        const uint32_t ah = smem_u32(st), bh = smem_u32(st + S::kA);
-        const uint32_t al = smem_u32(lo), bl = smem_u32(lo + S::kA);
-#pragma unroll
-        for (int ks = 0; ks < kBK / 8; ++ks) {  // K = 8 tf32 per MMA
-          const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
-          if (split_on) {
-            mma_tf32(tmem, desc_a(al, ks), desc_b(bh, ks), idesc, acc0);
-            mma_tf32(tmem, desc_a(ah, ks), desc_b(bl, ks), idesc, 1u);
-            mma_tf32(tmem, desc_a(ah, ks), desc_b(bh, ks), idesc, 1u);
-          } else {
-            mma_tf32(tmem, desc_a(ah, ks), desc_b(bh, ks), idesc, acc0);
-          }
+          skip_empty(pw, pkb);
         }
-        mma_commit(&bars[s]);
       }
-    }
-    // all MMAs of this tile done -> accumulator readable
-    if (threadIdx.x == 0) {
-      if (nkb > 0)
-        mma_commit(&bars[kS]);
-      else
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&bars[kS]))
-                     : "memory");
-    }
-    mbar_wait(&bars[kS], done_phase);
-    done_phase ^= 1;
-    tc_fence_after();
-
-    const int quarter = warp & 3, half = warp >> 2;
-    const int row = quarter * 32 + lane;
-    const int m = m0 + row;
-    const bool valid = row < rows_a;
-    constexpr int kHalf = BN / 2;
+      cp_async_commit();
+    };
 #pragma unroll 1
-    for (int c = half * kHalf; c < (half + 1) * kHalf; c += 16) {
-      float v[16];
-      if (nkb > 0) {
-        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    for (int i = 0; i < kL; ++i) issue_one();
+    while (cw < n_work) {
+      issue_one();                 // k-block q + kL
+      cp_async_wait<kL>();         // k-block q landed (own copies)
+      asm volatile("bar.sync 1, %0;" :: "n"(kProducers) : "memory");  // everyone's copies
+      const int s = q % kS;
+      // lo[q & 1] was last read by the MMAs of k-block q - 2 (at the stream's
+      // tail no later issue waited for them, so wait explicitly)
+      if (split_on && q >= 2) mbar_wait(&empty[(q - 2) % kS], ((q - 2) / kS) & 1);
+      if (split_on) make_lo<S::kStage, kProducers>(ring + s * S::kStage, lobuf + (q & 1) * S::kStage, tid);
+      fence_async_smem();
+      asm volatile("bar.sync 1, %0;" :: "n"(kProducers) : "memory");
+      if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&full[s])) : "memory");
+      ++q;
+      if (++ckb == item_nkb(cw, splits, k_chunk, k_total)) {
+        cw += gridDim.x;
+        skip_empty(cw, ckb);
       }
-      epi.chunk(m, valid, n0 + c, v, min(16, N - (n0 + c)), split);
     }
-    tc_fence_before();
-    __syncthreads();  // TMEM reads finished before the next tile's MMAs
-    tc_fence_after();
+    cp_async_wait<0>();
+  } else if (warp == (kProducers + kEpilogue) / 32) {
+    // ================================================================ MMA issuer
+    constexpr bool kAmn = VA && AL::kContigRow;
+    constexpr bool kBmn = VB && BL::kContigRow;
+    const uint32_t idesc = make_idesc_tf32(BN, kAmn, kBmn);
+    auto desc_a = [&](uint32_t addr, int ks) -> uint64_t {
+      if constexpr (kAmn)
+        return make_desc_mn(addr + ks * (kBM / 32) * 1024, 512, (kBM / 32) * 512);
+      else
+        return make_desc(addr + ks * 32);
+    };
+    auto desc_b = [&](uint32_t addr, int ks) -> uint64_t {
+      if constexpr (kBmn)
+        return make_desc_mn(addr + ks * (BN / 32) * 1024, 512, (BN / 32) * 512);
+      else
+        return make_desc(addr + ks * 32);
+    };
+    int q = 0, t = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
+      const int nkb = item_nkb(w, splits, k_chunk, k_total);
+      const int acc = t & 1;
+      if (t >= 2) mbar_wait(&tempty[acc], ((t >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < nkb; ++kb, ++q) {
+        const int s = q % kS;
+        mbar_wait(&full[s], (q / kS) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ah = smem_u32(ring + s * S::kStage), bh = ah + S::kA;
+          const uint32_t al = smem_u32(lobuf + (q & 1) * S::kStage), bl = al + S::kA;
+#pragma unroll
+          for (int ks = 0; ks < kBK / 8; ++ks) {
+            const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
+            if (split_on) {
+              mma_tf32(d, desc_a(al, ks), desc_b(bh, ks), idesc, acc0);
+              mma_tf32(d, desc_a(ah, ks), desc_b(bl, ks), idesc, 1u);
+              mma_tf32(d, desc_a(ah, ks), desc_b(bh, ks), idesc, 1u);
+            } else {
+              mma_tf32(d, desc_a(ah, ks), desc_b(bh, ks), idesc, acc0);
+            }
+          }
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (nkb > 0)
+          mma_commit(&tfull[acc]);
+        else
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tfull[acc])) : "memory");
+      }
+      __syncwarp();
+    }
+  } else {
+    // ================================================================ epilogue
+    const int quarter = warp & 3;
+    int t = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
+      int bm, bn, split;
+      tile_of(w, bm, bn, split);
+      const int nkb = item_nkb(w, splits, k_chunk, k_total);
+      const int acc = t & 1;
+      mbar_wait(&tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const int m0 = bm * kBM, n0 = bn * BN;
+      const int row = quarter * 32 + lane;
+      const int m = m0 + row;
+      const bool valid = row < min(kBM, m_total - m0);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        if (nkb > 0) {
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        epi.chunk(m, valid, n0 + c, v, min(16, N - (n0 + c)), split);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[acc])) : "memory");
+    }
   }
-  cp_async_wait<0>();
+  tc_fence_before();
+  __syncthreads();
   if (warp == 0) tmem_free<NC>(tmem);
 }
 
@@ -463,7 +512,7 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
   if (e != cudaSuccess) return e;
   const long long work = (long long)ceil_div(M, kBM) * ceil_div(N, BN) * splits;
   const int grid = (int)std::min<long long>(work, 148LL);
-  kern<<<grid, kThreads, smem, s>>>(M, M_dev, N, K, K_dev, k_chunk, splits, split3, a, b, epi);
+  kern<<<grid, kWSThreads, smem, s>>>(M, M_dev, N, K, K_dev, k_chunk, splits, split3, a, b, epi);
   return cudaGetLastError();
 }
 
@@ -497,6 +546,13 @@ inline int splits_for(long long M, long long N, long long K) {
 }
 
 // ---------------------------------------------------------------- epilogues
+// Epilogue stores: 16 consecutive floats per thread-row; when the whole chunk
+// is valid and 16-byte aligned they go out as 4 x st.global.v4 (2 full
+// sectors per thread), else element by element.
+__device__ __forceinline__ bool chunk_vec(const void* p, int nv) {
+  return nv == 16 && (((uintptr_t)p) & 15) == 0;
+}
+
 struct TcEpiBiasAct {  // out[m][n] = act(acc + bias[n])
   float* out;
   int ldo;
@@ -505,12 +561,20 @@ struct TcEpiBiasAct {  // out[m][n] = act(acc + bias[n])
   __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv, int) const {
     if (!valid) return;
     float* o = out + (long long)m * ldo + n;
+    float x[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      if (i < nv) {
-        const float x = v[i] + (bias ? bias[n + i] : 0.f);
-        o[i] = act ? tanhf(x) : x;
-      }
+      const float t = v[i] + (bias && i < nv ? bias[n + i] : 0.f);
+      x[i] = act ? tanhf(t) : t;
+    }
+    if (chunk_vec(o, nv)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<float4*>(o)[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < nv) o[i] = x[i];
     }
   }
 };
@@ -525,6 +589,34 @@ struct TcEpiSplitCols {  // cols [0, n1) -> o1 (+ add, * (1 - gate^2)), [n1, N) 
   const float* add;  // optional addend on the o1 columns (row stride ld1), before the gate
   __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv, int) const {
     if (!valid) return;
+    if (n + 16 <= n1 || n >= n1) {  // chunk entirely in one output
+      const bool first = n < n1;
+      float* o = first ? o1 + (long long)m * ld1 + n : o2 + (long long)m * ld2 + (n - n1);
+      float x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = v[i];
+      if (first && (add || gate)) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i >= nv) continue;
+          if (add) x[i] = add[(long long)m * ld1 + n + i] + x[i];
+          if (gate) {
+            const float gg = gate[(long long)m * ldg + n + i];
+            x[i] *= 1.f - gg * gg;
+          }
+        }
+      }
+      if (chunk_vec(o, nv)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<float4*>(o)[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < nv) o[i] = x[i];
+      }
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (i >= nv) continue;
@@ -551,9 +643,15 @@ struct TcEpiPartial {  // split-K partial tile ws[split][m][n] (row-major, width
   __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv, int split) const {
     if (!valid) return;
     float* o = ws + split * split_stride + (long long)m * N + n;
+    if (chunk_vec(o, nv)) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < nv) o[i] = v[i];
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < nv) o[i] = v[i];
+    }
   }
 };
 
