@@ -1,5 +1,5 @@
 """Run the bench workload's training step eagerly a few times (for ncu launch
-lists / full captures).  Usage: python tools/step_once.py [--steps 3] [--batch 1024]"""
+lists / full captures).  Usage: python tools/step_once.py [--config c2] [--steps 3]"""
 
 import argparse
 import os
@@ -11,22 +11,23 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from bench import WORKLOAD, make_structures  # noqa: E402
+from bench import CONFIGS, WORKLOAD, make_structures  # noqa: E402
 from paper_2406_12909_b200 import model as M, train as T  # noqa: E402
 
 ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
 ap.add_argument("--steps", type=int, default=3)
-ap.add_argument("--batch", type=int, default=WORKLOAD["batch"])
-ap.add_argument("--kind", default=WORKLOAD["kind"])
-ap.add_argument("--hidden", type=int, default=WORKLOAD["hidden"])
-ap.add_argument("--layers", type=int, default=WORKLOAD["layers"])
+ap.add_argument("--batch", type=int, default=None)
 a = ap.parse_args()
-B, n = a.batch, WORKLOAD["atoms"]
-cfg = M.ModelConfig(mpnn_kind=a.kind, mpnn_layers=a.layers, mpnn_width=a.hidden,
-                    fc_layers=2, fc_width=a.hidden, batch_size=B)
+WORKLOAD.update(CONFIGS[a.config])
+B, n = a.batch or WORKLOAD["batch"], WORKLOAD["atoms"]
+cfg = M.ModelConfig(mpnn_kind=WORKLOAD["kind"], mpnn_layers=WORKLOAD["layers"],
+                    mpnn_width=WORKLOAD["hidden"], fc_layers=2, fc_width=WORKLOAD["fc_width"],
+                    batch_size=B)
 tr = T.DataParallelTrainer(cfg, T.TrainConfig())
+cells = [[WORKLOAD["box"]] * 3] * B if WORKLOAD["periodic"] else None
 runner = T.StructureStepRunner(tr, (np.arange(B + 1) * n).astype(np.int32), WORKLOAD["rc"],
-                               WORKLOAD["max_nbr"], use_graph=False)
+                               WORKLOAD["max_nbr"], cells=cells, use_graph=False)
 z, pos, e, f = make_structures(B, 0)
 dev = tr.device
 runner.load(torch.as_tensor(pos.reshape(-1, 3), device=dev), torch.as_tensor(z.reshape(-1), device=dev),
