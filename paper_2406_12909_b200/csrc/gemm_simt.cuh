@@ -85,6 +85,7 @@ struct Cols2Ld {  // rows split over [X1 | X2 | 1]: X1[k*ld1 + r], X2[k*ld2 + r 
   int ld1, n1;
   const T* p2;
   int ld2, n2;
+  const T* ones = nullptr;  // optional [K][4] buffer (column 0 = 1): the ones row as a tensor
   __device__ T operator()(int r, int k) const {
     if (r < n1) return p1[(long long)k * ld1 + r];
     r -= n1;

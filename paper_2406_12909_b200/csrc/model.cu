@@ -238,8 +238,18 @@ template <typename T>
 size_t linear_bwd_weight_ws(int M, int N, int K1, int K2, int with_bias) {
   const int Kt = K1 + K2 + with_bias;
   const int splits = std::max(choose_splits(N, Kt, M), tc::splits_for(Kt, N, M));
-  return sizeof(T) * (size_t)splits * N * Kt;
+  // split-K partials + the [M][4] ones operand of the bias row
+  return sizeof(T) * ((size_t)splits * N * Kt + 64 + 4 * (size_t)(M > 0 ? M : 1) + 64);
 }
+
+template <typename T>
+__global__ void k_fill_ones(T* __restrict__ ones, int m) {  // ones[i][0] = 1, [1..3] = 0
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 4 * m; i += gridDim.x * blockDim.x)
+    ones[i] = (i & 3) == 0 ? T(1) : T(0);
+}
+
+template <typename T>
+cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s);  // force.cu
 
 // actual number of K splits after rounding the chunk to the engine's K step
 inline int real_splits(int K, int splits, int kstep) {
@@ -258,8 +268,15 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
     if (use_tc<T>()) {
       // tensor cores: C^T[Kt][N] = [X | 1]^T dY -- the wide operand X is read
       // once (one column tile), no half-empty 128-row tiles for N = H
+      // the bias gradient rides in the GEMM as one more A row: a ones vector
+      // [M][4] (column 0 = 1) that TMA loads as a third segment
       const int splits = tc::splits_for(Kt, N, M);
       Cols2Ld<T> a{X1, ld1, K1, X2, ld2, K2};
+      if (with_bias) {
+        T* ones = ws + (((size_t)splits * N * Kt + 63) & ~(size_t)63);
+        k_fill_ones<T><<<grid_1d(4LL * M), 256, 0, s>>>(ones, M);
+        a.ones = ones;
+      }
       ColsLd<T> b{dY, ldd};
       tc::TcEpiPartial epi{ws, (long long)N * Kt, Kt, N};
       e = tc::launch(Kt, nullptr, N, M, M_dev, splits, tc_split3(), a, b, epi, s);

@@ -28,12 +28,23 @@
 // thread) for column half w/4, 16 columns per tcgen05.ld.32x32b.x16.
 #pragma once
 
+#include <cuda.h>
+
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
+#include "gemm_simt.cuh"
 
 namespace gfm {
 namespace tc {
+
+// GFM_NO_TMA=1 forces the thread-staged (cp.async) engine (debug / A-B runs)
+inline bool tma_disabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("GFM_NO_TMA") ? atoi(getenv("GFM_NO_TMA")) : 0;
+  return v != 0;
+}
 
 constexpr int kBM = 128;       // MMA M (cta_group::1)
 constexpr int kBK = 32;        // fp32 elements per 128-byte swizzle row
@@ -497,11 +508,350 @@ __global__ void __launch_bounds__(kWSThreads, 1)
   if (warp == 0) tmem_free<NC>(tmem);
 }
 
+// ============================================================== TMA engine
+// Host-built operand: up to two 2D fp32 segments.  K-major (mn = 0): rows x K
+// with K contiguous, segments concatenated along K (split at k = split_at),
+// box {32 k, ROWS rows}, SWIZZLE_128B == the K-major smem layout above.
+// MN-major (mn = 1): memory X[k][row], segments concatenated along rows
+// (split at row = split_at), box {32 rows, 32 k} per 32-row atom, swizzle
+// 128B_ATOM_32B == SWIZZLE_128B_BASE32B with LBO = 4096 (atom), SBO = 512.
+struct TmaOp {
+  CUtensorMap map[3];
+  int split_at;  // start of segment 1
+  int split2;    // start of segment 2 (MN-major: the ones row of a bias gradient)
+  int mn;
+};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+
+// 2D fp32 map: inner (contiguous) extent x outer extent, row stride ld elems
+inline bool make_map(CUtensorMap* m, const float* base, long long inner, long long outer, long long ld,
+                     int box_inner, int box_outer, CUtensorMapSwizzle sw) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || !base || inner <= 0 || outer <= 0) return false;
+  if (((uintptr_t)base & 15) || ((ld * 4) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Loader -> TMA operand (false when the loader cannot be expressed)
+template <class L>
+inline bool build_tma(const L&, TmaOp*, int, long long, int) { return false; }
+
+template <typename T>
+inline bool build_tma(const RowsLd<T>& l, TmaOp* op, int rows_box, long long rows_total, int K) {
+  if (sizeof(T) != 4) return false;
+  op->mn = 0;
+  op->split_at = 1 << 30;
+  op->split2 = 1 << 30;
+  return make_map(&op->map[0], (const float*)l.p, K, rows_total, l.ld, kBK, rows_box,
+                  CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+template <typename T>
+inline bool build_tma(const Rows2Ld<T>& l, TmaOp* op, int rows_box, long long rows_total, int K) {
+  if (sizeof(T) != 4 || K > l.k1 + l.k2) return false;
+  op->mn = 0;
+  op->split_at = l.k2 > 0 ? l.k1 : (1 << 30);
+  op->split2 = 1 << 30;
+  if (l.k2 > 0 && l.k1 % kBK) return false;
+  if (!make_map(&op->map[0], (const float*)l.p1, l.k1, rows_total, l.ld1, kBK, rows_box,
+                CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
+  return l.k2 == 0 || make_map(&op->map[1], (const float*)l.p2, l.k2, rows_total, l.ld2, kBK,
+                               rows_box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+template <typename T>
+inline bool build_tma(const ColsLd<T>& l, TmaOp* op, int, long long rows_total, int K) {
+  if (sizeof(T) != 4) return false;
+  op->mn = 1;
+  op->split_at = 1 << 30;
+  op->split2 = 1 << 30;
+  return make_map(&op->map[0], (const float*)l.p, rows_total, K, l.ld, 32, kBK,
+                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
+template <typename T>
+inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int, long long rows_total, int K) {
+  // the virtual ones row (bias) needs the caller's ones buffer (a [K][4]
+  // tensor whose column 0 is 1: inner extent 1, the rest of each 32-row box
+  // is TMA zero fill)
+  const bool bias = rows_total == l.n1 + l.n2 + 1;
+  if (sizeof(T) != 4 || (rows_total > l.n1 + l.n2 && !(bias && l.ones))) return false;
+  if ((l.n2 > 0 && l.n1 % 32) || (bias && (l.n1 + l.n2) % 32)) return false;
+  op->mn = 1;
+  op->split_at = l.n2 > 0 ? l.n1 : (bias ? l.n1 : (1 << 30));
+  op->split2 = bias ? l.n1 + l.n2 : (1 << 30);
+  if (!make_map(&op->map[0], (const float*)l.p1, l.n1, K, l.ld1, 32, kBK,
+                CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return false;
+  if (l.n2 > 0 && !make_map(&op->map[1], (const float*)l.p2, l.n2, K, l.ld2, 32, kBK,
+                            CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return false;
+  if (bias && !make_map(&op->map[2], (const float*)l.ones, 1, K, 4, 32, kBK,
+                        CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return false;
+  if (bias && l.n2 == 0) op->map[1] = op->map[2];  // segment 1 empty: route to the ones map
+  return true;
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+
+// load one k-block of an operand (ROWS rows starting at r0, k from k0)
+template <int ROWS>
+__device__ __forceinline__ void tma_tile(const TmaOp& op, uint32_t dst, int r0, int k0, uint64_t* bar) {
+  if (op.mn == 0) {
+    const int seg = k0 >= op.split_at;
+    tma_load_2d(dst, &op.map[seg], seg ? k0 - op.split_at : k0, r0, bar);
+  } else {
+#pragma unroll
+    for (int at = 0; at < ROWS / 32; ++at) {
+      const int ra = r0 + at * 32;
+      const int seg = ra >= op.split2 ? 2 : (ra >= op.split_at ? 1 : 0);
+      const int c0 = seg == 2 ? ra - op.split2 : (seg == 1 ? ra - op.split_at : ra);
+      tma_load_2d(dst + at * 4096, &op.map[seg], c0, k0, bar);
+    }
+  }
+}
+
+template <int BN>
+struct SmemT {
+  static constexpr int kA = kBM * 128;
+  static constexpr int kB = BN * 128;
+  static constexpr int kRaw = kA + kB;
+  static constexpr int kStage = 2 * kRaw;  // raw (= hi) + lo
+  static constexpr int kS = BN >= 128 ? 3 : BN >= 64 ? 4 : 5;
+  static constexpr int kBytes = kS * kStage + 1024 + 512;
+};
+
+constexpr int kConvWarps = 8;
+constexpr int kTmaThreads = (1 + kConvWarps + 1 + 4) * 32;  // TMA, converters, MMA, epilogue
+
+template <int BN, class Epi>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    tc_gemm_tma_kernel(int M, const int* __restrict__ M_dev, int N, int K, int k_chunk, int splits,
+                       int split3, const __grid_constant__ TmaOp ta,
+                       const __grid_constant__ TmaOp tb, Epi epi) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  using S = SmemT<BN>;
+  constexpr int NC = tmem_cols(2 * BN);
+  constexpr int kS = S::kS;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* tfl = reinterpret_cast<uint64_t*>(base + kS * S::kStage);  // TMA landed [kS]
+  uint64_t* cvt = tfl + kS;     // lo written [kS]
+  uint64_t* empty = cvt + kS;   // MMAs done with the stage [kS]
+  uint64_t* tfull = empty + kS; // accumulator ready [2]
+  uint64_t* tempty = tfull + 2; // accumulator drained [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int m_total = M_dev ? *M_dev : M;
+  const int m_tiles = (m_total + kBM - 1) / kBM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int n_work = m_tiles * n_tiles * splits;
+  if ((int)blockIdx.x >= n_work) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool split_on = split3 != 0;
+  constexpr int kMmaWarp = 1 + kConvWarps, kEpiWarp0 = kMmaWarp + 1;
+
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kS; ++q) {
+      mbar_init(&tfl[q], 1);
+      mbar_init(&cvt[q], kConvWarps);
+      mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&tfull[q], 1);
+      mbar_init(&tempty[q], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&ta.map[0]) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tb.map[0]) : "memory");
+  }
+  if (warp == 0) tmem_alloc<NC>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto tile_of = [&](int w, int& bm, int& bn, int& split) {
+    split = w % splits;
+    bn = (w / splits) % n_tiles;
+    bm = w / (splits * n_tiles);
+  };
+  auto nkb_of = [&](int w) { return item_nkb(w, splits, k_chunk, K); };
+
+  if (warp == 0) {
+    // ============================================================ TMA producer
+    if (lane == 0) {
+      int p = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        int bm, bn, split;
+        tile_of(w, bm, bn, split);
+        const int nkb = nkb_of(w);
+        for (int kb = 0; kb < nkb; ++kb, ++p) {
+          const int s = p % kS;
+          if (p >= kS) mbar_wait(&empty[s], ((p / kS) - 1) & 1);
+          const int k0 = split * k_chunk + kb * kBK;
+          const uint32_t st = smem_u32(base + s * S::kStage);
+          mbar_expect_tx(&tfl[s], S::kRaw);
+          tma_tile<kBM>(ta, st, bm * kBM, k0, &tfl[s]);
+          tma_tile<BN>(tb, st + S::kA, bn * BN, k0, &tfl[s]);
+        }
+      }
+    }
+  } else if (warp <= kConvWarps) {
+    // ============================================================ lo converters
+    if (split_on) {
+      const int ctid = threadIdx.x - 32;
+      int q = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int nkb = nkb_of(w);
+        for (int kb = 0; kb < nkb; ++kb, ++q) {
+          const int s = q % kS;
+          mbar_wait(&tfl[s], (q / kS) & 1);
+          uint8_t* st = base + s * S::kStage;
+          make_lo<S::kRaw, kConvWarps * 32>(st, st + S::kRaw, ctid);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&cvt[s])) : "memory");
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ============================================================ MMA issuer
+    const bool a_mn = ta.mn != 0, b_mn = tb.mn != 0;
+    const uint32_t idesc = make_idesc_tf32(BN, a_mn, b_mn);
+    auto desc = [&](bool mn, uint32_t addr, int ks) -> uint64_t {
+      return mn ? make_desc_mn(addr + ks * 1024, 4096, 512) : make_desc(addr + ks * 32);
+    };
+    int q = 0, t = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
+      const int nkb = nkb_of(w);
+      const int acc = t & 1;
+      if (t >= 2) mbar_wait(&tempty[acc], ((t >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < nkb; ++kb, ++q) {
+        const int s = q % kS;
+        if (split_on)
+          mbar_wait(&cvt[s], (q / kS) & 1);
+        else
+          mbar_wait(&tfl[s], (q / kS) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ah = smem_u32(base + s * S::kStage), bh = ah + S::kA;
+          const uint32_t al = ah + S::kRaw, bl = al + S::kA;
+#pragma unroll
+          for (int ks = 0; ks < kBK / 8; ++ks) {
+            const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
+            if (split_on) {
+              mma_tf32(d, desc(a_mn, al, ks), desc(b_mn, bh, ks), idesc, acc0);
+              mma_tf32(d, desc(a_mn, ah, ks), desc(b_mn, bl, ks), idesc, 1u);
+              mma_tf32(d, desc(a_mn, ah, ks), desc(b_mn, bh, ks), idesc, 1u);
+            } else {
+              mma_tf32(d, desc(a_mn, ah, ks), desc(b_mn, bh, ks), idesc, acc0);
+            }
+          }
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (nkb > 0)
+          mma_commit(&tfull[acc]);
+        else
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tfull[acc])) : "memory");
+      }
+      __syncwarp();
+    }
+  } else {
+    // ============================================================ epilogue
+    const int quarter = warp & 3;
+    int t = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
+      int bm, bn, split;
+      tile_of(w, bm, bn, split);
+      const int nkb = nkb_of(w);
+      const int acc = t & 1;
+      mbar_wait(&tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const int m0 = bm * kBM, n0 = bn * BN;
+      const int row = quarter * 32 + lane;
+      const int m = m0 + row;
+      const bool valid = row < min(kBM, m_total - m0);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        if (nkb > 0) {
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        epi.chunk(m, valid, n0 + c, v, min(16, N - (n0 + c)), split);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[acc])) : "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<NC>(tmem);
+}
+
 template <int BN, class AL, class BL, class Epi>
 inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K_dev, int splits,
                              int split3, AL a, BL b, Epi epi, cudaStream_t s) {
   int k_chunk = ceil_div(ceil_div(K > 0 ? K : 1, splits), kBK) * kBK;
   splits = ceil_div(K > 0 ? K : 1, k_chunk);
+  const long long work = (long long)ceil_div(M, kBM) * ceil_div(N, BN) * splits;
+  const int grid = (int)std::min<long long>(work, 148LL);
+  if (!K_dev && !tma_disabled()) {
+    TmaOp ta, tb;
+    if (build_tma(a, &ta, kBM, M, K) && build_tma(b, &tb, BN, N, K)) {
+      auto kern = tc_gemm_tma_kernel<BN, Epi>;
+      const int smem = SmemT<BN>::kBytes;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kTmaThreads, smem, s>>>(M, M_dev, N, K, k_chunk, splits, split3, ta, tb, epi);
+      return cudaGetLastError();
+    }
+  }
   const int smem = Smem<BN>::kBytes;
   const bool va = a.vec_ok(K), vb = b.vec_ok(K);
   auto kern = va ? (vb ? tc_gemm_kernel<BN, true, true, AL, BL, Epi>
@@ -510,8 +860,6 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
                        : tc_gemm_kernel<BN, false, false, AL, BL, Epi>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const long long work = (long long)ceil_div(M, kBM) * ceil_div(N, BN) * splits;
-  const int grid = (int)std::min<long long>(work, 148LL);
   kern<<<grid, kWSThreads, smem, s>>>(M, M_dev, N, K, K_dev, k_chunk, splits, split3, a, b, epi);
   return cudaGetLastError();
 }

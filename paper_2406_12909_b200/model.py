@@ -113,25 +113,73 @@ def _device(device=None) -> torch.device:
     return torch.device(device)
 
 
-class ModelParams:
-    """All weights as one flat device tensor with named views.
+class ParamLayout:
+    """Device layout of the flat parameter vector: the reference's order
+    (model.py:120-132) with every array starting on a 16-byte boundary (so
+    each weight view is a TMA-loadable tensor).  ``P`` = reference length,
+    ``Pp`` = padded device length; padding entries stay exactly 0 (zero
+    gradient, zero Adam update)."""
 
-    The flat order is the reference's (embedding; per layer W, U, b; per head
-    layer A, c; force V, c, u), so ``flatten``/``from_flat`` round-trip
-    bit-exactly with ``gfmkit.model.ModelParams`` (float64 storage)."""
-
-    def __init__(self, config: ModelConfig, flat: torch.Tensor):
-        if flat.dim() != 1 or flat.shape[0] != count_params(config):
-            raise ValidationError(
-                f"flat vector has {tuple(flat.shape)}, model needs ({count_params(config)},)")
-        self.config = config
-        self.flat = flat
-        self._views = {}
+    def __init__(self, config: ModelConfig):
+        self.entries = []
         off = 0
         for name, shape in param_shapes(config):
             size = int(np.prod(shape))
-            self._views[name] = flat[off:off + size].view(shape)
-            off += size
+            self.entries.append((name, tuple(shape), off, size))
+            off += (size + 3) & ~3
+        self.Pp = off
+        self.P = count_params(config)
+        self.index_np = np.concatenate([np.arange(o, o + n) for _, _, o, n in self.entries])
+        self._index = {}
+
+    def index(self, device) -> torch.Tensor:
+        key = str(device)
+        if key not in self._index:
+            self._index[key] = torch.as_tensor(self.index_np, device=device)
+        return self._index[key]
+
+    def compact(self, padded: torch.Tensor) -> torch.Tensor:
+        """padded device vector -> reference-order flat vector"""
+        return padded[self.index(padded.device)]
+
+    def pad(self, flat, device, dtype) -> torch.Tensor:
+        """reference-order flat vector (numpy or tensor) -> padded device vector"""
+        t = flat.detach() if isinstance(flat, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(flat, dtype=np.float64))
+        if t.dim() != 1 or t.shape[0] != self.P:
+            raise ValidationError(f"flat vector has {tuple(t.shape)}, model needs ({self.P},)")
+        out = torch.zeros(self.Pp, dtype=dtype, device=device)
+        out[self.index(device)] = t.to(device=device, dtype=dtype)
+        return out
+
+
+_LAYOUTS: dict = {}
+
+
+def param_layout(config: ModelConfig) -> ParamLayout:
+    key = tuple(sorted(config.to_dict().items()))
+    if key not in _LAYOUTS:
+        _LAYOUTS[key] = ParamLayout(config)
+    return _LAYOUTS[key]
+
+
+class ModelParams:
+    """All weights as one padded device tensor with named views.
+
+    The element order is the reference's (embedding; per layer W, U, b; per
+    head layer A, c; force V, c, u); ``flatten``/``from_flat`` convert to and
+    from the reference's float64 flat vector bit-exactly (float64 storage)."""
+
+    def __init__(self, config: ModelConfig, flat: torch.Tensor):
+        lay = param_layout(config)
+        if flat.dim() != 1 or flat.shape[0] != lay.Pp:
+            raise ValidationError(
+                f"device parameter vector has {tuple(flat.shape)}, layout needs ({lay.Pp},)")
+        self.config = config
+        self.layout = lay
+        self.flat = flat
+        self._views = {name: flat[off:off + size].view(shape)
+                       for name, shape, off, size in lay.entries}
 
     # reference attribute names ------------------------------------------
     @property
@@ -179,32 +227,30 @@ class ModelParams:
 
     @property
     def n_params(self) -> int:
-        return int(self.flat.shape[0])
+        return self.layout.P
 
     @property
     def dtype(self):
         return self.flat.dtype
 
     def flatten(self) -> np.ndarray:
-        return self.flat.detach().to("cpu", torch.float64).numpy().copy()
+        return self.layout.compact(self.flat.detach()).to("cpu", torch.float64).numpy().copy()
 
     @classmethod
     def zeros(cls, config: ModelConfig, device=None, dtype=torch.float32) -> "ModelParams":
-        return cls(config, torch.zeros(count_params(config), dtype=dtype, device=_device(device)))
+        lay = param_layout(config)
+        return cls(config, torch.zeros(lay.Pp, dtype=dtype, device=_device(device)))
 
     @classmethod
     def from_flat(cls, config: ModelConfig, flat, device=None, dtype=None) -> "ModelParams":
+        lay = param_layout(config)
         if isinstance(flat, torch.Tensor):
-            t = flat.detach()
-            dtype = dtype or (t.dtype if t.is_floating_point() else torch.float32)
-            t = t.to(device=_device(device) if device or not t.is_cuda else t.device, dtype=dtype)
+            dev = _device(device) if device or not flat.is_cuda else flat.device
+            dtype = dtype or (flat.dtype if flat.is_floating_point() else torch.float32)
         else:
-            arr = np.asarray(flat, dtype=np.float64)
-            if arr.ndim != 1 or arr.shape[0] != count_params(config):
-                raise ValidationError(
-                    f"flat vector has {arr.shape}, model needs ({count_params(config)},)")
-            t = torch.from_numpy(arr.copy()).to(device=_device(device), dtype=dtype or torch.float32)
-        return cls(config, t.contiguous().clone())
+            dev = _device(device)
+            dtype = dtype or torch.float32
+        return cls(config, lay.pad(flat, dev, dtype))
 
 
 def init_params_flat(config: ModelConfig, seed: int = 0) -> np.ndarray:
@@ -644,7 +690,7 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     vals, de, df = _loss_kernel(e_pred, f_pred, batch.energy_true, batch.forces_true,
                                 batch.n_per_graph, cfg.alpha_energy, cfg.alpha_forces,
                                 scratch=sc, contrib=contrib)
-    grad = grad_out if grad_out is not None else torch.empty(params.n_params, dtype=dt,
+    grad = grad_out if grad_out is not None else torch.zeros(params.layout.Pp, dtype=dt,
                                                              device=batch.device)
     gp = ModelParams(cfg, grad)
 
@@ -709,7 +755,9 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     e_true, n_per = batch.energy_true, batch.n_per_graph
     lb = LossBreakdown(vals if scratch is not None else vals.clone(),
                        lambda: (e_pred - e_true) / n_per.to(e_pred.dtype))
-    return lb, grad
+    # API callers get the reference-order flat gradient; grad_out callers
+    # (the trainer) keep the padded device layout
+    return lb, (grad if grad_out is not None else params.layout.compact(grad))
 
 
 def backward(params: ModelParams, batch_or_records):

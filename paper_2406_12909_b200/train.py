@@ -26,7 +26,7 @@ from . import _lib
 from ._lib import call, ptr, stream_handle
 from .comm import Comm, LocalComm
 from .errors import ConfigError, ValidationError
-from .model import (ModelConfig, ModelParams, _Scratch, count_params, forward_batch,
+from .model import (ModelConfig, ModelParams, _Scratch, count_params, forward_batch, param_layout,
                     init_params_flat, loss_and_grad, make_batch)
 from .schedule import epoch_schedule
 from .telemetry import PhaseClock
@@ -177,7 +177,11 @@ class DataParallelTrainer:
             "cuda", torch.cuda.current_device())
         self.dtype = dtype
         self.flags = flags
-        P = count_params(model_config)
+        # device buffers use the padded parameter layout (16-byte aligned
+        # arrays); P is the padded length, the allreduce payload is
+        # [grad (P) | loss | 1]
+        self.layout = param_layout(model_config)
+        P = self.layout.Pp
         self.P = P
         if initial is None:
             flat = init_params_flat(model_config, self.tcfg.base_seed)
@@ -185,7 +189,7 @@ class DataParallelTrainer:
             flat = initial.flatten()
         else:
             flat = np.asarray(initial, np.float64)
-        self.master = torch.as_tensor(flat, dtype=torch.float64, device=self.device).clone()
+        self.master = self.layout.pad(flat, self.device, torch.float64)
         self.m = torch.zeros_like(self.master)
         self.v = torch.zeros_like(self.master)
         self.t_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
@@ -247,6 +251,14 @@ class DataParallelTrainer:
 
     def current_params(self) -> ModelParams:
         return ModelParams(self.cfg, self.master.clone())
+
+    def flat_master(self) -> np.ndarray:
+        """float64 master parameters in the reference's flat order"""
+        return self.layout.compact(self.master).cpu().numpy()
+
+    def flat_grad(self) -> np.ndarray:
+        """last step's (summed) gradient in the reference's flat order"""
+        return self.layout.compact(self.contrib[:self.P]).to(torch.float64).cpu().numpy()
 
 
 class StructureStepRunner:
