@@ -164,9 +164,12 @@ GFM_API int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_
                    const void* f_pred, const void* f_true, int n_nodes, double alpha_e,
                    double alpha_f, void* loss, void* de, void* df, float* contrib,
                    void* workspace, int dtype, void* stream);
-/* ds_i = de[g(i)]; dz = (ds_i a) * (1 - y^2)  (model.py:521-529) */
+/* ds_i = de[g(i)]; dz = (ds_i a) * (1 - y^2)  (model.py:521-529).
+ * ds is written as an [n_nodes][ld_ds] row-major column vector (column 0 =
+ * ds, columns 1..ld_ds-1 = 0) so ld_ds = 4 keeps rows 16-byte aligned for the
+ * TMA-fed weight-gradient GEMM that consumes it. */
 GFM_API int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const void* a,
-                    const void* y, void* ds, void* dz, int dtype, void* stream);
+                    const void* y, void* ds, int ld_ds, void* dz, int dtype, void* stream);
 
 /* ---- K12: embedding gradient (model.py:564) --------------------------- */
 /* grad[118][H] = onehot(z - 1)^T dh as a split-K GEMM (one-hot generated on

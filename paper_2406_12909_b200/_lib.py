@@ -65,7 +65,7 @@ SIGNATURES = {
     "gfm_energy_readout": (_I, [_P, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P]),
     "gfm_loss_workspace_bytes": (_S, []),
     "gfm_loss_seeds": (_I, [_P, _P, _P, _I, _P, _P, _I, _D, _D, _P, _P, _P, _P, _P, _I, _P]),
-    "gfm_energy_seed": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _I, _P]),
+    "gfm_energy_seed": (_I, [_P, _P, _I, _I, _P, _P, _P, _I, _P, _I, _P]),
     "gfm_embedding_grad_workspace_bytes": (_S, [_I, _I, _I]),
     "gfm_embedding_grad": (_I, [_P, _I, _P, _I, _P, _P, _I, _P]),
     "gfm_nonfinite_flag": (_I, [_P, _L, _I, _P, _P]),

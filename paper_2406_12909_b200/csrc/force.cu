@@ -289,20 +289,25 @@ __global__ void k_force_bwd_src_scalar(const T* __restrict__ P, int n, int H, co
 // (blockIdx.y * cw + t % cw) and rows r = t / cw, + 256 / cw, ... of the chunk
 // (coalesced row segments); the 256 / cw row-group sums are combined in a
 // fixed order in shared memory.
-constexpr int kColChunk = 512;
+constexpr int kColChunk = 128;
 template <typename T>
 __global__ void __launch_bounds__(256)
-    k_colsum_partial(const T* __restrict__ X, int n, int H, T* __restrict__ part) {
+    k_colsum_partial(const T* __restrict__ X, int n, int H, int chunk, int cw, T* __restrict__ part) {
+  // block (ch, cb): rows [ch*chunk, ch*chunk+chunk) x columns [cb*cw, cb*cw+cw);
+  // 256/cw row groups stride the rows, then a fixed-order smem combine, so the
+  // result depends only on (n, H, chunk, cw) -- deterministic
   __shared__ double red[256];
-  const int cw = H < 64 ? H : 64;  // columns per block
   const int groups = 256 / cw;
   const int ch = blockIdx.x;
-  const int lo = ch * kColChunk, hi = min(n, lo + kColChunk);
+  const long long lo = (long long)ch * chunk;
+  const long long hi = min((long long)n, lo + chunk);
   const int c = blockIdx.y * cw + threadIdx.x % cw;
   const int g = threadIdx.x / cw;
   double s = 0.0;
-  if (g < groups && c < H)
-    for (int i = lo + g; i < hi; i += groups) s += (double)X[(long long)i * H + c];
+  if (g < groups && c < H) {
+#pragma unroll 8  // independent loads in flight; the adds stay in row order
+    for (long long i = lo + g; i < hi; i += groups) s += (double)X[i * H + c];
+  }
   red[threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.x < cw && c < H) {
@@ -313,20 +318,18 @@ __global__ void __launch_bounds__(256)
 }
 
 template <typename T>
-__global__ void k_colsum_final(const T* __restrict__ part, int nch, int H, T* __restrict__ out) {
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < H; k += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int ch = 0; ch < nch; ++ch) s += (double)part[(long long)ch * H + k];
-    out[k] = (T)s;
-  }
-}
-
-template <typename T>
 cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s) {
-  const int nch = ceil_div(n > 0 ? n : 1, kColChunk);
-  dim3 g1(nch, ceil_div(H, H < 64 ? H : 64));
-  if (n > 0) k_colsum_partial<T><<<g1, 256, 0, s>>>(X, n, H, part);
-  k_colsum_final<T><<<ceil_div(H, 256), 256, 0, s>>>(part, n > 0 ? nch : 0, H, out);
+  if (H <= 0) return cudaSuccess;
+  const int cw = H < 64 ? H : 64;
+  if (n <= 0) {
+    cudaMemsetAsync(out, 0, sizeof(T) * H, s);
+    return cudaGetLastError();
+  }
+  const int nch = ceil_div(n, kColChunk);
+  k_colsum_partial<T><<<dim3(nch, ceil_div(H, cw)), 256, 0, s>>>(X, n, H, kColChunk, cw, part);
+  // second level: the nch partial rows, one block per column slab
+  const int cw2 = H < 32 ? H : 32;
+  k_colsum_partial<T><<<dim3(1, ceil_div(H, cw2)), 256, 0, s>>>(part, nch, H, nch, cw2, out);
   return cudaGetLastError();
 }
 

@@ -38,8 +38,10 @@ __global__ void __launch_bounds__(256)
   for (long long base = (long long)blockIdx.x * 32; base < total; base += (long long)gridDim.x * 32) {
     const long long idx = base + tx;
     double acc = 0.0;
-    if (idx < total)
+    if (idx < total) {
+#pragma unroll 8  // loads in flight; adds in split order
       for (int k = ty; k < splits; k += 8) acc += (double)ws[(long long)k * total + idx];
+    }
     red[ty][tx] = acc;
     __syncthreads();
     double a = 0.0;
@@ -158,13 +160,16 @@ __global__ void __launch_bounds__(256)
 template <typename T>
 __global__ void k_energy_seed(const T* __restrict__ de, const int* __restrict__ gnode, int n,
                               int G, const T* __restrict__ a, const T* __restrict__ y,
-                              T* __restrict__ ds, T* __restrict__ dz) {
+                              T* __restrict__ ds, int ld_ds, T* __restrict__ dz) {
   const long long total = (long long)n * G;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx / G), g = (int)(idx % G);
     const T s = de[gnode[i]];
-    if (g == 0) ds[i] = s;
+    if (g == 0) {
+      ds[(long long)i * ld_ds] = s;
+      for (int j = 1; j < ld_ds; ++j) ds[(long long)i * ld_ds + j] = T(0);
+    }
     const T yy = y[idx];
     dz[idx] = mul_rn(mul_rn(s, a[g]), sub_rn(T(1), mul_rn(yy, yy)));
   }
@@ -326,7 +331,7 @@ cudaError_t force_fwd_t(const T* h, int H, int n, const int* rowptr, const int* 
 template <typename T>
 size_t force_bwd_ws(int H, int n) {
   const size_t nh = (size_t)(n > 0 ? n : 1) * H;
-  const size_t parts = (size_t)ceil_div(n > 0 ? n : 1, 512) * H;
+  const size_t parts = (size_t)ceil_div(n > 0 ? n : 1, 128) * H;  // colsum chunk partials
   return sizeof(T) * (3 * nh + parts + 64) + linear_bwd_weight_ws<T>(n, H, H, 0, 0) + 4096;
 }
 
@@ -341,7 +346,7 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
   T* TU = Ddst + nh;
   T* S = TU + nh;
   T* part = S + nh;
-  T* wws = part + (size_t)ceil_div(n > 0 ? n : 1, 512) * H + 64;
+  T* wws = part + (size_t)ceil_div(n > 0 ? n : 1, 128) * H + 64;
   wws = (T*)(((uintptr_t)wws + 255) & ~(uintptr_t)255);
   cudaError_t e = force_bwd_edges<T>(P, n, H, rowptr, col_src, csc_ptr, csc_eid, csc_dst, dx, df,
                                      c, u, Ddst, TU, S, flags, s);
@@ -498,11 +503,13 @@ int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_per, int
 }
 
 int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const void* a,
-                    const void* y, void* ds, void* dz, int dtype, void* stream) {
+                    const void* y, void* ds, int ld_ds, void* dz, int dtype, void* stream) {
+  if (ld_ds < 1) return GFM_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   GFM_DISPATCH(dtype, "gfm_energy_seed",
                (k_energy_seed<T><<<grid_1d((long long)n_nodes * G), 256, 0, s>>>(
-                    (const T*)de, gnode, n_nodes, G, (const T*)a, (const T*)y, (T*)ds, (T*)dz),
+                    (const T*)de, gnode, n_nodes, G, (const T*)a, (const T*)y, (T*)ds, ld_ds,
+                    (T*)dz),
                 cudaGetLastError()))
 }
 

@@ -702,11 +702,13 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
 
     # energy head (model.py:520-533)
     ys = cache["head_inputs"]
-    ds = sc.get("ds", (max(N, 1),), dt)
+    # ds as an [N][4] column (cols 1..3 zero) so its rows are 16B aligned and
+    # the weight-gradient GEMM below can stream it with TMA
+    ds = sc.get("ds", (max(N, 1), 4), dt)
     dz = sc.get("dz_head", (N, G), dt)
     call("gfm_energy_seed", ptr(de), ptr(batch.graph_of_node), N, G,
-         ptr(params.view(f"head_{F - 1}.w")), ptr(ys[F - 1]), ptr(ds), ptr(dz), code, s)
-    wgrad(ds, 1, 1, ys[F - 1], G, G, None, 0, 0, gp.view(f"head_{F - 1}.w"), None,
+         ptr(params.view(f"head_{F - 1}.w")), ptr(ys[F - 1]), ptr(ds), 4, ptr(dz), code, s)
+    wgrad(ds, 4, 1, ys[F - 1], G, G, None, 0, 0, gp.view(f"head_{F - 1}.w"), None,
           gp.view(f"head_{F - 1}.b"))
     dh_e = sc.get("dh_energy", (N, H), dt)
     for f in range(F - 2, -1, -1):
