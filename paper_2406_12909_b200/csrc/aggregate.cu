@@ -126,6 +126,9 @@ __global__ void __launch_bounds__(256)
   const int sub = lane % LPN;
   const int node = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
   if (node >= n_nodes) return;
+  // blockIdx.y selects a slab of NV*LPN float4 columns (wide H uses several
+  // slabs instead of more registers per lane: occupancy hides gather latency)
+  const int cb = blockIdx.y * (NV * LPN) + sub;
   const AggLayout L = agg_layout(parts, H);
   const bool need_s = L.o_sum >= 0 || L.o_mean >= 0 || L.o_std >= 0;
   const bool need_q = L.o_std >= 0;
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < NV; ++v) r[u][v] = __ldg(h4 + (long long)sj[u] * H4 + v * LPN + sub);
+      for (int v = 0; v < NV; ++v) r[u][v] = __ldg(h4 + (long long)sj[u] * H4 + v * LPN + cb);
 #pragma unroll
     for (int u = 0; u < 4; ++u) consume(r[u], ww[u], p + u);
   }
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(256)
     const float ww = __ldg(w + p);
     float4 r[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) r[v] = __ldg(h4 + (long long)sj * H4 + v * LPN + sub);
+    for (int v = 0; v < NV; ++v) r[v] = __ldg(h4 + (long long)sj * H4 + v * LPN + cb);
     consume(r, ww, p);
   }
   const int deg = end - beg;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(256)
   float4* out4 = reinterpret_cast<float4*>(agg + (long long)node * L.K * H);
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const int c4 = v * LPN + sub;
+    const int c4 = v * LPN + cb;
     float4 mean = make_float4(s[v].x * inv, s[v].y * inv, s[v].z * inv, s[v].w * inv);
     if (L.o_sum >= 0) out4[(L.o_sum >> 2) + c4] = s[v];
     if (L.o_mean >= 0) out4[(L.o_mean >> 2) + c4] = mean;
@@ -349,43 +352,76 @@ __global__ void __launch_bounds__(256)
   const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
   if (j >= n_nodes) return;
   const int H4 = H >> 2;
+  const int cb = blockIdx.y * (NV * LPN) + sub;  // column slab (see k_agg_fwd_vec)
   float4 acc[NV], hj[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const long long o = (long long)j * H4 + v * LPN + sub;
+    const long long o = (long long)j * H4 + v * LPN + cb;
     acc[v] = reinterpret_cast<const float4*>(dh)[o];
     hj[v] = coef ? reinterpret_cast<const float4*>(h_in)[o] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int qb = csc_ptr[j], qe = csc_ptr[j + 1];
-  for (int q = qb; q < qe; ++q) {
-    const int p = __ldg(csc_eid + q), i = __ldg(csc_dst + q);
-    const float ww = __ldg(w + p);
+  // U CSC slots per batch: all their row loads issue before the (in-order)
+  // accumulation, so U x 3 gathers per lane are in flight
+  constexpr int U = 2;
+  for (int q = qb; q < qe; q += U) {
+    int p[U], i[U];
+    float ww[U];
+    float4 g[U][NV], cf[U][NV];
+    int4 a[U][NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int c4 = v * LPN + sub;
-      float4 dm = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (G) dm = __ldg(reinterpret_cast<const float4*>(G + (long long)i * ldg) + c4);
-      if (coef) {
-        const float4 cf = __ldg(reinterpret_cast<const float4*>(coef + (long long)i * H) + c4);
-        dm.x += cf.x * (hj[v].x * ww); dm.y += cf.y * (hj[v].y * ww);
-        dm.z += cf.z * (hj[v].z * ww); dm.w += cf.w * (hj[v].w * ww);
+    for (int u = 0; u < U; ++u) {
+      const bool ok = q + u < qe;
+      p[u] = ok ? __ldg(csc_eid + q + u) : -2;
+      i[u] = ok ? __ldg(csc_dst + q + u) : 0;
+      ww[u] = ok ? __ldg(w + p[u]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int c4 = v * LPN + cb;
+        const bool ok = q + u < qe;
+        g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        cf[u][v] = g[u][v];
+        a[u][v] = make_int4(-1, -1, -1, -1);
+        if (ok && G) g[u][v] = __ldg(reinterpret_cast<const float4*>(G + (long long)i[u] * ldg) + c4);
+        if (ok && coef)
+          cf[u][v] = __ldg(reinterpret_cast<const float4*>(coef + (long long)i[u] * H) + c4);
+        if (ok && argmax)
+          a[u][v] = __ldg(reinterpret_cast<const int4*>(argmax + (long long)i[u] * H) + c4);
       }
-      if (argmax) {
-        const int4 a = __ldg(reinterpret_cast<const int4*>(argmax + (long long)i * H) + c4);
-        if (a.x == p || a.y == p || a.z == p || a.w == p) {
-          const float4 d = __ldg(reinterpret_cast<const float4*>(dmax + (long long)i * ldm) + c4);
-          if (a.x == p) dm.x += d.x;
-          if (a.y == p) dm.y += d.y;
-          if (a.z == p) dm.z += d.z;
-          if (a.w == p) dm.w += d.w;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (q + u >= qe) break;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int c4 = v * LPN + cb;
+        float4 dm = g[u][v];
+        if (coef) {
+          dm.x += cf[u][v].x * (hj[v].x * ww[u]); dm.y += cf[u][v].y * (hj[v].y * ww[u]);
+          dm.z += cf[u][v].z * (hj[v].z * ww[u]); dm.w += cf[u][v].w * (hj[v].w * ww[u]);
         }
+        if (argmax) {
+          const int4 am = a[u][v];
+          const int pp = p[u];
+          if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
+            const float4 d =
+                __ldg(reinterpret_cast<const float4*>(dmax + (long long)i[u] * ldm) + c4);
+            if (am.x == pp) dm.x += d.x;
+            if (am.y == pp) dm.y += d.y;
+            if (am.z == pp) dm.z += d.z;
+            if (am.w == pp) dm.w += d.w;
+          }
+        }
+        const float wu = ww[u];
+        acc[v].x += dm.x * wu; acc[v].y += dm.y * wu; acc[v].z += dm.z * wu; acc[v].w += dm.w * wu;
       }
-      acc[v].x += dm.x * ww; acc[v].y += dm.y * ww; acc[v].z += dm.z * ww; acc[v].w += dm.w * ww;
     }
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const long long o = (long long)j * H4 + v * LPN + sub;
+    const long long o = (long long)j * H4 + v * LPN + cb;
     float4 r = acc[v];
     if (gate) {
       const float4 g = reinterpret_cast<const float4*>(gate)[o];
@@ -403,10 +439,21 @@ static inline int grid_1d(long long n, int threads = 256) {
   return (int)b;
 }
 
-// choose (NV, LPN) for the float4 path; returns false if H does not fit
-static bool vec_shape(int H, int& nv, int& lpn) {
+// choose (NV, LPN, slabs) for the float4 path; returns false if H does not
+// fit.  H/4 > 32 float4 columns are split into 32-lane slabs (gridDim.y)
+// rather than held as NV > 1 registers per lane.
+static bool vec_shape(int H, int& nv, int& lpn, int* slabs = nullptr) {
   if (H % 4) return false;
   const int h4 = H / 4;
+  if (slabs) {
+    *slabs = 1;
+    if (h4 > 32 && h4 % 32 == 0) {
+      nv = 1;
+      lpn = 32;
+      *slabs = h4 / 32;
+      return true;
+    }
+  }
   for (int v : {1, 2, 4}) {
     if (h4 % v) continue;
     int l = h4 / v;
@@ -426,10 +473,10 @@ cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, c
                     const void* w, int parts, void* agg, int* argmax, void* stat_mean,
                     int force_scalar, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  int nv = 0, lpn = 0;
-  if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn)) {
+  int nv = 0, lpn = 0, slabs = 1;
+  if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn, &slabs)) {
     const int nodes_per_block = 8 * (32 / lpn);
-    const int grid = ceil_div(n, nodes_per_block);
+    const dim3 grid(ceil_div(n, nodes_per_block), slabs);
 #define GFM_FWD_CASE(NV_, LPN_)                                                                \
   if (nv == NV_ && lpn == LPN_) {                                                              \
     k_agg_fwd_vec<NV_, LPN_><<<grid, 256, 0, s>>>((const float*)h, n, H, rowptr, col_src,      \
@@ -487,10 +534,10 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
   }
   const void* dmax = L.o_max >= 0 ? (const char*)dagg + esz * L.o_max : nullptr;
   const int* am = L.o_max >= 0 ? argmax : nullptr;
-  int nv = 0, lpn = 0;
-  if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn)) {
+  int nv = 0, lpn = 0, slabs = 1;
+  if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn, &slabs)) {
     const int nodes_per_block = 8 * (32 / lpn);
-    const int grid = ceil_div(n, nodes_per_block);
+    const dim3 grid(ceil_div(n, nodes_per_block), slabs);
 #define GFM_BWD_CASE(NV_, LPN_)                                                              \
   if (nv == NV_ && lpn == LPN_) {                                                            \
     k_agg_bwd_vec<NV_, LPN_><<<grid, 256, 0, s>>>(                                           \

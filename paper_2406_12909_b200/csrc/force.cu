@@ -24,9 +24,18 @@
 namespace gfm {
 
 // choose (NV float4 per lane, LPN lanes per node) for the float32 path
-static bool force_vec_shape(int H, int& nv, int& lpn) {
+static bool force_vec_shape(int H, int& nv, int& lpn, int* slabs = nullptr) {
   if (H % 4) return false;
   const int h4 = H / 4;
+  if (slabs) {  // wide H: 32-lane column slabs (gridDim.y / warps) instead of NV > 1
+    *slabs = 1;
+    if (h4 > 32 && h4 % 32 == 0 && (h4 / 32 == 2 || h4 / 32 == 4 || h4 / 32 == 8)) {
+      nv = 1;
+      lpn = 32;
+      *slabs = h4 / 32;
+      return true;
+    }
+  }
   for (int v : {1, 2, 4}) {
     if (h4 % v) continue;
     const int l = h4 / v;
@@ -121,6 +130,88 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// wide H (H/4 = 32*SL float4 columns): SL warps per node, one 32-lane column
+// slab each.  Per-edge slab partials of m_e meet in shared memory; the slab-0
+// warp combines them in slab order and accumulates the force in fp64.
+template <int SL>
+__global__ void __launch_bounds__(256)
+    k_force_fwd_slab(const float* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
+                     const int* __restrict__ col_src, const float* __restrict__ dx,
+                     const float* __restrict__ c, const float* __restrict__ u,
+                     float* __restrict__ f) {
+  constexpr int NPB = 8 / SL, CH = 32;  // nodes per block, edges per chunk
+  __shared__ float mpart[8][CH];
+  __shared__ int degs[NPB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slab = warp % SL, ln = warp / SL;
+  const int i = blockIdx.x * NPB + ln;
+  const bool live = i < n;
+  const int H4 = H >> 2, c4 = slab * 32 + lane;
+  const float4* P4 = reinterpret_cast<const float4*>(P);
+  float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), cu = pi, uu = pi;
+  int beg = 0, end = 0;
+  if (live) {
+    pi = __ldg(P4 + (long long)i * H4 + c4);
+    cu = ld4u(c, c4);
+    uu = ld4u(u, c4);
+    beg = rowptr[i];
+    end = rowptr[i + 1];
+  }
+  if (slab == 0 && lane == 0) degs[ln] = end - beg;
+  __syncthreads();
+  int maxdeg = 0;
+#pragma unroll
+  for (int k = 0; k < NPB; ++k) maxdeg = max(maxdeg, degs[k]);
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  for (int p0 = 0; p0 < maxdeg; p0 += CH) {
+    for (int e = 0; e < CH; e += 2) {
+      const int pa = beg + p0 + e, pb = pa + 1;
+      if (pa >= end) break;  // warp-uniform
+      const bool hb = pb < end;
+      const int sa = __ldg(col_src + pa), sb = hb ? __ldg(col_src + pb) : sa;
+      const float4 ra = __ldg(P4 + (long long)sa * H4 + c4);
+      const float4 rb = __ldg(P4 + (long long)sb * H4 + c4);
+      const float4 xa = f4add3(pi, ra, cu), xb = f4add3(pi, rb, cu);
+      float da = tanhf(xa.x) * uu.x + tanhf(xa.y) * uu.y + tanhf(xa.z) * uu.z + tanhf(xa.w) * uu.w;
+      float db = tanhf(xb.x) * uu.x + tanhf(xb.y) * uu.y + tanhf(xb.z) * uu.z + tanhf(xb.w) * uu.w;
+      da = group_sum<32>(da);
+      db = group_sum<32>(db);
+      if (lane == 0) {
+        mpart[warp][e] = da;
+        if (hb) mpart[warp][e + 1] = db;
+      }
+    }
+    __syncthreads();
+    if (slab == 0) {
+      const int p = beg + p0 + lane;
+      double gx = 0.0, gy = 0.0, gz = 0.0;
+      if (lane < CH && p < end) {
+        float m = mpart[warp][lane];
+#pragma unroll
+        for (int k = 1; k < SL; ++k) m += mpart[warp + k][lane];
+        gx = (double)m * dx[3LL * p + 0];
+        gy = (double)m * dx[3LL * p + 1];
+        gz = (double)m * dx[3LL * p + 2];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        gx += __shfl_xor_sync(0xffffffffu, gx, o);
+        gy += __shfl_xor_sync(0xffffffffu, gy, o);
+        gz += __shfl_xor_sync(0xffffffffu, gz, o);
+      }
+      fx += gx;
+      fy += gy;
+      fz += gz;
+    }
+    __syncthreads();
+  }
+  if (live && slab == 0 && lane == 0) {
+    f[3LL * i + 0] = (float)fx;
+    f[3LL * i + 1] = (float)fy;
+    f[3LL * i + 2] = (float)fz;
+  }
+}
+
 // generic: one warp per node, lanes over columns (any H, float or double)
 template <typename T>
 __global__ void k_force_fwd_warp(const T* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
@@ -162,11 +253,12 @@ __global__ void __launch_bounds__(256)
   const int i = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
   if (i >= n) return;
   const int H4 = H >> 2;
+  const int cb = blockIdx.y * (NV * LPN) + sub;  // column slab (wide H)
   const float4* P4 = reinterpret_cast<const float4*>(P);
   float4 pi[NV], cu[NV], uu[NV], dd[NV], tu[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const int c4 = v * LPN + sub;
+    const int c4 = v * LPN + cb;
     pi[v] = __ldg(P4 + (long long)i * H4 + c4);
     cu[v] = ld4u(c, c4);
     uu[v] = ld4u(u, c4);
@@ -181,7 +273,7 @@ __global__ void __launch_bounds__(256)
                                __fmul_rn(fz, dx[3LL * p + 2]));
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const float4 x = f4add3(pi[v], __ldg(P4 + (long long)s * H4 + v * LPN + sub), cu[v]);
+      const float4 x = f4add3(pi[v], __ldg(P4 + (long long)s * H4 + v * LPN + cb), cu[v]);
       const float4 t = make_float4(tanhf(x.x), tanhf(x.y), tanhf(x.z), tanhf(x.w));
       dd[v].x += dm * uu[v].x * (1.f - t.x * t.x); dd[v].y += dm * uu[v].y * (1.f - t.y * t.y);
       dd[v].z += dm * uu[v].z * (1.f - t.z * t.z); dd[v].w += dm * uu[v].w * (1.f - t.w * t.w);
@@ -190,7 +282,7 @@ __global__ void __launch_bounds__(256)
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const long long o = (long long)i * H4 + v * LPN + sub;
+    const long long o = (long long)i * H4 + v * LPN + cb;
     reinterpret_cast<float4*>(Ddst)[o] = dd[v];
     reinterpret_cast<float4*>(TU)[o] = tu[v];
   }
@@ -209,11 +301,12 @@ __global__ void __launch_bounds__(256)
   const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
   if (j >= n) return;
   const int H4 = H >> 2;
+  const int cb = blockIdx.y * (NV * LPN) + sub;  // column slab (wide H)
   const float4* P4 = reinterpret_cast<const float4*>(P);
   float4 pj[NV], cu[NV], uu[NV], acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const int c4 = v * LPN + sub;
+    const int c4 = v * LPN + cb;
     pj[v] = __ldg(P4 + (long long)j * H4 + c4);
     cu[v] = ld4u(c, c4);
     uu[v] = ld4u(u, c4);
@@ -225,7 +318,7 @@ __global__ void __launch_bounds__(256)
                                __fmul_rn(df[3LL * i + 2], dx[3LL * p + 2]));
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const float4 x = f4add3(__ldg(P4 + (long long)i * H4 + v * LPN + sub), pj[v], cu[v]);
+      const float4 x = f4add3(__ldg(P4 + (long long)i * H4 + v * LPN + cb), pj[v], cu[v]);
       const float4 t = make_float4(tanhf(x.x), tanhf(x.y), tanhf(x.z), tanhf(x.w));
       acc[v].x += dm * uu[v].x * (1.f - t.x * t.x); acc[v].y += dm * uu[v].y * (1.f - t.y * t.y);
       acc[v].z += dm * uu[v].z * (1.f - t.z * t.z); acc[v].w += dm * uu[v].w * (1.f - t.w * t.w);
@@ -233,7 +326,7 @@ __global__ void __launch_bounds__(256)
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v)
-    reinterpret_cast<float4*>(S)[(long long)j * H4 + v * LPN + sub] = acc[v];
+    reinterpret_cast<float4*>(S)[(long long)j * H4 + v * LPN + cb] = acc[v];
 }
 
 // generic (any H, float / double): thread per (node, column)
@@ -341,7 +434,15 @@ cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const i
   if (n <= 0) return cudaSuccess;
   int nv = 0, lpn = 0;
   if constexpr (std::is_same<T, float>::value) {
-    if (!(flags & GFM_FLAG_SCALAR) && force_vec_shape(H, nv, lpn)) {
+    int slabs = 1;
+    if (!(flags & GFM_FLAG_SCALAR) && force_vec_shape(H, nv, lpn, &slabs)) {
+      if (slabs == 2 || slabs == 4 || slabs == 8) {
+        const int grid = ceil_div(n, 8 / slabs);
+        if (slabs == 2) k_force_fwd_slab<2><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);
+        if (slabs == 4) k_force_fwd_slab<4><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);
+        if (slabs == 8) k_force_fwd_slab<8><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);
+        return cudaGetLastError();
+      }
       const int grid = ceil_div(n, 8 * (32 / lpn));
 #define GFM_FF(NV_, LPN_)                                                                    \
   if (nv == NV_ && lpn == LPN_) {                                                            \
@@ -364,8 +465,9 @@ cudaError_t force_bwd_edges(const T* P, int n, int H, const int* rowptr, const i
   if (n <= 0) return cudaSuccess;
   int nv = 0, lpn = 0;
   if constexpr (std::is_same<T, float>::value) {
-    if (!(flags & GFM_FLAG_SCALAR) && force_vec_shape(H, nv, lpn)) {
-      const int grid = ceil_div(n, 8 * (32 / lpn));
+    int slabs = 1;
+    if (!(flags & GFM_FLAG_SCALAR) && force_vec_shape(H, nv, lpn, &slabs)) {
+      const dim3 grid(ceil_div(n, 8 * (32 / lpn)), slabs);
 #define GFM_FB(NV_, LPN_)                                                                         \
   if (nv == NV_ && lpn == LPN_) {                                                                 \
     k_force_bwd_dst_vec<NV_, LPN_><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df, c, u,   \

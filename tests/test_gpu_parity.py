@@ -139,6 +139,90 @@ def test_aggregate_fp32_vectorised_vs_oracle(kind, H):
         assert (got_am == want_am).mean() > 0.999
 
 
+def _wide_batch(H, dtype, seed):
+    recs = O.synthetic(5, n_atoms_range=(20, 40), box_length=6.0, rc=3.5, seed=seed)
+    return recs, M.make_batch(as_records(recs), dtype=dtype)
+
+
+@pytest.mark.parametrize("kind", ["pna-agg", "max-agg"])
+@pytest.mark.parametrize("H", [64, 256, 512])
+def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H):
+    """float4 / column-slab backward (F32) against the scalar F64 kernel."""
+    rng = np.random.default_rng(H + 1)
+    parts, K = M.KIND_PARTS[kind], M._n_parts(kind)
+    outs = {}
+    for dtype, flags in ((F64, _lib.FLAG_SCALAR), (F32, 0)):
+        recs, b = _wide_batch(H, dtype, 3)
+        N = b.n_nodes
+        code = _lib.F64 if dtype == F64 else _lib.F32
+        rg = np.random.default_rng(H + 1)
+        h = torch.as_tensor(rg.normal(size=(N, H)), dtype=dtype, device="cuda")
+        dagg = torch.as_tensor(rg.normal(size=(N, K * H)), dtype=dtype, device="cuda")
+        dh = torch.as_tensor(rg.normal(size=(N, H)), dtype=dtype, device="cuda")
+        gate = torch.as_tensor(np.tanh(rg.normal(size=(N, H))), dtype=dtype, device="cuda")
+        agg = torch.empty(N, K * H, dtype=dtype, device="cuda")
+        am = torch.empty(N, H, dtype=torch.int32, device="cuda")
+        sm = torch.empty(N, H, dtype=dtype, device="cuda")
+        s = _lib.stream_handle()
+        # the forward of the SAME precision fixes argmax / std (F64 for both
+        # would make the comparison depend on near-ties only)
+        _lib.call("gfm_agg_fwd", _lib.ptr(h), N, H, _lib.ptr(b.rowptr), _lib.ptr(b.col_src),
+                  _lib.ptr(b.edge_w), parts, _lib.ptr(agg), _lib.ptr(am), _lib.ptr(sm), code,
+                  flags, s)
+        ws = torch.empty(_lib.query("gfm_agg_bwd_workspace_bytes", N, H, parts, code),
+                         dtype=torch.uint8, device="cuda")
+        out = torch.empty(N, H, dtype=dtype, device="cuda")
+        _lib.call("gfm_agg_bwd", _lib.ptr(dagg), _lib.ptr(agg), _lib.ptr(sm), _lib.ptr(am),
+                  _lib.ptr(h), _lib.ptr(b.rowptr), _lib.ptr(b.csc_ptr), _lib.ptr(b.csc_eid),
+                  _lib.ptr(b.csc_dst), _lib.ptr(b.edge_w), N, H, parts, _lib.ptr(dh),
+                  _lib.ptr(gate), _lib.ptr(out), _lib.ptr(ws), code, flags, s)
+        outs[code] = (out.cpu().numpy().astype(np.float64), am.cpu().numpy())
+    got, am32 = outs[_lib.F32]
+    want, am64 = outs[_lib.F64]
+    if parts & _lib.PART_MAX:
+        # random normal features: no fp32 near-ties, so the routing agrees
+        np.testing.assert_array_equal(am32, am64)
+    assert_close_scaled(got, want, 1e-4, FP32_FLOOR, what=f"{kind} H={H}")
+
+
+@pytest.mark.parametrize("H", [64, 256, 512])
+def test_force_head_fp32_wide_vs_fp64_scalar(H):
+    """force fwd (slab kernel for H/4 > 32) and bwd (column slabs) in F32
+    against the generic F64 kernels, through the C-ABI."""
+    res = {}
+    for dtype, flags in ((F64, _lib.FLAG_SCALAR), (F32, 0)):
+        recs, b = _wide_batch(H, dtype, 5)
+        N = b.n_nodes
+        code = _lib.F64 if dtype == F64 else _lib.F32
+        rg = np.random.default_rng(H)
+        t = lambda *sh, sc=1.0: torch.as_tensor(rg.normal(size=sh) * sc, dtype=dtype, device="cuda")
+        h = torch.tanh(t(N, H))
+        V, c, u = t(H, H, sc=H ** -0.5), t(H, sc=0.1), t(H, sc=0.3)
+        df, dhe = t(N, 3), t(N, H, sc=0.1)
+        P = torch.empty(N, H, dtype=dtype, device="cuda")
+        f = torch.empty(N, 3, dtype=dtype, device="cuda")
+        s = _lib.stream_handle()
+        _lib.call("gfm_force_fwd", _lib.ptr(h), H, N, _lib.ptr(b.rowptr), _lib.ptr(b.col_src),
+                  _lib.ptr(b.edge_dx), _lib.ptr(V), _lib.ptr(c), _lib.ptr(u), _lib.ptr(P),
+                  _lib.ptr(f), code, flags, s)
+        gV = torch.empty(H, H, dtype=dtype, device="cuda")
+        gc = torch.empty(H, dtype=dtype, device="cuda")
+        gu = torch.empty(H, dtype=dtype, device="cuda")
+        dz = torch.empty(N, H, dtype=dtype, device="cuda")
+        ws = torch.empty(_lib.query("gfm_force_bwd_workspace_bytes", H, N, code),
+                         dtype=torch.uint8, device="cuda")
+        _lib.call("gfm_force_bwd", _lib.ptr(h), _lib.ptr(P), H, N, _lib.ptr(b.rowptr),
+                  _lib.ptr(b.col_src), _lib.ptr(b.edge_dx), _lib.ptr(b.csc_ptr),
+                  _lib.ptr(b.csc_eid), _lib.ptr(b.csc_dst), _lib.ptr(V), _lib.ptr(c),
+                  _lib.ptr(u), _lib.ptr(df), _lib.ptr(dhe), _lib.ptr(gV), _lib.ptr(gc),
+                  _lib.ptr(gu), _lib.ptr(dz), _lib.ptr(ws), code, flags, s)
+        res[code] = [x.cpu().numpy().astype(np.float64) for x in (f, gV, gc, gu, dz)]
+    bar = ENGINE_BAR["tc3"][1]  # P = h V^T and the node GEMMs run on the tc3 engine
+    for name, got, want in zip(("f", "grad_V", "grad_c", "grad_u", "dz"), res[_lib.F32],
+                               res[_lib.F64]):
+        assert_close_scaled(got, want, bar, FP32_FLOOR, what=f"{name} H={H}")
+
+
 # ----------------------------------------------------------------- neighbour lists
 @pytest.mark.parametrize("case_id", range(4))
 def test_cutoff_edges_bit_exact(case_id):
