@@ -20,6 +20,9 @@
 //    sums follow numpy's reduceat order (x0 + pairwise(x1..)) with separately
 //    rounded operations, which makes the float64 result bit-identical to
 //    np.add.reduceat / np.maximum.reduceat.
+#include <climits>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gfm {
@@ -116,20 +119,15 @@ __global__ void k_agg_fwd_scalar(const T* __restrict__ h, int n_nodes, int H,
 }
 
 // ------------------------------------------------------------ forward, float4
-template <int NV, int LPN>
-__global__ void __launch_bounds__(256)
-    k_agg_fwd_vec(const float* __restrict__ h, int n_nodes, int H, const int* __restrict__ rowptr,
-                  const int* __restrict__ col_src, const float* __restrict__ w, int parts,
-                  float* __restrict__ agg, int* __restrict__ argmax, float* __restrict__ stat_mean) {
-  constexpr int NPW = 32 / LPN;  // nodes per warp
-  const int lane = threadIdx.x & 31;
-  const int sub = lane % LPN;
-  const int node = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
-  if (node >= n_nodes) return;
-  // blockIdx.y selects a slab of NV*LPN float4 columns (wide H uses several
-  // slabs instead of more registers per lane: occupancy hides gather latency)
-  const int cb = blockIdx.y * (NV * LPN) + sub;
-  const AggLayout L = agg_layout(parts, H);
+// One node's PNA row over the float4 columns v*LPN + cb (v < NV); `ld(sj, v)`
+// returns that column slice of source row sj (global or shared-memory staged).
+template <int NV, int LPN, typename Ld>
+__device__ __forceinline__ void agg_fwd_node(Ld ld, int node, int cb, int H,
+                                             const int* __restrict__ rowptr,
+                                             const int* __restrict__ col_src,
+                                             const float* __restrict__ w, const AggLayout& L,
+                                             float* __restrict__ agg, int* __restrict__ argmax,
+                                             float* __restrict__ stat_mean) {
   const bool need_s = L.o_sum >= 0 || L.o_mean >= 0 || L.o_std >= 0;
   const bool need_q = L.o_std >= 0;
   const bool need_m = L.o_max >= 0;
@@ -147,20 +145,18 @@ __global__ void __launch_bounds__(256)
     mx[v] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     am[v] = make_int4(-1, -1, -1, -1);
   }
-  const float4* __restrict__ h4 = reinterpret_cast<const float4*>(h);
-  const int H4 = H >> 2;
-  auto consume = [&](const float4 (&r)[NV], float ww, int p) {
+  // packed f32x2 updates (add4/mul4/fma4); `first` (a literal at each call)
+  // peels the x0 capture out of the edge loop
+  auto consume = [&](const float4 (&r)[NV], float ww, int p, bool first) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      float4 m = make_float4(r[v].x * ww, r[v].y * ww, r[v].z * ww, r[v].w * ww);
-      if (need_s) {
-        s[v].x += m.x; s[v].y += m.y; s[v].z += m.z; s[v].w += m.w;
-      }
+      const float4 m = mul4(r[v], bcast4(ww));
+      if (need_s) s[v] = add4(s[v], m);
       if (need_q) {
-        if (p == beg) x0[v] = m;
-        const float4 d = make_float4(m.x - x0[v].x, m.y - x0[v].y, m.z - x0[v].z, m.w - x0[v].w);
-        d1[v].x += d.x; d1[v].y += d.y; d1[v].z += d.z; d1[v].w += d.w;
-        q[v].x += d.x * d.x; q[v].y += d.y * d.y; q[v].z += d.z * d.z; q[v].w += d.w * d.w;
+        if (first) x0[v] = m;
+        const float4 d = sub4(m, x0[v]);
+        d1[v] = add4(d1[v], d);
+        q[v] = fma4(d, d, q[v]);
       }
       if (need_m) {
         if (m.x > mx[v].x) { mx[v].x = m.x; am[v].x = p; }
@@ -171,6 +167,15 @@ __global__ void __launch_bounds__(256)
     }
   };
   int p = beg;
+  if (p < end) {
+    const int sj = __ldg(col_src + p);
+    const float ww = __ldg(w + p);
+    float4 r[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) r[v] = ld(sj, v);
+    consume(r, ww, p, true);
+    ++p;
+  }
   for (; p + 4 <= end; p += 4) {
     int sj[4];
     float ww[4];
@@ -183,17 +188,17 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < NV; ++v) r[u][v] = __ldg(h4 + (long long)sj[u] * H4 + v * LPN + cb);
+      for (int v = 0; v < NV; ++v) r[u][v] = ld(sj[u], v);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) consume(r[u], ww[u], p + u);
+    for (int u = 0; u < 4; ++u) consume(r[u], ww[u], p + u, false);
   }
   for (; p < end; ++p) {
     const int sj = __ldg(col_src + p);
     const float ww = __ldg(w + p);
     float4 r[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) r[v] = __ldg(h4 + (long long)sj * H4 + v * LPN + cb);
-    consume(r, ww, p);
+    for (int v = 0; v < NV; ++v) r[v] = ld(sj, v);
+    consume(r, ww, p, false);
   }
   const int deg = end - beg;
   const float inv = deg > 0 ? 1.f / (float)deg : 0.f;
@@ -220,6 +225,105 @@ __global__ void __launch_bounds__(256)
       out4[(L.o_std >> 2) + c4] = o;
       if (stat_mean) reinterpret_cast<float4*>(stat_mean + (long long)node * H)[c4] = mean;
     }
+  }
+}
+
+template <int NV, int LPN>
+__global__ void __launch_bounds__(256)
+    k_agg_fwd_vec(const float* __restrict__ h, int n_nodes, int H, const int* __restrict__ rowptr,
+                  const int* __restrict__ col_src, const float* __restrict__ w, int parts,
+                  float* __restrict__ agg, int* __restrict__ argmax, float* __restrict__ stat_mean) {
+  constexpr int NPW = 32 / LPN;  // nodes per warp
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % LPN;
+  const int node = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
+  if (node >= n_nodes) return;
+  // blockIdx.y selects a slab of NV*LPN float4 columns (wide H uses several
+  // slabs instead of more registers per lane: occupancy hides gather latency)
+  const int cb = blockIdx.y * (NV * LPN) + sub;
+  const AggLayout L = agg_layout(parts, H);
+  const float4* __restrict__ h4 = reinterpret_cast<const float4*>(h);
+  const int H4 = H >> 2;
+  agg_fwd_node<NV, LPN>(
+      [&](int sj, int v) { return __ldg(h4 + (long long)sj * H4 + v * LPN + cb); }, node, cb, H,
+      rowptr, col_src, w, L, agg, argmax, stat_mean);
+}
+
+// 16-byte global -> shared copy without a register round trip: a block's
+// whole staging loop is in flight at once (cp.async.cg, L2-only)
+__device__ __forceinline__ void stage16(void* smem, const void* gptr) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void stage_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// Block-wide [lo, hi] of idx[e0, e1) (lo > hi when empty).
+__device__ __forceinline__ void block_minmax(const int* __restrict__ idx, int e0, int e1, int& lo,
+                                             int& hi) {
+  __shared__ int s_lo[8], s_hi[8];
+  int a = INT_MAX, b = -1;
+  for (int e = e0 + (int)threadIdx.x; e < e1; e += blockDim.x) {
+    const int v = __ldg(idx + e);
+    a = min(a, v);
+    b = max(b, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[threadIdx.x >> 5] = a;
+    s_hi[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  lo = s_lo[0];
+  hi = s_hi[0];
+  for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+    lo = min(lo, s_lo[k]);
+    hi = max(hi, s_hi[k]);
+  }
+}
+
+// Shared-memory staged forward.  A block owns `nb` consecutive dst nodes and
+// one LPN-float4 column slab.  Batched graphs keep every edge inside its graph,
+// so the block's sources span a short row range [lo, hi]: that slab of h is
+// staged once with coalesced 16-byte loads and every per-edge gather is then a
+// shared-memory read (HBM/L2 see each staged row once per block instead of
+// once per edge).  Ranges wider than cap_rows fall back to global gathers.
+template <int LPN>
+__global__ void __launch_bounds__(256)
+    k_agg_fwd_tile(const float* __restrict__ h, int n_nodes, int H, const int* __restrict__ rowptr,
+                   const int* __restrict__ col_src, const float* __restrict__ w, int parts,
+                   float* __restrict__ agg, int* __restrict__ argmax,
+                   float* __restrict__ stat_mean, int nb, int cap_rows) {
+  extern __shared__ float4 stage[];  // [cap_rows][LPN]
+  const int a = blockIdx.x * nb, b = min(n_nodes, a + nb);
+  const int cs = blockIdx.y * LPN;  // slab's first float4 column
+  const int H4 = H >> 2;
+  const float4* __restrict__ h4 = reinterpret_cast<const float4*>(h);
+  int lo, hi;
+  block_minmax(col_src, rowptr[a], rowptr[b], lo, hi);
+  const bool staged = hi >= lo && hi - lo < cap_rows;
+  if (staged) {
+    const int total = (hi - lo + 1) * LPN;
+    for (int t = threadIdx.x; t < total; t += blockDim.x)
+      stage16(stage + t, h4 + (long long)(lo + t / LPN) * H4 + cs + t % LPN);
+    stage_wait();
+  }
+  __syncthreads();
+  const AggLayout L = agg_layout(parts, H);
+  const int sub = threadIdx.x % LPN, cb = cs + sub;
+  const int npp = blockDim.x / LPN;
+  for (int node = a + (int)threadIdx.x / LPN; node < b; node += npp) {
+    if (staged)
+      agg_fwd_node<1, LPN>([&](int sj, int) { return stage[(sj - lo) * LPN + sub]; }, node, cb,
+                           H, rowptr, col_src, w, L, agg, argmax, stat_mean);
+    else
+      agg_fwd_node<1, LPN>([&](int sj, int) { return __ldg(h4 + (long long)sj * H4 + cb); },
+                           node, cb, H, rowptr, col_src, w, L, agg, argmax, stat_mean);
   }
 }
 
@@ -338,27 +442,28 @@ __global__ void k_agg_bwd_scalar(const T* __restrict__ G, int ldg, const T* __re
   }
 }
 
-template <int NV, int LPN>
-__global__ void __launch_bounds__(256)
-    k_agg_bwd_vec(const float* __restrict__ G, int ldg, const float* __restrict__ coef,
-                  const float* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
-                  const float* __restrict__ h_in, const int* __restrict__ csc_ptr,
-                  const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
-                  const float* __restrict__ w, int n_nodes, int H, float* __restrict__ dh,
-                  const float* __restrict__ gate, float* __restrict__ out) {
-  constexpr int NPW = 32 / LPN;
-  const int lane = threadIdx.x & 31;
-  const int sub = lane % LPN;
-  const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
-  if (j >= n_nodes) return;
+// One CSC node j over float4 columns v*LPN + cb: ldG/ldC/ldA(i, v) return the
+// dst row i slice of G / coef / argmax (global or staged); hasG/hasC/hasA say
+// which are present.
+template <int NV, int LPN, typename LG, typename LC, typename LA>
+__device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, bool hasC,
+                                             bool hasA, int j, int cb, int H,
+                                             const float* __restrict__ dmax, int ldm,
+                                             const float* __restrict__ h_in,
+                                             const int* __restrict__ csc_ptr,
+                                             const int* __restrict__ csc_eid,
+                                             const int* __restrict__ csc_dst,
+                                             const float* __restrict__ w,
+                                             const float* __restrict__ dh,
+                                             const float* __restrict__ gate,
+                                             float* __restrict__ out) {
   const int H4 = H >> 2;
-  const int cb = blockIdx.y * (NV * LPN) + sub;  // column slab (see k_agg_fwd_vec)
   float4 acc[NV], hj[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     const long long o = (long long)j * H4 + v * LPN + cb;
     acc[v] = reinterpret_cast<const float4*>(dh)[o];
-    hj[v] = coef ? reinterpret_cast<const float4*>(h_in)[o] : make_float4(0.f, 0.f, 0.f, 0.f);
+    hj[v] = hasC ? reinterpret_cast<const float4*>(h_in)[o] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int qb = csc_ptr[j], qe = csc_ptr[j + 1];
   // U CSC slots per batch: all their row loads issue before the (in-order)
@@ -380,16 +485,13 @@ __global__ void __launch_bounds__(256)
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        const int c4 = v * LPN + cb;
         const bool ok = q + u < qe;
         g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
         cf[u][v] = g[u][v];
         a[u][v] = make_int4(-1, -1, -1, -1);
-        if (ok && G) g[u][v] = __ldg(reinterpret_cast<const float4*>(G + (long long)i[u] * ldg) + c4);
-        if (ok && coef)
-          cf[u][v] = __ldg(reinterpret_cast<const float4*>(coef + (long long)i[u] * H) + c4);
-        if (ok && argmax)
-          a[u][v] = __ldg(reinterpret_cast<const int4*>(argmax + (long long)i[u] * H) + c4);
+        if (ok && hasG) g[u][v] = ldG(i[u], v);
+        if (ok && hasC) cf[u][v] = ldC(i[u], v);
+        if (ok && hasA) a[u][v] = ldA(i[u], v);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -398,11 +500,8 @@ __global__ void __launch_bounds__(256)
       for (int v = 0; v < NV; ++v) {
         const int c4 = v * LPN + cb;
         float4 dm = g[u][v];
-        if (coef) {
-          dm.x += cf[u][v].x * (hj[v].x * ww[u]); dm.y += cf[u][v].y * (hj[v].y * ww[u]);
-          dm.z += cf[u][v].z * (hj[v].z * ww[u]); dm.w += cf[u][v].w * (hj[v].w * ww[u]);
-        }
-        if (argmax) {
+        if (hasC) dm = fma4(cf[u][v], mul4(hj[v], bcast4(ww[u])), dm);
+        if (hasA) {
           const int4 am = a[u][v];
           const int pp = p[u];
           if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
@@ -414,8 +513,7 @@ __global__ void __launch_bounds__(256)
             if (am.w == pp) dm.w += d.w;
           }
         }
-        const float wu = ww[u];
-        acc[v].x += dm.x * wu; acc[v].y += dm.y * wu; acc[v].z += dm.z * wu; acc[v].w += dm.w * wu;
+        acc[v] = fma4(dm, bcast4(ww[u]), acc[v]);
       }
     }
   }
@@ -428,6 +526,93 @@ __global__ void __launch_bounds__(256)
       r.x *= 1.f - g.x * g.x; r.y *= 1.f - g.y * g.y; r.z *= 1.f - g.z * g.z; r.w *= 1.f - g.w * g.w;
     }
     reinterpret_cast<float4*>(out)[o] = r;
+  }
+}
+
+template <int NV, int LPN>
+__global__ void __launch_bounds__(256)
+    k_agg_bwd_vec(const float* __restrict__ G, int ldg, const float* __restrict__ coef,
+                  const float* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
+                  const float* __restrict__ h_in, const int* __restrict__ csc_ptr,
+                  const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
+                  const float* __restrict__ w, int n_nodes, int H, float* __restrict__ dh,
+                  const float* __restrict__ gate, float* __restrict__ out) {
+  constexpr int NPW = 32 / LPN;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % LPN;
+  const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
+  if (j >= n_nodes) return;
+  const int cb = blockIdx.y * (NV * LPN) + sub;  // column slab (see k_agg_fwd_vec)
+  agg_bwd_node<NV, LPN>(
+      [&](int i, int v) {
+        return __ldg(reinterpret_cast<const float4*>(G + (long long)i * ldg) + v * LPN + cb);
+      },
+      [&](int i, int v) {
+        return __ldg(reinterpret_cast<const float4*>(coef + (long long)i * H) + v * LPN + cb);
+      },
+      [&](int i, int v) {
+        return __ldg(reinterpret_cast<const int4*>(argmax + (long long)i * H) + v * LPN + cb);
+      },
+      G != nullptr, coef != nullptr, argmax != nullptr, j, cb, H, dmax, ldm, h_in, csc_ptr,
+      csc_eid, csc_dst, w, dh, gate, out);
+}
+
+// Shared-memory staged backward (see k_agg_fwd_tile): a block owns nb
+// consecutive CSC (source) nodes and one LPN-float4 column slab, stages the
+// dst-row range of G, coef and argmax it touches, then gathers from smem.
+template <int LPN>
+__global__ void __launch_bounds__(256)
+    k_agg_bwd_tile(const float* __restrict__ G, int ldg, const float* __restrict__ coef,
+                   const float* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
+                   const float* __restrict__ h_in, const int* __restrict__ csc_ptr,
+                   const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
+                   const float* __restrict__ w, int n_nodes, int H, float* __restrict__ dh,
+                   const float* __restrict__ gate, float* __restrict__ out, int nb,
+                   int cap_rows) {
+  extern __shared__ float4 stage[];  // [G | coef | argmax] each [cap_rows][LPN]
+  const int a0 = blockIdx.x * nb, b0 = min(n_nodes, a0 + nb);
+  const int cs = blockIdx.y * LPN;
+  const bool hasG = G != nullptr, hasC = coef != nullptr, hasA = argmax != nullptr;
+  int lo, hi;
+  block_minmax(csc_dst, csc_ptr[a0], csc_ptr[b0], lo, hi);
+  const bool staged = hi >= lo && hi - lo < cap_rows;
+  float4* sG = stage;
+  float4* sC = stage + (size_t)cap_rows * LPN;
+  int4* sA = reinterpret_cast<int4*>(stage + 2 * (size_t)cap_rows * LPN);
+  if (staged) {
+    const int total = (hi - lo + 1) * LPN;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const long long r = lo + t / LPN;
+      const int c = cs + t % LPN;
+      if (hasG) stage16(sG + t, reinterpret_cast<const float4*>(G + r * ldg) + c);
+      if (hasC) stage16(sC + t, reinterpret_cast<const float4*>(coef + r * H) + c);
+      if (hasA) stage16(sA + t, reinterpret_cast<const int4*>(argmax + r * H) + c);
+    }
+    stage_wait();
+  }
+  __syncthreads();
+  const int sub = threadIdx.x % LPN, cb = cs + sub;
+  const int npp = blockDim.x / LPN;
+  for (int j = a0 + (int)threadIdx.x / LPN; j < b0; j += npp) {
+    if (staged)
+      agg_bwd_node<1, LPN>([&](int i, int) { return sG[(i - lo) * LPN + sub]; },
+                           [&](int i, int) { return sC[(i - lo) * LPN + sub]; },
+                           [&](int i, int) { return sA[(i - lo) * LPN + sub]; }, hasG, hasC,
+                           hasA, j, cb, H, dmax, ldm, h_in, csc_ptr, csc_eid, csc_dst, w, dh,
+                           gate, out);
+    else
+      agg_bwd_node<1, LPN>(
+          [&](int i, int) {
+            return __ldg(reinterpret_cast<const float4*>(G + (long long)i * ldg) + cb);
+          },
+          [&](int i, int) {
+            return __ldg(reinterpret_cast<const float4*>(coef + (long long)i * H) + cb);
+          },
+          [&](int i, int) {
+            return __ldg(reinterpret_cast<const int4*>(argmax + (long long)i * H) + cb);
+          },
+          hasG, hasC, hasA, j, cb, H, dmax, ldm, h_in, csc_ptr, csc_eid, csc_dst, w, dh, gate,
+          out);
   }
 }
 
@@ -469,11 +654,32 @@ static bool vec_shape(int H, int& nv, int& lpn, int* slabs = nullptr) {
 #define GFM_VEC_CASES(MACRO) \
   MACRO(1, 1) MACRO(1, 2) MACRO(1, 4) MACRO(1, 8) MACRO(1, 16) MACRO(1, 32) MACRO(2, 32) MACRO(4, 32)
 
+// GFM_NO_AGG_TILE=1 selects the register-only gather kernels (A/B checks)
+static bool no_tile() {
+  static const bool v = [] {
+    const char* e = getenv("GFM_NO_AGG_TILE");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, const int* col_src,
                     const void* w, int parts, void* agg, int* argmax, void* stat_mean,
                     int force_scalar, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   int nv = 0, lpn = 0, slabs = 1;
+  if (dtype == GFM_F32 && !force_scalar && H % 64 == 0 && !no_tile()) {
+    // staged tiles: 16-lane (64-column) slabs, 128 dst nodes, <= 384 rows
+    constexpr int kLpn = 16, kNb = 128, kCap = 384;
+    const size_t smem = (size_t)kCap * kLpn * sizeof(float4);
+    cudaFuncSetAttribute(k_agg_fwd_tile<kLpn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const dim3 grid(ceil_div(n, kNb), H / 64);
+    k_agg_fwd_tile<kLpn><<<grid, 256, smem, s>>>((const float*)h, n, H, rowptr, col_src,
+                                                 (const float*)w, parts, (float*)agg, argmax,
+                                                 (float*)stat_mean, kNb, kCap);
+    return cudaGetLastError();
+  }
   if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn, &slabs)) {
     const int nodes_per_block = 8 * (32 / lpn);
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);
@@ -535,6 +741,20 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
   const void* dmax = L.o_max >= 0 ? (const char*)dagg + esz * L.o_max : nullptr;
   const int* am = L.o_max >= 0 ? argmax : nullptr;
   int nv = 0, lpn = 0, slabs = 1;
+  const bool g_ok = G == nullptr || ldg % 4 == 0;
+  if (dtype == GFM_F32 && !force_scalar && H % 32 == 0 && g_ok && ld % 4 == 0 && !no_tile()) {
+    // staged tiles: 8-lane (32-column) slabs, 64 CSC nodes, <= 256 dst rows
+    constexpr int kLpn = 8, kNb = 64, kCap = 256;
+    const size_t smem = 3 * (size_t)kCap * kLpn * sizeof(float4);
+    cudaFuncSetAttribute(k_agg_bwd_tile<kLpn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const dim3 grid(ceil_div(n, kNb), H / 32);
+    k_agg_bwd_tile<kLpn><<<grid, 256, smem, s>>>(
+        (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in,
+        csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,
+        (float*)out, kNb, kCap);
+    return cudaGetLastError();
+  }
   if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn, &slabs)) {
     const int nodes_per_block = 8 * (32 / lpn);
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);

@@ -119,4 +119,46 @@ __device__ __forceinline__ T np_pairwise(const Get& get, long long base, long lo
   return np_pairwise_deep<T>(get, base, n);
 }
 
+// ---- packed fp32x2 arithmetic (sm_100 FADD2 / FMUL2 / FFMA2): one issue slot
+// for two lanes of a float4; each half is rounded exactly like the scalar op.
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+#define GFM_F2OP(NAME, PTX)                                                               \
+  __device__ __forceinline__ float4 NAME(float4 a, float4 b) {                            \
+    unsigned long long lo, hi;                                                            \
+    asm(PTX " %0, %1, %2;" : "=l"(lo) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));          \
+    asm(PTX " %0, %1, %2;" : "=l"(hi) : "l"(pk2(a.z, a.w)), "l"(pk2(b.z, b.w)));          \
+    float4 r;                                                                             \
+    upk2(lo, r.x, r.y);                                                                   \
+    upk2(hi, r.z, r.w);                                                                   \
+    return r;                                                                             \
+  }
+GFM_F2OP(add4, "add.rn.f32x2")
+GFM_F2OP(sub4, "sub.rn.f32x2")
+GFM_F2OP(mul4, "mul.rn.f32x2")
+#undef GFM_F2OP
+// a * b + c, single rounding per element
+__device__ __forceinline__ float4 fma4(float4 a, float4 b, float4 c) {
+  unsigned long long lo, hi;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(lo)
+      : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)), "l"(pk2(c.x, c.y)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(hi)
+      : "l"(pk2(a.z, a.w)), "l"(pk2(b.z, b.w)), "l"(pk2(c.z, c.w)));
+  float4 r;
+  upk2(lo, r.x, r.y);
+  upk2(hi, r.z, r.w);
+  return r;
+}
+__device__ __forceinline__ float4 bcast4(float s) { return make_float4(s, s, s, s); }
+#endif
+
 }  // namespace gfm

@@ -277,20 +277,45 @@ __device__ __forceinline__ void issue_tile(const L& ld, int r0, int rows_valid, 
   }
 }
 
-// lo = x - trunc_tf32(x) for every 16-byte chunk of a raw stage
+// lo = x - trunc_tf32(x) for every 16-byte chunk of a raw stage.  Explicit
+// shared-space ld/st (the stage pointers are computed, so generic LD/ST would
+// otherwise go through the slower generic path); all of a thread's loads are
+// issued before its stores.
 template <int BYTES, int kThreads>
 __device__ __forceinline__ void make_lo(const uint8_t* raw, uint8_t* lo, int tid) {
   constexpr int kChunks = BYTES / 16;
-#pragma unroll 4
-  for (int c = tid; c < kChunks; c += kThreads) {
-    const uint4 x = reinterpret_cast<const uint4*>(raw)[c];
-    const uint32_t m = 0xFFFFE000u;
+  constexpr int kFull = kChunks / kThreads;
+  const uint32_t r0 = smem_u32(raw), l0 = smem_u32(lo);
+  const uint32_t m = 0xFFFFE000u;
+  auto split = [&](uint4 x) {
     float4 l;
     l.x = __uint_as_float(x.x) - __uint_as_float(x.x & m);
     l.y = __uint_as_float(x.y) - __uint_as_float(x.y & m);
     l.z = __uint_as_float(x.z) - __uint_as_float(x.z & m);
     l.w = __uint_as_float(x.w) - __uint_as_float(x.w & m);
-    reinterpret_cast<float4*>(lo)[c] = l;
+    return l;
+  };
+  uint4 x[kFull > 0 ? kFull : 1];
+#pragma unroll
+  for (int i = 0; i < kFull; ++i) {
+    const uint32_t a = r0 + 16u * (uint32_t)(tid + i * kThreads);
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(x[i].x), "=r"(x[i].y), "=r"(x[i].z), "=r"(x[i].w) : "r"(a));
+  }
+#pragma unroll
+  for (int i = 0; i < kFull; ++i) {
+    const float4 l = split(x[i]);
+    const uint32_t a = l0 + 16u * (uint32_t)(tid + i * kThreads);
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};"
+                 :: "r"(a), "f"(l.x), "f"(l.y), "f"(l.z), "f"(l.w) : "memory");
+  }
+  for (int c = kFull * kThreads + tid; c < kChunks; c += kThreads) {
+    uint4 y;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w) : "r"(r0 + 16u * (uint32_t)c));
+    const float4 l = split(y);
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};"
+                 :: "r"(l0 + 16u * (uint32_t)c), "f"(l.x), "f"(l.y), "f"(l.z), "f"(l.w) : "memory");
   }
 }
 
@@ -647,14 +672,20 @@ __device__ __forceinline__ void tma_tile(const TmaOp& op, uint32_t dst, int r0, 
   }
 }
 
+// Smem: a deep ring of raw (= hi) k-block stages fed by TMA, and a separate
+// 2-slot ring for the converted lo copies.  Decoupling the two lets TMA run
+// kR k-blocks ahead (enough to cover L2/HBM latency at full MMA rate) while
+// the lo buffers, which only live from conversion to MMA completion, stay few.
 template <int BN>
 struct SmemT {
   static constexpr int kA = kBM * 128;
   static constexpr int kB = BN * 128;
   static constexpr int kRaw = kA + kB;
-  static constexpr int kStage = 2 * kRaw;  // raw (= hi) + lo
-  static constexpr int kS = BN >= 128 ? 3 : BN >= 64 ? 4 : 5;
-  static constexpr int kBytes = kS * kStage + 1024 + 512;
+  static constexpr int kL = 2;  // lo slots
+  static constexpr int kR = (224 * 1024 - kL * kRaw) / kRaw;  // raw stages
+  static constexpr int kBars = (2 * kR + 2 * kL + 4) * 8 + 16;
+  static constexpr int kBytes = (kR + kL) * kRaw + 1024 + kBars;
+  static_assert(kBytes <= 232448, "smem");
 };
 
 constexpr int kConvWarps = 8;
@@ -668,14 +699,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = SmemT<BN>;
   constexpr int NC = tmem_cols(2 * BN);
-  constexpr int kS = S::kS;
+  constexpr int kR = S::kR, kL = S::kL;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* tfl = reinterpret_cast<uint64_t*>(base + kS * S::kStage);  // TMA landed [kS]
-  uint64_t* cvt = tfl + kS;     // lo written [kS]
-  uint64_t* empty = cvt + kS;   // MMAs done with the stage [kS]
-  uint64_t* tfull = empty + kS; // accumulator ready [2]
-  uint64_t* tempty = tfull + 2; // accumulator drained [2]
+  uint8_t* lo_base = base + kR * S::kRaw;
+  uint64_t* tfl = reinterpret_cast<uint64_t*>(lo_base + kL * S::kRaw);  // TMA landed [kR]
+  uint64_t* empty = tfl + kR;    // MMAs done with the raw stage [kR]
+  uint64_t* cvt = empty + kR;    // lo written [kL]
+  uint64_t* lofree = cvt + kL;   // MMAs done with the lo slot [kL]
+  uint64_t* tfull = lofree + kL; // accumulator ready [2]
+  uint64_t* tempty = tfull + 2;  // accumulator drained [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int m_total = M_dev ? *M_dev : M;
@@ -685,13 +718,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if ((int)blockIdx.x >= n_work) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool split_on = split3 != 0;
-  constexpr int kMmaWarp = 1 + kConvWarps, kEpiWarp0 = kMmaWarp + 1;
+  constexpr int kMmaWarp = 1 + kConvWarps;
 
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kS; ++q) {
+    for (int q = 0; q < kR; ++q) {
       mbar_init(&tfl[q], 1);
-      mbar_init(&cvt[q], kConvWarps);
       mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < kL; ++q) {
+      mbar_init(&cvt[q], kConvWarps);
+      mbar_init(&lofree[q], 1);
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&tfull[q], 1);
@@ -723,10 +759,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         tile_of(w, bm, bn, split);
         const int nkb = nkb_of(w);
         for (int kb = 0; kb < nkb; ++kb, ++p) {
-          const int s = p % kS;
-          if (p >= kS) mbar_wait(&empty[s], ((p / kS) - 1) & 1);
+          const int s = p % kR;
+          if (p >= kR) mbar_wait(&empty[s], ((p / kR) - 1) & 1);
           const int k0 = split * k_chunk + kb * kBK;
-          const uint32_t st = smem_u32(base + s * S::kStage);
+          const uint32_t st = smem_u32(base + s * S::kRaw);
           mbar_expect_tx(&tfl[s], S::kRaw);
           tma_tile<kBM>(ta, st, bm * kBM, k0, &tfl[s]);
           tma_tile<BN>(tb, st + S::kA, bn * BN, k0, &tfl[s]);
@@ -741,13 +777,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
         const int nkb = nkb_of(w);
         for (int kb = 0; kb < nkb; ++kb, ++q) {
-          const int s = q % kS;
-          mbar_wait(&tfl[s], (q / kS) & 1);
-          uint8_t* st = base + s * S::kStage;
-          make_lo<S::kRaw, kConvWarps * 32>(st, st + S::kRaw, ctid);
+          const int s = q % kR, l = q % kL;
+          mbar_wait(&tfl[s], (q / kR) & 1);
+          if (q >= kL) mbar_wait(&lofree[l], ((q / kL) - 1) & 1);
+          make_lo<S::kRaw, kConvWarps * 32>(base + s * S::kRaw, lo_base + l * S::kRaw, ctid);
           fence_async_smem();
           __syncwarp();
-          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&cvt[s])) : "memory");
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&cvt[l])) : "memory");
         }
       }
     }
@@ -766,15 +802,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       tc_fence_after();
       const uint32_t d = tmem + (uint32_t)(acc * BN);
       for (int kb = 0; kb < nkb; ++kb, ++q) {
-        const int s = q % kS;
-        if (split_on)
-          mbar_wait(&cvt[s], (q / kS) & 1);
-        else
-          mbar_wait(&tfl[s], (q / kS) & 1);
+        const int s = q % kR, l = q % kL;
+        mbar_wait(&tfl[s], (q / kR) & 1);
+        if (split_on) mbar_wait(&cvt[l], (q / kL) & 1);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t ah = smem_u32(base + s * S::kStage), bh = ah + S::kA;
-          const uint32_t al = ah + S::kRaw, bl = al + S::kA;
+          const uint32_t ah = smem_u32(base + s * S::kRaw), bh = ah + S::kA;
+          const uint32_t al = smem_u32(lo_base + l * S::kRaw), bl = al + S::kA;
 #pragma unroll
           for (int ks = 0; ks < kBK / 8; ++ks) {
             const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
@@ -787,6 +821,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             }
           }
           mma_commit(&empty[s]);
+          if (split_on) mma_commit(&lofree[l]);
         }
         __syncwarp();
       }

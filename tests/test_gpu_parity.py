@@ -139,20 +139,33 @@ def test_aggregate_fp32_vectorised_vs_oracle(kind, H):
         assert (got_am == want_am).mean() > 0.999
 
 
-def _wide_batch(H, dtype, seed):
+def _wide_batch(H, dtype, seed, scattered=False):
+    if scattered:
+        # one 1500-node graph with sources drawn from the whole graph: the
+        # staged kernels' row range exceeds their shared-memory capacity and
+        # they take the global-gather path
+        rng = np.random.default_rng(seed)
+        n, E = 1500, 12000
+        pos = rng.uniform(0, 50.0, size=(n, 3))
+        edges = np.stack([rng.integers(0, n, E), rng.integers(0, n, E)], 1)
+        edges = edges[edges[:, 0] != edges[:, 1]]
+        rec = GraphRecord(rng.integers(1, 9, n).astype(np.uint8), pos, edges, 0.0,
+                          np.zeros((n, 3)))
+        return None, M.make_batch([rec], dtype=dtype)
     recs = O.synthetic(5, n_atoms_range=(20, 40), box_length=6.0, rc=3.5, seed=seed)
     return recs, M.make_batch(as_records(recs), dtype=dtype)
 
 
+@pytest.mark.parametrize("scattered", [False, True])
 @pytest.mark.parametrize("kind", ["pna-agg", "max-agg"])
 @pytest.mark.parametrize("H", [64, 256, 512])
-def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H):
-    """float4 / column-slab backward (F32) against the scalar F64 kernel."""
-    rng = np.random.default_rng(H + 1)
+def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H, scattered):
+    """float4 / column-slab / smem-staged forward + backward (F32) against the
+    scalar F64 kernels."""
     parts, K = M.KIND_PARTS[kind], M._n_parts(kind)
     outs = {}
     for dtype, flags in ((F64, _lib.FLAG_SCALAR), (F32, 0)):
-        recs, b = _wide_batch(H, dtype, 3)
+        recs, b = _wide_batch(H, dtype, 3, scattered)
         N = b.n_nodes
         code = _lib.F64 if dtype == F64 else _lib.F32
         rg = np.random.default_rng(H + 1)
@@ -176,9 +189,11 @@ def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H):
                   _lib.ptr(h), _lib.ptr(b.rowptr), _lib.ptr(b.csc_ptr), _lib.ptr(b.csc_eid),
                   _lib.ptr(b.csc_dst), _lib.ptr(b.edge_w), N, H, parts, _lib.ptr(dh),
                   _lib.ptr(gate), _lib.ptr(out), _lib.ptr(ws), code, flags, s)
-        outs[code] = (out.cpu().numpy().astype(np.float64), am.cpu().numpy())
-    got, am32 = outs[_lib.F32]
-    want, am64 = outs[_lib.F64]
+        outs[code] = (out.cpu().numpy().astype(np.float64), am.cpu().numpy(),
+                      agg.cpu().numpy().astype(np.float64))
+    got, am32, agg32 = outs[_lib.F32]
+    want, am64, agg64 = outs[_lib.F64]
+    assert_close_scaled(agg32, agg64, 1e-4, FP32_FLOOR, what=f"fwd {kind} H={H}")
     if parts & _lib.PART_MAX:
         # random normal features: no fp32 near-ties, so the routing agrees
         np.testing.assert_array_equal(am32, am64)
