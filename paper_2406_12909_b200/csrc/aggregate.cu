@@ -654,13 +654,12 @@ static bool vec_shape(int H, int& nv, int& lpn, int* slabs = nullptr) {
 #define GFM_VEC_CASES(MACRO) \
   MACRO(1, 1) MACRO(1, 2) MACRO(1, 4) MACRO(1, 8) MACRO(1, 16) MACRO(1, 32) MACRO(2, 32) MACRO(4, 32)
 
-// GFM_NO_AGG_TILE=1 selects the register-only gather kernels (A/B checks)
+// The shared-memory staged tiles are opt-in (GFM_AGG_TILE=1): measured on
+// B200 they lose to the register gathers at C2 and C3 (the gathers are
+// issue-bound, not L2-bound, and staging adds a serial phase per block).
 static bool no_tile() {
-  static const bool v = [] {
-    const char* e = getenv("GFM_NO_AGG_TILE");
-    return e && e[0] == '1';
-  }();
-  return v;
+  const char* e = getenv("GFM_AGG_TILE");
+  return !(e && e[0] == '1');
 }
 
 cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, const int* col_src,

@@ -156,10 +156,20 @@ def _wide_batch(H, dtype, seed, scattered=False):
     return recs, M.make_batch(as_records(recs), dtype=dtype)
 
 
+@pytest.fixture(params=["gather", "tile"])
+def agg_path(request, monkeypatch):
+    """register-gather kernels (default) or the opt-in smem-staged tiles"""
+    if request.param == "tile":
+        monkeypatch.setenv("GFM_AGG_TILE", "1")
+    else:
+        monkeypatch.delenv("GFM_AGG_TILE", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("scattered", [False, True])
 @pytest.mark.parametrize("kind", ["pna-agg", "max-agg"])
 @pytest.mark.parametrize("H", [64, 256, 512])
-def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H, scattered):
+def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H, scattered, agg_path):
     """float4 / column-slab / smem-staged forward + backward (F32) against the
     scalar F64 kernels."""
     parts, K = M.KIND_PARTS[kind], M._n_parts(kind)

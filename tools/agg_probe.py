@@ -1,6 +1,6 @@
 """Time gfm_agg_fwd / gfm_agg_bwd / force fwd+bwd on the bench workload's
 batch (CUDA events, L2 flushed between reps).
-Usage: python tools/agg_probe.py [--config c3]   (GFM_NO_AGG_TILE=1 for A/B)"""
+Usage: python tools/agg_probe.py [--config c3]   (GFM_AGG_TILE=1 for A/B)"""
 import argparse
 import os
 import sys
@@ -80,6 +80,6 @@ tf, tb = timeit(fwd), timeit(bwd)
 fb = E * H * 4 + 8 * E + 4 * (N + 1) + K * N * H * 4 + 8 * N * H
 comp_f = N * H * 4 + 8 * E + 4 * (N + 1) + K * N * H * 4 + 8 * N * H
 comp_b = 5 * N * H * 4 + 8 * E + 4 * (N + 1) + 2 * N * H * 4 + N * H * 4 * 2
-print(f"{a.config} N={N} E={E} H={H} tile={'off' if os.environ.get('GFM_NO_AGG_TILE') == '1' else 'on'}"
+print(f"{a.config} N={N} E={E} H={H} tile={'on' if os.environ.get('GFM_AGG_TILE') == '1' else 'off'}"
       f"  fwd {tf:8.1f} us ({comp_f / tf / 1e3:6.0f} GB/s compulsory, {fb / tf / 1e3:6.0f} GB/s survey)"
       f"  bwd {tb:8.1f} us ({comp_b / tb / 1e3:6.0f} GB/s compulsory)")
