@@ -46,6 +46,13 @@ inline bool tma_disabled() {
   return v != 0;
 }
 
+// GFM_NO_TMEM_A=1 keeps A in shared memory in the 3xTF32 TMA kernel (A/B runs)
+inline bool at_disabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("GFM_NO_TMEM_A") ? atoi(getenv("GFM_NO_TMEM_A")) : 0;
+  return v != 0;
+}
+
 constexpr int kBM = 128;       // MMA M (cta_group::1)
 constexpr int kBK = 32;        // fp32 elements per 128-byte swizzle row
 constexpr int kThreads = 256;  // 8 warps: staging + epilogue; thread 0 issues MMAs
@@ -676,34 +683,140 @@ __device__ __forceinline__ void tma_tile(const TmaOp& op, uint32_t dst, int r0, 
 // 2-slot ring for the converted lo copies.  Decoupling the two lets TMA run
 // kR k-blocks ahead (enough to cover L2/HBM latency at full MMA rate) while
 // the lo buffers, which only live from conversion to MMA completion, stay few.
-template <int BN>
+//
+// AT (A in TMEM, 3xTF32 with a K-major A): the converter warps read each raw
+// A row from smem once, split it into hi / lo in registers and tcgen05.st both
+// into TMEM; the MMAs take A from TMEM, so per k-block the smem traffic drops
+// from TMA 32K + lo pass 64K + 3 MMA reads of (A + B) 96K to TMA 32K + A read
+// 16K + B lo pass 32K + 3 MMA reads of B 48K (BN = 128) -- the MMA loop is
+// shared-memory-bandwidth bound, so this is its speed of light lever.
+template <int BN, bool AT = false>
 struct SmemT {
   static constexpr int kA = kBM * 128;
   static constexpr int kB = BN * 128;
   static constexpr int kRaw = kA + kB;
-  static constexpr int kL = 2;  // lo slots
-  static constexpr int kR = (224 * 1024 - kL * kRaw) / kRaw;  // raw stages
+  static constexpr int kLo = AT ? kB : kRaw;  // lo slot: B only when A lives in TMEM
+  // lo slots: conversion of k-block q + kL waits for the MMAs of q, so kL
+  // bounds how far the converters run ahead of the tensor pipe
+  static constexpr int kL = AT ? 4 : 3;
+  static constexpr int kR = (224 * 1024 - kL * kLo) / kRaw;  // raw stages
   static constexpr int kBars = (2 * kR + 2 * kL + 4) * 8 + 16;
-  static constexpr int kBytes = (kR + kL) * kRaw + 1024 + kBars;
+  static constexpr int kBytes = kR * kRaw + kL * kLo + 1024 + kBars;
   static_assert(kBytes <= 232448, "smem");
 };
+
+// 16 consecutive 32-bit TMEM columns of this warp's 32 lanes <- registers
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+      :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+         "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),
+         "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+}
+
+// D += A(TMEM) * B(smem descriptor)
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+      :: "r"(tmem_d), "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 
 constexpr int kConvWarps = 8;
 constexpr int kTmaThreads = (1 + kConvWarps + 1 + 4) * 32;  // TMA, converters, MMA, epilogue
 
-template <int BN, class Epi>
+// One 32-deep k-block of MMAs + the commits that release its buffers, issued
+// by the whole (converged) MMA warp with one elected lane inside the asm, so
+// descriptors stay in uniform registers (no per-MMA waterfall) and advance by
+// one 64-bit add per k-step (K-major: +32 B, MN-major: +1024 B).
+//   kb_at3: 3xTF32, A hi/lo in TMEM (ta = hi column; lo = ta + 32)
+//   kb_ss3: 3xTF32, all operands in smem descriptors
+//   kb_ss1: 1xTF32
+#define GFM_KB_PRE(ACC)                                             \
+  "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a0, a1, b0, b1;\n\t"        \
+  ".reg .b32 h, l;\n\t"                                              \
+  "elect.sync _|e, 0xffffffff;\n\t"                                  \
+  "setp.ne.b32 p, " ACC ", 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+#define GFM_MMA_T(A, B, EN, ID) \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [" A "], " B ", " ID ", " EN ";\n\t"
+#define GFM_MMA_S(A, B, EN, ID) \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], " A ", " B ", " ID ", " EN ";\n\t"
+#define GFM_COMMIT(BAR) \
+  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [" BAR "];\n\t"
+#define GFM_STEP_T(BI) \
+  "add.u32 h, h, 8;\n\tadd.u32 l, l, 8;\n\tadd.s64 b0, b0, " BI ";\n\tadd.s64 b1, b1, " BI ";\n\t"
+#define GFM_STEP_S(AI, BI) \
+  "add.s64 a0, a0, " AI ";\n\tadd.s64 a1, a1, " AI ";\n\tadd.s64 b0, b0, " BI ";\n\tadd.s64 b1, b1, " BI ";\n\t"
+
+__device__ __forceinline__ void kb_at3(uint32_t d, uint32_t ta, uint64_t bh, uint64_t bl,
+                                       uint64_t binc, uint32_t idesc, uint32_t acc0,
+                                       uint32_t bar0, uint32_t bar1) {
+#define T3 GFM_MMA_T("l", "b0", "t", "%5") GFM_MMA_T("h", "b1", "t", "%5") GFM_MMA_T("h", "b0", "t", "%5")
+  asm volatile(
+      GFM_KB_PRE("%6")
+      "mov.b64 b0, %2;\n\tmov.b64 b1, %3;\n\tmov.b32 h, %1;\n\tadd.u32 l, h, 32;\n\t"
+      GFM_MMA_T("l", "b0", "p", "%5") GFM_MMA_T("h", "b1", "t", "%5") GFM_MMA_T("h", "b0", "t", "%5")
+      GFM_STEP_T("%4") T3 GFM_STEP_T("%4") T3 GFM_STEP_T("%4") T3
+      GFM_COMMIT("%7") GFM_COMMIT("%8") "}\n"
+      :: "r"(d), "r"(ta), "l"(bh), "l"(bl), "l"(binc), "r"(idesc), "r"(acc0), "r"(bar0),
+         "r"(bar1) : "memory");
+#undef T3
+}
+
+__device__ __forceinline__ void kb_ss3(uint32_t d, uint64_t ah, uint64_t al, uint64_t ainc,
+                                       uint64_t bh, uint64_t bl, uint64_t binc, uint32_t idesc,
+                                       uint32_t acc0, uint32_t bar0, uint32_t bar1) {
+#define S3 GFM_MMA_S("a1", "b0", "t", "%7") GFM_MMA_S("a0", "b1", "t", "%7") GFM_MMA_S("a0", "b0", "t", "%7")
+  asm volatile(
+      GFM_KB_PRE("%8")
+      "mov.b64 a0, %1;\n\tmov.b64 a1, %2;\n\tmov.b64 b0, %4;\n\tmov.b64 b1, %5;\n\t"
+      GFM_MMA_S("a1", "b0", "p", "%7") GFM_MMA_S("a0", "b1", "t", "%7") GFM_MMA_S("a0", "b0", "t", "%7")
+      GFM_STEP_S("%3", "%6") S3 GFM_STEP_S("%3", "%6") S3 GFM_STEP_S("%3", "%6") S3
+      GFM_COMMIT("%9") GFM_COMMIT("%10") "}\n"
+      :: "r"(d), "l"(ah), "l"(al), "l"(ainc), "l"(bh), "l"(bl), "l"(binc), "r"(idesc),
+         "r"(acc0), "r"(bar0), "r"(bar1) : "memory");
+#undef S3
+}
+
+__device__ __forceinline__ void kb_ss1(uint32_t d, uint64_t ah, uint64_t ainc, uint64_t bh,
+                                       uint64_t binc, uint32_t idesc, uint32_t acc0,
+                                       uint32_t bar0) {
+  asm volatile(
+      GFM_KB_PRE("%6")
+      "mov.b64 a0, %1;\n\tmov.b64 b0, %3;\n\tmov.b64 a1, 0;\n\tmov.b64 b1, 0;\n\t"
+      GFM_MMA_S("a0", "b0", "p", "%5") GFM_STEP_S("%2", "%4")
+      GFM_MMA_S("a0", "b0", "t", "%5") GFM_STEP_S("%2", "%4")
+      GFM_MMA_S("a0", "b0", "t", "%5") GFM_STEP_S("%2", "%4")
+      GFM_MMA_S("a0", "b0", "t", "%5")
+      GFM_COMMIT("%7") "}\n"
+      :: "r"(d), "l"(ah), "l"(ainc), "l"(bh), "l"(binc), "r"(idesc), "r"(acc0), "r"(bar0)
+      : "memory");
+}
+#undef GFM_KB_PRE
+#undef GFM_MMA_T
+#undef GFM_MMA_S
+#undef GFM_COMMIT
+#undef GFM_STEP_T
+#undef GFM_STEP_S
+
+template <int BN, class Epi, bool AT>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     tc_gemm_tma_kernel(int M, const int* __restrict__ M_dev, int N, int K, int k_chunk, int splits,
                        int split3, const __grid_constant__ TmaOp ta,
                        const __grid_constant__ TmaOp tb, Epi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  using S = SmemT<BN>;
-  constexpr int NC = tmem_cols(2 * BN);
+  using S = SmemT<BN, AT>;
+  // TMEM: two BN-column accumulators, then (AT) kL A slots of 32 hi + 32 lo columns
+  constexpr int kACol = 2 * BN;
+  constexpr int NC = tmem_cols(2 * BN + (AT ? S::kL * 64 : 0));
   constexpr int kR = S::kR, kL = S::kL;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* lo_base = base + kR * S::kRaw;
-  uint64_t* tfl = reinterpret_cast<uint64_t*>(lo_base + kL * S::kRaw);  // TMA landed [kR]
+  uint64_t* tfl = reinterpret_cast<uint64_t*>(lo_base + kL * S::kLo);  // TMA landed [kR]
   uint64_t* empty = tfl + kR;    // MMAs done with the raw stage [kR]
   uint64_t* cvt = empty + kR;    // lo written [kL]
   uint64_t* lofree = cvt + kL;   // MMAs done with the lo slot [kL]
@@ -780,7 +893,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           const int s = q % kR, l = q % kL;
           mbar_wait(&tfl[s], (q / kR) & 1);
           if (q >= kL) mbar_wait(&lofree[l], ((q / kL) - 1) & 1);
-          make_lo<S::kRaw, kConvWarps * 32>(base + s * S::kRaw, lo_base + l * S::kRaw, ctid);
+          if constexpr (AT) {
+            // A row r = 32 * (warp % 4) + lane (this warp's TMEM lane quarter),
+            // k half h = (warp - 1) / 4: 4 swizzled 16-byte chunks -> hi / lo
+            const int q4 = warp & 3, h = (warp - 1) >> 2;
+            const int r = q4 * 32 + lane;
+            const uint32_t ra = smem_u32(base + s * S::kRaw) + (uint32_t)(r * 128);
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t a = ra + (uint32_t)((((4 * h + j) ^ (r & 7)) & 7) << 4);
+              uint32_t x[4];
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(a));
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                hi[4 * j + e] = x[e] & 0xFFFFE000u;
+                lo[4 * j + e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(hi[4 * j + e]));
+              }
+            }
+            const uint32_t ta_ = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(kACol + l * 64 + 16 * h);
+            tmem_st16(ta_, hi);
+            tmem_st16(ta_ + 32, lo);
+            make_lo<S::kB, kConvWarps * 32>(base + s * S::kRaw + S::kA, lo_base + l * S::kLo, ctid);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+          } else {
+            make_lo<S::kRaw, kConvWarps * 32>(base + s * S::kRaw, lo_base + l * S::kRaw, ctid);
+          }
           fence_async_smem();
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&cvt[l])) : "memory");
@@ -791,9 +931,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     // ============================================================ MMA issuer
     const bool a_mn = ta.mn != 0, b_mn = tb.mn != 0;
     const uint32_t idesc = make_idesc_tf32(BN, a_mn, b_mn);
-    auto desc = [&](bool mn, uint32_t addr, int ks) -> uint64_t {
-      return mn ? make_desc_mn(addr + ks * 1024, 4096, 512) : make_desc(addr + ks * 32);
+    // k-step 0 descriptor; later k-steps add ainc / binc (address field is >> 4)
+    auto desc0 = [&](bool mn, uint32_t addr) -> uint64_t {
+      return mn ? make_desc_mn(addr, 4096, 512) : make_desc(addr);
     };
+    const uint64_t ainc = a_mn ? 1024 >> 4 : 32 >> 4, binc = b_mn ? 1024 >> 4 : 32 >> 4;
     int q = 0, t = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
       const int nkb = nkb_of(w);
@@ -806,22 +948,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         mbar_wait(&tfl[s], (q / kR) & 1);
         if (split_on) mbar_wait(&cvt[l], (q / kL) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t ah = smem_u32(base + s * S::kRaw), bh = ah + S::kA;
-          const uint32_t al = smem_u32(lo_base + l * S::kRaw), bl = al + S::kA;
-#pragma unroll
-          for (int ks = 0; ks < kBK / 8; ++ks) {
-            const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
-            if (split_on) {
-              mma_tf32(d, desc(a_mn, al, ks), desc(b_mn, bh, ks), idesc, acc0);
-              mma_tf32(d, desc(a_mn, ah, ks), desc(b_mn, bl, ks), idesc, 1u);
-              mma_tf32(d, desc(a_mn, ah, ks), desc(b_mn, bh, ks), idesc, 1u);
-            } else {
-              mma_tf32(d, desc(a_mn, ah, ks), desc(b_mn, bh, ks), idesc, acc0);
-            }
-          }
-          mma_commit(&empty[s]);
-          if (split_on) mma_commit(&lofree[l]);
+        const uint32_t ah = smem_u32(base + s * S::kRaw), bh = ah + S::kA;
+        const uint32_t al = smem_u32(lo_base + l * S::kLo), bl = AT ? al : al + S::kA;
+        const uint32_t acc0 = kb > 0 ? 1u : 0u;
+        const uint32_t e_bar = smem_u32(&empty[s]), l_bar = smem_u32(&lofree[l]);
+        if constexpr (AT) {
+          kb_at3(d, tmem + (uint32_t)(kACol + l * 64), desc0(b_mn, bh), desc0(b_mn, bl), binc,
+                 idesc, acc0, e_bar, l_bar);
+        } else if (split_on) {
+          kb_ss3(d, desc0(a_mn, ah), desc0(a_mn, al), ainc, desc0(b_mn, bh), desc0(b_mn, bl),
+                 binc, idesc, acc0, e_bar, l_bar);
+        } else {
+          kb_ss1(d, desc0(a_mn, ah), ainc, desc0(b_mn, bh), binc, idesc, acc0, e_bar);
         }
         __syncwarp();
       }
@@ -879,8 +1017,9 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
   if (!K_dev && !tma_disabled()) {
     TmaOp ta, tb;
     if (build_tma(a, &ta, kBM, M, K) && build_tma(b, &tb, BN, N, K)) {
-      auto kern = tc_gemm_tma_kernel<BN, Epi>;
-      const int smem = SmemT<BN>::kBytes;
+      const bool at = split3 != 0 && ta.mn == 0 && !at_disabled();
+      auto kern = at ? tc_gemm_tma_kernel<BN, Epi, true> : tc_gemm_tma_kernel<BN, Epi, false>;
+      const int smem = at ? SmemT<BN, true>::kBytes : SmemT<BN, false>::kBytes;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
       kern<<<grid, kTmaThreads, smem, s>>>(M, M_dev, N, K, k_chunk, splits, split3, ta, tb, epi);
