@@ -326,9 +326,12 @@ __device__ __forceinline__ void make_lo(const uint8_t* raw, uint8_t* lo, int tid
   }
 }
 
+// Work items are ordered split-major (w = split * tiles + tile): the CTAs in
+// flight together share one K range, so a split-K GEMM streams each operand
+// slice from HBM once and reuses it from L2 across all output tiles.
 // Work item -> number of 32-wide k-blocks
-__device__ __forceinline__ int item_nkb(int w, int splits, int k_chunk, int k_total) {
-  const int split = w % splits;
+__device__ __forceinline__ int item_nkb(int w, int tiles, int k_chunk, int k_total) {
+  const int split = w / tiles;
   const int kb0 = split * k_chunk, kb1 = min(k_total, kb0 + k_chunk);
   return kb1 > kb0 ? (kb1 - kb0 + kBK - 1) / kBK : 0;
 }
@@ -392,9 +395,9 @@ __global__ void __launch_bounds__(kWSThreads, 1)
   const bool split_on = split3 != 0;
 
   auto tile_of = [&](int w, int& bm, int& bn, int& split) {
-    split = w % splits;
-    bn = (w / splits) % n_tiles;
-    bm = w / (splits * n_tiles);
+    split = w / (m_tiles * n_tiles);
+    bn = (w % (m_tiles * n_tiles)) % n_tiles;
+    bm = (w % (m_tiles * n_tiles)) / n_tiles;
   };
 
   if (warp < kProducers / 32) {
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(kWSThreads, 1)
     int pw = blockIdx.x, pkb = 0, p = 0;  // issue cursor
     int cw = blockIdx.x, ckb = 0, q = 0;  // convert cursor
     auto skip_empty = [&](int& w, int& kb) {
-      while (w < n_work && item_nkb(w, splits, k_chunk, k_total) == 0) w += gridDim.x;
+      while (w < n_work && item_nkb(w, m_tiles * n_tiles, k_chunk, k_total) == 0) w += gridDim.x;
       kb = 0;
     };
     skip_empty(pw, pkb);
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(kWSThreads, 1)
         issue_tile<kBM, VA, kProducers>(a, bm * kBM, min(kBM, m_total - bm * kBM), k0, kv, st, tid);
         issue_tile<BN, VB, kProducers>(b, bn * BN, min(BN, N - bn * BN), k0, kv, st + S::kA, tid);
         ++p;
-        if (++pkb == item_nkb(pw, splits, k_chunk, k_total)) {
+        if (++pkb == item_nkb(pw, m_tiles * n_tiles, k_chunk, k_total)) {
           pw += gridDim.x;
           skip_empty(pw, pkb);
         }
@@ -444,7 +447,7 @@ __global__ void __launch_bounds__(kWSThreads, 1)
       asm volatile("bar.sync 1, %0;" :: "n"(kProducers) : "memory");
       if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&full[s])) : "memory");
       ++q;
-      if (++ckb == item_nkb(cw, splits, k_chunk, k_total)) {
+      if (++ckb == item_nkb(cw, m_tiles * n_tiles, k_chunk, k_total)) {
         cw += gridDim.x;
         skip_empty(cw, ckb);
       }
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(kWSThreads, 1)
     };
     int q = 0, t = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
-      const int nkb = item_nkb(w, splits, k_chunk, k_total);
+      const int nkb = item_nkb(w, m_tiles * n_tiles, k_chunk, k_total);
       const int acc = t & 1;
       if (t >= 2) mbar_wait(&tempty[acc], ((t >> 1) - 1) & 1);
       tc_fence_after();
@@ -511,7 +514,7 @@ __global__ void __launch_bounds__(kWSThreads, 1)
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
       int bm, bn, split;
       tile_of(w, bm, bn, split);
-      const int nkb = item_nkb(w, splits, k_chunk, k_total);
+      const int nkb = item_nkb(w, m_tiles * n_tiles, k_chunk, k_total);
       const int acc = t & 1;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
@@ -549,6 +552,12 @@ __global__ void __launch_bounds__(kWSThreads, 1)
 // 128B_ATOM_32B == SWIZZLE_128B_BASE32B with LBO = 4096 (atom), SBO = 512.
 struct TmaOp {
   CUtensorMap map[3];
+  // MN-major only: 3D view {32, K, extent / 32} of a segment whose extent is a
+  // multiple of 32, so one TMA instruction fetches a whole 128-row tile (four
+  // 32-row atoms, smem [atom][k][32]) instead of four 4 KB boxes -- the per-box
+  // cost of narrow boxes, not bandwidth, bounds MN-major streaming
+  CUtensorMap map3[3];
+  int has3[3];
   int split_at;  // start of segment 1
   int split2;    // start of segment 2 (MN-major: the ones row of a bias gradient)
   int mn;
@@ -588,6 +597,21 @@ inline bool make_map(CUtensorMap* m, const float* base, long long inner, long lo
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3D MN-major view: dims {32, K, extent / 32}, strides {ld, 32} elements,
+// box {32, kBK, 4}
+inline bool make_map3(CUtensorMap* m, const float* base, long long extent, long long K, long long ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || !base || extent <= 0 || extent % 32 || K <= 0) return false;
+  if (((uintptr_t)base & 15) || ((ld * 4) & 15)) return false;
+  cuuint64_t dims[3] = {32, (cuuint64_t)K, (cuuint64_t)(extent / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), 128};
+  cuuint32_t box[3] = {32, (cuuint32_t)kBK, 4};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Loader -> TMA operand (false when the loader cannot be expressed)
 template <class L>
 inline bool build_tma(const L&, TmaOp*, int, long long, int) { return false; }
@@ -598,6 +622,7 @@ inline bool build_tma(const RowsLd<T>& l, TmaOp* op, int rows_box, long long row
   op->mn = 0;
   op->split_at = 1 << 30;
   op->split2 = 1 << 30;
+  op->has3[0] = op->has3[1] = op->has3[2] = 0;
   return make_map(&op->map[0], (const float*)l.p, K, rows_total, l.ld, kBK, rows_box,
                   CU_TENSOR_MAP_SWIZZLE_128B);
 }
@@ -608,6 +633,7 @@ inline bool build_tma(const Rows2Ld<T>& l, TmaOp* op, int rows_box, long long ro
   op->mn = 0;
   op->split_at = l.k2 > 0 ? l.k1 : (1 << 30);
   op->split2 = 1 << 30;
+  op->has3[0] = op->has3[1] = op->has3[2] = 0;
   if (l.k2 > 0 && l.k1 % kBK) return false;
   if (!make_map(&op->map[0], (const float*)l.p1, l.k1, rows_total, l.ld1, kBK, rows_box,
                 CU_TENSOR_MAP_SWIZZLE_128B))
@@ -622,8 +648,12 @@ inline bool build_tma(const ColsLd<T>& l, TmaOp* op, int, long long rows_total, 
   op->mn = 1;
   op->split_at = 1 << 30;
   op->split2 = 1 << 30;
-  return make_map(&op->map[0], (const float*)l.p, rows_total, K, l.ld, 32, kBK,
-                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  op->has3[0] = op->has3[1] = op->has3[2] = 0;
+  if (!make_map(&op->map[0], (const float*)l.p, rows_total, K, l.ld, 32, kBK,
+                CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return false;
+  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p, rows_total, K, l.ld);
+  return true;
 }
 
 template <typename T>
@@ -635,6 +665,7 @@ inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int, long long rows_total,
   if (sizeof(T) != 4 || (rows_total > l.n1 + l.n2 && !(bias && l.ones))) return false;
   if ((l.n2 > 0 && l.n1 % 32) || (bias && (l.n1 + l.n2) % 32)) return false;
   op->mn = 1;
+  op->has3[0] = op->has3[1] = op->has3[2] = 0;
   op->split_at = l.n2 > 0 ? l.n1 : (bias ? l.n1 : (1 << 30));
   op->split2 = bias ? l.n1 + l.n2 : (1 << 30);
   if (!make_map(&op->map[0], (const float*)l.p1, l.n1, K, l.ld1, 32, kBK,
@@ -647,6 +678,9 @@ inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int, long long rows_total,
                         CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return false;
   if (bias && l.n2 == 0) op->map[1] = op->map[2];  // segment 1 empty: route to the ones map
+  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p1, l.n1, K, l.ld1);
+  op->has3[1] = l.n2 > 0 && make_map3(&op->map3[1], (const float*)l.p2, l.n2, K, l.ld2);
+  op->has3[2] = 0;
   return true;
 }
 
@@ -655,6 +689,13 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      :: "r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -669,6 +710,19 @@ __device__ __forceinline__ void tma_tile(const TmaOp& op, uint32_t dst, int r0, 
     const int seg = k0 >= op.split_at;
     tma_load_2d(dst, &op.map[seg], seg ? k0 - op.split_at : k0, r0, bar);
   } else {
+    // one 3D load when the whole tile lies in a segment with a 3D view (rows
+    // past the last segment's end are TMA zero fill either way)
+    if constexpr (ROWS % 128 == 0) {
+      const int seg = r0 >= op.split2 ? 2 : (r0 >= op.split_at ? 1 : 0);
+      const int s0 = seg == 2 ? op.split2 : (seg == 1 ? op.split_at : 0);
+      const int s1 = seg == 0 ? op.split_at : (seg == 1 ? op.split2 : (1 << 30));
+      if (op.has3[seg] && (r0 + ROWS <= s1 || s1 >= (1 << 30))) {
+#pragma unroll
+        for (int at = 0; at < ROWS / 128; ++at)
+          tma_load_3d(dst + at * 16384, &op.map3[seg], 0, k0, (r0 - s0) / 32 + at * 4, bar);
+        return;
+      }
+    }
 #pragma unroll
     for (int at = 0; at < ROWS / 32; ++at) {
       const int ra = r0 + at * 32;
@@ -857,11 +911,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   auto tile_of = [&](int w, int& bm, int& bn, int& split) {
-    split = w % splits;
-    bn = (w / splits) % n_tiles;
-    bm = w / (splits * n_tiles);
+    split = w / (m_tiles * n_tiles);
+    bn = (w % (m_tiles * n_tiles)) % n_tiles;
+    bm = (w % (m_tiles * n_tiles)) / n_tiles;
   };
-  auto nkb_of = [&](int w) { return item_nkb(w, splits, k_chunk, K); };
+  auto nkb_of = [&](int w) { return item_nkb(w, m_tiles * n_tiles, k_chunk, K); };
 
   if (warp == 0) {
     // ============================================================ TMA producer
