@@ -599,7 +599,8 @@ inline bool make_map(CUtensorMap* m, const float* base, long long inner, long lo
 
 // 3D MN-major view: dims {32, K, extent / 32}, strides {ld, 32} elements,
 // box {32, kBK, 4}
-inline bool make_map3(CUtensorMap* m, const float* base, long long extent, long long K, long long ld) {
+inline bool make_map3(CUtensorMap* m, const float* base, long long extent, long long K, long long ld,
+                      CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn || !base || extent <= 0 || extent % 32 || K <= 0) return false;
   if (((uintptr_t)base & 15) || ((ld * 4) & 15)) return false;
@@ -608,16 +609,20 @@ inline bool make_map3(CUtensorMap* m, const float* base, long long extent, long 
   cuuint32_t box[3] = {32, (cuuint32_t)kBK, 4};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Loader -> TMA operand (false when the loader cannot be expressed)
 template <class L>
-inline bool build_tma(const L&, TmaOp*, int, long long, int) { return false; }
+inline bool build_tma(const L&, TmaOp*, int, long long, int,
+                      CUtensorMapSwizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
+  return false;
+}
 
 template <typename T>
-inline bool build_tma(const RowsLd<T>& l, TmaOp* op, int rows_box, long long rows_total, int K) {
+inline bool build_tma(const RowsLd<T>& l, TmaOp* op, int rows_box, long long rows_total, int K,
+                      CUtensorMapSwizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
   if (sizeof(T) != 4) return false;
   op->mn = 0;
   op->split_at = 1 << 30;
@@ -628,7 +633,8 @@ inline bool build_tma(const RowsLd<T>& l, TmaOp* op, int rows_box, long long row
 }
 
 template <typename T>
-inline bool build_tma(const Rows2Ld<T>& l, TmaOp* op, int rows_box, long long rows_total, int K) {
+inline bool build_tma(const Rows2Ld<T>& l, TmaOp* op, int rows_box, long long rows_total, int K,
+                      CUtensorMapSwizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
   if (sizeof(T) != 4 || K > l.k1 + l.k2) return false;
   op->mn = 0;
   op->split_at = l.k2 > 0 ? l.k1 : (1 << 30);
@@ -643,21 +649,22 @@ inline bool build_tma(const Rows2Ld<T>& l, TmaOp* op, int rows_box, long long ro
 }
 
 template <typename T>
-inline bool build_tma(const ColsLd<T>& l, TmaOp* op, int, long long rows_total, int K) {
+inline bool build_tma(const ColsLd<T>& l, TmaOp* op, int, long long rows_total, int K,
+                      CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
   if (sizeof(T) != 4) return false;
   op->mn = 1;
   op->split_at = 1 << 30;
   op->split2 = 1 << 30;
   op->has3[0] = op->has3[1] = op->has3[2] = 0;
-  if (!make_map(&op->map[0], (const float*)l.p, rows_total, K, l.ld, 32, kBK,
-                CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+  if (!make_map(&op->map[0], (const float*)l.p, rows_total, K, l.ld, 32, kBK, sw))
     return false;
-  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p, rows_total, K, l.ld);
+  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p, rows_total, K, l.ld, sw);
   return true;
 }
 
 template <typename T>
-inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int, long long rows_total, int K) {
+inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int, long long rows_total, int K,
+                      CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
   // the virtual ones row (bias) needs the caller's ones buffer (a [K][4]
   // tensor whose column 0 is 1: inner extent 1, the rest of each 32-row box
   // is TMA zero fill)
@@ -668,18 +675,15 @@ inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int, long long rows_total,
   op->has3[0] = op->has3[1] = op->has3[2] = 0;
   op->split_at = l.n2 > 0 ? l.n1 : (bias ? l.n1 : (1 << 30));
   op->split2 = bias ? l.n1 + l.n2 : (1 << 30);
-  if (!make_map(&op->map[0], (const float*)l.p1, l.n1, K, l.ld1, 32, kBK,
-                CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+  if (!make_map(&op->map[0], (const float*)l.p1, l.n1, K, l.ld1, 32, kBK, sw))
     return false;
-  if (l.n2 > 0 && !make_map(&op->map[1], (const float*)l.p2, l.n2, K, l.ld2, 32, kBK,
-                            CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+  if (l.n2 > 0 && !make_map(&op->map[1], (const float*)l.p2, l.n2, K, l.ld2, 32, kBK, sw))
     return false;
-  if (bias && !make_map(&op->map[2], (const float*)l.ones, 1, K, 4, 32, kBK,
-                        CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+  if (bias && !make_map(&op->map[2], (const float*)l.ones, 1, K, 4, 32, kBK, sw))
     return false;
   if (bias && l.n2 == 0) op->map[1] = op->map[2];  // segment 1 empty: route to the ones map
-  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p1, l.n1, K, l.ld1);
-  op->has3[1] = l.n2 > 0 && make_map3(&op->map3[1], (const float*)l.p2, l.n2, K, l.ld2);
+  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p1, l.n1, K, l.ld1, sw);
+  op->has3[1] = l.n2 > 0 && make_map3(&op->map3[1], (const float*)l.p2, l.n2, K, l.ld2, sw);
   op->has3[2] = 0;
   return true;
 }
@@ -856,13 +860,16 @@ __device__ __forceinline__ void kb_ss1(uint32_t d, uint64_t ah, uint64_t ainc, u
 #undef GFM_STEP_T
 #undef GFM_STEP_S
 
-template <int BN, class Epi, bool AT>
+// AT: 0 = A in smem; 1 = A in TMEM, staged K-major SWIZZLE_128B; 2 = A in
+// TMEM, staged MN-major without swizzle ([32-row atom][k][32], so converter
+// lane r reads its row down the k column conflict-free)
+template <int BN, class Epi, int AT>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     tc_gemm_tma_kernel(int M, const int* __restrict__ M_dev, int N, int K, int k_chunk, int splits,
                        int split3, const __grid_constant__ TmaOp ta,
                        const __grid_constant__ TmaOp tb, Epi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  using S = SmemT<BN, AT>;
+  using S = SmemT<BN, AT != 0>;
   // TMEM: two BN-column accumulators, then (AT) kL A slots of 32 hi + 32 lo columns
   constexpr int kACol = 2 * BN;
   constexpr int NC = tmem_cols(2 * BN + (AT ? S::kL * 64 : 0));
@@ -947,24 +954,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           const int s = q % kR, l = q % kL;
           mbar_wait(&tfl[s], (q / kR) & 1);
           if (q >= kL) mbar_wait(&lofree[l], ((q / kL) - 1) & 1);
-          if constexpr (AT) {
+          if constexpr (AT != 0) {
             // A row r = 32 * (warp % 4) + lane (this warp's TMEM lane quarter),
-            // k half h = (warp - 1) / 4: 4 swizzled 16-byte chunks -> hi / lo
+            // k half h = (warp - 1) / 4 -> 16 hi / lo values
             const int q4 = warp & 3, h = (warp - 1) >> 2;
             const int r = q4 * 32 + lane;
-            const uint32_t ra = smem_u32(base + s * S::kRaw) + (uint32_t)(r * 128);
             uint32_t hi[16], lo[16];
+            if constexpr (AT == 1) {  // 4 swizzled 16-byte chunks of the row
+              const uint32_t ra = smem_u32(base + s * S::kRaw) + (uint32_t)(r * 128);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t a = ra + (uint32_t)((((4 * h + j) ^ (r & 7)) & 7) << 4);
-              uint32_t x[4];
-              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(a));
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                hi[4 * j + e] = x[e] & 0xFFFFE000u;
-                lo[4 * j + e] = __float_as_uint(__uint_as_float(x[e]) - __uint_as_float(hi[4 * j + e]));
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t a = ra + (uint32_t)((((4 * h + j) ^ (r & 7)) & 7) << 4);
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(hi[4 * j]), "=r"(hi[4 * j + 1]), "=r"(hi[4 * j + 2]),
+                               "=r"(hi[4 * j + 3]) : "r"(a));
               }
+            } else {  // atom q4, column lane, k rows 16h.. (128-byte row stride)
+              const uint32_t ra = smem_u32(base + s * S::kRaw) +
+                                  (uint32_t)(q4 * 4096 + (16 * h) * 128 + lane * 4);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(hi[j]) : "r"(ra + 128u * j));
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t x = hi[e];
+              hi[e] = x & 0xFFFFE000u;
+              lo[e] = __float_as_uint(__uint_as_float(x) - __uint_as_float(hi[e]));
             }
             const uint32_t ta_ = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(kACol + l * 64 + 16 * h);
             tmem_st16(ta_, hi);
@@ -983,7 +999,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ============================================================ MMA issuer
-    const bool a_mn = ta.mn != 0, b_mn = tb.mn != 0;
+    // (A from TMEM is always row = lane, k = column: K-major in the idesc)
+    const bool a_mn = AT == 0 && ta.mn != 0, b_mn = tb.mn != 0;
     const uint32_t idesc = make_idesc_tf32(BN, a_mn, b_mn);
     // k-step 0 descriptor; later k-steps add ainc / binc (address field is >> 4)
     auto desc0 = [&](bool mn, uint32_t addr) -> uint64_t {
@@ -1003,10 +1020,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         if (split_on) mbar_wait(&cvt[l], (q / kL) & 1);
         tc_fence_after();
         const uint32_t ah = smem_u32(base + s * S::kRaw), bh = ah + S::kA;
-        const uint32_t al = smem_u32(lo_base + l * S::kLo), bl = AT ? al : al + S::kA;
+        const uint32_t al = smem_u32(lo_base + l * S::kLo), bl = AT != 0 ? al : al + S::kA;
         const uint32_t acc0 = kb > 0 ? 1u : 0u;
         const uint32_t e_bar = smem_u32(&empty[s]), l_bar = smem_u32(&lofree[l]);
-        if constexpr (AT) {
+        if constexpr (AT != 0) {
           kb_at3(d, tmem + (uint32_t)(kACol + l * 64), desc0(b_mn, bh), desc0(b_mn, bl), binc,
                  idesc, acc0, e_bar, l_bar);
         } else if (split_on) {
@@ -1071,8 +1088,20 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
   if (!K_dev && !tma_disabled()) {
     TmaOp ta, tb;
     if (build_tma(a, &ta, kBM, M, K) && build_tma(b, &tb, BN, N, K)) {
-      const bool at = split3 != 0 && ta.mn == 0 && !at_disabled();
-      auto kern = at ? tc_gemm_tma_kernel<BN, Epi, true> : tc_gemm_tma_kernel<BN, Epi, false>;
+      // 3xTF32: A goes through TMEM (K-major as staged; MN-major re-mapped
+      // without swizzle for the converters)
+      int at = 0;
+      if (split3 != 0 && !at_disabled()) {
+        if (ta.mn == 0)
+          at = 1;
+        else if (build_tma(a, &ta, kBM, M, K, CU_TENSOR_MAP_SWIZZLE_NONE))
+          at = 2;
+        else
+          build_tma(a, &ta, kBM, M, K);
+      }
+      auto kern = at == 1   ? tc_gemm_tma_kernel<BN, Epi, 1>
+                  : at == 2 ? tc_gemm_tma_kernel<BN, Epi, 2>
+                            : tc_gemm_tma_kernel<BN, Epi, 0>;
       const int smem = at ? SmemT<BN, true>::kBytes : SmemT<BN, false>::kBytes;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
