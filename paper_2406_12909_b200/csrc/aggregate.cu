@@ -467,8 +467,10 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
   }
   const int qb = csc_ptr[j], qe = csc_ptr[j + 1];
   // U CSC slots per batch: all their row loads issue before the (in-order)
-  // accumulation, so U x 3 gathers per lane are in flight
-  constexpr int U = 2;
+  // accumulation, so U x 3 gathers per lane are in flight.  Narrow rows
+  // (LPN < 32: several nodes per warp) are issue-bound rather than latency-
+  // bound and measure faster unbatched.
+  constexpr int U = LPN == 32 ? 2 : 1;
   for (int q = qb; q < qe; q += U) {
     int p[U], i[U];
     float ww[U];

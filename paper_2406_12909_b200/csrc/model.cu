@@ -24,13 +24,68 @@ static inline int grid_1d(long long n, int threads = 256) {
 // ------------------------------------------------------------ reductions
 // out segment mapping for split-K weight grads: result matrix R[N][Kt] with
 // Kt = K1 + K2 (+1 bias column) is written to three destinations.
-// Block = 32 x 8 threads: x over 32 consecutive outputs, y over split groups
-// (split = y, y + 8, ...); the 8 group sums are combined in order in smem --
-// float64 accumulation, fixed order, 8x the parallelism of a serial walk.
+// Split-K reduction: partials ws[split][R][C] (R x C = N x Kt, or Kt x N when
+// trans) summed in split order in fp64.  A block owns a 32 x 32 tile; each
+// thread keeps 4 independent sums (rows ty, ty + 8, ...) so 4 x unroll loads
+// are in flight, then the tile goes out through smem so the [N][K] gradient
+// rows are written coalesced in both layouts.
 template <typename T>
 __global__ void __launch_bounds__(256)
     k_splitk_reduce(const T* __restrict__ ws, int splits, int N, int K1, int K2, int with_bias,
                     T* __restrict__ g1, T* __restrict__ g2, T* __restrict__ gb, int trans) {
+  __shared__ T tile[32][33];
+  const int Kt = K1 + K2 + with_bias;
+  const int R = trans ? Kt : N, C = trans ? N : Kt;
+  const long long total = (long long)R * C;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int c = c0 + tx;
+#pragma unroll 4
+  for (int sp = 0; sp < splits; ++sp) {
+    const T* w = ws + (long long)sp * total;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = r0 + ty + 8 * j;
+      if (r < R && c < C) acc[j] += (double)w[(long long)r * C + c];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) tile[ty + 8 * j][tx] = (T)acc[j];
+  __syncthreads();
+  // write: element (n, k) of the [N][Kt] gradient; threads walk k fastest
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int n, k;
+    T v;
+    if (trans) {  // tile rows = k (r0..), cols = n (c0..)
+      n = c0 + ty + 8 * j;
+      k = r0 + tx;
+      v = tile[tx][ty + 8 * j];
+    } else {      // tile rows = n, cols = k
+      n = r0 + ty + 8 * j;
+      k = c0 + tx;
+      v = tile[ty + 8 * j][tx];
+    }
+    if (n >= N || k >= Kt) continue;
+    if (k < K1)
+      g1[(long long)n * K1 + k] = v;
+    else if (k < K1 + K2)
+      g2[(long long)n * K2 + (k - K1)] = v;
+    else
+      gb[n] = v;
+  }
+}
+
+// Small outputs: block = 32 x 8 threads, x over 32 consecutive partial
+// elements, y over split groups (split = y, y + 8, ...); the 8 group sums are
+// combined in order in smem -- fixed order, 8x the parallelism of a serial
+// walk when there are too few 32 x 32 tiles to fill the GPU.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_splitk_reduce_narrow(const T* __restrict__ ws, int splits, int N, int K1, int K2,
+                           int with_bias, T* __restrict__ g1, T* __restrict__ g2,
+                           T* __restrict__ gb, int trans) {
   __shared__ double red[8][33];
   const int Kt = K1 + K2 + with_bias;
   const long long total = (long long)N * Kt;
@@ -49,17 +104,31 @@ __global__ void __launch_bounds__(256)
       for (int q = 0; q < 8; ++q) a += red[q][tx];
     __syncthreads();
     if (ty != 0 || idx >= total) continue;
-    const T s = (T)a;
+    const T v = (T)a;
     // partials are [N][Kt] (trans = 0) or [Kt][N] (trans = 1); idx walks them
     const int n = trans ? (int)(idx % N) : (int)(idx / Kt);
     const int k = trans ? (int)(idx / N) : (int)(idx % Kt);
     if (k < K1)
-      g1[(long long)n * K1 + k] = s;
+      g1[(long long)n * K1 + k] = v;
     else if (k < K1 + K2)
-      g2[(long long)n * K2 + (k - K1)] = s;
+      g2[(long long)n * K2 + (k - K1)] = v;
     else
-      gb[n] = s;
+      gb[n] = v;
   }
+}
+
+template <typename T>
+void splitk_reduce(const T* ws, int splits, int N, int K1, int K2, int with_bias, T* g1, T* g2,
+                   T* gb, int trans, cudaStream_t s) {
+  const int Kt = K1 + K2 + with_bias;
+  const int R = trans ? Kt : N, C = trans ? N : Kt;
+  const long long tiles = (long long)ceil_div(C, 32) * ceil_div(R, 32);
+  if (tiles >= 2 * 148)
+    k_splitk_reduce<T><<<dim3(ceil_div(C, 32), ceil_div(R, 32)), 256, 0, s>>>(
+        ws, splits, N, K1, K2, with_bias, g1, g2, gb, trans);
+  else
+    k_splitk_reduce_narrow<T><<<grid_1d((long long)N * Kt, 32), 256, 0, s>>>(
+        ws, splits, N, K1, K2, with_bias, g1, g2, gb, trans);
 }
 
 // node_e[i] = y[i] . a + c   (model.py:372)
@@ -301,8 +370,7 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
   }
 reduce:
   if (e != cudaSuccess) return e;
-  k_splitk_reduce<T><<<grid_1d((long long)N * Kt, 32), 256, 0, s>>>(ws, real, N, K1, K2, with_bias,
-                                                                 g1, g2, gb, trans);
+  splitk_reduce<T>(ws, real, N, K1, K2, with_bias, g1, g2, gb, trans, s);
   return cudaGetLastError();
 }
 
@@ -386,8 +454,7 @@ cudaError_t embedding_grad_t(const int* z, int n_nodes, const T* dh, int H, T* g
   }
 reduce:
   if (e != cudaSuccess) return e;
-  k_splitk_reduce<T><<<grid_1d((long long)E * H, 32), 256, 0, s>>>(ws, real, E, H, 0, 0, grad,
-                                                                    nullptr, nullptr, 0);
+  splitk_reduce<T>(ws, real, E, H, 0, 0, grad, nullptr, nullptr, 0, s);
   return cudaGetLastError();
 }
 
