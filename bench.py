@@ -299,48 +299,95 @@ def run_native(args):
     e2e_value = world * B * args.steps / float(e2e_s.item())
     graph = runner.graph
 
-    # ---- roofline of the aggregation kernel (CUDA events on the launch stream)
+    # ---- roofline of the aggregation kernels (CUDA events on the launch
+    # stream, L2 flushed before every launch): the backward CSC gather is the
+    # step's largest kernel at C2 and C3 (profiles/r01_launches_*), the forward
+    # is reported beside it
     load_slot(0)
     runner._eager()
     b = runner.batch
     torch.cuda.synchronize()
     E = b.n_edges
     H, K = cfg.mpnn_width, cfg.n_parts
+    parts = M.KIND_PARTS[cfg.mpnn_kind]
     h_in = torch.randn(N, H, device=dev)
     agg = torch.empty(N, K * H, device=dev)
     am = torch.empty(N, H, dtype=torch.int32, device=dev)
     sm_ = torch.empty(N, H, device=dev)
+    dagg = torch.randn(N, K * H, device=dev)
+    dh_b = torch.randn(N, H, device=dev)
+    out_b = torch.empty(N, H, device=dev)
+    ws_b = torch.empty(_lib.query("gfm_agg_bwd_workspace_bytes", N, H, parts, _lib.F32),
+                       dtype=torch.uint8, device=dev)
     sh = _lib.stream_handle()
+    P_ = _lib.ptr
 
-    def agg_call():
-        _lib.call("gfm_agg_fwd", _lib.ptr(h_in), N, H, _lib.ptr(b.rowptr), _lib.ptr(b.col_src),
-                  _lib.ptr(b.edge_w), M.KIND_PARTS[cfg.mpnn_kind], _lib.ptr(agg), _lib.ptr(am),
-                  _lib.ptr(sm_), _lib.F32, 0, sh)
+    def agg_fwd_call():
+        _lib.call("gfm_agg_fwd", P_(h_in), N, H, P_(b.rowptr), P_(b.col_src), P_(b.edge_w),
+                  parts, P_(agg), P_(am), P_(sm_), _lib.F32, 0, sh)
+
+    def agg_bwd_call():
+        _lib.call("gfm_agg_bwd", P_(dagg), P_(agg), P_(sm_), P_(am), P_(h_in), P_(b.rowptr),
+                  P_(b.csc_ptr), P_(b.csc_eid), P_(b.csc_dst), P_(b.edge_w), N, H, parts,
+                  P_(dh_b), P_(h_in), P_(out_b), P_(ws_b), _lib.F32, 0, sh)
 
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
-    for _ in range(3):
-        agg_call()
-    reps, tot = 20, 0.0
-    for _ in range(reps):
-        flush.zero_()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(s)
-        agg_call()
-        a1.record(s)
-        torch.cuda.synchronize()
-        tot += a0.elapsed_time(a1)
-    agg_ms = tot / reps
-    # SURVEY 8(d) C5 forward formula (fused h + src + w mode), s = 4 bytes:
-    # E*H*s (gathered rows) + 4E src + 4E w + 4(N+1) rowptr + K*N*H*s out
-    # + 4*N*H argmax + 4*N*H std mean
-    agg_bytes = E * H * 4 + 8 * E + 4 * (N + 1) + K * N * H * 4 + 4 * N * H + 4 * N * H
+
+    def launch_ms(fn, reps=20):
+        for _ in range(3):
+            fn()
+        tot = 0.0
+        for _ in range(reps):
+            flush.zero_()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(s)
+            fn()
+            a1.record(s)
+            torch.cuda.synchronize()
+            tot += a0.elapsed_time(a1)
+        return tot / reps
+
+    agg_fwd_call()
+    fwd_ms, bwd_ms = launch_ms(agg_fwd_call), launch_ms(agg_bwd_call)
+    # SURVEY 8(d) C5 formulas (fused h + src + w mode), s = 4 bytes.
+    # fwd: E*H*s gathered rows + 4E src + 4E w + 4(N+1) rowptr + K*N*H*s out
+    #      + 4*N*H argmax + 4*N*H std mean
+    fwd_bytes = E * H * 4 + 8 * E + 4 * (N + 1) + K * N * H * 4 + 4 * N * H + 4 * N * H
+    # bwd (CSC gather): E*H*s (G rows) + 8E (eid, dst) + 4(N+1) + N*H*s (dh in)
+    #      + E*H*4 argmax (max part) + E*H*s coef (std part) + 4E w + N*H*s out
+    #      + N*H*s h_in (std coef) + N*H*s gate
+    #      + 7*N*H*s for the prep pass the same call launches first (reads dsum,
+    #      dmean, dstd, std, mean; writes G, coef)
+    bwd_bytes = (E * H * 4 + 8 * E + 4 * (N + 1) + N * H * 4 + E * H * 4 + E * H * 4 + 4 * E
+                 + 3 * N * H * 4 + 7 * N * H * 4)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = agg_bytes / (agg_ms / 1e3) / 1e9
+    # DRAM bytes per launch from the committed ncu --set full capture of the
+    # same kernels on this workload (tools/ncu_agg_traffic.sh), when present
+    traffic = {}
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", f"r01_agg_traffic_{args.config}.json")))
+        if tr.get("config") == args.config:
+            traffic = tr
+    except Exception:
+        pass
+
+    def roof(kernel, nbytes, ms_, key):
+        ach = nbytes / (ms_ / 1e3) / 1e9
+        return dict(kernel=kernel, bound="hbm", achieved=ach, peak=peak, unit="GB/s",
+                    frac=ach / peak, traffic=traffic.get(key), launch_ms=ms_,
+                    algorithmic_bytes=nbytes,
+                    peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                    note=("algorithmic bytes per SURVEY 8(d) count every per-edge row gather; "
+                          "those are mostly L2 hits, so frac can exceed 1 -- traffic is the "
+                          "DRAM bytes ncu measured for one launch"))
+
+    roof_bwd = roof("gfm_agg_bwd (pna CSC gather)", bwd_bytes, bwd_ms, "agg_bwd_dram_bytes")
+    roof_fwd = roof("gfm_agg_fwd (pna: sum|mean|max|std)", fwd_bytes, fwd_ms, "agg_fwd_dram_bytes")
 
     # ---- launches per step (one extra untimed step under the profiler)
     launches = None
@@ -374,10 +421,7 @@ def run_native(args):
                         l2=("step working set (activations, E x H workspaces) > 126 MB L2; "
                             "8-batch input pool cycled")),
             e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
-            roofline=dict(kernel="gfm_agg_fwd (pna: sum|mean|max|std)", bound="hbm",
-                          achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                          traffic=None, launch_ms=agg_ms, algorithmic_bytes=agg_bytes,
-                          peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"),
+            roofline=roof_bwd, roofline_agg_fwd=roof_fwd,
             cpu_baseline=cpu, clocks=clocks, gpu_launches=launches)
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -16,6 +16,7 @@ from paper_2406_12909_b200 import _lib, model as M, train as T  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--once", action="store_true", help="one fwd + one bwd call (ncu target)")
 a = ap.parse_args()
 WORKLOAD.update(CONFIGS[a.config])
 B, n = WORKLOAD["batch"], WORKLOAD["atoms"]
@@ -76,6 +77,12 @@ def timeit(fn):
     return tot / a.reps * 1e3
 
 
+if a.once:
+    fwd()
+    bwd()
+    torch.cuda.synchronize()
+    print("once ok")
+    sys.exit(0)
 tf, tb = timeit(fwd), timeit(bwd)
 fb = E * H * 4 + 8 * E + 4 * (N + 1) + K * N * H * 4 + 8 * N * H
 comp_f = N * H * 4 + 8 * E + 4 * (N + 1) + K * N * H * 4 + 8 * N * H
