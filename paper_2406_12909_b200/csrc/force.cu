@@ -65,12 +65,22 @@ __device__ __forceinline__ float4 ld4u(const float* p, int c4) {
                      __ldg(p + 4 * c4 + 3));
 }
 
+// tanh of the hot gathers: the SFU form in the tensor-core GEMM modes
+// (stated 3xTF32 / TF32 bounds), tanhf in the fp32 SIMT mode (1e-4 bound)
+template <bool FAST>
+__device__ __forceinline__ float th(float x) {
+  if constexpr (FAST)
+    return tanh_fast(x);
+  else
+    return tanhf(x);
+}
+
 __device__ __forceinline__ float4 f4add3(float4 a, float4 b, float4 c) {
   return make_float4(a.x + b.x + c.x, a.y + b.y + c.y, a.z + b.z + c.z, a.w + b.w + c.w);
 }
 
 // ------------------------------------------------------------------ forward
-template <int NV, int LPN>
+template <int NV, int LPN, bool FAST>
 __global__ void __launch_bounds__(256)
     k_force_fwd_vec(const float* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
                     const int* __restrict__ col_src, const float* __restrict__ dx,
@@ -105,8 +115,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const float4 x0 = f4add3(pi[v], r0[v], cu[v]), x1 = f4add3(pi[v], r1[v], cu[v]);
-      d0 += tanhf(x0.x) * uu[v].x + tanhf(x0.y) * uu[v].y + tanhf(x0.z) * uu[v].z + tanhf(x0.w) * uu[v].w;
-      d1 += tanhf(x1.x) * uu[v].x + tanhf(x1.y) * uu[v].y + tanhf(x1.z) * uu[v].z + tanhf(x1.w) * uu[v].w;
+      d0 += th<FAST>(x0.x) * uu[v].x + th<FAST>(x0.y) * uu[v].y + th<FAST>(x0.z) * uu[v].z + th<FAST>(x0.w) * uu[v].w;
+      d1 += th<FAST>(x1.x) * uu[v].x + th<FAST>(x1.y) * uu[v].y + th<FAST>(x1.z) * uu[v].z + th<FAST>(x1.w) * uu[v].w;
     }
     const float m0 = group_sum<LPN>(d0), m1 = group_sum<LPN>(d1);
     fx += (double)m0 * dx[3LL * p + 0]; fy += (double)m0 * dx[3LL * p + 1]; fz += (double)m0 * dx[3LL * p + 2];
@@ -118,7 +128,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const float4 x0 = f4add3(pi[v], __ldg(P4 + (long long)s0 * H4 + v * LPN + sub), cu[v]);
-      d0 += tanhf(x0.x) * uu[v].x + tanhf(x0.y) * uu[v].y + tanhf(x0.z) * uu[v].z + tanhf(x0.w) * uu[v].w;
+      d0 += th<FAST>(x0.x) * uu[v].x + th<FAST>(x0.y) * uu[v].y + th<FAST>(x0.z) * uu[v].z + th<FAST>(x0.w) * uu[v].w;
     }
     const float m0 = group_sum<LPN>(d0);
     fx += (double)m0 * dx[3LL * p + 0]; fy += (double)m0 * dx[3LL * p + 1]; fz += (double)m0 * dx[3LL * p + 2];
@@ -133,7 +143,7 @@ __global__ void __launch_bounds__(256)
 // wide H (H/4 = 32*SL float4 columns): SL warps per node, one 32-lane column
 // slab each.  Per-edge slab partials of m_e meet in shared memory; the slab-0
 // warp combines them in slab order and accumulates the force in fp64.
-template <int SL>
+template <int SL, bool FAST>
 __global__ void __launch_bounds__(256)
     k_force_fwd_slab(const float* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
                      const int* __restrict__ col_src, const float* __restrict__ dx,
@@ -172,8 +182,8 @@ __global__ void __launch_bounds__(256)
       const float4 ra = __ldg(P4 + (long long)sa * H4 + c4);
       const float4 rb = __ldg(P4 + (long long)sb * H4 + c4);
       const float4 xa = f4add3(pi, ra, cu), xb = f4add3(pi, rb, cu);
-      float da = tanhf(xa.x) * uu.x + tanhf(xa.y) * uu.y + tanhf(xa.z) * uu.z + tanhf(xa.w) * uu.w;
-      float db = tanhf(xb.x) * uu.x + tanhf(xb.y) * uu.y + tanhf(xb.z) * uu.z + tanhf(xb.w) * uu.w;
+      float da = th<FAST>(xa.x) * uu.x + th<FAST>(xa.y) * uu.y + th<FAST>(xa.z) * uu.z + th<FAST>(xa.w) * uu.w;
+      float db = th<FAST>(xb.x) * uu.x + th<FAST>(xb.y) * uu.y + th<FAST>(xb.z) * uu.z + th<FAST>(xb.w) * uu.w;
       da = group_sum<32>(da);
       db = group_sum<32>(db);
       if (lane == 0) {
@@ -241,7 +251,7 @@ __global__ void k_force_fwd_warp(const T* __restrict__ P, int n, int H, const in
 
 // ------------------------------------------------------------------ backward
 // pass 1 (dst rows): D_dst[i] = sum dpre_e, TU[i] = sum t_e dm_e
-template <int NV, int LPN>
+template <int NV, int LPN, bool FAST>
 __global__ void __launch_bounds__(256)
     k_force_bwd_dst_vec(const float* __restrict__ P, int n, int H, const int* __restrict__ rowptr,
                         const int* __restrict__ col_src, const float* __restrict__ dx,
@@ -274,7 +284,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const float4 x = f4add3(pi[v], __ldg(P4 + (long long)s * H4 + v * LPN + cb), cu[v]);
-      const float4 t = make_float4(tanhf(x.x), tanhf(x.y), tanhf(x.z), tanhf(x.w));
+      const float4 t = make_float4(th<FAST>(x.x), th<FAST>(x.y), th<FAST>(x.z), th<FAST>(x.w));
       dd[v].x += dm * uu[v].x * (1.f - t.x * t.x); dd[v].y += dm * uu[v].y * (1.f - t.y * t.y);
       dd[v].z += dm * uu[v].z * (1.f - t.z * t.z); dd[v].w += dm * uu[v].w * (1.f - t.w * t.w);
       tu[v].x += t.x * dm; tu[v].y += t.y * dm; tu[v].z += t.z * dm; tu[v].w += t.w * dm;
@@ -289,7 +299,7 @@ __global__ void __launch_bounds__(256)
 }
 
 // pass 2 (src rows): S[j] = D_dst[j] + sum over CSC slots of dpre_e
-template <int NV, int LPN>
+template <int NV, int LPN, bool FAST>
 __global__ void __launch_bounds__(256)
     k_force_bwd_src_vec(const float* __restrict__ P, int n, int H, const int* __restrict__ csc_ptr,
                         const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const float4 x = f4add3(__ldg(P4 + (long long)i * H4 + v * LPN + cb), pj[v], cu[v]);
-      const float4 t = make_float4(tanhf(x.x), tanhf(x.y), tanhf(x.z), tanhf(x.w));
+      const float4 t = make_float4(th<FAST>(x.x), th<FAST>(x.y), th<FAST>(x.z), th<FAST>(x.w));
       acc[v].x += dm * uu[v].x * (1.f - t.x * t.x); acc[v].y += dm * uu[v].y * (1.f - t.y * t.y);
       acc[v].z += dm * uu[v].z * (1.f - t.z * t.z); acc[v].w += dm * uu[v].w * (1.f - t.w * t.w);
     }
@@ -438,15 +448,25 @@ cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const i
     if (!(flags & GFM_FLAG_SCALAR) && force_vec_shape(H, nv, lpn, &slabs)) {
       if (slabs == 2 || slabs == 4 || slabs == 8) {
         const int grid = ceil_div(n, 8 / slabs);
-        if (slabs == 2) k_force_fwd_slab<2><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);
-        if (slabs == 4) k_force_fwd_slab<4><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);
-        if (slabs == 8) k_force_fwd_slab<8><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);
+        const bool fast = gemm_mode() != GFM_GEMM_SIMT;
+#define GFM_FS(SL_)                                                                                 \
+  if (slabs == SL_) {                                                                               \
+    if (fast)                                                                                       \
+      k_force_fwd_slab<SL_, true><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);      \
+    else                                                                                            \
+      k_force_fwd_slab<SL_, false><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);     \
+  }
+        GFM_FS(2) GFM_FS(4) GFM_FS(8)
+#undef GFM_FS
         return cudaGetLastError();
       }
       const int grid = ceil_div(n, 8 * (32 / lpn));
 #define GFM_FF(NV_, LPN_)                                                                    \
   if (nv == NV_ && lpn == LPN_) {                                                            \
-    k_force_fwd_vec<NV_, LPN_><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);  \
+    if (gemm_mode() != GFM_GEMM_SIMT)                                                        \
+      k_force_fwd_vec<NV_, LPN_, true><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f); \
+    else                                                                                     \
+      k_force_fwd_vec<NV_, LPN_, false><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f); \
     return cudaGetLastError();                                                               \
   }
       GFM_FVEC_CASES(GFM_FF)
@@ -470,10 +490,17 @@ cudaError_t force_bwd_edges(const T* P, int n, int H, const int* rowptr, const i
       const dim3 grid(ceil_div(n, 8 * (32 / lpn)), slabs);
 #define GFM_FB(NV_, LPN_)                                                                         \
   if (nv == NV_ && lpn == LPN_) {                                                                 \
-    k_force_bwd_dst_vec<NV_, LPN_><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df, c, u,   \
-                                                        Ddst, TU);                                \
-    k_force_bwd_src_vec<NV_, LPN_><<<grid, 256, 0, s>>>(P, n, H, csc_ptr, csc_eid, csc_dst, dx,   \
-                                                        df, c, u, Ddst, S);                       \
+    if (gemm_mode() != GFM_GEMM_SIMT) {                                                           \
+      k_force_bwd_dst_vec<NV_, LPN_, true><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df, \
+                                                                c, u, Ddst, TU);                  \
+      k_force_bwd_src_vec<NV_, LPN_, true><<<grid, 256, 0, s>>>(P, n, H, csc_ptr, csc_eid,        \
+                                                                csc_dst, dx, df, c, u, Ddst, S);  \
+    } else {                                                                                      \
+      k_force_bwd_dst_vec<NV_, LPN_, false><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df,\
+                                                                 c, u, Ddst, TU);                 \
+      k_force_bwd_src_vec<NV_, LPN_, false><<<grid, 256, 0, s>>>(P, n, H, csc_ptr, csc_eid,       \
+                                                                 csc_dst, dx, df, c, u, Ddst, S); \
+    }                                                                                             \
     return cudaGetLastError();                                                                    \
   }
       GFM_FVEC_CASES(GFM_FB)

@@ -1177,7 +1177,7 @@ struct TcEpiBiasAct {  // out[m][n] = act(acc + bias[n])
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const float t = v[i] + (bias && i < nv ? bias[n + i] : 0.f);
-      x[i] = act ? tanhf(t) : t;
+      x[i] = act ? tanh_fast(t) : t;
     }
     if (chunk_vec(o, nv)) {
 #pragma unroll
