@@ -122,7 +122,10 @@ GFM_API int gfm_linear_fwd(const void* X1, int ld1, int K1, const void* X2, int 
 GFM_API int gfm_linear_bwd_data(const void* dY, int ldd, int M, const int* M_dev, int N, const void* W1,
                         int ldw1, int K1, const void* W2, int ldw2, int K2, void* out1, int ldo1,
                         void* out2, int ldo2, const void* gate, int ldg, int dtype, void* stream);
-/* g1 = dY^T X1, g2 = dY^T X2, gb = colsum(dY): deterministic split-K */
+/* g1 = dY^T X1, g2 = dY^T X2, gb = colsum(dY): deterministic split-K.
+ * with_bias: 0 = no gb; 1 = gb (the float32 tensor-core path writes a [M][4]
+ * ones operand into the workspace); 2 = as 1 when this workspace already
+ * holds that ones operand from an earlier call with the same M (skips it). */
 GFM_API size_t gfm_linear_bwd_weight_workspace_bytes(int M, int N, int K1, int K2, int with_bias,
                                              int dtype);
 GFM_API int gfm_linear_bwd_weight(const void* dY, int ldd, int M, const int* M_dev, int N,

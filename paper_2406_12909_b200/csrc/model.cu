@@ -335,6 +335,9 @@ template <typename T>
 cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, int N, const T* X1,
                                 int ld1, int K1, const T* X2, int ld2, int K2, int with_bias,
                                 T* g1, T* g2, T* gb, T* ws, cudaStream_t s) {
+  // with_bias == 2: the workspace already holds the ones operand (same M)
+  const bool ones_ready = with_bias == 2;
+  with_bias = with_bias ? 1 : 0;
   const int Kt = K1 + K2 + with_bias;
   cudaError_t e;
   int real, trans = 0;
@@ -348,7 +351,7 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
       Cols2Ld<T> a{X1, ld1, K1, X2, ld2, K2};
       if (with_bias) {
         T* ones = ws + (((size_t)splits * N * Kt + 63) & ~(size_t)63);
-        k_fill_ones<T><<<grid_1d(4LL * M), 256, 0, s>>>(ones, M);
+        if (!ones_ready) k_fill_ones<T><<<grid_1d(4LL * M), 256, 0, s>>>(ones, M);
         a.ones = ones;
       }
       ColsLd<T> b{dY, ldd};

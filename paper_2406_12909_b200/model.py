@@ -484,6 +484,7 @@ class _Scratch:
     def __init__(self, device):
         self.device = device
         self.bufs = {}
+        self.ones_ready = {}  # wgrad workspace -> (address, rows) its ones operand was written for
 
     def get(self, name, shape, dtype):
         shape = tuple(int(x) for x in shape)
@@ -696,9 +697,13 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
 
     def wgrad(dY, ldd, n_out, X1, ld1, K1, X2, ld2, K2, g1, g2, gb):
         nb = query("gfm_linear_bwd_weight_workspace_bytes", N, n_out, K1, K2, 1, code)
-        ws = sc.bytes(f"wgrad_ws_{n_out}_{K1}_{K2}", nb)
+        key = f"wgrad_ws_{n_out}_{K1}_{K2}"
+        ws = sc.bytes(key, nb)
+        # the workspace's ones operand survives between calls: fill it once
+        bias = 2 if sc.ones_ready.get(key) == (ws.data_ptr(), N) else 1
         call("gfm_linear_bwd_weight", ptr(dY), ldd, N, None, n_out, ptr(X1), ld1, K1, ptr(X2),
-             ld2, K2, 1, ptr(g1), ptr(g2), ptr(gb), ptr(ws), code, s)
+             ld2, K2, bias, ptr(g1), ptr(g2), ptr(gb), ptr(ws), code, s)
+        sc.ones_ready[key] = (ws.data_ptr(), N)
 
     # energy head (model.py:520-533)
     ys = cache["head_inputs"]
