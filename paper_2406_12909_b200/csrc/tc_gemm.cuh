@@ -757,9 +757,11 @@ struct SmemT {
   // lo slots: conversion of k-block q + kL waits for the MMAs of q, so kL
   // bounds how far the converters run ahead of the tensor pipe
   static constexpr int kL = AT ? 4 : 3;
-  static constexpr int kR = (224 * 1024 - kL * kLo) / kRaw;  // raw stages
+  // epilogue transpose staging: 8 warps x 32 rows x (16 + 4 pad) floats
+  static constexpr int kEpi = 8 * 32 * 20 * 4;
+  static constexpr int kR = (224 * 1024 - kL * kLo - kEpi) / kRaw;  // raw stages
   static constexpr int kBars = (2 * kR + 2 * kL + 4) * 8 + 16;
-  static constexpr int kBytes = kR * kRaw + kL * kLo + 1024 + kBars;
+  static constexpr int kBytes = kR * kRaw + kL * kLo + kEpi + 1024 + kBars;
   static_assert(kBytes <= 232448, "smem");
 };
 
@@ -879,7 +881,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* lo_base = base + kR * S::kRaw;
-  uint64_t* tfl = reinterpret_cast<uint64_t*>(lo_base + kL * S::kLo);  // TMA landed [kR]
+  float* epi_stage = reinterpret_cast<float*>(lo_base + kL * S::kLo);  // [8][32][20]
+  uint64_t* tfl = reinterpret_cast<uint64_t*>(lo_base + kL * S::kLo + S::kEpi);  // TMA landed [kR]
   uint64_t* empty = tfl + kR;    // MMAs done with the raw stage [kR]
   uint64_t* cvt = empty + kR;    // lo written [kL]
   uint64_t* lofree = cvt + kL;   // MMAs done with the lo slot [kL]
@@ -1061,6 +1064,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       const int row = quarter * 32 + lane;
       const int m = m0 + row;
       const bool valid = row < min(kBM, m_total - m0);
+      // per 16-column chunk: TMEM -> registers (row = lane) -> this warp's smem
+      // stage -> read back transposed so each store instruction writes 8 rows
+      // x 64 contiguous bytes (full sectors) instead of 32 rows x 16 bytes
+      float* stg = epi_stage + (warp - (kMmaWarp + 1)) * (32 * 20);
+      const int m_lim = min(kBM, m_total - m0);
 #pragma unroll 1
       for (int c = half * kHalf; c < min(BN, (half + 1) * kHalf); c += 16) {
         float v[16];
@@ -1070,8 +1078,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
-        epi.chunk(m, valid, n0 + c, v, min(16, N - (n0 + c)), split);
+        if (n0 + c >= N) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(stg + lane * 20 + 4 * q) =
+              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = 8 * j + (lane >> 2), q = lane & 3;
+          const int col = n0 + c + 4 * q;
+          const int rr = quarter * 32 + r;
+          if (rr < m_lim && col < N)
+            epi.store4(m0 + rr, col, *reinterpret_cast<const float4*>(stg + r * 20 + 4 * q),
+                       min(4, N - col), split);
+        }
+        __syncwarp();
       }
+      (void)m;
+      (void)valid;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[acc])) : "memory");
@@ -1164,6 +1189,16 @@ inline int splits_for(long long M, long long N, long long K) {
 __device__ __forceinline__ bool chunk_vec(const void* p, int nv) {
   return nv == 16 && (((uintptr_t)p) & 15) == 0;
 }
+// 4 consecutive outputs (nv valid) -> one st.global.v4 when aligned
+__device__ __forceinline__ void put4(float* o, const float (&x)[4], int nv) {
+  if (nv == 4 && (((uintptr_t)o) & 15) == 0) {
+    *reinterpret_cast<float4*>(o) = make_float4(x[0], x[1], x[2], x[3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < nv) o[i] = x[i];
+  }
+}
 
 struct TcEpiBiasAct {  // out[m][n] = act(acc + bias[n])
   float* out;
@@ -1189,7 +1224,23 @@ struct TcEpiBiasAct {  // out[m][n] = act(acc + bias[n])
         if (i < nv) o[i] = x[i];
     }
   }
+  __device__ void store4(int m, int n, float4 v, int nv, int) const;
 };
+
+// (TcEpiBiasAct::store4) the transposed-epilogue entry: row m, columns n..n+3
+__device__ __forceinline__ void bias_act4(float (&x)[4], const float* bias, int n, int nv, int act) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float t = x[i] + (bias && i < nv ? bias[n + i] : 0.f);
+    x[i] = act ? tanh_fast(t) : t;
+  }
+}
+
+__device__ __forceinline__ void TcEpiBiasAct::store4(int m, int n, float4 v, int nv, int) const {
+  float x[4] = {v.x, v.y, v.z, v.w};
+  bias_act4(x, bias, n, nv, act);
+  put4(out + (long long)m * ldo + n, x, nv);
+}
 
 struct TcEpiSplitCols {  // cols [0, n1) -> o1 (+ add, * (1 - gate^2)), [n1, N) -> o2
   float* o1;
@@ -1261,7 +1312,60 @@ struct TcEpiSplitCols {  // cols [0, n1) -> o1 (+ add, * (1 - gate^2)), [n1, N) 
       }
     }
   }
+  __device__ void store4(int m, int n, float4 v, int nv, int) const;
 };
+
+__device__ __forceinline__ void split_cols4(const TcEpiSplitCols& e, int m, int n, float4 v,
+                                            int nv) {
+  float x[4] = {v.x, v.y, v.z, v.w};
+  if (n + 4 <= e.n1 || n >= e.n1) {
+    const bool first = n < e.n1;
+    if (first && (e.add || e.gate)) {
+      const float* ap = e.add ? e.add + (long long)m * e.ld1 + n : nullptr;
+      const float* gp = e.gate ? e.gate + (long long)m * e.ldg + n : nullptr;
+      if (nv == 4 && (!ap || (((uintptr_t)ap) & 15) == 0) && (!gp || (((uintptr_t)gp) & 15) == 0)) {
+        if (ap) {
+          const float4 a4 = *reinterpret_cast<const float4*>(ap);
+          x[0] = a4.x + x[0]; x[1] = a4.y + x[1]; x[2] = a4.z + x[2]; x[3] = a4.w + x[3];
+        }
+        if (gp) {
+          const float4 g4 = *reinterpret_cast<const float4*>(gp);
+          x[0] *= 1.f - g4.x * g4.x; x[1] *= 1.f - g4.y * g4.y;
+          x[2] *= 1.f - g4.z * g4.z; x[3] *= 1.f - g4.w * g4.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i >= nv) continue;
+          if (ap) x[i] = ap[i] + x[i];
+          if (gp) x[i] *= 1.f - gp[i] * gp[i];
+        }
+      }
+    }
+    put4(first ? e.o1 + (long long)m * e.ld1 + n : e.o2 + (long long)m * e.ld2 + (n - e.n1), x, nv);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i >= nv) continue;
+    const int c = n + i;
+    float y = x[i];
+    if (c < e.n1) {
+      if (e.add) y = e.add[(long long)m * e.ld1 + c] + y;
+      if (e.gate) {
+        const float gg = e.gate[(long long)m * e.ldg + c];
+        y *= 1.f - gg * gg;
+      }
+      e.o1[(long long)m * e.ld1 + c] = y;
+    } else {
+      e.o2[(long long)m * e.ld2 + (c - e.n1)] = y;
+    }
+  }
+}
+
+__device__ __forceinline__ void TcEpiSplitCols::store4(int m, int n, float4 v, int nv, int) const {
+  split_cols4(*this, m, n, v, nv);
+}
 
 struct TcEpiPartial {  // split-K partial tile ws[split][m][n] (row-major, width N)
   float* ws;
@@ -1279,6 +1383,10 @@ struct TcEpiPartial {  // split-K partial tile ws[split][m][n] (row-major, width
       for (int i = 0; i < 16; ++i)
         if (i < nv) o[i] = v[i];
     }
+  }
+  __device__ void store4(int m, int n, float4 v, int nv, int split) const {
+    const float x[4] = {v.x, v.y, v.z, v.w};
+    put4(ws + split * split_stride + (long long)m * N + n, x, nv);
   }
 };
 
