@@ -301,6 +301,10 @@ class StructureStepRunner:
         self.graph = None
         self.batch = None
         self.loss_host = torch.empty(2, dtype=torch.float32).pin_memory()
+        # pipelined stepping: two pinned loss slots, each with its copy event
+        self._loss_slots = [torch.empty(2, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self._loss_events = [None, None]
+        self._slot = 0
 
     def load(self, pos, z, energy, forces):
         for key, v in (("pos", pos), ("z", z), ("e", energy), ("f", forces)):
@@ -341,6 +345,36 @@ class StructureStepRunner:
         self.loss_host.copy_(self.tr.contrib[P:P + 2].float(), non_blocking=True)
         torch.cuda.current_stream().synchronize()
         tot, cnt = float(self.loss_host[0]), float(self.loss_host[1])
+        return tot / cnt if cnt else float("nan")
+
+    def step_pipelined(self, pos, z, energy, forces):
+        """As ``step``, but the host reads this step's loss one call later, so
+        enqueueing step i + 1 (input copies, graph launch) overlaps step i on
+        the GPU -- the usual asynchronous loss logging of a training loop.
+        Returns the previous step's mean loss (None on the first call); call
+        ``drain()`` after the last step for its loss."""
+        self.load(pos, z, energy, forces)
+        self.run()
+        P = self.tr.P
+        k = self._slot
+        self._loss_slots[k].copy_(self.tr.contrib[P:P + 2].float(), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._loss_events[k] = ev
+        self._slot = k ^ 1
+        return self._read_slot(k ^ 1)
+
+    def drain(self):
+        """Loss of the last ``step_pipelined`` call (waits for it)."""
+        return self._read_slot(self._slot ^ 1)
+
+    def _read_slot(self, k):
+        ev = self._loss_events[k]
+        if ev is None:
+            return None
+        ev.synchronize()
+        self._loss_events[k] = None
+        tot, cnt = float(self._loss_slots[k][0]), float(self._loss_slots[k][1])
         return tot / cnt if cnt else float("nan")
 
 

@@ -459,3 +459,33 @@ def test_trainer_nan_guard_discards_update():
     tr.step(b)
     assert tr.nan_event
     assert torch.equal(tr.master, before)
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_runner_pipelined_step_matches_blocking_step(use_graph):
+    """StructureStepRunner.step_pipelined (loss read one call later) produces
+    the same loss sequence and parameters as the blocking step()."""
+    B, n = 8, 12
+    rng = np.random.default_rng(3)
+    pos = [rng.uniform(0, 6.0, size=(B * n, 3)) for _ in range(3)]
+    z = rng.choice(np.array([1, 6, 8]), size=B * n).astype(np.int32)
+    e = rng.normal(size=B)
+    f = rng.normal(size=(B * n, 3))
+    cfg = cfg_of("pna-agg", 2, 32, 2, 16)
+    out = {}
+    for mode in ("blocking", "pipelined"):
+        tr = T.DataParallelTrainer(cfg, T.TrainConfig(), initial=O.init_flat(
+            O.config("pna-agg", layers=2, hidden=32, fc_layers=2, fc_width=16), 7))
+        run = T.StructureStepRunner(tr, np.arange(B + 1) * n, 3.0, 8, use_graph=use_graph)
+        args = [(torch.as_tensor(p).pin_memory(), torch.as_tensor(z).pin_memory(),
+                 torch.as_tensor(e, dtype=torch.float32).pin_memory(),
+                 torch.as_tensor(f, dtype=torch.float32).pin_memory()) for p in pos]
+        if mode == "blocking":
+            losses = [run.step(*a) for a in args]
+        else:
+            losses = [run.step_pipelined(*a) for a in args]
+            assert losses[0] is None
+            losses = losses[1:] + [run.drain()]
+        out[mode] = (losses, tr.flat_master())
+    assert out["blocking"][0] == out["pipelined"][0]
+    np.testing.assert_array_equal(out["blocking"][1], out["pipelined"][1])
