@@ -20,6 +20,7 @@
 //    sums follow numpy's reduceat order (x0 + pairwise(x1..)) with separately
 //    rounded operations, which makes the float64 result bit-identical to
 //    np.add.reduceat / np.maximum.reduceat.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 
@@ -47,11 +48,22 @@ __host__ __device__ inline AggLayout agg_layout(int parts, int H) {
 template <typename T>
 __global__ void k_embed(const int* __restrict__ z, int n, const T* __restrict__ emb, int H,
                         T* __restrict__ h) {
-  long long total = (long long)n * H;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    int i = (int)(idx / H), c = (int)(idx % H);
-    h[idx] = emb[(long long)(z[i] - 1) * H + c];  // model.py:351
+  // 2D: blockIdx.y / threadIdx.y over rows, x over columns (no 64-bit divides)
+  for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
+    const T* src = emb + (long long)(z[i] - 1) * H;  // model.py:351
+    T* dst = h + (long long)i * H;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < H; c += gridDim.x * blockDim.x)
+      dst[c] = src[c];
+  }
+}
+
+// float4 rows (H % 4 == 0, 16-byte aligned rows)
+__global__ void k_embed4(const int* __restrict__ z, int n, const float4* __restrict__ emb, int H4,
+                         float4* __restrict__ h) {
+  for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
+    const float4* src = emb + (long long)(z[i] - 1) * H4;
+    float4* dst = h + (long long)i * H4;
+    for (int c = threadIdx.x; c < H4; c += blockDim.x) dst[c] = __ldg(src + c);
   }
 }
 
@@ -800,9 +812,19 @@ int gfm_embed(const int* z, int n, const void* emb, int H, void* h, int dtype, v
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == GFM_F32)
-    k_embed<float><<<grid_1d((long long)n * H), 256, 0, s>>>(z, n, (const float*)emb, H, (float*)h);
+  {
+    if (H % 4 == 0 && ((uintptr_t)emb & 15) == 0 && ((uintptr_t)h & 15) == 0) {
+      const int tx = std::min(32, H / 4), ty = 256 / tx;
+      k_embed4<<<dim3(1, std::min(ceil_div(n, ty), 65535)), dim3(tx, ty), 0, s>>>(
+          z, n, (const float4*)emb, H / 4, (float4*)h);
+    } else {
+      k_embed<float><<<dim3(1, std::min(ceil_div(n, 8), 65535)), dim3(32, 8), 0, s>>>(
+          z, n, (const float*)emb, H, (float*)h);
+    }
+  }
   else if (dtype == GFM_F64)
-    k_embed<double><<<grid_1d((long long)n * H), 256, 0, s>>>(z, n, (const double*)emb, H, (double*)h);
+    k_embed<double><<<dim3(1, std::min(ceil_div(n, 8), 65535)), dim3(32, 8), 0, s>>>(
+        z, n, (const double*)emb, H, (double*)h);
   else {
     set_error("gfm_embed: bad dtype %d", dtype);
     return GFM_EINVAL;

@@ -230,17 +230,15 @@ template <typename T>
 __global__ void k_energy_seed(const T* __restrict__ de, const int* __restrict__ gnode, int n,
                               int G, const T* __restrict__ a, const T* __restrict__ y,
                               T* __restrict__ ds, int ld_ds, T* __restrict__ dz) {
-  const long long total = (long long)n * G;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx / G), g = (int)(idx % G);
+  // 2D: y over nodes, x over the G columns (no 64-bit divides)
+  for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
     const T s = de[gnode[i]];
-    if (g == 0) {
-      ds[(long long)i * ld_ds] = s;
-      for (int j = 1; j < ld_ds; ++j) ds[(long long)i * ld_ds + j] = T(0);
+    if (threadIdx.x < ld_ds) ds[(long long)i * ld_ds + threadIdx.x] = threadIdx.x == 0 ? s : T(0);
+    const long long row = (long long)i * G;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+      const T yy = y[row + g];
+      dz[row + g] = mul_rn(mul_rn(s, a[g]), sub_rn(T(1), mul_rn(yy, yy)));
     }
-    const T yy = y[idx];
-    dz[idx] = mul_rn(mul_rn(s, a[g]), sub_rn(T(1), mul_rn(yy, yy)));
   }
 }
 
@@ -577,7 +575,8 @@ int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const 
   if (ld_ds < 1) return GFM_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   GFM_DISPATCH(dtype, "gfm_energy_seed",
-               (k_energy_seed<T><<<grid_1d((long long)n_nodes * G), 256, 0, s>>>(
+               (k_energy_seed<T><<<dim3(1, std::min(ceil_div(std::max(n_nodes, 1), 8), 65535)),
+                                   dim3(32, 8), 0, s>>>(
                     (const T*)de, gnode, n_nodes, G, (const T*)a, (const T*)y, (T*)ds, ld_ds,
                     (T*)dz),
                 cudaGetLastError()))
