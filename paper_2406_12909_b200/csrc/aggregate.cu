@@ -48,6 +48,7 @@ __host__ __device__ inline AggLayout agg_layout(int parts, int H) {
 template <typename T>
 __global__ void k_embed(const int* __restrict__ z, int n, const T* __restrict__ emb, int H,
                         T* __restrict__ h) {
+  pdl_entry();
   // 2D: blockIdx.y / threadIdx.y over rows, x over columns (no 64-bit divides)
   for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
     const T* src = emb + (long long)(z[i] - 1) * H;  // model.py:351
@@ -60,6 +61,7 @@ __global__ void k_embed(const int* __restrict__ z, int n, const T* __restrict__ 
 // float4 rows (H % 4 == 0, 16-byte aligned rows)
 __global__ void k_embed4(const int* __restrict__ z, int n, const float4* __restrict__ emb, int H4,
                          float4* __restrict__ h) {
+  pdl_entry();
   for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
     const float4* src = emb + (long long)(z[i] - 1) * H4;
     float4* dst = h + (long long)i * H4;
@@ -73,6 +75,7 @@ __global__ void k_agg_fwd_scalar(const T* __restrict__ h, int n_nodes, int H,
                                  const int* __restrict__ rowptr, const int* __restrict__ col_src,
                                  const T* __restrict__ w, int parts, T* __restrict__ agg,
                                  int* __restrict__ argmax, T* __restrict__ stat_mean) {
+  pdl_entry();
   const AggLayout L = agg_layout(parts, H);
   const int ld = L.K * H;
   const long long total = (long long)n_nodes * H;
@@ -245,6 +248,7 @@ __global__ void __launch_bounds__(256)
     k_agg_fwd_vec(const float* __restrict__ h, int n_nodes, int H, const int* __restrict__ rowptr,
                   const int* __restrict__ col_src, const float* __restrict__ w, int parts,
                   float* __restrict__ agg, int* __restrict__ argmax, float* __restrict__ stat_mean) {
+  pdl_entry();
   constexpr int NPW = 32 / LPN;  // nodes per warp
   const int lane = threadIdx.x & 31;
   const int sub = lane % LPN;
@@ -311,6 +315,7 @@ __global__ void __launch_bounds__(256)
                    const int* __restrict__ col_src, const float* __restrict__ w, int parts,
                    float* __restrict__ agg, int* __restrict__ argmax,
                    float* __restrict__ stat_mean, int nb, int cap_rows) {
+  pdl_entry();
   extern __shared__ float4 stage[];  // [cap_rows][LPN]
   const int a = blockIdx.x * nb, b = min(n_nodes, a + nb);
   const int cs = blockIdx.y * LPN;  // slab's first float4 column
@@ -346,6 +351,7 @@ __global__ void k_agg_bwd_prep(const T* __restrict__ dagg, const int* __restrict
                                int n_nodes, int H, int parts, const T* __restrict__ agg,
                                const T* __restrict__ stat_mean, T* __restrict__ G,
                                T* __restrict__ coef) {
+  pdl_entry();
   const AggLayout L = agg_layout(parts, H);
   const int ld = L.K * H;
   const long long total = (long long)n_nodes * H;
@@ -379,6 +385,7 @@ __global__ void __launch_bounds__(256)
                        int H, int parts, const float* __restrict__ agg,
                        const float* __restrict__ stat_mean, float* __restrict__ G,
                        float* __restrict__ coef) {
+  pdl_entry();
   const AggLayout L = agg_layout(parts, H);
   const int H4 = H >> 2, ld4 = (L.K * H) >> 2;
   const long long total = (long long)n_nodes * H4;
@@ -428,6 +435,7 @@ __global__ void k_agg_bwd_scalar(const T* __restrict__ G, int ldg, const T* __re
                                  const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
                                  const T* __restrict__ w, int n_nodes, int H, T* __restrict__ dh,
                                  const T* __restrict__ gate, T* __restrict__ out) {
+  pdl_entry();
   const long long total = (long long)n_nodes * H;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -551,6 +559,7 @@ __global__ void __launch_bounds__(256)
                   const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
                   const float* __restrict__ w, int n_nodes, int H, float* __restrict__ dh,
                   const float* __restrict__ gate, float* __restrict__ out) {
+  pdl_entry();
   constexpr int NPW = 32 / LPN;
   const int lane = threadIdx.x & 31;
   const int sub = lane % LPN;
@@ -583,6 +592,7 @@ __global__ void __launch_bounds__(256)
                    const float* __restrict__ w, int n_nodes, int H, float* __restrict__ dh,
                    const float* __restrict__ gate, float* __restrict__ out, int nb,
                    int cap_rows) {
+  pdl_entry();
   extern __shared__ float4 stage[];  // [G | coef | argmax] each [cap_rows][LPN]
   const int a0 = blockIdx.x * nb, b0 = min(n_nodes, a0 + nb);
   const int cs = blockIdx.y * LPN;
@@ -688,7 +698,7 @@ cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, c
     cudaFuncSetAttribute(k_agg_fwd_tile<kLpn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     const dim3 grid(ceil_div(n, kNb), H / 64);
-    k_agg_fwd_tile<kLpn><<<grid, 256, smem, s>>>((const float*)h, n, H, rowptr, col_src,
+    launch_k(k_agg_fwd_tile<kLpn>, grid, 256, smem, s, (const float*)h, n, H, rowptr, col_src,
                                                  (const float*)w, parts, (float*)agg, argmax,
                                                  (float*)stat_mean, kNb, kCap);
     return cudaGetLastError();
@@ -698,7 +708,7 @@ cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, c
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);
 #define GFM_FWD_CASE(NV_, LPN_)                                                                \
   if (nv == NV_ && lpn == LPN_) {                                                              \
-    k_agg_fwd_vec<NV_, LPN_><<<grid, 256, 0, s>>>((const float*)h, n, H, rowptr, col_src,      \
+    launch_k(k_agg_fwd_vec<NV_, LPN_>, grid, 256, 0, s, (const float*)h, n, H, rowptr, col_src,      \
                                                   (const float*)w, parts, (float*)agg, argmax, \
                                                   (float*)stat_mean);                          \
     return cudaGetLastError();                                                                 \
@@ -707,11 +717,11 @@ cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, c
 #undef GFM_FWD_CASE
   }
   if (dtype == GFM_F32)
-    k_agg_fwd_scalar<float><<<grid_1d((long long)n * H), 256, 0, s>>>(
+    launch_k(k_agg_fwd_scalar<float>, grid_1d((long long)n * H), 256, 0, s,
         (const float*)h, n, H, rowptr, col_src, (const float*)w, parts, (float*)agg, argmax,
         (float*)stat_mean);
   else
-    k_agg_fwd_scalar<double><<<grid_1d((long long)n * H), 256, 0, s>>>(
+    launch_k(k_agg_fwd_scalar<double>, grid_1d((long long)n * H), 256, 0, s,
         (const double*)h, n, H, rowptr, col_src, (const double*)w, parts, (double*)agg, argmax,
         (double*)stat_mean);
   return cudaGetLastError();
@@ -734,15 +744,15 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
     void* Gw = ws;
     void* Cw = L.o_std >= 0 ? (void*)((char*)ws + esz * (size_t)n * H) : nullptr;
     if (dtype == GFM_F32 && H % 4 == 0 && !force_scalar)
-      k_agg_bwd_prep_vec<<<grid_1d((long long)n * (H / 4)), 256, 0, s>>>(
+      launch_k(k_agg_bwd_prep_vec, grid_1d((long long)n * (H / 4)), 256, 0, s,
           (const float*)dagg, rowptr, n, H, parts, (const float*)agg, (const float*)stat_mean,
           (float*)Gw, (float*)Cw);
     else if (dtype == GFM_F32)
-      k_agg_bwd_prep<float><<<grid_1d((long long)n * H), 256, 0, s>>>(
+      launch_k(k_agg_bwd_prep<float>, grid_1d((long long)n * H), 256, 0, s,
           (const float*)dagg, rowptr, n, H, parts, (const float*)agg, (const float*)stat_mean,
           (float*)Gw, (float*)Cw);
     else
-      k_agg_bwd_prep<double><<<grid_1d((long long)n * H), 256, 0, s>>>(
+      launch_k(k_agg_bwd_prep<double>, grid_1d((long long)n * H), 256, 0, s,
           (const double*)dagg, rowptr, n, H, parts, (const double*)agg, (const double*)stat_mean,
           (double*)Gw, (double*)Cw);
     G = Gw;
@@ -762,7 +772,7 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
     cudaFuncSetAttribute(k_agg_bwd_tile<kLpn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     const dim3 grid(ceil_div(n, kNb), H / 32);
-    k_agg_bwd_tile<kLpn><<<grid, 256, smem, s>>>(
+    launch_k(k_agg_bwd_tile<kLpn>, grid, 256, smem, s,
         (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in,
         csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,
         (float*)out, kNb, kCap);
@@ -773,7 +783,7 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);
 #define GFM_BWD_CASE(NV_, LPN_)                                                              \
   if (nv == NV_ && lpn == LPN_) {                                                            \
-    k_agg_bwd_vec<NV_, LPN_><<<grid, 256, 0, s>>>(                                           \
+    launch_k(k_agg_bwd_vec<NV_, LPN_>, grid, 256, 0, s,                                            \
         (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am,                \
         (const float*)h_in, csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh,    \
         (const float*)gate, (float*)out);                                                    \
@@ -783,12 +793,12 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
 #undef GFM_BWD_CASE
   }
   if (dtype == GFM_F32)
-    k_agg_bwd_scalar<float><<<grid_1d((long long)n * H), 256, 0, s>>>(
+    launch_k(k_agg_bwd_scalar<float>, grid_1d((long long)n * H), 256, 0, s,
         (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in,
         csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,
         (float*)out);
   else
-    k_agg_bwd_scalar<double><<<grid_1d((long long)n * H), 256, 0, s>>>(
+    launch_k(k_agg_bwd_scalar<double>, grid_1d((long long)n * H), 256, 0, s,
         (const double*)G, ldg, (const double*)coef, (const double*)dmax, ld, am,
         (const double*)h_in, csc_ptr, csc_eid, csc_dst, (const double*)w, n, H, (double*)dh,
         (const double*)gate, (double*)out);
@@ -815,15 +825,15 @@ int gfm_embed(const int* z, int n, const void* emb, int H, void* h, int dtype, v
   {
     if (H % 4 == 0 && ((uintptr_t)emb & 15) == 0 && ((uintptr_t)h & 15) == 0) {
       const int tx = std::min(32, H / 4), ty = 256 / tx;
-      k_embed4<<<dim3(1, std::min(ceil_div(n, ty), 65535)), dim3(tx, ty), 0, s>>>(
+      launch_k(k_embed4, dim3(1, std::min(ceil_div(n, ty), 65535)), dim3(tx, ty), 0, s,
           z, n, (const float4*)emb, H / 4, (float4*)h);
     } else {
-      k_embed<float><<<dim3(1, std::min(ceil_div(n, 8), 65535)), dim3(32, 8), 0, s>>>(
+      launch_k(k_embed<float>, dim3(1, std::min(ceil_div(n, 8), 65535)), dim3(32, 8), 0, s,
           z, n, (const float*)emb, H, (float*)h);
     }
   }
   else if (dtype == GFM_F64)
-    k_embed<double><<<dim3(1, std::min(ceil_div(n, 8), 65535)), dim3(32, 8), 0, s>>>(
+    launch_k(k_embed<double>, dim3(1, std::min(ceil_div(n, 8), 65535)), dim3(32, 8), 0, s,
         z, n, (const double*)emb, H, (double*)h);
   else {
     set_error("gfm_embed: bad dtype %d", dtype);

@@ -1,4 +1,5 @@
 // C-ABI housekeeping: version, thread-local error text, device sync helper.
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 
@@ -9,6 +10,13 @@ static thread_local char g_err[512] = "";
 static int g_gemm_mode = GFM_GEMM_TC3;
 
 int gemm_mode() { return g_gemm_mode; }
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("GFM_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;

@@ -1,6 +1,7 @@
 // Shared device helpers for the gfm_b200 kernels (sm_100a).
 #pragma once
 
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -170,5 +171,39 @@ __device__ __forceinline__ float4 fma4(float4 a, float4 b, float4 c) {
 }
 __device__ __forceinline__ float4 bcast4(float s) { return make_float4(s, s, s, s); }
 #endif
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Kernels launched through launch_k() may start while the previous kernel on
+// the stream drains: every such kernel calls pdl_entry() first -- it waits for
+// the previous grid's completion and memory flush (griddepcontrol.wait) before
+// touching any input, then lets the next kernel launch early.  This hides the
+// launch latency and prologue (barrier init, TMEM alloc, descriptor prefetch)
+// of the ~70 small kernels of a step behind their predecessors' tails.
+// GFM_NO_PDL=1 launches normally (pdl_entry() is then a no-op wait).
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef GFM_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+#endif
+bool pdl_enabled();
+
+template <typename... KP, typename... A>
+inline cudaError_t launch_k(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
 
 }  // namespace gfm

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(256)
                     const int* __restrict__ col_src, const float* __restrict__ dx,
                     const float* __restrict__ c, const float* __restrict__ u,
                     float* __restrict__ f) {
+  pdl_entry();
   constexpr int NPW = 32 / LPN;
   const int lane = threadIdx.x & 31, sub = lane % LPN;
   const int i = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(256)
                      const int* __restrict__ col_src, const float* __restrict__ dx,
                      const float* __restrict__ c, const float* __restrict__ u,
                      float* __restrict__ f) {
+  pdl_entry();
   constexpr int NPB = 8 / SL, CH = 32;  // nodes per block, edges per chunk
   __shared__ float mpart[8][CH];
   __shared__ int degs[NPB];
@@ -228,6 +230,7 @@ __global__ void k_force_fwd_warp(const T* __restrict__ P, int n, int H, const in
                                  const int* __restrict__ col_src, const T* __restrict__ dx,
                                  const T* __restrict__ c, const T* __restrict__ u,
                                  T* __restrict__ f) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= n) return;
@@ -258,6 +261,7 @@ __global__ void __launch_bounds__(256)
                         const float* __restrict__ df, const float* __restrict__ c,
                         const float* __restrict__ u, float* __restrict__ Ddst,
                         float* __restrict__ TU) {
+  pdl_entry();
   constexpr int NPW = 32 / LPN;
   const int lane = threadIdx.x & 31, sub = lane % LPN;
   const int i = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
@@ -306,6 +310,7 @@ __global__ void __launch_bounds__(256)
                         const float* __restrict__ dx, const float* __restrict__ df,
                         const float* __restrict__ c, const float* __restrict__ u,
                         const float* __restrict__ Ddst, float* __restrict__ S) {
+  pdl_entry();
   constexpr int NPW = 32 / LPN;
   const int lane = threadIdx.x & 31, sub = lane % LPN;
   const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
@@ -346,6 +351,7 @@ __global__ void k_force_bwd_dst_scalar(const T* __restrict__ P, int n, int H, co
                                        const T* __restrict__ df, const T* __restrict__ c,
                                        const T* __restrict__ u, T* __restrict__ Ddst,
                                        T* __restrict__ TU) {
+  pdl_entry();
   const long long total = (long long)n * H;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -370,6 +376,7 @@ __global__ void k_force_bwd_src_scalar(const T* __restrict__ P, int n, int H, co
                                        const T* __restrict__ dx, const T* __restrict__ df,
                                        const T* __restrict__ c, const T* __restrict__ u,
                                        const T* __restrict__ Ddst, T* __restrict__ S) {
+  pdl_entry();
   const long long total = (long long)n * H;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -396,6 +403,7 @@ constexpr int kColChunk = 128;
 template <typename T>
 __global__ void __launch_bounds__(256)
     k_colsum_partial(const T* __restrict__ X, int n, int H, int chunk, int cw, T* __restrict__ part) {
+  pdl_entry();
   // block (ch, cb): rows [ch*chunk, ch*chunk+chunk) x columns [cb*cw, cb*cw+cw);
   // 256/cw row groups stride the rows, then a fixed-order smem combine, so the
   // result depends only on (n, H, chunk, cw) -- deterministic
@@ -429,10 +437,10 @@ cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s) {
     return cudaGetLastError();
   }
   const int nch = ceil_div(n, kColChunk);
-  k_colsum_partial<T><<<dim3(nch, ceil_div(H, cw)), 256, 0, s>>>(X, n, H, kColChunk, cw, part);
+  launch_k(k_colsum_partial<T>, dim3(nch, ceil_div(H, cw)), 256, 0, s, X, n, H, kColChunk, cw, part);
   // second level: the nch partial rows, one block per column slab
   const int cw2 = H < 32 ? H : 32;
-  k_colsum_partial<T><<<dim3(1, ceil_div(H, cw2)), 256, 0, s>>>(part, nch, H, nch, cw2, out);
+  launch_k(k_colsum_partial<T>, dim3(1, ceil_div(H, cw2)), 256, 0, s, part, nch, H, nch, cw2, out);
   return cudaGetLastError();
 }
 
@@ -452,9 +460,9 @@ cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const i
 #define GFM_FS(SL_)                                                                                 \
   if (slabs == SL_) {                                                                               \
     if (fast)                                                                                       \
-      k_force_fwd_slab<SL_, true><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);      \
+      launch_k(k_force_fwd_slab<SL_, true>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, c, u, f);      \
     else                                                                                            \
-      k_force_fwd_slab<SL_, false><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);     \
+      launch_k(k_force_fwd_slab<SL_, false>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, c, u, f);     \
   }
         GFM_FS(2) GFM_FS(4) GFM_FS(8)
 #undef GFM_FS
@@ -464,16 +472,16 @@ cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const i
 #define GFM_FF(NV_, LPN_)                                                                    \
   if (nv == NV_ && lpn == LPN_) {                                                            \
     if (gemm_mode() != GFM_GEMM_SIMT)                                                        \
-      k_force_fwd_vec<NV_, LPN_, true><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f); \
+      launch_k(k_force_fwd_vec<NV_, LPN_, true>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, c, u, f); \
     else                                                                                     \
-      k_force_fwd_vec<NV_, LPN_, false><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f); \
+      launch_k(k_force_fwd_vec<NV_, LPN_, false>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, c, u, f); \
     return cudaGetLastError();                                                               \
   }
       GFM_FVEC_CASES(GFM_FF)
 #undef GFM_FF
     }
   }
-  k_force_fwd_warp<T><<<ceil_div(n, 8), 256, 0, s>>>(P, n, H, rowptr, col_src, dx, c, u, f);
+  launch_k(k_force_fwd_warp<T>, ceil_div(n, 8), 256, 0, s, P, n, H, rowptr, col_src, dx, c, u, f);
   return cudaGetLastError();
 }
 
@@ -491,14 +499,14 @@ cudaError_t force_bwd_edges(const T* P, int n, int H, const int* rowptr, const i
 #define GFM_FB(NV_, LPN_)                                                                         \
   if (nv == NV_ && lpn == LPN_) {                                                                 \
     if (gemm_mode() != GFM_GEMM_SIMT) {                                                           \
-      k_force_bwd_dst_vec<NV_, LPN_, true><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df, \
+      launch_k(k_force_bwd_dst_vec<NV_, LPN_, true>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, df, \
                                                                 c, u, Ddst, TU);                  \
-      k_force_bwd_src_vec<NV_, LPN_, true><<<grid, 256, 0, s>>>(P, n, H, csc_ptr, csc_eid,        \
+      launch_k(k_force_bwd_src_vec<NV_, LPN_, true>, grid, 256, 0, s, P, n, H, csc_ptr, csc_eid,        \
                                                                 csc_dst, dx, df, c, u, Ddst, S);  \
     } else {                                                                                      \
-      k_force_bwd_dst_vec<NV_, LPN_, false><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df,\
+      launch_k(k_force_bwd_dst_vec<NV_, LPN_, false>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, df,\
                                                                  c, u, Ddst, TU);                 \
-      k_force_bwd_src_vec<NV_, LPN_, false><<<grid, 256, 0, s>>>(P, n, H, csc_ptr, csc_eid,       \
+      launch_k(k_force_bwd_src_vec<NV_, LPN_, false>, grid, 256, 0, s, P, n, H, csc_ptr, csc_eid,       \
                                                                  csc_dst, dx, df, c, u, Ddst, S); \
     }                                                                                             \
     return cudaGetLastError();                                                                    \
@@ -509,8 +517,8 @@ cudaError_t force_bwd_edges(const T* P, int n, int H, const int* rowptr, const i
   }
   const long long total = (long long)n * H;
   const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
-  k_force_bwd_dst_scalar<T><<<grid, 256, 0, s>>>(P, n, H, rowptr, col_src, dx, df, c, u, Ddst, TU);
-  k_force_bwd_src_scalar<T><<<grid, 256, 0, s>>>(P, n, H, csc_ptr, csc_eid, csc_dst, dx, df, c, u,
+  launch_k(k_force_bwd_dst_scalar<T>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, df, c, u, Ddst, TU);
+  launch_k(k_force_bwd_src_scalar<T>, grid, 256, 0, s, P, n, H, csc_ptr, csc_eid, csc_dst, dx, df, c, u,
                                                  Ddst, S);
   return cudaGetLastError();
 }

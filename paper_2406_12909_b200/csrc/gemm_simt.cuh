@@ -229,6 +229,7 @@ template <typename T, class AL, class BL, class Epi>
 __global__ void __launch_bounds__(kGemmThreads)
     simt_gemm_kernel(int M, const int* M_dev, int N, int K, const int* K_dev, int k_chunk, AL a, BL b,
                      Epi epi) {
+  pdl_entry();
   __shared__ __align__(16) T As[kBK][kBM + 4];
   __shared__ __align__(16) T Bs[kBK][kBN + 4];
   const int m_total = M_dev ? *M_dev : M;
@@ -298,7 +299,7 @@ inline cudaError_t launch_simt_gemm(int M, const int* M_dev, int N, int K, const
   k_chunk = ceil_div(k_chunk, kBK) * kBK;
   splits = ceil_div(K > 0 ? K : 1, k_chunk);
   dim3 grid(ceil_div(M, kBM), ceil_div(N, kBN), splits);
-  simt_gemm_kernel<T, AL, BL, Epi><<<grid, kGemmThreads, 0, s>>>(M, M_dev, N, K, K_dev, k_chunk, a, b,
+  launch_k(simt_gemm_kernel<T, AL, BL, Epi>, grid, kGemmThreads, 0, s, M, M_dev, N, K, K_dev, k_chunk, a, b,
                                                                  epi);
   return cudaGetLastError();
 }

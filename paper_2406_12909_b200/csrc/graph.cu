@@ -16,15 +16,18 @@ namespace gfm {
 
 // ---------------------------------------------------------------- helpers
 __global__ void k_graph_of_node(const int* __restrict__ off, int n_graphs, int* __restrict__ gnode) {
+  pdl_entry();
   for (int g = blockIdx.x; g < n_graphs; g += gridDim.x)
     for (int i = off[g] + threadIdx.x; i < off[g + 1]; i += blockDim.x) gnode[i] = g;
 }
 
 __global__ void k_iota(int* __restrict__ out, int n) {
+  pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
 }
 
 __global__ void k_zero_i32(int* __restrict__ out, int n) {
+  pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 0;
 }
 
@@ -32,6 +35,7 @@ __global__ void k_zero_i32(int* __restrict__ out, int n) {
 // the result is order independent, hence deterministic).
 __global__ void k_histogram(const int* __restrict__ keys, int n_cap, const int* __restrict__ n_dev,
                             int* __restrict__ count) {
+  pdl_entry();
   const int n = n_dev ? *n_dev : n_cap;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     atomicAdd(&count[keys[i]], 1);
@@ -69,6 +73,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* tmp, int& total) {
 }
 
 __global__ void k_scan_partials(const int* __restrict__ in, int n, int* __restrict__ partial) {
+  pdl_entry();
   __shared__ int tmp[32];
   const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
   int s = 0;
@@ -81,6 +86,7 @@ __global__ void k_scan_partials(const int* __restrict__ in, int n, int* __restri
 }
 
 __global__ void k_scan_totals(int* __restrict__ partial, int nb) {
+  pdl_entry();
   __shared__ int tmp[32];
   int carry = 0;
   for (int c = 0; c < nb; c += kScanThreads) {
@@ -97,6 +103,7 @@ __global__ void k_scan_totals(int* __restrict__ partial, int nb) {
 
 __global__ void k_scan_final(const int* __restrict__ in, int n, const int* __restrict__ partial,
                              int* __restrict__ out) {
+  pdl_entry();
   __shared__ int tmp[32];
   const long long base = (long long)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
   int v[kScanItems];
@@ -121,9 +128,9 @@ size_t scan_ws_bytes(int n) { return sizeof(int) * ((size_t)ceil_div(n > 0 ? n :
 cudaError_t exclusive_scan(const int* in, int n, int* out, int* ws, cudaStream_t s) {
   if (n <= 0) return cudaMemsetAsync(out, 0, sizeof(int), s);
   int nb = ceil_div(n, kScanTile);
-  k_scan_partials<<<nb, kScanThreads, 0, s>>>(in, n, ws);
-  k_scan_totals<<<1, kScanThreads, 0, s>>>(ws, nb);
-  k_scan_final<<<nb, kScanThreads, 0, s>>>(in, n, ws, out);
+  launch_k(k_scan_partials, nb, kScanThreads, 0, s, in, n, ws);
+  launch_k(k_scan_totals, 1, kScanThreads, 0, s, ws, nb);
+  launch_k(k_scan_final, nb, kScanThreads, 0, s, in, n, ws, out);
   return cudaGetLastError();
 }
 
@@ -168,6 +175,7 @@ __global__ void __launch_bounds__(kRadiusWarps * 32)
              int max_nbr, int* __restrict__ deg, const int* __restrict__ rowptr,
              int* __restrict__ col_src, int* __restrict__ edge_dst, T* __restrict__ edge_w,
              T* __restrict__ edge_dx) {
+  pdl_entry();
   __shared__ double s_d[kRadiusWarps][kCapBuf];
   __shared__ int s_j[kRadiusWarps][kCapBuf];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -280,6 +288,7 @@ __global__ void __launch_bounds__(kRadiusWarps * 32)
 // a cursor.  Output perm[position] = input edge index.
 __global__ void k_stable_bucket(const int* __restrict__ keys, const int* __restrict__ seg,
                                 int n_segs, int* __restrict__ cursor, int* __restrict__ perm) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= n_segs) return;
@@ -302,11 +311,13 @@ __global__ void k_stable_bucket(const int* __restrict__ keys, const int* __restr
 }
 
 __global__ void k_copy_i32(const int* __restrict__ in, int n, int* __restrict__ out) {
+  pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i];
 }
 
 __global__ void k_edge_offsets(const int* __restrict__ rowptr, const int* __restrict__ node_off,
                                int n_graphs, int* __restrict__ eoff) {
+  pdl_entry();
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g <= n_graphs; g += gridDim.x * blockDim.x)
     eoff[g] = rowptr[node_off[g]];
 }
@@ -319,6 +330,7 @@ __global__ void k_csr_gather(const int* __restrict__ perm, int n_edges, const in
                              const double* __restrict__ shift, int* __restrict__ col_src,
                              int* __restrict__ edge_dst, T* __restrict__ edge_w,
                              T* __restrict__ edge_dx, int* __restrict__ inv) {
+  pdl_entry();
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_edges; p += gridDim.x * blockDim.x) {
     const int e = perm[p];
     const int s = src[e], d = dst[e];
@@ -345,6 +357,7 @@ __global__ void k_csr_gather(const int* __restrict__ perm, int n_edges, const in
 __global__ void k_csc_finish(const int* __restrict__ perm_csc, int n_cap, const int* __restrict__ n_dev,
                              const int* __restrict__ inv, const int* __restrict__ dst,
                              int* __restrict__ csc_eid, int* __restrict__ csc_dst) {
+  pdl_entry();
   const int n = n_dev ? *n_dev : n_cap;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     const int e = perm_csc[q];
@@ -359,7 +372,7 @@ cudaError_t radius_fill_t(const double* pos, const int* node_off, const int* gno
                           const double* cells, double rc, int max_nbr, const int* rowptr,
                           int* col_src, int* edge_dst, void* w, void* dx, cudaStream_t s) {
   if (n_nodes <= 0) return cudaSuccess;
-  k_radius<T, true><<<ceil_div(n_nodes, kRadiusWarps), kRadiusWarps * 32, 0, s>>>(
+  launch_k(k_radius<T, true>, ceil_div(n_nodes, kRadiusWarps), kRadiusWarps * 32, 0, s,
       pos, node_off, gnode, n_nodes, cells, rc, max_nbr, nullptr, rowptr, col_src, edge_dst,
       (T*)w, (T*)dx);
   return cudaGetLastError();
@@ -389,7 +402,7 @@ extern "C" {
 
 int gfm_graph_of_node(const int* node_offsets, int n_graphs, int* gnode, void* stream) {
   if (n_graphs <= 0) return 0;
-  k_graph_of_node<<<grid_for(n_graphs, 1), 128, 0, (cudaStream_t)stream>>>(node_offsets, n_graphs, gnode);
+  launch_k(k_graph_of_node, grid_for(n_graphs, 1), 128, 0, (cudaStream_t)stream, node_offsets, n_graphs, gnode);
   GFM_TRY(cudaGetLastError());
   return 0;
 }
@@ -404,8 +417,7 @@ int gfm_exclusive_scan(const int* in, int n, int* out, void* workspace, void* st
 int gfm_radius_count(const double* pos, const int* node_offsets, const int* gnode, int n_nodes,
                      const double* cells, double rc, int max_nbr, int* deg, void* stream) {
   if (n_nodes <= 0) return 0;
-  k_radius<float, false><<<ceil_div(n_nodes, kRadiusWarps), kRadiusWarps * 32, 0,
-                           (cudaStream_t)stream>>>(pos, node_offsets, gnode, n_nodes, cells, rc,
+  launch_k(k_radius<float, false>, ceil_div(n_nodes, kRadiusWarps), kRadiusWarps * 32, 0, (cudaStream_t)stream, pos, node_offsets, gnode, n_nodes, cells, rc,
                                                    max_nbr, deg, nullptr, nullptr, nullptr, nullptr,
                                                    nullptr);
   GFM_TRY(cudaGetLastError());
@@ -461,30 +473,30 @@ int gfm_csr_build(const int* src, const int* dst, const int* edge_offsets, int n
   int* perm_csc = (int*)carve(p, sizeof(int) * (n_edges + 1));
   const int nt = 256;
   // dst-sorted CSR (stable): order[p] = original edge index (model.py:260)
-  k_zero_i32<<<grid_for(n_nodes), nt, 0, s>>>(count, n_nodes);
-  if (n_edges > 0) k_histogram<<<grid_for(n_edges), nt, 0, s>>>(dst, n_edges, nullptr, count);
+  launch_k(k_zero_i32, grid_for(n_nodes), nt, 0, s, count, n_nodes);
+  if (n_edges > 0) launch_k(k_histogram, grid_for(n_edges), nt, 0, s, dst, n_edges, nullptr, count);
   GFM_TRY(exclusive_scan(count, n_nodes, rowptr, scan_ws, s));
-  k_copy_i32<<<grid_for(n_nodes), nt, 0, s>>>(rowptr, n_nodes, cursor);
+  launch_k(k_copy_i32, grid_for(n_nodes), nt, 0, s, rowptr, n_nodes, cursor);
   if (n_edges > 0 && n_graphs > 0)
-    k_stable_bucket<<<ceil_div(n_graphs, 4), 128, 0, s>>>(dst, edge_offsets, n_graphs, cursor, order);
+    launch_k(k_stable_bucket, ceil_div(n_graphs, 4), 128, 0, s, dst, edge_offsets, n_graphs, cursor, order);
   if (n_edges > 0) {
     if (dtype == GFM_F32)
-      k_csr_gather<float><<<grid_for(n_edges), nt, 0, s>>>(order, n_edges, src, dst, pos, shift,
+      launch_k(k_csr_gather<float>, grid_for(n_edges), nt, 0, s, order, n_edges, src, dst, pos, shift,
                                                            col_src, edge_dst, (float*)edge_w,
                                                            (float*)edge_dx, inv);
     else
-      k_csr_gather<double><<<grid_for(n_edges), nt, 0, s>>>(order, n_edges, src, dst, pos, shift,
+      launch_k(k_csr_gather<double>, grid_for(n_edges), nt, 0, s, order, n_edges, src, dst, pos, shift,
                                                             col_src, edge_dst, (double*)edge_w,
                                                             (double*)edge_dx, inv);
   }
   // src-sorted CSC (stable over original order)
-  k_zero_i32<<<grid_for(n_nodes), nt, 0, s>>>(count, n_nodes);
-  if (n_edges > 0) k_histogram<<<grid_for(n_edges), nt, 0, s>>>(src, n_edges, nullptr, count);
+  launch_k(k_zero_i32, grid_for(n_nodes), nt, 0, s, count, n_nodes);
+  if (n_edges > 0) launch_k(k_histogram, grid_for(n_edges), nt, 0, s, src, n_edges, nullptr, count);
   GFM_TRY(exclusive_scan(count, n_nodes, csc_ptr, scan_ws, s));
-  k_copy_i32<<<grid_for(n_nodes), nt, 0, s>>>(csc_ptr, n_nodes, cursor);
+  launch_k(k_copy_i32, grid_for(n_nodes), nt, 0, s, csc_ptr, n_nodes, cursor);
   if (n_edges > 0 && n_graphs > 0) {
-    k_stable_bucket<<<ceil_div(n_graphs, 4), 128, 0, s>>>(src, edge_offsets, n_graphs, cursor, perm_csc);
-    k_csc_finish<<<grid_for(n_edges), nt, 0, s>>>(perm_csc, n_edges, nullptr, inv, dst, csc_eid, csc_dst);
+    launch_k(k_stable_bucket, ceil_div(n_graphs, 4), 128, 0, s, src, edge_offsets, n_graphs, cursor, perm_csc);
+    launch_k(k_csc_finish, grid_for(n_edges), nt, 0, s, perm_csc, n_edges, nullptr, inv, dst, csc_eid, csc_dst);
   }
   GFM_TRY(cudaGetLastError());
   return 0;
@@ -503,16 +515,16 @@ int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* edge_dst,
   int* eoff = (int*)carve(p, sizeof(int) * (n_graphs + 1));
   const int nt = 256;
   const int* n_dev = rowptr + n_nodes;
-  k_zero_i32<<<grid_for(n_nodes), nt, 0, s>>>(count, n_nodes);
-  if (e_cap > 0) k_histogram<<<grid_for(e_cap), nt, 0, s>>>(col_src, e_cap, n_dev, count);
+  launch_k(k_zero_i32, grid_for(n_nodes), nt, 0, s, count, n_nodes);
+  if (e_cap > 0) launch_k(k_histogram, grid_for(e_cap), nt, 0, s, col_src, e_cap, n_dev, count);
   GFM_TRY(exclusive_scan(count, n_nodes, csc_ptr, scan_ws, s));
-  k_copy_i32<<<grid_for(n_nodes), nt, 0, s>>>(csc_ptr, n_nodes, cursor);
+  launch_k(k_copy_i32, grid_for(n_nodes), nt, 0, s, csc_ptr, n_nodes, cursor);
   if (n_graphs > 0) {
-    k_edge_offsets<<<grid_for(n_graphs + 1), nt, 0, s>>>(rowptr, node_offsets, n_graphs, eoff);
-    k_stable_bucket<<<ceil_div(n_graphs, 4), 128, 0, s>>>(col_src, eoff, n_graphs, cursor, perm_csc);
+    launch_k(k_edge_offsets, grid_for(n_graphs + 1), nt, 0, s, rowptr, node_offsets, n_graphs, eoff);
+    launch_k(k_stable_bucket, ceil_div(n_graphs, 4), 128, 0, s, col_src, eoff, n_graphs, cursor, perm_csc);
   }
   if (e_cap > 0)
-    k_csc_finish<<<grid_for(e_cap), nt, 0, s>>>(perm_csc, e_cap, n_dev, nullptr, edge_dst, csc_eid, csc_dst);
+    launch_k(k_csc_finish, grid_for(e_cap), nt, 0, s, perm_csc, e_cap, n_dev, nullptr, edge_dst, csc_eid, csc_dst);
   GFM_TRY(cudaGetLastError());
   return 0;
 }

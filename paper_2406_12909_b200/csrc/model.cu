@@ -33,6 +33,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     k_splitk_reduce(const T* __restrict__ ws, int splits, int N, int K1, int K2, int with_bias,
                     T* __restrict__ g1, T* __restrict__ g2, T* __restrict__ gb, int trans) {
+  pdl_entry();
   __shared__ T tile[32][33];
   const int Kt = K1 + K2 + with_bias;
   const int R = trans ? Kt : N, C = trans ? N : Kt;
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(256)
     k_splitk_reduce_narrow(const T* __restrict__ ws, int splits, int N, int K1, int K2,
                            int with_bias, T* __restrict__ g1, T* __restrict__ g2,
                            T* __restrict__ gb, int trans) {
+  pdl_entry();
   __shared__ double red[8][33];
   const int Kt = K1 + K2 + with_bias;
   const long long total = (long long)N * Kt;
@@ -124,10 +126,10 @@ void splitk_reduce(const T* ws, int splits, int N, int K1, int K2, int with_bias
   const int R = trans ? Kt : N, C = trans ? N : Kt;
   const long long tiles = (long long)ceil_div(C, 32) * ceil_div(R, 32);
   if (tiles >= 2 * 148)
-    k_splitk_reduce<T><<<dim3(ceil_div(C, 32), ceil_div(R, 32)), 256, 0, s>>>(
+    launch_k(k_splitk_reduce<T>, dim3(ceil_div(C, 32), ceil_div(R, 32)), 256, 0, s,
         ws, splits, N, K1, K2, with_bias, g1, g2, gb, trans);
   else
-    k_splitk_reduce_narrow<T><<<grid_1d((long long)N * Kt, 32), 256, 0, s>>>(
+    launch_k(k_splitk_reduce_narrow<T>, grid_1d((long long)N * Kt, 32), 256, 0, s,
         ws, splits, N, K1, K2, with_bias, g1, g2, gb, trans);
 }
 
@@ -135,6 +137,7 @@ void splitk_reduce(const T* ws, int splits, int N, int K1, int K2, int with_bias
 template <typename T>
 __global__ void k_node_energy(const T* __restrict__ y, int n, int G, const T* __restrict__ a,
                               const T* __restrict__ c, T* __restrict__ node_e) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
        i += gridDim.x * (blockDim.x >> 5)) {
@@ -149,6 +152,7 @@ __global__ void k_node_energy(const T* __restrict__ y, int n, int G, const T* __
 template <typename T>
 __global__ void k_graph_pool(const T* __restrict__ node_e, const int* __restrict__ off,
                              int n_graphs, T* __restrict__ e_pred) {
+  pdl_entry();
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n_graphs; b += gridDim.x * blockDim.x) {
     const int lo = off[b], hi = off[b + 1];
     auto get = [&](long long i) -> T { return node_e[i]; };
@@ -167,6 +171,7 @@ __global__ void __launch_bounds__(256)
                  const T* __restrict__ f_true, int N, T aE, T aF, T* __restrict__ loss,
                  T* __restrict__ de, T* __restrict__ df, float* __restrict__ contrib,
                  double* __restrict__ partial, unsigned* __restrict__ ticket) {
+  pdl_entry();
   __shared__ double red[2][8];
   __shared__ bool last;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
@@ -230,6 +235,7 @@ template <typename T>
 __global__ void k_energy_seed(const T* __restrict__ de, const int* __restrict__ gnode, int n,
                               int G, const T* __restrict__ a, const T* __restrict__ y,
                               T* __restrict__ ds, int ld_ds, T* __restrict__ dz) {
+  pdl_entry();
   // 2D: y over nodes, x over the G columns (no 64-bit divides)
   for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
     const T s = de[gnode[i]];
@@ -316,6 +322,7 @@ size_t linear_bwd_weight_ws(int M, int N, int K1, int K2, int with_bias) {
 
 template <typename T>
 __global__ void k_fill_ones(T* __restrict__ ones, int m) {  // ones[i][0] = 1, [1..3] = 0
+  pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 4 * m; i += gridDim.x * blockDim.x)
     ones[i] = (i & 3) == 0 ? T(1) : T(0);
 }
@@ -349,7 +356,7 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
       Cols2Ld<T> a{X1, ld1, K1, X2, ld2, K2};
       if (with_bias) {
         T* ones = ws + (((size_t)splits * N * Kt + 63) & ~(size_t)63);
-        if (!ones_ready) k_fill_ones<T><<<grid_1d(4LL * M), 256, 0, s>>>(ones, M);
+        if (!ones_ready) launch_k(k_fill_ones<T>, grid_1d(4LL * M), 256, 0, s, ones, M);
         a.ones = ones;
       }
       ColsLd<T> b{dY, ldd};
@@ -546,9 +553,9 @@ int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const v
                        int dtype, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   GFM_DISPATCH(dtype, "gfm_energy_readout",
-               (k_node_energy<T><<<grid_1d((long long)n_nodes * 32), 256, 0, s>>>(
+               (launch_k(k_node_energy<T>, grid_1d((long long)n_nodes * 32), 256, 0, s,
                     (const T*)y, n_nodes, G, (const T*)a, (const T*)c, (T*)node_e),
-                k_graph_pool<T><<<grid_1d(n_graphs), 256, 0, s>>>((const T*)node_e, node_offsets,
+                launch_k(k_graph_pool<T>, grid_1d(n_graphs), 256, 0, s, (const T*)node_e, node_offsets,
                                                                  n_graphs, (T*)e_pred),
                 cudaGetLastError()))
 }
@@ -563,7 +570,7 @@ int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_per, int
   double* partial = (double*)workspace;
   unsigned* ticket = (unsigned*)(partial + 2 * kLossBlocks);
   GFM_DISPATCH(dtype, "gfm_loss_seeds",
-               (k_loss_seeds<T><<<kLossBlocks, 256, 0, s>>>(
+               (launch_k(k_loss_seeds<T>, kLossBlocks, 256, 0, s,
                     (const T*)e_pred, (const T*)e_true, n_per, n_graphs, (const T*)f_pred,
                     (const T*)f_true, n_nodes, (T)alpha_e, (T)alpha_f, (T*)loss, (T*)de, (T*)df,
                     contrib, partial, ticket),
@@ -575,8 +582,7 @@ int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const 
   if (ld_ds < 1) return GFM_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   GFM_DISPATCH(dtype, "gfm_energy_seed",
-               (k_energy_seed<T><<<dim3(1, std::min(ceil_div(std::max(n_nodes, 1), 8), 65535)),
-                                   dim3(32, 8), 0, s>>>(
+               (launch_k(k_energy_seed<T>, dim3(1, std::min(ceil_div(std::max(n_nodes, 1), 8), 65535)), dim3(32, 8), 0, s,
                     (const T*)de, gnode, n_nodes, G, (const T*)a, (const T*)y, (T*)ds, ld_ds,
                     (T*)dz),
                 cudaGetLastError()))

@@ -11,6 +11,7 @@ namespace gfm {
 
 template <typename G>
 __global__ void k_nonfinite(const G* __restrict__ v, long long n, int* __restrict__ flag) {
+  pdl_entry();
   int bad = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -27,6 +28,7 @@ __global__ void k_adam(const G* __restrict__ grad_sum, long long n, double world
                        const double* __restrict__ bc, double lr, double b1, double b2,
                        double one_m_b1, double one_m_b2, double eps,
                        const int* __restrict__ skip, float* __restrict__ out32) {
+  pdl_entry();
   if (skip && *skip) return;  // train.py:264-274: update discarded
   const double bc1 = bc[0], bc2 = bc[1];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -48,6 +50,7 @@ template <typename G>
 __global__ void k_sgd(const G* __restrict__ grad_sum, long long n, double world,
                       double* __restrict__ master, double lr, const int* __restrict__ skip,
                       float* __restrict__ out32) {
+  pdl_entry();
   if (skip && *skip) return;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -59,6 +62,7 @@ __global__ void k_sgd(const G* __restrict__ grad_sum, long long n, double world,
 }
 
 __global__ void k_cast_f64_f32(const double* __restrict__ in, long long n, float* __restrict__ out) {
+  pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     out[i] = (float)in[i];
@@ -68,6 +72,7 @@ __global__ void k_cast_f64_f32(const double* __restrict__ in, long long n, float
 // no host round trip; frozen once the non-finite flag is set.
 __global__ void k_adam_advance(long long* t, double b1, double b2, double* bc,
                                const int* __restrict__ skip) {
+  pdl_entry();
   if (skip && *skip) return;
   const long long tt = *t + 1;
   *t = tt;
@@ -92,9 +97,9 @@ int gfm_nonfinite_flag(const void* v, long long n, int dtype, int* flag, void* s
   cudaStream_t s = (cudaStream_t)stream;
   if (n <= 0) return 0;
   if (dtype == GFM_F32)
-    k_nonfinite<float><<<grid_for(n), 256, 0, s>>>((const float*)v, n, flag);
+    launch_k(k_nonfinite<float>, grid_for(n), 256, 0, s, (const float*)v, n, flag);
   else if (dtype == GFM_F64)
-    k_nonfinite<double><<<grid_for(n), 256, 0, s>>>((const double*)v, n, flag);
+    launch_k(k_nonfinite<double>, grid_for(n), 256, 0, s, (const double*)v, n, flag);
   else {
     set_error("gfm_nonfinite_flag: bad dtype %d", dtype);
     return GFM_EINVAL;
@@ -111,11 +116,11 @@ int gfm_adam_step(const void* grad_sum, int grad_dtype, long long n, double worl
   if (n <= 0) return 0;
   const double omb1 = 1.0 - beta1, omb2 = 1.0 - beta2;  // as Python evaluates (1.0 - beta)
   if (grad_dtype == GFM_F32)
-    k_adam<float><<<grid_for(n), 256, 0, s>>>((const float*)grad_sum, n, world, master, m, v,
+    launch_k(k_adam<float>, grid_for(n), 256, 0, s, (const float*)grad_sum, n, world, master, m, v,
                                               bias_corr, lr, beta1, beta2, omb1, omb2, eps,
                                               skip_flag, params32);
   else if (grad_dtype == GFM_F64)
-    k_adam<double><<<grid_for(n), 256, 0, s>>>((const double*)grad_sum, n, world, master, m, v,
+    launch_k(k_adam<double>, grid_for(n), 256, 0, s, (const double*)grad_sum, n, world, master, m, v,
                                                bias_corr, lr, beta1, beta2, omb1, omb2, eps,
                                                skip_flag, params32);
   else {
@@ -132,10 +137,10 @@ int gfm_sgd_step(const void* grad_sum, int grad_dtype, long long n, double world
   cudaStream_t s = (cudaStream_t)stream;
   if (n <= 0) return 0;
   if (grad_dtype == GFM_F32)
-    k_sgd<float><<<grid_for(n), 256, 0, s>>>((const float*)grad_sum, n, world, master, lr,
+    launch_k(k_sgd<float>, grid_for(n), 256, 0, s, (const float*)grad_sum, n, world, master, lr,
                                              skip_flag, params32);
   else if (grad_dtype == GFM_F64)
-    k_sgd<double><<<grid_for(n), 256, 0, s>>>((const double*)grad_sum, n, world, master, lr,
+    launch_k(k_sgd<double>, grid_for(n), 256, 0, s, (const double*)grad_sum, n, world, master, lr,
                                               skip_flag, params32);
   else {
     set_error("gfm_sgd_step: bad grad dtype %d", grad_dtype);
@@ -148,7 +153,7 @@ int gfm_sgd_step(const void* grad_sum, int grad_dtype, long long n, double world
 
 int gfm_adam_advance(long long* step, double beta1, double beta2, double* bias_corr,
                      const int* skip_flag, void* stream) {
-  k_adam_advance<<<1, 1, 0, (cudaStream_t)stream>>>(step, beta1, beta2, bias_corr, skip_flag);
+  launch_k(k_adam_advance, 1, 1, 0, (cudaStream_t)stream, step, beta1, beta2, bias_corr, skip_flag);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) set_error("gfm_adam_advance: %s", cudaGetErrorString(e));
   return (int)e;
@@ -156,7 +161,7 @@ int gfm_adam_advance(long long* step, double beta1, double beta2, double* bias_c
 
 int gfm_cast_f64_to_f32(const double* in, long long n, float* out, void* stream) {
   if (n <= 0) return 0;
-  k_cast_f64_f32<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(in, n, out);
+  launch_k(k_cast_f64_f32, grid_for(n), 256, 0, (cudaStream_t)stream, in, n, out);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) set_error("gfm_cast_f64_to_f32: %s", cudaGetErrorString(e));
   return (int)e;

@@ -354,6 +354,7 @@ template <int BN, bool VA, bool VB, class AL, class BL, class Epi>
 __global__ void __launch_bounds__(kWSThreads, 1)
     tc_gemm_kernel(int M, const int* __restrict__ M_dev, int N, int K, const int* __restrict__ K_dev,
                    int k_chunk, int splits, int split3, AL a, BL b, Epi epi) {
+  pdl_entry();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = Smem<BN>;
   constexpr int NC = tmem_cols(2 * BN);  // two accumulators
@@ -872,6 +873,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     tc_gemm_tma_kernel(int M, const int* __restrict__ M_dev, int N, int K, int k_chunk, int splits,
                        int split3, const __grid_constant__ TmaOp ta,
                        const __grid_constant__ TmaOp tb, Epi epi) {
+  pdl_entry();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = SmemT<BN, AT != 0>;
   // TMEM: two BN-column accumulators, then (AT) kL A slots of 32 hi + 32 lo columns
@@ -1134,7 +1136,7 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
       const int smem = at ? SmemT<BN, true>::kBytes : SmemT<BN, false>::kBytes;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      kern<<<grid, kTmaThreads, smem, s>>>(M, M_dev, N, K, k_chunk, splits, split3, ta, tb, epi);
+      launch_k(kern, grid, kTmaThreads, smem, s, M, M_dev, N, K, k_chunk, splits, split3, ta, tb, epi);
       return cudaGetLastError();
     }
   }
@@ -1146,7 +1148,7 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
                        : tc_gemm_kernel<BN, false, false, AL, BL, Epi>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kWSThreads, smem, s>>>(M, M_dev, N, K, K_dev, k_chunk, splits, split3, a, b, epi);
+  launch_k(kern, grid, kWSThreads, smem, s, M, M_dev, N, K, K_dev, k_chunk, splits, split3, a, b, epi);
   return cudaGetLastError();
 }
 
