@@ -191,29 +191,72 @@ __device__ __forceinline__ void agg_fwd_node(Ld ld, int node, int cb, int H,
     consume(r, ww, p, true);
     ++p;
   }
-  for (; p + 4 <= end; p += 4) {
-    int sj[4];
-    float ww[4];
+  if constexpr (LPN == 32) {
+    // the node's LPN lanes load LPN (src, w) pairs at once (one coalesced load
+    // each) and broadcast them with shuffles, instead of every lane loading
+    // every index
+    const int gl = (threadIdx.x & 31) % LPN;
+    const unsigned gmask =
+        LPN == 32 ? 0xffffffffu : (((1u << LPN) - 1u) << ((threadIdx.x & 31) - gl));
+    for (int c0 = p; c0 < end; c0 += LPN) {
+      const int cnt = min(LPN, end - c0);
+      int my_s = 0;
+      float my_w = 0.f;
+      if (gl < cnt) {
+        my_s = __ldg(col_src + c0 + gl);
+        my_w = __ldg(w + c0 + gl);
+      }
+      int e = 0;
+      for (; e + 4 <= cnt; e += 4) {
+        int sj[4];
+        float ww[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      sj[u] = __ldg(col_src + p + u);
-      ww[u] = __ldg(w + p + u);
+        for (int u = 0; u < 4; ++u) {
+          sj[u] = __shfl_sync(gmask, my_s, e + u, LPN);
+          ww[u] = __shfl_sync(gmask, my_w, e + u, LPN);
+        }
+        float4 r[4][NV];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) r[u][v] = ld(sj[u], v);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) consume(r[u], ww[u], c0 + e + u, false);
+      }
+      for (; e < cnt; ++e) {
+        const int sj = __shfl_sync(gmask, my_s, e, LPN);
+        const float ww = __shfl_sync(gmask, my_w, e, LPN);
+        float4 r[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) r[v] = ld(sj, v);
+        consume(r, ww, c0 + e, false);
+      }
     }
-    float4 r[4][NV];
+  } else {  // narrow rows: the node's whole CSR row fits in a few unrolled loads
+    for (; p + 4 <= end; p += 4) {
+      int sj[4];
+      float ww[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 4; ++u) {
+        sj[u] = __ldg(col_src + p + u);
+        ww[u] = __ldg(w + p + u);
+      }
+      float4 r[4][NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) r[u][v] = ld(sj[u], v);
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) consume(r[u], ww[u], p + u, false);
-  }
-  for (; p < end; ++p) {
-    const int sj = __ldg(col_src + p);
-    const float ww = __ldg(w + p);
-    float4 r[NV];
+        for (int v = 0; v < NV; ++v) r[u][v] = ld(sj[u], v);
 #pragma unroll
-    for (int v = 0; v < NV; ++v) r[v] = ld(sj, v);
-    consume(r, ww, p, false);
+      for (int u = 0; u < 4; ++u) consume(r[u], ww[u], p + u, false);
+    }
+    for (; p < end; ++p) {
+      const int sj = __ldg(col_src + p);
+      const float ww = __ldg(w + p);
+      float4 r[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) r[v] = ld(sj, v);
+      consume(r, ww, p, false);
+    }
   }
   const int deg = end - beg;
   const float inv = deg > 0 ? 1.f / (float)deg : 0.f;
@@ -486,56 +529,131 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
     hj[v] = hasC ? reinterpret_cast<const float4*>(h_in)[o] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int qb = csc_ptr[j], qe = csc_ptr[j + 1];
-  // U CSC slots per batch: all their row loads issue before the (in-order)
-  // accumulation, so U x 3 gathers per lane are in flight.  Narrow rows
-  // (LPN < 32: several nodes per warp) are issue-bound rather than latency-
-  // bound and measure faster unbatched.
-  constexpr int U = LPN == 32 ? 2 : 1;
-  for (int q = qb; q < qe; q += U) {
-    int p[U], i[U];
-    float ww[U];
-    float4 g[U][NV], cf[U][NV];
-    int4 a[U][NV];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const bool ok = q + u < qe;
-      p[u] = ok ? __ldg(csc_eid + q + u) : -2;
-      i[u] = ok ? __ldg(csc_dst + q + u) : 0;
-      ww[u] = ok ? __ldg(w + p[u]) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const bool ok = q + u < qe;
-        g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        cf[u][v] = g[u][v];
-        a[u][v] = make_int4(-1, -1, -1, -1);
-        if (ok && hasG) g[u][v] = ldG(i[u], v);
-        if (ok && hasC) cf[u][v] = ldC(i[u], v);
-        if (ok && hasA) a[u][v] = ldA(i[u], v);
+  if constexpr (LPN == 32) {
+    // U CSC slots per batch: all their row loads issue before the (in-order)
+    // accumulation, so U x 3 gathers per lane are in flight.  Narrow rows
+    // (LPN < 32: several nodes per warp) are issue-bound rather than latency-
+    // bound and measure faster unbatched.
+    constexpr int U = LPN == 32 ? 2 : 1;
+    // the node's LPN lanes load LPN CSC slots (eid, dst, w[eid]) at once and
+    // broadcast them with shuffles
+    const int gl = (threadIdx.x & 31) % LPN;
+    const unsigned gmask =
+        LPN == 32 ? 0xffffffffu : (((1u << LPN) - 1u) << ((threadIdx.x & 31) - gl));
+    for (int c0 = qb; c0 < qe; c0 += LPN) {
+      const int cnt = min(LPN, qe - c0);
+      int my_p = -2, my_i = 0;
+      float my_w = 0.f;
+      if (gl < cnt) {
+        my_p = __ldg(csc_eid + c0 + gl);
+        my_i = __ldg(csc_dst + c0 + gl);
+        my_w = __ldg(w + my_p);
       }
+      for (int e = 0; e < cnt; e += U) {
+        int p[U], i[U];
+        float ww[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (q + u >= qe) break;
+        for (int u = 0; u < U; ++u) {
+          const bool ok = e + u < cnt;
+          const int src = ok ? e + u : 0;
+          const int pp = __shfl_sync(gmask, my_p, src, LPN);
+          const int ii = __shfl_sync(gmask, my_i, src, LPN);
+          const float wv = __shfl_sync(gmask, my_w, src, LPN);
+          p[u] = ok ? pp : -2;
+          i[u] = ok ? ii : 0;
+          ww[u] = ok ? wv : 0.f;
+        }
+        float4 g[U][NV], cf[U][NV];
+        int4 a[U][NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int c4 = v * LPN + cb;
-        float4 dm = g[u][v];
-        if (hasC) dm = fma4(cf[u][v], mul4(hj[v], bcast4(ww[u])), dm);
-        if (hasA) {
-          const int4 am = a[u][v];
-          const int pp = p[u];
-          if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
-            const float4 d =
-                __ldg(reinterpret_cast<const float4*>(dmax + (long long)i[u] * ldm) + c4);
-            if (am.x == pp) dm.x += d.x;
-            if (am.y == pp) dm.y += d.y;
-            if (am.z == pp) dm.z += d.z;
-            if (am.w == pp) dm.w += d.w;
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const bool ok = e + u < cnt;
+            g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            cf[u][v] = g[u][v];
+            a[u][v] = make_int4(-1, -1, -1, -1);
+            if (ok && hasG) g[u][v] = ldG(i[u], v);
+            if (ok && hasC) cf[u][v] = ldC(i[u], v);
+            if (ok && hasA) a[u][v] = ldA(i[u], v);
+          }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (e + u >= cnt) break;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int c4 = v * LPN + cb;
+            float4 dm = g[u][v];
+            if (hasC) dm = fma4(cf[u][v], mul4(hj[v], bcast4(ww[u])), dm);
+            if (hasA) {
+              const int4 am = a[u][v];
+              const int pp = p[u];
+              if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
+                const float4 d =
+                    __ldg(reinterpret_cast<const float4*>(dmax + (long long)i[u] * ldm) + c4);
+                if (am.x == pp) dm.x += d.x;
+                if (am.y == pp) dm.y += d.y;
+                if (am.z == pp) dm.z += d.z;
+                if (am.w == pp) dm.w += d.w;
+              }
+            }
+            acc[v] = fma4(dm, bcast4(ww[u]), acc[v]);
           }
         }
-        acc[v] = fma4(dm, bcast4(ww[u]), acc[v]);
+      }
+    }
+  } else {
+    // U CSC slots per batch: all their row loads issue before the (in-order)
+    // accumulation, so U x 3 gathers per lane are in flight.  Narrow rows
+    // (LPN < 32: several nodes per warp) are issue-bound rather than latency-
+    // bound and measure faster unbatched.
+    constexpr int U = LPN == 32 ? 2 : 1;
+    for (int q = qb; q < qe; q += U) {
+      int p[U], i[U];
+      float ww[U];
+      float4 g[U][NV], cf[U][NV];
+      int4 a[U][NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = q + u < qe;
+        p[u] = ok ? __ldg(csc_eid + q + u) : -2;
+        i[u] = ok ? __ldg(csc_dst + q + u) : 0;
+        ww[u] = ok ? __ldg(w + p[u]) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const bool ok = q + u < qe;
+          g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+          cf[u][v] = g[u][v];
+          a[u][v] = make_int4(-1, -1, -1, -1);
+          if (ok && hasG) g[u][v] = ldG(i[u], v);
+          if (ok && hasC) cf[u][v] = ldC(i[u], v);
+          if (ok && hasA) a[u][v] = ldA(i[u], v);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (q + u >= qe) break;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int c4 = v * LPN + cb;
+          float4 dm = g[u][v];
+          if (hasC) dm = fma4(cf[u][v], mul4(hj[v], bcast4(ww[u])), dm);
+          if (hasA) {
+            const int4 am = a[u][v];
+            const int pp = p[u];
+            if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
+              const float4 d =
+                  __ldg(reinterpret_cast<const float4*>(dmax + (long long)i[u] * ldm) + c4);
+              if (am.x == pp) dm.x += d.x;
+              if (am.y == pp) dm.y += d.y;
+              if (am.z == pp) dm.z += d.z;
+              if (am.w == pp) dm.w += d.w;
+            }
+          }
+          acc[v] = fma4(dm, bcast4(ww[u]), acc[v]);
+        }
       }
     }
   }
