@@ -176,11 +176,14 @@ __global__ void __launch_bounds__(256)
   for (int k = 0; k < NPB; ++k) maxdeg = max(maxdeg, degs[k]);
   double fx = 0.0, fy = 0.0, fz = 0.0;
   for (int p0 = 0; p0 < maxdeg; p0 += CH) {
+    // this chunk's sources: one coalesced load, broadcast by shuffles
+    const int my_s = beg + p0 + lane < end ? __ldg(col_src + beg + p0 + lane) : 0;
     for (int e = 0; e < CH; e += 2) {
       const int pa = beg + p0 + e, pb = pa + 1;
       if (pa >= end) break;  // warp-uniform
       const bool hb = pb < end;
-      const int sa = __ldg(col_src + pa), sb = hb ? __ldg(col_src + pb) : sa;
+      const int sa = __shfl_sync(0xffffffffu, my_s, e);
+      const int sb = __shfl_sync(0xffffffffu, my_s, hb ? e + 1 : e);
       const float4 ra = __ldg(P4 + (long long)sa * H4 + c4);
       const float4 rb = __ldg(P4 + (long long)sb * H4 + c4);
       const float4 xa = f4add3(pi, ra, cu), xb = f4add3(pi, rb, cu);
@@ -280,18 +283,56 @@ __global__ void __launch_bounds__(256)
     tu[v] = dd[v];
   }
   const float fx = df[3LL * i + 0], fy = df[3LL * i + 1], fz = df[3LL * i + 2];
-  for (int p = rowptr[i]; p < rowptr[i + 1]; ++p) {
-    const int s = __ldg(col_src + p);
-    // model.py:537-538 (sum over xyz left to right)
-    const float dm = __fadd_rn(__fadd_rn(__fmul_rn(fx, dx[3LL * p]), __fmul_rn(fy, dx[3LL * p + 1])),
-                               __fmul_rn(fz, dx[3LL * p + 2]));
+  // model.py:537-538 (sum over xyz left to right)
+  auto dm_of = [&](int p) {
+    return __fadd_rn(__fadd_rn(__fmul_rn(fx, dx[3LL * p]), __fmul_rn(fy, dx[3LL * p + 1])),
+                     __fmul_rn(fz, dx[3LL * p + 2]));
+  };
+  auto edge = [&](float4 (&r)[NV], float dm) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const float4 x = f4add3(pi[v], __ldg(P4 + (long long)s * H4 + v * LPN + cb), cu[v]);
+      const float4 x = f4add3(pi[v], r[v], cu[v]);
       const float4 t = make_float4(th<FAST>(x.x), th<FAST>(x.y), th<FAST>(x.z), th<FAST>(x.w));
       dd[v].x += dm * uu[v].x * (1.f - t.x * t.x); dd[v].y += dm * uu[v].y * (1.f - t.y * t.y);
       dd[v].z += dm * uu[v].z * (1.f - t.z * t.z); dd[v].w += dm * uu[v].w * (1.f - t.w * t.w);
       tu[v].x += t.x * dm; tu[v].y += t.y * dm; tu[v].z += t.z * dm; tu[v].w += t.w * dm;
+    }
+  };
+  const int beg = rowptr[i], end = rowptr[i + 1];
+  if constexpr (LPN == 32) {
+    // 32-lane rows: lane k computes (src, dm) of edge c0 + k once; shuffles
+    // broadcast them; two P rows in flight per lane
+    for (int c0 = beg; c0 < end; c0 += 32) {
+      const int cnt = min(32, end - c0);
+      int my_s = 0;
+      float my_dm = 0.f;
+      if (lane < cnt) {
+        my_s = __ldg(col_src + c0 + lane);
+        my_dm = dm_of(c0 + lane);
+      }
+      for (int e = 0; e < cnt; e += 2) {
+        const bool two = e + 1 < cnt;
+        const int s0 = __shfl_sync(0xffffffffu, my_s, e);
+        const float d0 = __shfl_sync(0xffffffffu, my_dm, e);
+        const int s1 = __shfl_sync(0xffffffffu, my_s, two ? e + 1 : e);
+        const float d1 = __shfl_sync(0xffffffffu, my_dm, two ? e + 1 : e);
+        float4 r0[NV], r1[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          r0[v] = __ldg(P4 + (long long)s0 * H4 + v * LPN + cb);
+          r1[v] = __ldg(P4 + (long long)s1 * H4 + v * LPN + cb);
+        }
+        edge(r0, d0);
+        if (two) edge(r1, d1);
+      }
+    }
+  } else {
+    for (int p = beg; p < end; ++p) {
+      const int s = __ldg(col_src + p);
+      float4 r[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) r[v] = __ldg(P4 + (long long)s * H4 + v * LPN + cb);
+      edge(r, dm_of(p));
     }
   }
 #pragma unroll
@@ -327,16 +368,54 @@ __global__ void __launch_bounds__(256)
     uu[v] = ld4u(u, c4);
     acc[v] = reinterpret_cast<const float4*>(Ddst)[(long long)j * H4 + c4];
   }
-  for (int q = csc_ptr[j]; q < csc_ptr[j + 1]; ++q) {
-    const int p = __ldg(csc_eid + q), i = __ldg(csc_dst + q);
-    const float dm = __fadd_rn(__fadd_rn(__fmul_rn(df[3LL * i], dx[3LL * p]), __fmul_rn(df[3LL * i + 1], dx[3LL * p + 1])),
-                               __fmul_rn(df[3LL * i + 2], dx[3LL * p + 2]));
+  auto dm_of = [&](int p, int i) {
+    return __fadd_rn(__fadd_rn(__fmul_rn(df[3LL * i], dx[3LL * p]), __fmul_rn(df[3LL * i + 1], dx[3LL * p + 1])),
+                     __fmul_rn(df[3LL * i + 2], dx[3LL * p + 2]));
+  };
+  auto edge = [&](float4 (&r)[NV], float dm) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const float4 x = f4add3(__ldg(P4 + (long long)i * H4 + v * LPN + cb), pj[v], cu[v]);
+      const float4 x = f4add3(r[v], pj[v], cu[v]);
       const float4 t = make_float4(th<FAST>(x.x), th<FAST>(x.y), th<FAST>(x.z), th<FAST>(x.w));
       acc[v].x += dm * uu[v].x * (1.f - t.x * t.x); acc[v].y += dm * uu[v].y * (1.f - t.y * t.y);
       acc[v].z += dm * uu[v].z * (1.f - t.z * t.z); acc[v].w += dm * uu[v].w * (1.f - t.w * t.w);
+    }
+  };
+  const int qb = csc_ptr[j], qe = csc_ptr[j + 1];
+  if constexpr (LPN == 32) {
+    // lane k computes (dst, dm) of CSC slot c0 + k once; shuffles broadcast
+    for (int c0 = qb; c0 < qe; c0 += 32) {
+      const int cnt = min(32, qe - c0);
+      int my_i = 0;
+      float my_dm = 0.f;
+      if (lane < cnt) {
+        const int p = __ldg(csc_eid + c0 + lane);
+        my_i = __ldg(csc_dst + c0 + lane);
+        my_dm = dm_of(p, my_i);
+      }
+      for (int e = 0; e < cnt; e += 2) {
+        const bool two = e + 1 < cnt;
+        const int i0 = __shfl_sync(0xffffffffu, my_i, e);
+        const float d0 = __shfl_sync(0xffffffffu, my_dm, e);
+        const int i1 = __shfl_sync(0xffffffffu, my_i, two ? e + 1 : e);
+        const float d1 = __shfl_sync(0xffffffffu, my_dm, two ? e + 1 : e);
+        float4 r0[NV], r1[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          r0[v] = __ldg(P4 + (long long)i0 * H4 + v * LPN + cb);
+          r1[v] = __ldg(P4 + (long long)i1 * H4 + v * LPN + cb);
+        }
+        edge(r0, d0);
+        if (two) edge(r1, d1);
+      }
+    }
+  } else {
+    for (int q = qb; q < qe; ++q) {
+      const int p = __ldg(csc_eid + q), i = __ldg(csc_dst + q);
+      float4 r[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) r[v] = __ldg(P4 + (long long)i * H4 + v * LPN + cb);
+      edge(r, dm_of(p, i));
     }
   }
 #pragma unroll
