@@ -26,6 +26,10 @@
 
 #include "common.cuh"
 
+#ifndef GFM_AGG_FWD_UF
+#define GFM_AGG_FWD_UF 4
+#endif
+
 namespace gfm {
 
 struct AggLayout {
@@ -207,21 +211,22 @@ __device__ __forceinline__ void agg_fwd_node(Ld ld, int node, int cb, int H,
         my_w = __ldg(w + c0 + gl);
       }
       int e = 0;
-      for (; e + 4 <= cnt; e += 4) {
-        int sj[4];
-        float ww[4];
+      constexpr int UF = GFM_AGG_FWD_UF;  // rows in flight per lane
+      for (; e + UF <= cnt; e += UF) {
+        int sj[UF];
+        float ww[UF];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < UF; ++u) {
           sj[u] = __shfl_sync(gmask, my_s, e + u, LPN);
           ww[u] = __shfl_sync(gmask, my_w, e + u, LPN);
         }
-        float4 r[4][NV];
+        float4 r[UF][NV];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < UF; ++u)
 #pragma unroll
           for (int v = 0; v < NV; ++v) r[u][v] = ld(sj[u], v);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) consume(r[u], ww[u], c0 + e + u, false);
+        for (int u = 0; u < UF; ++u) consume(r[u], ww[u], c0 + e + u, false);
       }
       for (; e < cnt; ++e) {
         const int sj = __shfl_sync(gmask, my_s, e, LPN);
