@@ -92,6 +92,18 @@ GFM_API int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* e
                      const int* node_offsets, int n_graphs, int n_nodes, int e_cap, int* csc_ptr,
                      int* csc_eid, int* csc_dst, void* workspace, void* stream);
 
+/* Fused batch assembly (replaces graph_of_node + radius_count + scan +
+ * radius_fill + csc_from_csr): one CTA per graph (graphs of up to 256 atoms;
+ * GFM_EINVAL otherwise -- use the separate calls), same predicate, cap, order
+ * and outputs.  `workspace` (gfm_radius_batch_workspace_bytes) must be
+ * ZERO-initialised once; each call leaves it ready for the next. */
+GFM_API size_t gfm_radius_batch_workspace_bytes(int n_graphs);
+GFM_API int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, int n_nodes,
+                             int max_atoms, const double* cells, double rc, int max_nbr,
+                             int* gnode, int* rowptr, int* col_src, int* edge_dst, void* edge_w,
+                             void* edge_dx, int* csc_ptr, int* csc_eid, int* csc_dst,
+                             void* workspace, int dtype, void* stream);
+
 /* ---- K3/K4/K11: embedding and aggregation (model.py:293-341, 351-356) - */
 /* h = emb[z - 1] (model.py:351) */
 GFM_API int gfm_embed(const int* z, int n, const void* emb, int H, void* h, int dtype, void* stream);

@@ -45,6 +45,9 @@ SIGNATURES = {
     "gfm_csr_build": (_I, [_P, _P, _P, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P,
                            _P, _I, _P, _P]),
     "gfm_csc_from_csr": (_I, [_P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "gfm_radius_batch_workspace_bytes": (_S, [_I]),
+    "gfm_radius_batch": (_I, [_P, _P, _I, _I, _I, _P, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P,
+                              _P, _P, _I, _P]),
     "gfm_embed": (_I, [_P, _I, _P, _I, _P, _I, _P]),
     "gfm_agg_parts_count": (_I, [_I]),
     "gfm_agg_fwd": (_I, [_P, _I, _I, _P, _P, _P, _I, _P, _P, _P, _I, _I, _P]),

@@ -366,6 +366,238 @@ __global__ void k_csc_finish(const int* __restrict__ perm_csc, int n_cap, const 
   }
 }
 
+
+// ------------------------------------------- fused per-graph batch assembly
+// One CTA per graph builds that graph's whole slice of the batch in one pass:
+// neighbour search over the graph's atoms (positions staged in smem, same
+// fp64 predicate / cap / minimum image as k_radius), the dst-sorted CSR rows,
+// the src-sorted CSC (within a graph, CSC order of src j = ascending dst, so a
+// walk over dst rows with per-src cursors is already stable), graph_of_node,
+// and the graph's global edge offset by a decoupled look-back over the
+// graph CTAs (status words reset by the last CTA, so the kernel is CUDA-graph
+// replayable).  Replaces the 15 launches of count / scan / fill / CSC build.
+constexpr int kFusedMaxAtoms = 256, kFusedWarps = 8;
+
+__host__ __device__ inline int fused_stride(int n_max, int max_nbr) {
+  const int full = n_max > 1 ? n_max - 1 : 1;
+  return max_nbr > 0 && max_nbr < full ? max_nbr : full;
+}
+
+__host__ __device__ inline size_t fused_smem_bytes(int n_max, int max_nbr) {
+  const size_t a = kFusedMaxAtoms;
+  return a * 3 * sizeof(double)                                  // positions
+         + (size_t)kFusedWarps * a * (sizeof(double) + sizeof(int))  // cap candidates
+         + (3 * a + 16) * sizeof(int)                             // rowptr, csc start, cursor, base
+         + (size_t)n_max * fused_stride(n_max, max_nbr) * sizeof(int);  // neighbour lists
+}
+
+__device__ __forceinline__ PairGeom pair_geom_s(const double* __restrict__ sp, int j, int i,
+                                                const double* cell) {
+  PairGeom g;
+  g.dx = __dsub_rn(sp[3 * j + 0], sp[3 * i + 0]);
+  g.dy = __dsub_rn(sp[3 * j + 1], sp[3 * i + 1]);
+  g.dz = __dsub_rn(sp[3 * j + 2], sp[3 * i + 2]);
+  if (cell) {
+    g.dx = __dadd_rn(g.dx, __dmul_rn(-cell[0], rint(__ddiv_rn(g.dx, cell[0]))));
+    g.dy = __dadd_rn(g.dy, __dmul_rn(-cell[1], rint(__ddiv_rn(g.dy, cell[1]))));
+    g.dz = __dadd_rn(g.dz, __dmul_rn(-cell[2], rint(__ddiv_rn(g.dz, cell[2]))));
+  }
+  g.d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(g.dx, g.dx), __dmul_rn(g.dy, g.dy)),
+                             __dmul_rn(g.dz, g.dz)));
+  return g;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kFusedWarps * 32)
+    k_radius_batch(const double* __restrict__ pos, const int* __restrict__ node_off, int n_graphs,
+                   int n_nodes, const double* __restrict__ cells, double rc, int max_nbr,
+                   int stride, int* __restrict__ gnode, int* __restrict__ rowptr,
+                   int* __restrict__ col_src, int* __restrict__ edge_dst, T* __restrict__ edge_w,
+                   T* __restrict__ edge_dx, int* __restrict__ csc_ptr, int* __restrict__ csc_eid,
+                   int* __restrict__ csc_dst, unsigned long long* __restrict__ status,
+                   unsigned* __restrict__ done) {
+  pdl_entry();
+  extern __shared__ __align__(16) unsigned char fsm[];
+  const int A = kFusedMaxAtoms;
+  double* s_pos = reinterpret_cast<double*>(fsm);
+  double* s_cd = s_pos + 3 * A;                                  // [warps][A]
+  int* s_cj = reinterpret_cast<int*>(s_cd + kFusedWarps * A);    // [warps][A]
+  int* s_rp = s_cj + kFusedWarps * A;                            // [A + 1] local rowptr
+  int* s_cs = s_rp + A + 1;                                      // [A + 1] local csc start
+  int* s_cur = s_cs + A + 1;                                     // [A]
+  int* s_base = s_cur + A;                                       // [1] graph edge base
+  int* s_nb = s_base + 8;                                        // [n][stride] sources
+  const int g = blockIdx.x;
+  const int lo = node_off[g], hi = node_off[g + 1], n = hi - lo;
+  const double* cell = cells ? cells + 3 * g : nullptr;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) s_pos[t] = pos[3LL * lo + t];
+  for (int t = threadIdx.x; t <= n; t += blockDim.x) s_cs[t] = 0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) gnode[lo + t] = g;
+  __syncthreads();
+
+  // A. per destination (warp-strided): neighbours in src order into s_nb
+  for (int i = wib; i < n; i += kFusedWarps) {
+    double* cd = s_cd + wib * A;
+    int* cj = s_cj + wib * A;
+    int c = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      bool hit = false;
+      double d = 0.0;
+      if (j < n && j != i) {
+        d = pair_geom_s(s_pos, j, i, cell).d;
+        hit = d <= rc;
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        const int k = c + __popc(b & lt);
+        cd[k] = d;
+        cj[k] = j;
+      }
+      c += __popc(b);
+    }
+    __syncwarp();
+    int deg = c;
+    if (max_nbr > 0 && c > max_nbr) {
+      // rank by (d, j); keep rank < max_nbr, in j order (same rule as k_radius)
+      int k = 0;
+      for (int a0 = 0; a0 < c; a0 += 32) {
+        const int a = a0 + lane;
+        bool keep = false;
+        int ja = 0;
+        if (a < c) {
+          const double da = cd[a];
+          ja = cj[a];
+          int rank = 0;
+          for (int q = 0; q < c; ++q) rank += key_less(cd[q], cj[q], da, ja);
+          keep = rank < max_nbr;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) s_nb[i * stride + k + __popc(b & lt)] = ja;
+        k += __popc(b);
+      }
+      deg = max_nbr;
+    } else {
+      for (int a = lane; a < c; a += 32) s_nb[i * stride + a] = cj[a];
+    }
+    if (lane == 0) s_rp[i] = deg;
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // B. local scans: rowptr over dst degrees; csc starts over src counts
+  if (wib == 0) {
+    int carry = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      int v = i < n ? s_rp[i] : 0, x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < n) s_rp[i] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) s_rp[n] = carry;
+  }
+  __syncthreads();
+  for (int i = wib; i < n; i += kFusedWarps)
+    for (int k = lane; k < s_rp[i + 1] - s_rp[i]; k += 32) atomicAdd(&s_cs[s_nb[i * stride + k]], 1);
+  __syncthreads();
+  if (wib == 0) {
+    int carry = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      int v = j < n ? s_cs[j] : 0, x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (j < n) {
+        s_cs[j] = carry + x - v;
+        s_cur[j] = carry + x - v;
+      }
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+
+  // C. graph edge base: decoupled look-back (flag 1 = aggregate, 2 = prefix)
+  if (threadIdx.x == 0) {
+    const unsigned long long E_g = (unsigned long long)s_rp[n];
+    const unsigned long long AGG = 1ull << 62, INC = 2ull << 62, VAL = (1ull << 62) - 1;
+    unsigned long long base = 0;
+    if (g == 0) {
+      atomicExch(status, INC | E_g);
+    } else {
+      atomicExch(status + g, AGG | E_g);
+      for (int k = g - 1; k >= 0;) {
+        const unsigned long long v = atomicAdd(status + k, 0ull);
+        if (v == 0) continue;  // predecessor not published yet
+        base += v & VAL;
+        if (v & INC) break;
+        --k;
+      }
+      atomicExch(status + g, INC | (base + E_g));
+    }
+    *s_base = (int)base;
+  }
+  __syncthreads();
+  const int base = *s_base;
+
+  // D. outputs
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    rowptr[lo + t] = base + s_rp[t];
+    csc_ptr[lo + t] = base + s_cs[t];
+  }
+  if (g == n_graphs - 1 && threadIdx.x == 0) {
+    rowptr[n_nodes] = base + s_rp[n];
+    csc_ptr[n_nodes] = base + s_rp[n];
+  }
+  for (int i = wib; i < n; i += kFusedWarps) {
+    const int r0 = s_rp[i], deg = s_rp[i + 1] - r0;
+    for (int k = lane; k < deg; k += 32) {
+      const int j = s_nb[i * stride + k];
+      const PairGeom pg = pair_geom_s(s_pos, j, i, cell);
+      const long long p = (long long)base + r0 + k;
+      col_src[p] = lo + j;
+      edge_dst[p] = lo + i;
+      edge_dx[3 * p + 0] = (T)pg.dx;
+      edge_dx[3 * p + 1] = (T)pg.dy;
+      edge_dx[3 * p + 2] = (T)pg.dz;
+      // make_batch (model.py:256-258): w = 1 / (1 + |pos[src] - pos[dst]|)
+      edge_w[p] = (T)__ddiv_rn(1.0, __dadd_rn(1.0, pg.d));
+    }
+  }
+  // CSC slots: walk dst rows in order (sources within a row are distinct)
+  if (wib == 0) {
+    for (int i = 0; i < n; ++i) {
+      const int r0 = s_rp[i], deg = s_rp[i + 1] - r0;
+      for (int k = lane; k < deg; k += 32) {
+        const int j = s_nb[i * stride + k];
+        const int slot = s_cur[j]++;
+        csc_eid[base + slot] = base + r0 + k;
+        csc_dst[base + slot] = lo + i;
+      }
+      __syncwarp();
+    }
+  }
+
+  // E. the last CTA resets the status words for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == (unsigned)n_graphs - 1) {
+      for (int k = 0; k < n_graphs; ++k) status[k] = 0ull;
+      __threadfence();
+      *done = 0u;
+    }
+  }
+}
+
 // ------------------------------------------------------------ entry points
 template <typename T>
 cudaError_t radius_fill_t(const double* pos, const int* node_off, const int* gnode, int n_nodes,
@@ -525,6 +757,49 @@ int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* edge_dst,
   }
   if (e_cap > 0)
     launch_k(k_csc_finish, grid_for(e_cap), nt, 0, s, perm_csc, e_cap, n_dev, nullptr, edge_dst, csc_eid, csc_dst);
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+size_t gfm_radius_batch_workspace_bytes(int n_graphs) {
+  return sizeof(unsigned long long) * (size_t)(n_graphs > 0 ? n_graphs : 1) + 256;
+}
+
+int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, int n_nodes,
+                     int max_atoms, const double* cells, double rc, int max_nbr, int* gnode,
+                     int* rowptr, int* col_src, int* edge_dst, void* edge_w, void* edge_dx,
+                     int* csc_ptr, int* csc_eid, int* csc_dst, void* workspace, int dtype,
+                     void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (max_atoms > kFusedMaxAtoms || max_atoms < 0 || n_graphs <= 0) {
+    set_error("gfm_radius_batch: graphs of up to %d atoms (got %d), n_graphs >= 1",
+              kFusedMaxAtoms, max_atoms);
+    return GFM_EINVAL;
+  }
+  const int stride = fused_stride(max_atoms, max_nbr);
+  const size_t smem = fused_smem_bytes(max_atoms, max_nbr);
+  if (smem > 227 * 1024) {
+    set_error("gfm_radius_batch: %d atoms x %d neighbours exceed shared memory", max_atoms, stride);
+    return GFM_EINVAL;
+  }
+  unsigned long long* status = (unsigned long long*)workspace;
+  unsigned* done = (unsigned*)((char*)workspace + sizeof(unsigned long long) * n_graphs);
+  if (dtype == GFM_F32) {
+    GFM_TRY(cudaFuncSetAttribute(k_radius_batch<float>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch_k(k_radius_batch<float>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
+             n_graphs, n_nodes, cells, rc, max_nbr, stride, gnode, rowptr, col_src, edge_dst,
+             (float*)edge_w, (float*)edge_dx, csc_ptr, csc_eid, csc_dst, status, done);
+  } else if (dtype == GFM_F64) {
+    GFM_TRY(cudaFuncSetAttribute(k_radius_batch<double>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch_k(k_radius_batch<double>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
+             n_graphs, n_nodes, cells, rc, max_nbr, stride, gnode, rowptr, col_src, edge_dst,
+             (double*)edge_w, (double*)edge_dx, csc_ptr, csc_eid, csc_dst, status, done);
+  } else {
+    set_error("gfm_radius_batch: bad dtype %d", dtype);
+    return GFM_EINVAL;
+  }
   GFM_TRY(cudaGetLastError());
   return 0;
 }

@@ -406,13 +406,15 @@ def make_batch(records, device=None, dtype=torch.float32) -> Batch:
 def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
                  host_offsets: np.ndarray, rc: float, max_nbr: int = 0, cells=None,
                  energy_true=None, forces_true=None, dtype=torch.float32, e_cap=None,
-                 out: dict | None = None) -> Batch:
+                 out: dict | None = None, fused: bool | None = None) -> Batch:
     """Batch assembly from device-resident raw structures: the radius graph
     (build_cutoff_edges, preprocess.py:90-104, plus cap / minimum-image
     extensions) is built on the GPU directly as the dst-sorted CSR.
 
     ``e_cap`` bounds the edge buffers (default: exact count, one host sync);
-    pass ``n_nodes * max_nbr`` to stay sync-free (CUDA-graph capture)."""
+    pass ``n_nodes * max_nbr`` to stay sync-free (CUDA-graph capture).
+    ``fused`` (default: when ``e_cap`` is given and the graphs are small
+    enough) builds everything in one per-graph kernel (gfm_radius_batch)."""
     dev = pos.device
     code = _lib.dtype_code(dtype)
     N = int(pos.shape[0])
@@ -428,6 +430,34 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
         return t
 
     gnode = buf("gnode", (max(N, 1),), torch.int32)
+    n_per = np.diff(host_offsets)
+    max_atoms = int(n_per.max()) if n_per.size else 0
+    can_fuse = e_cap is not None and B > 0 and max_atoms <= _FUSED_MAX_ATOMS and (
+        bool(max_nbr) or max_atoms <= _FUSED_UNCAPPED_ATOMS)
+    if fused and not can_fuse:
+        raise ValidationError("fused batch assembly needs e_cap and graphs of <= 256 atoms")
+    if can_fuse and fused is not False:
+        # one fused kernel: neighbour search + CSR + CSC + graph_of_node
+        Ec = max(int(e_cap), 1)
+        rowptr = buf("rowptr", (N + 1,), torch.int32)
+        col_src = buf("col_src", (Ec,), torch.int32)
+        edge_dst = buf("edge_dst", (Ec,), torch.int32)
+        edge_w = buf("edge_w", (Ec,), dtype)
+        edge_dx = buf("edge_dx", (Ec, 3), dtype)
+        csc_ptr = buf("csc_ptr", (N + 1,), torch.int32)
+        csc_eid = buf("csc_eid", (Ec,), torch.int32)
+        csc_dst = buf("csc_dst", (Ec,), torch.int32)
+        nws = query("gfm_radius_batch_workspace_bytes", B)
+        ws = o.get("rb_ws")
+        if ws is None or ws.numel() < nws:
+            ws = torch.zeros(nws, dtype=torch.uint8, device=dev)  # zeroed once (status words)
+            o["rb_ws"] = ws
+        call("gfm_radius_batch", ptr(pos), ptr(node_offsets), B, N, max_atoms, ptr(cells),
+             float(rc), int(max_nbr or 0), ptr(gnode), ptr(rowptr), ptr(col_src), ptr(edge_dst),
+             ptr(edge_w), ptr(edge_dx), ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), ptr(ws), code, s)
+        return _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets,
+                                    energy_true, forces_true, rowptr, col_src, edge_dst, edge_w,
+                                    edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, None)
     call("gfm_graph_of_node", ptr(node_offsets), B, ptr(gnode), s)
     deg = buf("deg", (max(N, 1),), torch.int32)
     cells_t = None if cells is None else cells
@@ -455,6 +485,22 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
     ws = buf("csr_ws", (query("gfm_csr_workspace_bytes", N, Ec, B),), torch.uint8)
     call("gfm_csc_from_csr", ptr(rowptr), ptr(col_src), ptr(edge_dst), ptr(node_offsets), B, N,
          int(e_cap), ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), ptr(ws), s)
+    return _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets,
+                                energy_true, forces_true, rowptr, col_src, edge_dst, edge_w,
+                                edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, n_edges)
+
+
+# fused batch assembly limits (gfm_radius_batch: <= 256 atoms per graph; the
+# uncapped neighbour lists must fit in shared memory)
+_FUSED_MAX_ATOMS = 256
+_FUSED_UNCAPPED_ATOMS = 96
+
+
+def _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets, energy_true,
+                         forces_true, rowptr, col_src, edge_dst, edge_w, edge_dx, csc_ptr,
+                         csc_eid, csc_dst, e_cap, n_edges):
+    B = int(host_offsets.shape[0] - 1)
+    N = int(pos.shape[0])
     n_per = np.diff(host_offsets)
     npg = o.get("n_per_graph")
     if npg is None:

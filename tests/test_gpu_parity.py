@@ -295,6 +295,37 @@ def test_radius_batch_matches_record_batch():
     np.testing.assert_array_equal(b.edge_w.cpu().numpy(), rb.edge_w.cpu().numpy())
 
 
+@pytest.mark.parametrize("dtype", [F32, F64])
+@pytest.mark.parametrize("max_nbr,periodic", [(0, False), (12, False), (20, True), (3, True)])
+def test_fused_radius_batch_matches_multi_kernel_path(max_nbr, periodic, dtype):
+    """gfm_radius_batch (one CTA per graph, look-back edge offsets) against the
+    count / scan / fill / CSC-build path: every output bitwise equal, ragged
+    graph sizes incl. 0- and 1-atom graphs, and a second call (status words
+    reset) reproduces the first."""
+    rng = np.random.default_rng(max_nbr + 7)
+    sizes = np.array([32, 0, 1, 17, 90, 5, 64, 32, 2, 77])
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    N, B = int(off[-1]), sizes.shape[0]
+    box = 9.0
+    pos = torch.as_tensor(rng.uniform(0, box, size=(N, 3)), device="cuda")
+    z = torch.ones(N, dtype=torch.int32, device="cuda")
+    cells = torch.full((B, 3), box, dtype=torch.float64, device="cuda") if periodic else None
+    offd = torch.as_tensor(off, device="cuda")
+    e_cap = N * max_nbr if max_nbr else int((sizes * np.maximum(sizes - 1, 0)).sum())
+    kw = dict(dtype=dtype, e_cap=e_cap, cells=cells)
+    ref = M.radius_batch(pos, z, offd, off, 4.0, max_nbr, fused=False, **kw)
+    for _ in range(2):
+        got = M.radius_batch(pos, z, offd, off, 4.0, max_nbr, fused=True, out={}, **kw)
+        E = int(ref.rowptr[N].item())
+        assert int(got.rowptr[N].item()) == E
+        for k in ("rowptr", "csc_ptr", "graph_of_node"):
+            np.testing.assert_array_equal(getattr(got, k).cpu().numpy(),
+                                          getattr(ref, k).cpu().numpy(), err_msg=k)
+        for k in ("col_src", "edge_dst", "csc_eid", "csc_dst", "edge_w", "edge_dx"):
+            np.testing.assert_array_equal(getattr(got, k).cpu().numpy()[:E],
+                                          getattr(ref, k).cpu().numpy()[:E], err_msg=k)
+
+
 # ----------------------------------------------------------------- whole model
 # engine -> relative bar for float32 runs.  simt: IEEE fp32 FFMA GEMMs (the
 # north star's 1e-4).  tc3: tcgen05 3xTF32 GEMMs (~3x the fp32 GEMM error,
