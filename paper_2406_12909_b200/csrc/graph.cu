@@ -383,8 +383,11 @@ __host__ __device__ inline int fused_stride(int n_max, int max_nbr) {
   return max_nbr > 0 && max_nbr < full ? max_nbr : full;
 }
 
+// per-CTA buffers are sized by the batch's largest graph (rounded up to 32)
+__host__ __device__ inline int fused_rows(int n_max) { return ((n_max > 1 ? n_max : 1) + 31) / 32 * 32; }
+
 __host__ __device__ inline size_t fused_smem_bytes(int n_max, int max_nbr) {
-  const size_t a = kFusedMaxAtoms;
+  const size_t a = fused_rows(n_max);
   return a * 3 * sizeof(double)                                  // positions
          + (size_t)kFusedWarps * a * (sizeof(double) + sizeof(int))  // cap candidates
          + (3 * a + 16) * sizeof(int)                             // rowptr, csc start, cursor, base
@@ -415,10 +418,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
                    int* __restrict__ col_src, int* __restrict__ edge_dst, T* __restrict__ edge_w,
                    T* __restrict__ edge_dx, int* __restrict__ csc_ptr, int* __restrict__ csc_eid,
                    int* __restrict__ csc_dst, unsigned long long* __restrict__ status,
-                   unsigned* __restrict__ done) {
+                   unsigned* __restrict__ done, int A) {
   pdl_entry();
   extern __shared__ __align__(16) unsigned char fsm[];
-  const int A = kFusedMaxAtoms;
   double* s_pos = reinterpret_cast<double*>(fsm);
   double* s_cd = s_pos + 3 * A;                                  // [warps][A]
   int* s_cj = reinterpret_cast<int*>(s_cd + kFusedWarps * A);    // [warps][A]
@@ -525,25 +527,36 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
     }
   }
 
-  // C. graph edge base: decoupled look-back (flag 1 = aggregate, 2 = prefix)
-  if (threadIdx.x == 0) {
+  // C. graph edge base: decoupled look-back (flag 1 = aggregate, 2 = prefix),
+  // warp-parallel: 32 predecessors per probe, stop at the nearest prefix
+  if (wib == 0) {
     const unsigned long long E_g = (unsigned long long)s_rp[n];
     const unsigned long long AGG = 1ull << 62, INC = 2ull << 62, VAL = (1ull << 62) - 1;
+    if (lane == 0)
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(status + g),
+                   "l"((g == 0 ? INC : AGG) | E_g) : "memory");
     unsigned long long base = 0;
-    if (g == 0) {
-      atomicExch(status, INC | E_g);
-    } else {
-      atomicExch(status + g, AGG | E_g);
-      for (int k = g - 1; k >= 0;) {
-        const unsigned long long v = atomicAdd(status + k, 0ull);
-        if (v == 0) continue;  // predecessor not published yet
-        base += v & VAL;
-        if (v & INC) break;
-        --k;
-      }
-      atomicExch(status + g, INC | (base + E_g));
+    for (int hi_k = g - 1; hi_k >= 0;) {
+      const int k = hi_k - lane;
+      unsigned long long v = INC;  // below graph 0: a zero prefix
+      if (k >= 0)
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(status + k) : "memory");
+      if (__any_sync(0xffffffffu, v == 0ull)) continue;  // a predecessor still computing
+      const unsigned inc = __ballot_sync(0xffffffffu, (v & INC) != 0ull);
+      const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest lane holding a prefix
+      unsigned long long x = lane <= stop ? (v & VAL) : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      base += x;
+      if (inc) break;
+      hi_k -= 32;
     }
-    *s_base = (int)base;
+    if (lane == 0) {
+      if (g > 0)
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(status + g),
+                     "l"(INC | (base + E_g)) : "memory");
+      *s_base = (int)base;
+    }
   }
   __syncthreads();
   const int base = *s_base;
@@ -789,13 +802,15 @@ int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, i
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_k(k_radius_batch<float>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
              n_graphs, n_nodes, cells, rc, max_nbr, stride, gnode, rowptr, col_src, edge_dst,
-             (float*)edge_w, (float*)edge_dx, csc_ptr, csc_eid, csc_dst, status, done);
+             (float*)edge_w, (float*)edge_dx, csc_ptr, csc_eid, csc_dst, status, done,
+             fused_rows(max_atoms));
   } else if (dtype == GFM_F64) {
     GFM_TRY(cudaFuncSetAttribute(k_radius_batch<double>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_k(k_radius_batch<double>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
              n_graphs, n_nodes, cells, rc, max_nbr, stride, gnode, rowptr, col_src, edge_dst,
-             (double*)edge_w, (double*)edge_dx, csc_ptr, csc_eid, csc_dst, status, done);
+             (double*)edge_w, (double*)edge_dx, csc_ptr, csc_eid, csc_dst, status, done,
+             fused_rows(max_atoms));
   } else {
     set_error("gfm_radius_batch: bad dtype %d", dtype);
     return GFM_EINVAL;
