@@ -95,8 +95,7 @@ GFM_API int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* e
 /* Fused batch assembly (replaces graph_of_node + radius_count + scan +
  * radius_fill + csc_from_csr): one CTA per graph (graphs of up to 256 atoms;
  * GFM_EINVAL otherwise -- use the separate calls), same predicate, cap, order
- * and outputs.  `workspace` (gfm_radius_batch_workspace_bytes) must be
- * ZERO-initialised once; each call leaves it ready for the next. */
+ * and outputs.  `workspace`: gfm_radius_batch_workspace_bytes (scratch). */
 GFM_API size_t gfm_radius_batch_workspace_bytes(int n_graphs);
 GFM_API int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, int n_nodes,
                              int max_atoms, const double* cells, double rc, int max_nbr,

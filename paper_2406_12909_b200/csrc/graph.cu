@@ -373,9 +373,11 @@ __global__ void k_csc_finish(const int* __restrict__ perm_csc, int n_cap, const 
 // fp64 predicate / cap / minimum image as k_radius), the dst-sorted CSR rows,
 // the src-sorted CSC (within a graph, CSC order of src j = ascending dst, so a
 // walk over dst rows with per-src cursors is already stable), graph_of_node,
-// and the graph's global edge offset by a decoupled look-back over the
-// graph CTAs (status words reset by the last CTA, so the kernel is CUDA-graph
-// replayable).  Replaces the 15 launches of count / scan / fill / CSC build.
+// and graph_of_node.  Three launches replace the 15 of count / scan / fill /
+// CSC build: a count pass (per-graph edge totals), one single-block scan of
+// those totals, and the fill pass (the neighbour search is cheap enough to
+// run twice; a one-pass decoupled look-back measured slower -- with every
+// graph CTA resident at once its prefix chain is the critical path).
 constexpr int kFusedMaxAtoms = 256, kFusedWarps = 8;
 
 __host__ __device__ inline int fused_stride(int n_max, int max_nbr) {
@@ -410,15 +412,14 @@ __device__ __forceinline__ PairGeom pair_geom_s(const double* __restrict__ sp, i
   return g;
 }
 
-template <typename T>
+template <typename T, bool kFill>
 __global__ void __launch_bounds__(kFusedWarps * 32)
     k_radius_batch(const double* __restrict__ pos, const int* __restrict__ node_off, int n_graphs,
                    int n_nodes, const double* __restrict__ cells, double rc, int max_nbr,
                    int stride, int* __restrict__ gnode, int* __restrict__ rowptr,
                    int* __restrict__ col_src, int* __restrict__ edge_dst, T* __restrict__ edge_w,
                    T* __restrict__ edge_dx, int* __restrict__ csc_ptr, int* __restrict__ csc_eid,
-                   int* __restrict__ csc_dst, unsigned long long* __restrict__ status,
-                   unsigned* __restrict__ done, int A) {
+                   int* __restrict__ csc_dst, int* __restrict__ gcount, int A) {
   pdl_entry();
   extern __shared__ __align__(16) unsigned char fsm[];
   double* s_pos = reinterpret_cast<double*>(fsm);
@@ -436,7 +437,8 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
   const unsigned lt = (1u << lane) - 1u;
   for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) s_pos[t] = pos[3LL * lo + t];
   for (int t = threadIdx.x; t <= n; t += blockDim.x) s_cs[t] = 0;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) gnode[lo + t] = g;
+  if (kFill)
+    for (int t = threadIdx.x; t < n; t += blockDim.x) gnode[lo + t] = g;
   __syncthreads();
 
   // A. per destination (warp-strided): neighbours in src order into s_nb
@@ -506,6 +508,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
     if (lane == 0) s_rp[n] = carry;
   }
   __syncthreads();
+  if (!kFill) {  // count pass: the graph's edge total (scanned between the passes)
+    if (threadIdx.x == 0) gcount[g] = s_rp[n];
+    return;
+  }
   for (int i = wib; i < n; i += kFusedWarps)
     for (int k = lane; k < s_rp[i + 1] - s_rp[i]; k += 32) atomicAdd(&s_cs[s_nb[i * stride + k]], 1);
   __syncthreads();
@@ -527,39 +533,8 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
     }
   }
 
-  // C. graph edge base: decoupled look-back (flag 1 = aggregate, 2 = prefix),
-  // warp-parallel: 32 predecessors per probe, stop at the nearest prefix
-  if (wib == 0) {
-    const unsigned long long E_g = (unsigned long long)s_rp[n];
-    const unsigned long long AGG = 1ull << 62, INC = 2ull << 62, VAL = (1ull << 62) - 1;
-    if (lane == 0)
-      asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(status + g),
-                   "l"((g == 0 ? INC : AGG) | E_g) : "memory");
-    unsigned long long base = 0;
-    for (int hi_k = g - 1; hi_k >= 0;) {
-      const int k = hi_k - lane;
-      unsigned long long v = INC;  // below graph 0: a zero prefix
-      if (k >= 0)
-        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(status + k) : "memory");
-      if (__any_sync(0xffffffffu, v == 0ull)) continue;  // a predecessor still computing
-      const unsigned inc = __ballot_sync(0xffffffffu, (v & INC) != 0ull);
-      const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest lane holding a prefix
-      unsigned long long x = lane <= stop ? (v & VAL) : 0ull;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      base += x;
-      if (inc) break;
-      hi_k -= 32;
-    }
-    if (lane == 0) {
-      if (g > 0)
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(status + g),
-                     "l"(INC | (base + E_g)) : "memory");
-      *s_base = (int)base;
-    }
-  }
   __syncthreads();
-  const int base = *s_base;
+  const int base = gcount[g];  // exclusive prefix of the graph edge counts
 
   // D. outputs
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
@@ -596,17 +571,6 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
         csc_dst[base + slot] = lo + i;
       }
       __syncwarp();
-    }
-  }
-
-  // E. the last CTA resets the status words for the next launch
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(done, 1u) == (unsigned)n_graphs - 1) {
-      for (int k = 0; k < n_graphs; ++k) status[k] = 0ull;
-      __threadfence();
-      *done = 0u;
     }
   }
 }
@@ -775,7 +739,7 @@ int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* edge_dst,
 }
 
 size_t gfm_radius_batch_workspace_bytes(int n_graphs) {
-  return sizeof(unsigned long long) * (size_t)(n_graphs > 0 ? n_graphs : 1) + 256;
+  return sizeof(int) * (size_t)((n_graphs > 0 ? n_graphs : 1) + 1) + 256;
 }
 
 int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, int n_nodes,
@@ -795,27 +759,33 @@ int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, i
     set_error("gfm_radius_batch: %d atoms x %d neighbours exceed shared memory", max_atoms, stride);
     return GFM_EINVAL;
   }
-  unsigned long long* status = (unsigned long long*)workspace;
-  unsigned* done = (unsigned*)((char*)workspace + sizeof(unsigned long long) * n_graphs);
-  if (dtype == GFM_F32) {
-    GFM_TRY(cudaFuncSetAttribute(k_radius_batch<float>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_k(k_radius_batch<float>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
+  int* gcount = (int*)workspace;  // [n_graphs + 1] counts -> exclusive prefix
+  const int A = fused_rows(max_atoms);
+  auto run = [&](auto t) -> cudaError_t {
+    using T = decltype(t);
+    cudaError_t e = cudaFuncSetAttribute(k_radius_batch<T, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_radius_batch<T, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    launch_k(k_radius_batch<T, false>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
              n_graphs, n_nodes, cells, rc, max_nbr, stride, gnode, rowptr, col_src, edge_dst,
-             (float*)edge_w, (float*)edge_dx, csc_ptr, csc_eid, csc_dst, status, done,
-             fused_rows(max_atoms));
-  } else if (dtype == GFM_F64) {
-    GFM_TRY(cudaFuncSetAttribute(k_radius_batch<double>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_k(k_radius_batch<double>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
+             (T*)edge_w, (T*)edge_dx, csc_ptr, csc_eid, csc_dst, gcount, A);
+    launch_k(k_scan_totals, 1, kScanThreads, 0, s, gcount, n_graphs);
+    launch_k(k_radius_batch<T, true>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
              n_graphs, n_nodes, cells, rc, max_nbr, stride, gnode, rowptr, col_src, edge_dst,
-             (double*)edge_w, (double*)edge_dx, csc_ptr, csc_eid, csc_dst, status, done,
-             fused_rows(max_atoms));
-  } else {
+             (T*)edge_w, (T*)edge_dx, csc_ptr, csc_eid, csc_dst, gcount, A);
+    return cudaGetLastError();
+  };
+  if (dtype == GFM_F32)
+    GFM_TRY(run(float{}));
+  else if (dtype == GFM_F64)
+    GFM_TRY(run(double{}));
+  else {
     set_error("gfm_radius_batch: bad dtype %d", dtype);
     return GFM_EINVAL;
   }
-  GFM_TRY(cudaGetLastError());
   return 0;
 }
 

@@ -447,11 +447,7 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
         csc_ptr = buf("csc_ptr", (N + 1,), torch.int32)
         csc_eid = buf("csc_eid", (Ec,), torch.int32)
         csc_dst = buf("csc_dst", (Ec,), torch.int32)
-        nws = query("gfm_radius_batch_workspace_bytes", B)
-        ws = o.get("rb_ws")
-        if ws is None or ws.numel() < nws:
-            ws = torch.zeros(nws, dtype=torch.uint8, device=dev)  # zeroed once (status words)
-            o["rb_ws"] = ws
+        ws = buf("rb_ws", (query("gfm_radius_batch_workspace_bytes", B),), torch.uint8)
         call("gfm_radius_batch", ptr(pos), ptr(node_offsets), B, N, max_atoms, ptr(cells),
              float(rc), int(max_nbr or 0), ptr(gnode), ptr(rowptr), ptr(col_src), ptr(edge_dst),
              ptr(edge_w), ptr(edge_dx), ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), ptr(ws), code, s)
