@@ -45,6 +45,10 @@ enum { GFM_EINVAL = -1 };
 /* aggregation parts (bit order = column-block order of the output) */
 enum { GFM_PART_SUM = 1, GFM_PART_MEAN = 2, GFM_PART_MAX = 4, GFM_PART_STD = 8 };
 enum { GFM_FLAG_SCALAR = 1 }; /* force the scalar (numpy-order) kernels */
+/* aggregation: argmax is a uint8 [N][H] buffer holding the LOW BYTE of the CSR
+ * position (unique within a row; valid when every CSR row has <= 256 edges,
+ * e.g. a neighbour cap <= 256) -- 4x fewer bytes gathered by the backward */
+enum { GFM_FLAG_ARGMAX_U8 = 2 };
 /* float32 GEMM engine: tcgen05 3xTF32 (default, fp32-level accuracy),
  * tcgen05 1xTF32 (faster, ~1e-3 relative), or the SIMT fp32 engine */
 enum { GFM_GEMM_SIMT = 0, GFM_GEMM_TC3 = 1, GFM_GEMM_TC1 = 2 };

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libgfm_b200.so")
 F32, F64 = 0, 1
 PART_SUM, PART_MEAN, PART_MAX, PART_STD = 1, 2, 4, 8
 FLAG_SCALAR = 1
+FLAG_ARGMAX_U8 = 2
 ABI_VERSION = 1
 
 _P = ctypes.c_void_p

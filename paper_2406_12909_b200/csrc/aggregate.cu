@@ -48,6 +48,19 @@ __host__ __device__ inline AggLayout agg_layout(int parts, int H) {
   return L;
 }
 
+// argmax storage: int32 CSR positions, or (GFM_FLAG_ARGMAX_U8) their low
+// byte -- unique within a row of <= 256 edges, which is all the backward's
+// "is this edge the row's argmax" test needs (4x fewer gathered bytes)
+__device__ __forceinline__ void am_store(int* am, long long idx, int p, bool u8) {
+  if (u8)
+    reinterpret_cast<unsigned char*>(am)[idx] = (unsigned char)(p & 0xFF);
+  else
+    am[idx] = p;
+}
+__device__ __forceinline__ int am_load(const int* am, long long idx, bool u8) {
+  return u8 ? (int)reinterpret_cast<const unsigned char*>(am)[idx] : am[idx];
+}
+
 // ------------------------------------------------------------ embedding
 template <typename T>
 __global__ void k_embed(const int* __restrict__ z, int n, const T* __restrict__ emb, int H,
@@ -78,7 +91,7 @@ template <typename T>
 __global__ void k_agg_fwd_scalar(const T* __restrict__ h, int n_nodes, int H,
                                  const int* __restrict__ rowptr, const int* __restrict__ col_src,
                                  const T* __restrict__ w, int parts, T* __restrict__ agg,
-                                 int* __restrict__ argmax, T* __restrict__ stat_mean) {
+                                 int* __restrict__ argmax, T* __restrict__ stat_mean, int am_u8) {
   pdl_entry();
   const AggLayout L = agg_layout(parts, H);
   const int ld = L.K * H;
@@ -94,7 +107,7 @@ __global__ void k_agg_fwd_scalar(const T* __restrict__ h, int n_nodes, int H,
       if (L.o_mean >= 0) out[L.o_mean + c] = T(0);
       if (L.o_max >= 0) out[L.o_max + c] = T(0);
       if (L.o_std >= 0) out[L.o_std + c] = T(0);
-      if (argmax && L.o_max >= 0) argmax[idx] = -1;
+      if (argmax && L.o_max >= 0) am_store(argmax, idx, -1, am_u8);
       if (stat_mean) stat_mean[idx] = T(0);
       continue;
     }
@@ -132,7 +145,7 @@ __global__ void k_agg_fwd_scalar(const T* __restrict__ h, int n_nodes, int H,
         }
       }
       out[L.o_max + c] = best;
-      if (argmax) argmax[idx] = arg;
+      if (argmax) am_store(argmax, idx, arg, am_u8);
     }
   }
 }
@@ -146,7 +159,7 @@ __device__ __forceinline__ void agg_fwd_node(Ld ld, int node, int cb, int H,
                                              const int* __restrict__ col_src,
                                              const float* __restrict__ w, const AggLayout& L,
                                              float* __restrict__ agg, int* __restrict__ argmax,
-                                             float* __restrict__ stat_mean) {
+                                             float* __restrict__ stat_mean, bool am_u8) {
   const bool need_s = L.o_sum >= 0 || L.o_mean >= 0 || L.o_std >= 0;
   const bool need_q = L.o_std >= 0;
   const bool need_m = L.o_max >= 0;
@@ -275,7 +288,14 @@ __device__ __forceinline__ void agg_fwd_node(Ld ld, int node, int cb, int H,
     if (need_m) {
       float4 o = deg > 0 ? mx[v] : make_float4(0.f, 0.f, 0.f, 0.f);
       out4[(L.o_max >> 2) + c4] = o;
-      if (argmax) reinterpret_cast<int4*>(argmax + (long long)node * H)[c4] = am[v];
+      if (argmax) {
+        if (am_u8)  // 4 low bytes -> one 32-bit store
+          reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(argmax) + (long long)node * H)[c4] =
+              (unsigned)(am[v].x & 0xFF) | (unsigned)(am[v].y & 0xFF) << 8 |
+              (unsigned)(am[v].z & 0xFF) << 16 | (unsigned)(am[v].w & 0xFF) << 24;
+        else
+          reinterpret_cast<int4*>(argmax + (long long)node * H)[c4] = am[v];
+      }
     }
     if (need_q) {
       auto sd = [&](float sq, float sd1) {
@@ -291,7 +311,7 @@ __device__ __forceinline__ void agg_fwd_node(Ld ld, int node, int cb, int H,
   }
 }
 
-template <int NV, int LPN>
+template <int NV, int LPN, bool U8>
 __global__ void __launch_bounds__(256)
     k_agg_fwd_vec(const float* __restrict__ h, int n_nodes, int H, const int* __restrict__ rowptr,
                   const int* __restrict__ col_src, const float* __restrict__ w, int parts,
@@ -310,7 +330,7 @@ __global__ void __launch_bounds__(256)
   const int H4 = H >> 2;
   agg_fwd_node<NV, LPN>(
       [&](int sj, int v) { return __ldg(h4 + (long long)sj * H4 + v * LPN + cb); }, node, cb, H,
-      rowptr, col_src, w, L, agg, argmax, stat_mean);
+      rowptr, col_src, w, L, agg, argmax, stat_mean, U8);
 }
 
 // 16-byte global -> shared copy without a register round trip: a block's
@@ -385,10 +405,10 @@ __global__ void __launch_bounds__(256)
   for (int node = a + (int)threadIdx.x / LPN; node < b; node += npp) {
     if (staged)
       agg_fwd_node<1, LPN>([&](int sj, int) { return stage[(sj - lo) * LPN + sub]; }, node, cb,
-                           H, rowptr, col_src, w, L, agg, argmax, stat_mean);
+                           H, rowptr, col_src, w, L, agg, argmax, stat_mean, false);
     else
       agg_fwd_node<1, LPN>([&](int sj, int) { return __ldg(h4 + (long long)sj * H4 + cb); },
-                           node, cb, H, rowptr, col_src, w, L, agg, argmax, stat_mean);
+                           node, cb, H, rowptr, col_src, w, L, agg, argmax, stat_mean, false);
   }
 }
 
@@ -482,7 +502,7 @@ __global__ void k_agg_bwd_scalar(const T* __restrict__ G, int ldg, const T* __re
                                  const T* __restrict__ h_in, const int* __restrict__ csc_ptr,
                                  const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
                                  const T* __restrict__ w, int n_nodes, int H, T* __restrict__ dh,
-                                 const T* __restrict__ gate, T* __restrict__ out) {
+                                 const T* __restrict__ gate, T* __restrict__ out, int am_u8) {
   pdl_entry();
   const long long total = (long long)n_nodes * H;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -496,8 +516,8 @@ __global__ void k_agg_bwd_scalar(const T* __restrict__ G, int ldg, const T* __re
       T dm = G ? G[(long long)i * ldg + c] : T(0);
       if (coef) dm = dm + coef[(long long)i * H + c] * (hj * ww);
       if (argmax) {
-        if (argmax[(long long)i * H + c] == p) dm = G || coef ? dm + dmax[(long long)i * ldm + c]
-                                                              : dmax[(long long)i * ldm + c];
+        if (am_load(argmax, (long long)i * H + c, am_u8) == (am_u8 ? (p & 0xFF) : p))
+          dm = G || coef ? dm + dmax[(long long)i * ldm + c] : dmax[(long long)i * ldm + c];
       }
       acc = add_rn(acc, mul_rn(dm, ww));
     }
@@ -524,7 +544,7 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
                                              const float* __restrict__ w,
                                              const float* __restrict__ dh,
                                              const float* __restrict__ gate,
-                                             float* __restrict__ out) {
+                                             float* __restrict__ out, bool am_u8 = false) {
   const int H4 = H >> 2;
   float4 acc[NV], hj[NV];
 #pragma unroll
@@ -592,7 +612,7 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
             if (hasC) dm = fma4(cf[u][v], mul4(hj[v], bcast4(ww[u])), dm);
             if (hasA) {
               const int4 am = a[u][v];
-              const int pp = p[u];
+              const int pp = am_u8 ? (p[u] & 0xFF) : p[u];
               if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
                 const float4 d =
                     __ldg(reinterpret_cast<const float4*>(dmax + (long long)i[u] * ldm) + c4);
@@ -647,7 +667,7 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
           if (hasC) dm = fma4(cf[u][v], mul4(hj[v], bcast4(ww[u])), dm);
           if (hasA) {
             const int4 am = a[u][v];
-            const int pp = p[u];
+            const int pp = am_u8 ? (p[u] & 0xFF) : p[u];
             if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
               const float4 d =
                   __ldg(reinterpret_cast<const float4*>(dmax + (long long)i[u] * ldm) + c4);
@@ -674,7 +694,7 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
   }
 }
 
-template <int NV, int LPN>
+template <int NV, int LPN, bool U8>
 __global__ void __launch_bounds__(256)
     k_agg_bwd_vec(const float* __restrict__ G, int ldg, const float* __restrict__ coef,
                   const float* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
@@ -697,10 +717,16 @@ __global__ void __launch_bounds__(256)
         return __ldg(reinterpret_cast<const float4*>(coef + (long long)i * H) + v * LPN + cb);
       },
       [&](int i, int v) {
+        if constexpr (U8) {  // 4 low-byte argmaxes in one 32-bit load
+          const unsigned b = __ldg(reinterpret_cast<const unsigned*>(
+                                       reinterpret_cast<const unsigned char*>(argmax) + (long long)i * H) +
+                                   v * LPN + cb);
+          return make_int4(b & 0xFF, (b >> 8) & 0xFF, (b >> 16) & 0xFF, b >> 24);
+        }
         return __ldg(reinterpret_cast<const int4*>(argmax + (long long)i * H) + v * LPN + cb);
       },
       G != nullptr, coef != nullptr, argmax != nullptr, j, cb, H, dmax, ldm, h_in, csc_ptr,
-      csc_eid, csc_dst, w, dh, gate, out);
+      csc_eid, csc_dst, w, dh, gate, out, U8);
 }
 
 // Shared-memory staged backward (see k_agg_fwd_tile): a block owns nb
@@ -811,10 +837,10 @@ static bool no_tile() {
 
 cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, const int* col_src,
                     const void* w, int parts, void* agg, int* argmax, void* stat_mean,
-                    int force_scalar, cudaStream_t s) {
+                    int force_scalar, int am_u8, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   int nv = 0, lpn = 0, slabs = 1;
-  if (dtype == GFM_F32 && !force_scalar && H % 64 == 0 && !no_tile()) {
+  if (dtype == GFM_F32 && !force_scalar && !am_u8 && H % 64 == 0 && !no_tile()) {
     // staged tiles: 16-lane (64-column) slabs, 128 dst nodes, <= 384 rows
     constexpr int kLpn = 16, kNb = 128, kCap = 384;
     const size_t smem = (size_t)kCap * kLpn * sizeof(float4);
@@ -831,9 +857,12 @@ cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, c
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);
 #define GFM_FWD_CASE(NV_, LPN_)                                                                \
   if (nv == NV_ && lpn == LPN_) {                                                              \
-    launch_k(k_agg_fwd_vec<NV_, LPN_>, grid, 256, 0, s, (const float*)h, n, H, rowptr, col_src,      \
-                                                  (const float*)w, parts, (float*)agg, argmax, \
-                                                  (float*)stat_mean);                          \
+    if (am_u8)                                                                                 \
+      launch_k(k_agg_fwd_vec<NV_, LPN_, true>, grid, 256, 0, s, (const float*)h, n, H, rowptr,   \
+               col_src, (const float*)w, parts, (float*)agg, argmax, (float*)stat_mean);      \
+    else                                                                                       \
+      launch_k(k_agg_fwd_vec<NV_, LPN_, false>, grid, 256, 0, s, (const float*)h, n, H, rowptr,  \
+               col_src, (const float*)w, parts, (float*)agg, argmax, (float*)stat_mean);      \
     return cudaGetLastError();                                                                 \
   }
     GFM_VEC_CASES(GFM_FWD_CASE)
@@ -842,18 +871,18 @@ cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, c
   if (dtype == GFM_F32)
     launch_k(k_agg_fwd_scalar<float>, grid_1d((long long)n * H), 256, 0, s,
         (const float*)h, n, H, rowptr, col_src, (const float*)w, parts, (float*)agg, argmax,
-        (float*)stat_mean);
+        (float*)stat_mean, am_u8);
   else
     launch_k(k_agg_fwd_scalar<double>, grid_1d((long long)n * H), 256, 0, s,
         (const double*)h, n, H, rowptr, col_src, (const double*)w, parts, (double*)agg, argmax,
-        (double*)stat_mean);
+        (double*)stat_mean, am_u8);
   return cudaGetLastError();
 }
 
 cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* stat_mean,
                     const int* argmax, const void* h_in, const int* rowptr, const int* csc_ptr,
                     const int* csc_eid, const int* csc_dst, const void* w, int n, int H, int parts,
-                    void* dh, const void* gate, void* out, void* ws, int force_scalar,
+                    void* dh, const void* gate, void* out, void* ws, int force_scalar, int am_u8,
                     cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const AggLayout L = agg_layout(parts, H);
@@ -888,7 +917,8 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
   const int* am = L.o_max >= 0 ? argmax : nullptr;
   int nv = 0, lpn = 0, slabs = 1;
   const bool g_ok = G == nullptr || ldg % 4 == 0;
-  if (dtype == GFM_F32 && !force_scalar && H % 32 == 0 && g_ok && ld % 4 == 0 && !no_tile()) {
+  if (dtype == GFM_F32 && !force_scalar && !am_u8 && H % 32 == 0 && g_ok && ld % 4 == 0 &&
+      !no_tile()) {
     // staged tiles: 8-lane (32-column) slabs, 64 CSC nodes, <= 256 dst rows
     constexpr int kLpn = 8, kNb = 64, kCap = 256;
     const size_t smem = 3 * (size_t)kCap * kLpn * sizeof(float4);
@@ -906,10 +936,16 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);
 #define GFM_BWD_CASE(NV_, LPN_)                                                              \
   if (nv == NV_ && lpn == LPN_) {                                                            \
-    launch_k(k_agg_bwd_vec<NV_, LPN_>, grid, 256, 0, s,                                            \
-        (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am,                \
-        (const float*)h_in, csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh,    \
-        (const float*)gate, (float*)out);                                                    \
+    if (am_u8)                                                                               \
+      launch_k(k_agg_bwd_vec<NV_, LPN_, true>, grid, 256, 0, s, (const float*)G, ldg,          \
+               (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in, csc_ptr,    \
+               csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,        \
+               (float*)out);                                                                  \
+    else                                                                                     \
+      launch_k(k_agg_bwd_vec<NV_, LPN_, false>, grid, 256, 0, s, (const float*)G, ldg,         \
+               (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in, csc_ptr,    \
+               csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,        \
+               (float*)out);                                                                  \
     return cudaGetLastError();                                                               \
   }
     GFM_VEC_CASES(GFM_BWD_CASE)
@@ -919,12 +955,12 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
     launch_k(k_agg_bwd_scalar<float>, grid_1d((long long)n * H), 256, 0, s,
         (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in,
         csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,
-        (float*)out);
+        (float*)out, am_u8);
   else
     launch_k(k_agg_bwd_scalar<double>, grid_1d((long long)n * H), 256, 0, s,
         (const double*)G, ldg, (const double*)coef, (const double*)dmax, ld, am,
         (const double*)h_in, csc_ptr, csc_eid, csc_dst, (const double*)w, n, H, (double*)dh,
-        (const double*)gate, (double*)out);
+        (const double*)gate, (double*)out, am_u8);
   return cudaGetLastError();
 }
 
@@ -975,7 +1011,8 @@ int gfm_agg_fwd(const void* h, int n_nodes, int H, const int* rowptr, const int*
     return GFM_EINVAL;
   }
   cudaError_t e = agg_fwd(dtype, h, n_nodes, H, rowptr, col_src, edge_w, parts, agg, argmax,
-                          stat_mean, flags & GFM_FLAG_SCALAR, (cudaStream_t)stream);
+                          stat_mean, flags & GFM_FLAG_SCALAR,
+                          (flags & GFM_FLAG_ARGMAX_U8) != 0, (cudaStream_t)stream);
   if (e != cudaSuccess) set_error("gfm_agg_fwd: %s", cudaGetErrorString(e));
   return (int)e;
 }
@@ -990,7 +1027,8 @@ int gfm_agg_bwd(const void* dagg, const void* agg, const void* stat_mean, const 
   }
   cudaError_t e = agg_bwd(dtype, dagg, agg, stat_mean, argmax, h_in, rowptr, csc_ptr, csc_eid,
                           csc_dst, edge_w, n_nodes, H, parts, dh, gate, out, workspace,
-                          flags & GFM_FLAG_SCALAR, (cudaStream_t)stream);
+                          flags & GFM_FLAG_SCALAR, (flags & GFM_FLAG_ARGMAX_U8) != 0,
+                          (cudaStream_t)stream);
   if (e != cudaSuccess) set_error("gfm_agg_bwd: %s", cudaGetErrorString(e));
   return (int)e;
 }

@@ -398,7 +398,8 @@ def make_batch(records, device=None, dtype=torch.float32) -> Batch:
               forces_true=forces, rowptr=rowptr, col_src=col_src, edge_dst=edge_dst,
               edge_w=edge_w, edge_dx=edge_dx, csc_ptr=csc_ptr, csc_eid=csc_eid,
               csc_dst=csc_dst, order=order, n_nodes=N, e_cap=E, _n_edges=E,
-              host_offsets=offsets, host_n_per=n_per)
+              host_offsets=offsets, host_n_per=n_per,
+              max_deg=int(np.bincount(dst, minlength=1).max()) if E else 0)
     b._keep = (t_src, t_dst, t_eoff, t_shift, ws)
     return b
 
@@ -453,7 +454,8 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
              ptr(edge_w), ptr(edge_dx), ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), ptr(ws), code, s)
         return _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets,
                                     energy_true, forces_true, rowptr, col_src, edge_dst, edge_w,
-                                    edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, None)
+                                    edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, None,
+                                    _deg_bound(max_atoms, max_nbr))
     call("gfm_graph_of_node", ptr(node_offsets), B, ptr(gnode), s)
     deg = buf("deg", (max(N, 1),), torch.int32)
     cells_t = None if cells is None else cells
@@ -483,7 +485,8 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
          int(e_cap), ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), ptr(ws), s)
     return _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets,
                                 energy_true, forces_true, rowptr, col_src, edge_dst, edge_w,
-                                edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, n_edges)
+                                edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, n_edges,
+                                _deg_bound(max_atoms, max_nbr))
 
 
 # fused batch assembly limits (gfm_radius_batch: <= 256 atoms per graph; the
@@ -492,9 +495,15 @@ _FUSED_MAX_ATOMS = 256
 _FUSED_UNCAPPED_ATOMS = 96
 
 
+def _deg_bound(max_atoms: int, max_nbr: int) -> int:
+    """upper bound of any CSR row length of a radius batch"""
+    full = max(max_atoms - 1, 0)
+    return min(int(max_nbr), full) if max_nbr else full
+
+
 def _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets, energy_true,
                          forces_true, rowptr, col_src, edge_dst, edge_w, edge_dx, csc_ptr,
-                         csc_eid, csc_dst, e_cap, n_edges):
+                         csc_eid, csc_dst, e_cap, n_edges, max_deg):
     B = int(host_offsets.shape[0] - 1)
     N = int(pos.shape[0])
     n_per = np.diff(host_offsets)
@@ -511,7 +520,7 @@ def _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offset
                  forces_true=forces_true, rowptr=rowptr, col_src=col_src, edge_dst=edge_dst,
                  edge_w=edge_w, edge_dx=edge_dx, csc_ptr=csc_ptr, csc_eid=csc_eid,
                  csc_dst=csc_dst, order=None, n_nodes=N, e_cap=int(e_cap), _n_edges=n_edges,
-                 host_offsets=np.asarray(host_offsets), host_n_per=n_per)
+                 host_offsets=np.asarray(host_offsets), host_n_per=n_per, max_deg=max_deg)
 
 
 # --------------------------------------------------------------------------
@@ -544,6 +553,12 @@ def _scratch_for(owner, device):
     return owner if owner is not None else _Scratch(device)
 
 
+def _argmax_flag(batch) -> int:
+    """uint8 argmax storage when every CSR row is known to hold <= 256 edges"""
+    md = getattr(batch, "max_deg", None)
+    return _lib.FLAG_ARGMAX_U8 if md is not None and md <= 256 else 0
+
+
 def forward_batch(params: ModelParams, batch: Batch, cache: dict | None = None,
                   scratch: _Scratch | None = None, flags: int = 0):
     """forward_batch (model.py:344-400): returns (e_pred (B,), f_pred (N, 3))
@@ -561,12 +576,15 @@ def forward_batch(params: ModelParams, batch: Batch, cache: dict | None = None,
     h = sc.get("h0", (N, H), dt)
     call("gfm_embed", ptr(batch.z), N, ptr(params.embedding), H, ptr(h), code, s)
     layers = []
+    am_flag = _argmax_flag(batch)
     for l in range(cfg.mpnn_layers):
         agg = sc.get(f"agg{l}", (N, K * H), dt)
-        argmax = sc.get(f"argmax{l}", (N, H), torch.int32) if parts & _lib.PART_MAX else None
+        argmax = sc.get(f"argmax{l}", (N, H), torch.uint8 if am_flag else torch.int32) \
+            if parts & _lib.PART_MAX else None
         smean = sc.get(f"smean{l}", (N, H), dt) if parts & _lib.PART_STD else None
         call("gfm_agg_fwd", ptr(h), N, H, ptr(batch.rowptr), ptr(batch.col_src),
-             ptr(batch.edge_w), parts, ptr(agg), ptr(argmax), ptr(smean), code, flags, s)
+             ptr(batch.edge_w), parts, ptr(agg), ptr(argmax), ptr(smean), code, flags | am_flag,
+             s)
         h_out = sc.get(f"h{l + 1}", (N, H), dt)
         call("gfm_linear_fwd", ptr(h), H, H, ptr(agg), K * H, K * H,
              ptr(params.view(f"layer_{l}.w")), H, ptr(params.view(f"layer_{l}.u")), K * H,
@@ -796,7 +814,8 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
         call("gfm_agg_bwd", ptr(dagg), ptr(lay["agg"]), ptr(lay["smean"]), ptr(lay["argmax"]),
              ptr(lay["h_in"]), ptr(batch.rowptr), ptr(batch.csc_ptr), ptr(batch.csc_eid),
              ptr(batch.csc_dst), ptr(batch.edge_w), N, H, parts, ptr(dh_in),
-             ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code, flags, s)
+             ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
+             flags | _argmax_flag(batch), s)
         dz = out
     ews = sc.bytes("emb_ws", query("gfm_embedding_grad_workspace_bytes", N, H, code))
     call("gfm_embedding_grad", ptr(batch.z), N, ptr(dz), H, ptr(gp.embedding), ptr(ews), code, s)

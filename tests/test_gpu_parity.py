@@ -166,15 +166,18 @@ def agg_path(request, monkeypatch):
     return request.param
 
 
+@pytest.mark.parametrize("u8", [False, True])
 @pytest.mark.parametrize("scattered", [False, True])
 @pytest.mark.parametrize("kind", ["pna-agg", "max-agg"])
 @pytest.mark.parametrize("H", [64, 256, 512])
-def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H, scattered, agg_path):
+def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H, scattered, agg_path, u8):
     """float4 / column-slab / smem-staged forward + backward (F32) against the
-    scalar F64 kernels."""
+    scalar F64 kernels; u8: both sides store argmax as the CSR position's low
+    byte (GFM_FLAG_ARGMAX_U8)."""
     parts, K = M.KIND_PARTS[kind], M._n_parts(kind)
     outs = {}
-    for dtype, flags in ((F64, _lib.FLAG_SCALAR), (F32, 0)):
+    uf = _lib.FLAG_ARGMAX_U8 if u8 else 0
+    for dtype, flags in ((F64, _lib.FLAG_SCALAR | uf), (F32, uf)):
         recs, b = _wide_batch(H, dtype, 3, scattered)
         N = b.n_nodes
         code = _lib.F64 if dtype == F64 else _lib.F32
@@ -184,7 +187,7 @@ def test_aggregate_bwd_fp32_wide_vs_fp64_scalar(kind, H, scattered, agg_path):
         dh = torch.as_tensor(rg.normal(size=(N, H)), dtype=dtype, device="cuda")
         gate = torch.as_tensor(np.tanh(rg.normal(size=(N, H))), dtype=dtype, device="cuda")
         agg = torch.empty(N, K * H, dtype=dtype, device="cuda")
-        am = torch.empty(N, H, dtype=torch.int32, device="cuda")
+        am = torch.empty(N, H, dtype=torch.uint8 if u8 else torch.int32, device="cuda")
         sm = torch.empty(N, H, dtype=dtype, device="cuda")
         s = _lib.stream_handle()
         # the forward of the SAME precision fixes argmax / std (F64 for both
