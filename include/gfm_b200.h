@@ -189,6 +189,25 @@ GFM_API int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_
 GFM_API int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const void* a,
                     const void* y, void* ds, int ld_ds, void* dz, int dtype, void* stream);
 
+/* Deferred split-K: gfm_linear_bwd_weight without the final reduction; the
+ * partials stay in `workspace` (which must then not be reused until reduced)
+ * and `job` receives their descriptor.  gfm_splitk_reduce_batch reduces any
+ * number of such jobs in one launch (fp64 sums in split order, fixed shape-
+ * only grid: deterministic; float32 results equal the per-call reduction). */
+typedef struct gfm_reduce_job {
+  const void* ws;
+  int splits, N, K1, K2, with_bias, trans;
+  void* g1;
+  void* g2;
+  void* gb;
+} gfm_reduce_job;
+GFM_API int gfm_linear_bwd_weight_partials(const void* dY, int ldd, int M, const int* M_dev, int N,
+                                           const void* X1, int ld1, int K1, const void* X2,
+                                           int ld2, int K2, int with_bias, void* g1, void* g2,
+                                           void* gb, void* workspace, gfm_reduce_job* job,
+                                           int dtype, void* stream);
+GFM_API int gfm_splitk_reduce_batch(const gfm_reduce_job* jobs, int n_jobs, int dtype, void* stream);
+
 /* ---- K12: embedding gradient (model.py:564) --------------------------- */
 /* grad[118][H] = onehot(z - 1)^T dh as a split-K GEMM (one-hot generated on
  * the fly, deterministic; absent elements exactly 0) */

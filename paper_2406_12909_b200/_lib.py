@@ -29,6 +29,16 @@ _D = ctypes.c_double
 _L = ctypes.c_longlong
 _S = ctypes.c_size_t
 
+class ReduceJob(ctypes.Structure):
+    """gfm_reduce_job (include/gfm_b200.h): one deferred split-K reduction"""
+    _fields_ = [("ws", ctypes.c_void_p), ("splits", ctypes.c_int), ("N", ctypes.c_int),
+                ("K1", ctypes.c_int), ("K2", ctypes.c_int), ("with_bias", ctypes.c_int),
+                ("trans", ctypes.c_int), ("g1", ctypes.c_void_p), ("g2", ctypes.c_void_p),
+                ("gb", ctypes.c_void_p)]
+
+
+_JOBP = ctypes.POINTER(ReduceJob)
+
 # name -> (restype, argtypes); the single source of truth for the Python side
 SIGNATURES = {
     "gfm_abi_version": (_I, []),
@@ -62,6 +72,9 @@ SIGNATURES = {
     "gfm_linear_bwd_weight_workspace_bytes": (_S, [_I, _I, _I, _I, _I, _I]),
     "gfm_linear_bwd_weight": (_I, [_P, _I, _I, _P, _I, _P, _I, _I, _P, _I, _I, _I, _P, _P, _P,
                                    _P, _I, _P]),
+    "gfm_linear_bwd_weight_partials": (_I, [_P, _I, _I, _P, _I, _P, _I, _I, _P, _I, _I, _I, _P,
+                                            _P, _P, _P, _JOBP, _I, _P]),
+    "gfm_splitk_reduce_batch": (_I, [_JOBP, _I, _I, _P]),
     "gfm_force_fwd": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "gfm_force_bwd_workspace_bytes": (_S, [_I, _I, _I]),
     "gfm_force_bwd": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,

@@ -339,7 +339,8 @@ inline int real_splits(int K, int splits, int kstep) {
 template <typename T>
 cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, int N, const T* X1,
                                 int ld1, int K1, const T* X2, int ld2, int K2, int with_bias,
-                                T* g1, T* g2, T* gb, T* ws, cudaStream_t s) {
+                                T* g1, T* g2, T* gb, T* ws, cudaStream_t s,
+                                gfm_reduce_job* defer = nullptr) {
   // with_bias == 2: the workspace already holds the ones operand (same M)
   const bool ones_ready = with_bias == 2;
   with_bias = with_bias ? 1 : 0;
@@ -378,7 +379,112 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
   }
 reduce:
   if (e != cudaSuccess) return e;
+  if (defer) {  // the caller reduces later, batched with other weight gradients
+    *defer = gfm_reduce_job{ws, real, N, K1, K2, with_bias, trans, g1, g2, gb};
+    return cudaGetLastError();
+  }
   splitk_reduce<T>(ws, real, N, K1, K2, with_bias, g1, g2, gb, trans, s);
+  return cudaGetLastError();
+}
+
+// All deferred split-K reductions of a backward pass in ONE launch: the 32x32
+// tiles of every job form one flat grid (job found by prefix over the tile
+// counts); each tile is k_splitk_reduce's (fp64 ordered sums, coalesced
+// writes) -- deterministic and identical to the per-call reduce.
+constexpr int kMaxReduceJobs = 24;
+struct ReduceJobs {
+  gfm_reduce_job job[kMaxReduceJobs];
+  int tile0[kMaxReduceJobs + 1];  // first flat tile of each job
+  int ncx[kMaxReduceJobs];        // tiles along C
+  int rows[kMaxReduceJobs];       // tile height: 32 (4 sums / thread) or 8 (many splits)
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_splitk_reduce_batch(const __grid_constant__ ReduceJobs J,
+                                                             int n_jobs) {
+  pdl_entry();
+  __shared__ T tile[32][33];
+  int q = 0;
+  while (q + 1 < n_jobs && (int)blockIdx.x >= J.tile0[q + 1]) ++q;
+  const gfm_reduce_job& jb = J.job[q];
+  const int t = blockIdx.x - J.tile0[q];
+  const T* ws = (const T*)jb.ws;
+  const int N = jb.N, K1 = jb.K1, K2 = jb.K2, trans = jb.trans;
+  const int Kt = K1 + K2 + jb.with_bias;
+  const int R = trans ? Kt : N, C = trans ? N : Kt;
+  const long long total = (long long)R * C;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int th = J.rows[q], nj = th / 8;
+  const int r0 = (t / J.ncx[q]) * th, c0 = (t % J.ncx[q]) * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int c = c0 + tx;
+  if (nj == 1) {  // one sum per thread, splits unrolled 8 deep (many-split jobs)
+    const int r = r0 + ty;
+    if (r < R && c < C) {
+      const T* w = ws + (long long)r * C + c;
+#pragma unroll 8
+      for (int sp = 0; sp < jb.splits; ++sp) acc[0] += (double)w[(long long)sp * total];
+    }
+  } else {
+#pragma unroll 4
+    for (int sp = 0; sp < jb.splits; ++sp) {
+      const T* w = ws + (long long)sp * total;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + ty + 8 * j;
+        if (r < R && c < C) acc[j] += (double)w[(long long)r * C + c];
+      }
+    }
+  }
+  for (int j = 0; j < nj; ++j) tile[ty + 8 * j][tx] = (T)acc[j];
+  __syncthreads();
+  T* g1 = (T*)jb.g1;
+  T* g2 = (T*)jb.g2;
+  T* gb = (T*)jb.gb;
+  // write: element (n, k) of the [N][Kt] gradient; th x 32 tile
+  for (int e = threadIdx.x; e < th * 32; e += blockDim.x) {
+    int n, k;
+    T v;
+    if (trans) {  // tile rows = k (r0 ..), cols = n (c0 ..): walk k fastest
+      const int kk = e % th, nn = e / th;
+      n = c0 + nn;
+      k = r0 + kk;
+      v = tile[kk][nn];
+    } else {
+      const int nn = e / 32, kk = e % 32;
+      n = r0 + nn;
+      k = c0 + kk;
+      v = tile[nn][kk];
+    }
+    if (n >= N || k >= Kt) continue;
+    if (k < K1)
+      g1[(long long)n * K1 + k] = v;
+    else if (k < K1 + K2)
+      g2[(long long)n * K2 + (k - K1)] = v;
+    else
+      gb[n] = v;
+  }
+}
+
+template <typename T>
+cudaError_t splitk_reduce_batch(const gfm_reduce_job* jobs, int n_jobs, cudaStream_t s) {
+  for (int base = 0; base < n_jobs; base += kMaxReduceJobs) {
+    ReduceJobs J{};
+    const int n = std::min(kMaxReduceJobs, n_jobs - base);
+    int tiles = 0;
+    for (int q = 0; q < n; ++q) {
+      const gfm_reduce_job& jb = jobs[base + q];
+      J.job[q] = jb;
+      const int Kt = jb.K1 + jb.K2 + jb.with_bias;
+      const int R = jb.trans ? Kt : jb.N, C = jb.trans ? jb.N : Kt;
+      J.tile0[q] = tiles;
+      J.ncx[q] = ceil_div(C, 32);
+      J.rows[q] = jb.splits > 16 ? 8 : 32;
+      tiles += J.ncx[q] * ceil_div(R, J.rows[q]);
+    }
+    J.tile0[n] = tiles;
+    if (tiles > 0) launch_k(k_splitk_reduce_batch<T>, tiles, 256, 0, s, J, n);
+  }
   return cudaGetLastError();
 }
 
@@ -506,6 +612,30 @@ int gfm_linear_bwd_data(const void* dY, int ldd, int M, const int* M_dev, int N,
                linear_bwd_data_t<T>((const T*)dY, ldd, M, M_dev, N, (const T*)W1, ldw1, K1,
                                     (const T*)W2, ldw2, K2, (T*)out1, ldo1, (T*)out2, ldo2,
                                     (const T*)gate, ldg, (cudaStream_t)stream))
+}
+
+int gfm_linear_bwd_weight_partials(const void* dY, int ldd, int M, const int* M_dev, int N,
+                                   const void* X1, int ld1, int K1, const void* X2, int ld2,
+                                   int K2, int with_bias, void* g1, void* g2, void* gb,
+                                   void* workspace, gfm_reduce_job* job, int dtype,
+                                   void* stream) {
+  if (!job) {
+    set_error("gfm_linear_bwd_weight_partials: job descriptor is NULL");
+    return GFM_EINVAL;
+  }
+  GFM_DISPATCH(dtype, "gfm_linear_bwd_weight_partials",
+               linear_bwd_weight_t<T>((const T*)dY, ldd, M, M_dev, N, (const T*)X1, ld1, K1,
+                                      (const T*)X2, ld2, K2, with_bias, (T*)g1, (T*)g2, (T*)gb,
+                                      (T*)workspace, (cudaStream_t)stream, job))
+}
+
+int gfm_splitk_reduce_batch(const gfm_reduce_job* jobs, int n_jobs, int dtype, void* stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) {
+    set_error("gfm_splitk_reduce_batch: bad job list");
+    return GFM_EINVAL;
+  }
+  GFM_DISPATCH(dtype, "gfm_splitk_reduce_batch",
+               splitk_reduce_batch<T>(jobs, n_jobs, (cudaStream_t)stream))
 }
 
 size_t gfm_linear_bwd_weight_workspace_bytes(int M, int N, int K1, int K2, int with_bias, int dtype) {

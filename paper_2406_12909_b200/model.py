@@ -17,6 +17,7 @@ call raises ``ExtensionMissingError``.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -755,14 +756,21 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
                                                              device=batch.device)
     gp = ModelParams(cfg, grad)
 
-    def wgrad(dY, ldd, n_out, X1, ld1, K1, X2, ld2, K2, g1, g2, gb):
+    # weight gradients: split-K partials now, all reductions in one batched
+    # launch after the last layer (each call keeps its own workspace)
+    jobs = []
+
+    def wgrad(dY, ldd, n_out, X1, ld1, K1, X2, ld2, K2, g1, g2, gb, tag):
         nb = query("gfm_linear_bwd_weight_workspace_bytes", N, n_out, K1, K2, 1, code)
-        key = f"wgrad_ws_{n_out}_{K1}_{K2}"
+        key = f"wgrad_ws_{tag}"
         ws = sc.bytes(key, nb)
         # the workspace's ones operand survives between calls: fill it once
         bias = 2 if sc.ones_ready.get(key) == (ws.data_ptr(), N) else 1
-        call("gfm_linear_bwd_weight", ptr(dY), ldd, N, None, n_out, ptr(X1), ld1, K1, ptr(X2),
-             ld2, K2, bias, ptr(g1), ptr(g2), ptr(gb), ptr(ws), code, s)
+        job = _lib.ReduceJob()
+        call("gfm_linear_bwd_weight_partials", ptr(dY), ldd, N, None, n_out, ptr(X1), ld1, K1,
+             ptr(X2), ld2, K2, bias, ptr(g1), ptr(g2), ptr(gb), ptr(ws), ctypes.byref(job),
+             code, s)
+        jobs.append(job)
         sc.ones_ready[key] = (ws.data_ptr(), N)
 
     # energy head (model.py:520-533)
@@ -774,12 +782,12 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     call("gfm_energy_seed", ptr(de), ptr(batch.graph_of_node), N, G,
          ptr(params.view(f"head_{F - 1}.w")), ptr(ys[F - 1]), ptr(ds), 4, ptr(dz), code, s)
     wgrad(ds, 4, 1, ys[F - 1], G, G, None, 0, 0, gp.view(f"head_{F - 1}.w"), None,
-          gp.view(f"head_{F - 1}.b"))
+          gp.view(f"head_{F - 1}.b"), f"head{F - 1}")
     dh_e = sc.get("dh_energy", (N, H), dt)
     for f in range(F - 2, -1, -1):
         kin = ys[f].shape[1]
         wgrad(dz, G, G, ys[f], kin, kin, None, 0, 0, gp.view(f"head_{f}.w"), None,
-              gp.view(f"head_{f}.b"))
+              gp.view(f"head_{f}.b"), f"head{f}")
         if f > 0:
             dz2 = sc.get(f"dz_head{f}", (N, kin), dt)
             call("gfm_linear_bwd_data", ptr(dz), G, N, None, G, ptr(params.view(f"head_{f}.w")),
@@ -804,7 +812,7 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     for l in range(cfg.mpnn_layers - 1, -1, -1):
         lay = cache["layers"][l]
         wgrad(dz, H, H, lay["h_in"], H, H, lay["agg"], K * H, K * H, gp.view(f"layer_{l}.w"),
-              gp.view(f"layer_{l}.u"), gp.view(f"layer_{l}.b"))
+              gp.view(f"layer_{l}.u"), gp.view(f"layer_{l}.b"), f"layer{l}")
         dh_in = sc.get("dh_in", (N, H), dt)
         dagg = sc.get("dagg", (N, K * H), dt)
         call("gfm_linear_bwd_data", ptr(dz), H, N, None, H, ptr(params.view(f"layer_{l}.w")), H, H,
@@ -817,6 +825,8 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
              ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
              flags | _argmax_flag(batch), s)
         dz = out
+    arr = (_lib.ReduceJob * len(jobs))(*jobs)
+    call("gfm_splitk_reduce_batch", arr, len(jobs), code, s)
     ews = sc.bytes("emb_ws", query("gfm_embedding_grad_workspace_bytes", N, H, code))
     call("gfm_embedding_grad", ptr(batch.z), N, ptr(dz), H, ptr(gp.embedding), ptr(ews), code, s)
 

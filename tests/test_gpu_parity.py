@@ -523,3 +523,53 @@ def test_runner_pipelined_step_matches_blocking_step(use_graph):
         out[mode] = (losses, tr.flat_master())
     assert out["blocking"][0] == out["pipelined"][0]
     np.testing.assert_array_equal(out["blocking"][1], out["pipelined"][1])
+
+
+@pytest.mark.parametrize("dtype", [F32, F64])
+def test_deferred_batched_splitk_reduce_bitwise(dtype):
+    """gfm_linear_bwd_weight_partials + one gfm_splitk_reduce_batch over
+    several jobs == per-call gfm_linear_bwd_weight (bitwise in float32)."""
+    import ctypes
+
+    code = _lib.F32 if dtype == F32 else _lib.F64
+    rng = np.random.default_rng(9)
+    shapes = [(3000, 64, 64, 256, 1), (3000, 1, 16, 0, 1), (777, 32, 40, 0, 0)]
+    jobs, want, got = [], [], []
+    keep = []
+    for M_, N_, K1, K2, bias in shapes:
+        t = lambda *sh: torch.as_tensor(rng.normal(size=sh), dtype=dtype, device="cuda")
+        dY, X1 = t(M_, max(N_, 4)), t(M_, K1)
+        X2 = t(M_, max(K2, 1))
+        ld_dy = dY.shape[1]
+        nb = _lib.query("gfm_linear_bwd_weight_workspace_bytes", M_, N_, K1, K2, bias, code)
+        outs = []
+        for mode in ("now", "defer"):
+            g1 = torch.zeros(N_, K1, dtype=dtype, device="cuda")
+            g2 = torch.zeros(N_, max(K2, 1), dtype=dtype, device="cuda")
+            gb = torch.zeros(N_, dtype=dtype, device="cuda")
+            ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            args = (_lib.ptr(dY), ld_dy, M_, None, N_, _lib.ptr(X1), K1, K1,
+                    _lib.ptr(X2) if K2 else None, max(K2, 1), K2, bias, _lib.ptr(g1),
+                    _lib.ptr(g2), _lib.ptr(gb), _lib.ptr(ws))
+            if mode == "now":
+                _lib.call("gfm_linear_bwd_weight", *args, code, _lib.stream_handle())
+            else:
+                job = _lib.ReduceJob()
+                _lib.call("gfm_linear_bwd_weight_partials", *args, ctypes.byref(job), code,
+                          _lib.stream_handle())
+                jobs.append(job)
+            outs.append((g1, g2, gb))
+            keep.append(ws)
+        want.append(outs[0])
+        got.append(outs[1])
+    arr = (_lib.ReduceJob * len(jobs))(*jobs)
+    _lib.call("gfm_splitk_reduce_batch", arr, len(jobs), code, _lib.stream_handle())
+    # same fp64 sums; the per-call reduce groups the splits differently for
+    # small outputs (k_splitk_reduce_narrow), which shows only in float64
+    for w, g in zip(want, got):
+        for a, b in zip(w, g):
+            if dtype == F32:
+                np.testing.assert_array_equal(a.cpu().numpy(), b.cpu().numpy())
+            else:
+                np.testing.assert_allclose(b.cpu().numpy(), a.cpu().numpy(), rtol=1e-12,
+                                           atol=1e-12)
