@@ -549,6 +549,12 @@ class _Scratch:
     def bytes(self, name, n):
         return self.get(name, (max(int(n), 1),), torch.uint8)
 
+    def side_stream(self):
+        """second stream for work with no consumer until a later join"""
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
+
 
 def _scratch_for(owner, device):
     return owner if owner is not None else _Scratch(device)
@@ -756,9 +762,14 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
                                                              device=batch.device)
     gp = ModelParams(cfg, grad)
 
-    # weight gradients: split-K partials now, all reductions in one batched
-    # launch after the last layer (each call keeps its own workspace)
+    # weight gradients: split-K partials on a side stream (nothing downstream
+    # consumes them until the end), so each tensor-core GEMM overlaps the
+    # L2-bound gathers of the main stream; all reductions in one batched
+    # launch after the last layer (each call keeps its own workspace and its
+    # inputs stay untouched: per-layer dz buffers)
     jobs = []
+    main = torch.cuda.current_stream(batch.device)
+    side = sc.side_stream()
 
     def wgrad(dY, ldd, n_out, X1, ld1, K1, X2, ld2, K2, g1, g2, gb, tag):
         nb = query("gfm_linear_bwd_weight_workspace_bytes", N, n_out, K1, K2, 1, code)
@@ -767,9 +778,12 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
         # the workspace's ones operand survives between calls: fill it once
         bias = 2 if sc.ones_ready.get(key) == (ws.data_ptr(), N) else 1
         job = _lib.ReduceJob()
+        ready = torch.cuda.Event()
+        ready.record(main)
+        side.wait_event(ready)
         call("gfm_linear_bwd_weight_partials", ptr(dY), ldd, N, None, n_out, ptr(X1), ld1, K1,
              ptr(X2), ld2, K2, bias, ptr(g1), ptr(g2), ptr(gb), ptr(ws), ctypes.byref(job),
-             code, s)
+             code, side.cuda_stream)
         jobs.append(job)
         sc.ones_ready[key] = (ws.data_ptr(), N)
 
@@ -818,13 +832,16 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
         call("gfm_linear_bwd_data", ptr(dz), H, N, None, H, ptr(params.view(f"layer_{l}.w")), H, H,
              ptr(params.view(f"layer_{l}.u")), K * H, K * H, ptr(dh_in), H, ptr(dagg), K * H, None,
              0, code, s)
-        out = sc.get("dz_a" if l % 2 else "dz_b", (N, H), dt)
+        out = sc.get(f"dz_l{l}", (N, H), dt)
         call("gfm_agg_bwd", ptr(dagg), ptr(lay["agg"]), ptr(lay["smean"]), ptr(lay["argmax"]),
              ptr(lay["h_in"]), ptr(batch.rowptr), ptr(batch.csc_ptr), ptr(batch.csc_eid),
              ptr(batch.csc_dst), ptr(batch.edge_w), N, H, parts, ptr(dh_in),
              ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
              flags | _argmax_flag(batch), s)
         dz = out
+    done = torch.cuda.Event()
+    done.record(side)
+    main.wait_event(done)
     arr = (_lib.ReduceJob * len(jobs))(*jobs)
     call("gfm_splitk_reduce_batch", arr, len(jobs), code, s)
     ews = sc.bytes("emb_ws", query("gfm_embedding_grad_workspace_bytes", N, H, code))
