@@ -598,13 +598,21 @@ def forward_batch(params: ModelParams, batch: Batch, cache: dict | None = None,
              ptr(params.view(f"layer_{l}.b")), N, None, H, 1, ptr(h_out), H, code, s)
         layers.append(dict(h_in=h, agg=agg, argmax=argmax, smean=smean, h_out=h_out))
         h = h_out
+    # the two heads only share h: the energy head runs on a side stream (a
+    # parallel CUDA-graph branch) while the force head runs here
+    main = torch.cuda.current_stream(batch.device)
+    side = sc.side_stream()
+    fork = torch.cuda.Event()
+    fork.record(main)
+    side.wait_event(fork)
+    ss = side.cuda_stream
     ys = [h]
     y = h
     for f in range(cfg.fc_layers - 1):
         kin = y.shape[1]
         y2 = sc.get(f"y{f + 1}", (N, G), dt)
         call("gfm_linear_fwd", ptr(y), kin, kin, None, 0, 0, ptr(params.view(f"head_{f}.w")), kin,
-             None, 0, ptr(params.view(f"head_{f}.b")), N, None, G, 1, ptr(y2), G, code, s)
+             None, 0, ptr(params.view(f"head_{f}.b")), N, None, G, 1, ptr(y2), G, code, ss)
         ys.append(y2)
         y = y2
     node_e = sc.get("node_e", (max(N, 1),), dt)
@@ -612,12 +620,15 @@ def forward_batch(params: ModelParams, batch: Batch, cache: dict | None = None,
     F = cfg.fc_layers
     call("gfm_energy_readout", ptr(y), N, G, ptr(params.view(f"head_{F - 1}.w")),
          ptr(params.view(f"head_{F - 1}.b")), ptr(batch.node_offsets), B, ptr(node_e),
-         ptr(e_pred), code, s)
+         ptr(e_pred), code, ss)
     f_pred = sc.get("f_pred", (N, 3), dt)
     P = sc.get("force_P", (N, H), dt)  # h V^T, reused by the backward
     call("gfm_force_fwd", ptr(h), H, N, ptr(batch.rowptr), ptr(batch.col_src), ptr(batch.edge_dx),
          ptr(params.force_v), ptr(params.force_c), ptr(params.force_u), ptr(P), ptr(f_pred), code,
          flags, s)
+    join = torch.cuda.Event()
+    join.record(side)
+    main.wait_event(join)
     if cache is not None:
         cache.update(layers=layers, h_final=h, head_inputs=ys, force_P=P)
     if scratch is None:
