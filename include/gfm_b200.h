@@ -161,6 +161,19 @@ GFM_API int gfm_force_fwd(const void* h, int H, int n_nodes, const int* rowptr,
  * with src i, grad_V = S^T h and dh_final = dh_energy + S V; dz_out =
  * dh_final * (1 - h^2) (model.py:553) feeds the last message-passing layer. */
 GFM_API size_t gfm_force_bwd_workspace_bytes(int H, int n_nodes, int dtype);
+/* gfm_force_bwd in two stream-ordered halves sharing `workspace`: the edge
+ * passes and grad_V / grad_c / grad_u (no dh_energy needed yet), then
+ * dz_out = (dh_energy + S V) * (1 - h^2) -- so the energy-head backward
+ * producing dh_energy can run concurrently with the first half. */
+GFM_API int gfm_force_bwd_edges(const void* h, const void* P, int H, int n_nodes,
+                                const int* rowptr, const int* col_src, const void* edge_dx,
+                                const int* csc_ptr, const int* csc_eid, const int* csc_dst,
+                                const void* V, const void* c, const void* u, const void* df,
+                                void* grad_v, void* grad_c, void* grad_u, void* workspace,
+                                int dtype, int flags, void* stream);
+GFM_API int gfm_force_bwd_finish(const void* h, int H, int n_nodes, const void* V,
+                                 const void* dh_energy, void* dz_out, void* workspace, int dtype,
+                                 void* stream);
 GFM_API int gfm_force_bwd(const void* h, const void* P, int H, int n_nodes, const int* rowptr,
                           const int* col_src, const void* edge_dx, const int* csc_ptr,
                           const int* csc_eid, const int* csc_dst, const void* V, const void* c,

@@ -79,6 +79,9 @@ SIGNATURES = {
     "gfm_force_bwd_workspace_bytes": (_S, [_I, _I, _I]),
     "gfm_force_bwd": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                            _P, _P, _P, _I, _I, _P]),
+    "gfm_force_bwd_edges": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                 _P, _P, _P, _I, _I, _P]),
+    "gfm_force_bwd_finish": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),
     "gfm_energy_readout": (_I, [_P, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P]),
     "gfm_loss_workspace_bytes": (_S, []),
     "gfm_loss_seeds": (_I, [_P, _P, _P, _I, _P, _P, _I, _D, _D, _P, _P, _P, _P, _P, _I, _P]),

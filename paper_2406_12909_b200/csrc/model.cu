@@ -522,7 +522,9 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
                         const int* col_src, const T* dx, const int* csc_ptr, const int* csc_eid,
                         const int* csc_dst, const T* V, const T* c, const T* u, const T* df,
                         const T* dh_e, T* gV, T* gc, T* gu, T* dz_out, void* ws, int flags,
-                        cudaStream_t s) {
+                        cudaStream_t s, int stage = 3) {
+  // stage bit 1: edge passes + grad_V / grad_c / grad_u (S left in ws);
+  // stage bit 2: dz_out from S in ws (lets the caller overlap dh_energy)
   const size_t nh = (size_t)(n > 0 ? n : 1) * H;
   T* Ddst = (T*)ws;
   T* TU = Ddst + nh;
@@ -530,8 +532,10 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
   T* part = S + nh;
   T* wws = part + (size_t)ceil_div(n > 0 ? n : 1, 128) * H + 64;
   wws = (T*)(((uintptr_t)wws + 255) & ~(uintptr_t)255);
-  cudaError_t e = force_bwd_edges<T>(P, n, H, rowptr, col_src, csc_ptr, csc_eid, csc_dst, dx, df,
-                                     c, u, Ddst, TU, S, flags, s);
+  cudaError_t e;
+  if (!(stage & 1)) goto finish;
+  e = force_bwd_edges<T>(P, n, H, rowptr, col_src, csc_ptr, csc_eid, csc_dst, dx, df, c, u, Ddst,
+                         TU, S, flags, s);
   if (e != cudaSuccess) return e;
   // grad_V = S^T h   (= sum_e dpre_e pair_e^T, model.py:543)
   e = linear_bwd_weight_t<T>(S, H, n, nullptr, H, h, H, H, nullptr, 0, 0, 0, gV, nullptr, nullptr,
@@ -539,6 +543,8 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
   if (e != cudaSuccess) return e;
   if ((e = colsum<T>(Ddst, n, H, gc, part, s)) != cudaSuccess) return e;  // model.py:544
   if ((e = colsum<T>(TU, n, H, gu, part, s)) != cudaSuccess) return e;    // model.py:540
+finish:
+  if (!(stage & 2)) return cudaGetLastError();
   // dz_last = (dh_energy + S V) * (1 - h^2)   (model.py:545-547, 553)
   return linear_bwd_data_t<T>(S, H, n, nullptr, H, V, H, H, nullptr, 0, 0, dz_out, H, nullptr, 0,
                               h, H, s, dh_e);
@@ -676,6 +682,28 @@ int gfm_force_bwd(const void* h, const void* P, int H, int n_nodes, const int* r
                               (const T*)c, (const T*)u, (const T*)df, (const T*)dh_energy,
                               (T*)grad_v, (T*)grad_c, (T*)grad_u, (T*)dz_out, workspace, flags,
                               (cudaStream_t)stream))
+}
+
+int gfm_force_bwd_edges(const void* h, const void* P, int H, int n_nodes, const int* rowptr,
+                        const int* col_src, const void* edge_dx, const int* csc_ptr,
+                        const int* csc_eid, const int* csc_dst, const void* V, const void* c,
+                        const void* u, const void* df, void* grad_v, void* grad_c, void* grad_u,
+                        void* workspace, int dtype, int flags, void* stream) {
+  GFM_DISPATCH(dtype, "gfm_force_bwd_edges",
+               force_bwd_t<T>((const T*)h, (const T*)P, H, n_nodes, rowptr, col_src,
+                              (const T*)edge_dx, csc_ptr, csc_eid, csc_dst, (const T*)V,
+                              (const T*)c, (const T*)u, (const T*)df, nullptr, (T*)grad_v,
+                              (T*)grad_c, (T*)grad_u, nullptr, workspace, flags,
+                              (cudaStream_t)stream, 1))
+}
+
+int gfm_force_bwd_finish(const void* h, int H, int n_nodes, const void* V, const void* dh_energy,
+                         void* dz_out, void* workspace, int dtype, void* stream) {
+  GFM_DISPATCH(dtype, "gfm_force_bwd_finish",
+               force_bwd_t<T>((const T*)h, nullptr, H, n_nodes, nullptr, nullptr, nullptr,
+                              nullptr, nullptr, nullptr, (const T*)V, nullptr, nullptr, nullptr,
+                              (const T*)dh_energy, nullptr, nullptr, nullptr, (T*)dz_out,
+                              workspace, 0, (cudaStream_t)stream, 2))
 }
 
 int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const void* c,

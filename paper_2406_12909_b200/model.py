@@ -782,54 +782,65 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     main = torch.cuda.current_stream(batch.device)
     side = sc.side_stream()
 
-    def wgrad(dY, ldd, n_out, X1, ld1, K1, X2, ld2, K2, g1, g2, gb, tag):
+    def wgrad(dY, ldd, n_out, X1, ld1, K1, X2, ld2, K2, g1, g2, gb, tag, inputs_on_side=False):
         nb = query("gfm_linear_bwd_weight_workspace_bytes", N, n_out, K1, K2, 1, code)
         key = f"wgrad_ws_{tag}"
         ws = sc.bytes(key, nb)
         # the workspace's ones operand survives between calls: fill it once
         bias = 2 if sc.ones_ready.get(key) == (ws.data_ptr(), N) else 1
         job = _lib.ReduceJob()
-        ready = torch.cuda.Event()
-        ready.record(main)
-        side.wait_event(ready)
+        if not inputs_on_side:  # inputs produced on the main stream
+            ready = torch.cuda.Event()
+            ready.record(main)
+            side.wait_event(ready)
         call("gfm_linear_bwd_weight_partials", ptr(dY), ldd, N, None, n_out, ptr(X1), ld1, K1,
              ptr(X2), ld2, K2, bias, ptr(g1), ptr(g2), ptr(gb), ptr(ws), ctypes.byref(job),
              code, side.cuda_stream)
         jobs.append(job)
         sc.ones_ready[key] = (ws.data_ptr(), N)
 
-    # energy head (model.py:520-533)
+    # energy head (model.py:520-533) on the side stream, concurrent with the
+    # force head's edge passes on this one; they meet at dh_energy
+    fork = torch.cuda.Event()
+    fork.record(main)
+    side.wait_event(fork)
+    ss = side.cuda_stream
     ys = cache["head_inputs"]
     # ds as an [N][4] column (cols 1..3 zero) so its rows are 16B aligned and
     # the weight-gradient GEMM below can stream it with TMA
     ds = sc.get("ds", (max(N, 1), 4), dt)
     dz = sc.get("dz_head", (N, G), dt)
     call("gfm_energy_seed", ptr(de), ptr(batch.graph_of_node), N, G,
-         ptr(params.view(f"head_{F - 1}.w")), ptr(ys[F - 1]), ptr(ds), 4, ptr(dz), code, s)
+         ptr(params.view(f"head_{F - 1}.w")), ptr(ys[F - 1]), ptr(ds), 4, ptr(dz), code, ss)
     wgrad(ds, 4, 1, ys[F - 1], G, G, None, 0, 0, gp.view(f"head_{F - 1}.w"), None,
-          gp.view(f"head_{F - 1}.b"), f"head{F - 1}")
+          gp.view(f"head_{F - 1}.b"), f"head{F - 1}", inputs_on_side=True)
     dh_e = sc.get("dh_energy", (N, H), dt)
     for f in range(F - 2, -1, -1):
         kin = ys[f].shape[1]
         wgrad(dz, G, G, ys[f], kin, kin, None, 0, 0, gp.view(f"head_{f}.w"), None,
-              gp.view(f"head_{f}.b"), f"head{f}")
+              gp.view(f"head_{f}.b"), f"head{f}", inputs_on_side=True)
         if f > 0:
             dz2 = sc.get(f"dz_head{f}", (N, kin), dt)
             call("gfm_linear_bwd_data", ptr(dz), G, N, None, G, ptr(params.view(f"head_{f}.w")),
-                 kin, kin, None, 0, 0, ptr(dz2), kin, None, 0, ptr(ys[f]), kin, code, s)
+                 kin, kin, None, 0, 0, ptr(dz2), kin, None, 0, ptr(ys[f]), kin, code, ss)
             dz = dz2
         else:
             call("gfm_linear_bwd_data", ptr(dz), G, N, None, G, ptr(params.view(f"head_{f}.w")),
-                 kin, kin, None, 0, 0, ptr(dh_e), H, None, 0, None, 0, code, s)
+                 kin, kin, None, 0, 0, ptr(dh_e), H, None, 0, None, 0, code, ss)
+    head_done = torch.cuda.Event()
+    head_done.record(side)
 
     # force head (model.py:535-547) -> dz of the last message-passing layer
     dzl = sc.get("dz_layer", (N, H), dt)
     ws = sc.bytes("force_bwd_ws", query("gfm_force_bwd_workspace_bytes", H, N, code))
-    call("gfm_force_bwd", ptr(cache["h_final"]), ptr(cache["force_P"]), H, N, ptr(batch.rowptr),
-         ptr(batch.col_src), ptr(batch.edge_dx), ptr(batch.csc_ptr), ptr(batch.csc_eid),
-         ptr(batch.csc_dst), ptr(params.force_v), ptr(params.force_c), ptr(params.force_u),
-         ptr(df), ptr(dh_e), ptr(gp.force_v), ptr(gp.force_c), ptr(gp.force_u), ptr(dzl),
+    call("gfm_force_bwd_edges", ptr(cache["h_final"]), ptr(cache["force_P"]), H, N,
+         ptr(batch.rowptr), ptr(batch.col_src), ptr(batch.edge_dx), ptr(batch.csc_ptr),
+         ptr(batch.csc_eid), ptr(batch.csc_dst), ptr(params.force_v), ptr(params.force_c),
+         ptr(params.force_u), ptr(df), ptr(gp.force_v), ptr(gp.force_c), ptr(gp.force_u),
          ptr(ws), code, flags, s)
+    main.wait_event(head_done)
+    call("gfm_force_bwd_finish", ptr(cache["h_final"]), H, N, ptr(params.force_v), ptr(dh_e),
+         ptr(dzl), ptr(ws), code, s)
 
     # message-passing layers (model.py:549-562)
     dz = dzl
