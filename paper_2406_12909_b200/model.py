@@ -861,13 +861,15 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
              ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
              flags | _argmax_flag(batch), s)
         dz = out
+    # the batched reduction follows the weight-gradient GEMMs on the side
+    # stream while the embedding gradient runs here; join before returning
+    arr = (_lib.ReduceJob * len(jobs))(*jobs)
+    call("gfm_splitk_reduce_batch", arr, len(jobs), code, side.cuda_stream)
+    ews = sc.bytes("emb_ws", query("gfm_embedding_grad_workspace_bytes", N, H, code))
+    call("gfm_embedding_grad", ptr(batch.z), N, ptr(dz), H, ptr(gp.embedding), ptr(ews), code, s)
     done = torch.cuda.Event()
     done.record(side)
     main.wait_event(done)
-    arr = (_lib.ReduceJob * len(jobs))(*jobs)
-    call("gfm_splitk_reduce_batch", arr, len(jobs), code, s)
-    ews = sc.bytes("emb_ws", query("gfm_embedding_grad_workspace_bytes", N, H, code))
-    call("gfm_embedding_grad", ptr(batch.z), N, ptr(dz), H, ptr(gp.embedding), ptr(ews), code, s)
 
     e_true, n_per = batch.energy_true, batch.n_per_graph
     lb = LossBreakdown(vals if scratch is not None else vals.clone(),
