@@ -347,14 +347,65 @@ class StructureStepRunner:
         tot, cnt = float(self.loss_host[0]), float(self.loss_host[1])
         return tot / cnt if cnt else float("nan")
 
+    def _from_stage(self, k):
+        for key, dst in self.slot.items():
+            dst.copy_(self._stage[k][key])
+
+    def _build_stages(self):
+        """Two device staging copies of the input slots (+ the copy stream)."""
+        dev = self.tr.device
+        self._stage = [{k: torch.empty_like(v) for k, v in self.slot.items()} for _ in range(2)]
+        self._copy_stream = torch.cuda.Stream(device=dev)
+        self._stage_free = [None, None]
+        self._stage_i = 0
+        self._graphs = None
+
+    def _capture_stages(self):
+        """One captured step per staging copy, each starting with the device
+        copy stage -> slot.  Capture records without executing, so building
+        these never adds a training step."""
+        torch.cuda.synchronize()
+        self._graphs = []
+        for k in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._from_stage(k)
+                self._eager()
+            self._graphs.append(g)
+
     def step_pipelined(self, pos, z, energy, forces):
-        """As ``step``, but the host reads this step's loss one call later, so
-        enqueueing step i + 1 (input copies, graph launch) overlaps step i on
-        the GPU -- the usual asynchronous loss logging of a training loop.
-        Returns the previous step's mean loss (None on the first call); call
-        ``drain()`` after the last step for its loss."""
-        self.load(pos, z, energy, forces)
-        self.run()
+        """As ``step``, but pipelined: the host->device copy of this step's
+        inputs runs on a copy stream into one of two staging buffers while the
+        previous step computes, and the host reads this step's loss one call
+        later (asynchronous loss logging).  The caller must not modify a
+        (pinned) input buffer until two calls later.  Returns the previous
+        step's mean loss (None on the first call); call ``drain()`` after the
+        last step for its loss."""
+        if getattr(self, "_stage", None) is None:
+            self._build_stages()
+        main = torch.cuda.current_stream(self.tr.device)
+        k = self._stage_i
+        cs = self._copy_stream
+        if self._stage_free[k] is not None:
+            cs.wait_event(self._stage_free[k])  # the step that last read stage k is done
+        with torch.cuda.stream(cs):
+            for key, v in (("pos", pos), ("z", z), ("e", energy), ("f", forces)):
+                dst = self._stage[k][key]
+                dst.copy_(v.reshape(dst.shape), non_blocking=True)
+        copied = torch.cuda.Event()
+        copied.record(cs)
+        main.wait_event(copied)
+        if self.use_graph and self._graphs is None and self.batch is not None:
+            self._capture_stages()  # buffers exist (an earlier eager step allocated them)
+        if self._graphs is not None:
+            self._graphs[k].replay()
+        else:
+            self._from_stage(k)
+            self._eager()
+        free = torch.cuda.Event()
+        free.record(main)
+        self._stage_free[k] = free
+        self._stage_i = k ^ 1
         P = self.tr.P
         k = self._slot
         self._loss_slots[k].copy_(self.tr.contrib[P:P + 2].float(), non_blocking=True)
