@@ -49,6 +49,9 @@ enum { GFM_FLAG_SCALAR = 1 }; /* force the scalar (numpy-order) kernels */
  * position (unique within a row; valid when every CSR row has <= 256 edges,
  * e.g. a neighbour cap <= 256) -- 4x fewer bytes gathered by the backward */
 enum { GFM_FLAG_ARGMAX_U8 = 2 };
+/* gfm_agg_bwd: G | coef already in `workspace` and `dagg` is the max part's
+ * gradient [N][H] (as written by gfm_layer_bwd_data_agg) -- no prep pass */
+enum { GFM_FLAG_AGG_PREPPED = 4 };
 /* float32 GEMM engine: tcgen05 3xTF32 (default, fp32-level accuracy),
  * tcgen05 1xTF32 (faster, ~1e-3 relative), or the SIMT fp32 engine */
 enum { GFM_GEMM_SIMT = 0, GFM_GEMM_TC3 = 1, GFM_GEMM_TC1 = 2 };
@@ -137,6 +140,18 @@ GFM_API int gfm_linear_fwd(const void* X1, int ld1, int K1, const void* X2, int 
 GFM_API int gfm_linear_bwd_data(const void* dY, int ldd, int M, const int* M_dev, int N, const void* W1,
                         int ldw1, int K1, const void* W2, int ldw2, int K2, void* out1, int ldo1,
                         void* out2, int ldo2, const void* gate, int ldg, int dtype, void* stream);
+/* Layer backward-data fused with the PNA (parts = 15) aggregation-backward
+ * prep, float32 tensor-core engine only: dh_in = dz W; with dagg = dz U
+ * (never stored) G = dsum + dmean/deg - coef*mean, coef = dstd/(deg*std),
+ * dmax = the max part -- then gfm_agg_bwd(..., dagg = dmax, workspace =
+ * [G | coef], GFM_FLAG_AGG_PREPPED).  G and coef are [N][H] at the head of
+ * the gfm_agg_bwd workspace; `workspace` here holds U permuted channel-major
+ * (gfm_layer_bwd_data_agg_workspace_bytes). */
+GFM_API size_t gfm_layer_bwd_data_agg_workspace_bytes(int H);
+GFM_API int gfm_layer_bwd_data_agg(const void* dz, int M, int H, const void* W, const void* U,
+                                   const void* agg, const void* stat_mean, const int* rowptr,
+                                   void* dh_in, void* G, void* coef, void* dmax, void* workspace,
+                                   void* stream);
 /* g1 = dY^T X1, g2 = dY^T X2, gb = colsum(dY): deterministic split-K.
  * with_bias: 0 = no gb; 1 = gb (the float32 tensor-core path writes a [M][4]
  * ones operand into the workspace); 2 = as 1 when this workspace already

@@ -21,6 +21,7 @@ F32, F64 = 0, 1
 PART_SUM, PART_MEAN, PART_MAX, PART_STD = 1, 2, 4, 8
 FLAG_SCALAR = 1
 FLAG_ARGMAX_U8 = 2
+FLAG_AGG_PREPPED = 4
 ABI_VERSION = 1
 
 _P = ctypes.c_void_p
@@ -79,6 +80,8 @@ SIGNATURES = {
     "gfm_force_bwd_workspace_bytes": (_S, [_I, _I, _I]),
     "gfm_force_bwd": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                            _P, _P, _P, _I, _I, _P]),
+    "gfm_layer_bwd_data_agg_workspace_bytes": (_S, [_I]),
+    "gfm_layer_bwd_data_agg": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "gfm_force_bwd_edges": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                  _P, _P, _P, _I, _I, _P]),
     "gfm_force_bwd_finish": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),

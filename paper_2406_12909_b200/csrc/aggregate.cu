@@ -883,16 +883,22 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
                     const int* argmax, const void* h_in, const int* rowptr, const int* csc_ptr,
                     const int* csc_eid, const int* csc_dst, const void* w, int n, int H, int parts,
                     void* dh, const void* gate, void* out, void* ws, int force_scalar, int am_u8,
-                    cudaStream_t s) {
+                    cudaStream_t s, int prepped = 0) {
   if (n <= 0) return cudaSuccess;
   const AggLayout L = agg_layout(parts, H);
-  const int ld = L.K * H;
+  int ld = L.K * H;
   const size_t esz = dtype == GFM_F32 ? 4 : 8;
   // G: dsum alone needs no prep (read dagg in place); mean/std need G/coef
   const void* G = nullptr;
   int ldg = ld;
   const void* coef = nullptr;
-  if (L.o_mean >= 0 || L.o_std >= 0) {
+  if (prepped) {
+    // gfm_layer_bwd_data_agg already wrote G | coef into ws and the max part's
+    // gradient as `dagg` [N][H]
+    G = ws;
+    ldg = H;
+    coef = L.o_std >= 0 ? (const void*)((const char*)ws + esz * (size_t)n * H) : nullptr;
+  } else if (L.o_mean >= 0 || L.o_std >= 0) {
     void* Gw = ws;
     void* Cw = L.o_std >= 0 ? (void*)((char*)ws + esz * (size_t)n * H) : nullptr;
     if (dtype == GFM_F32 && H % 4 == 0 && !force_scalar)
@@ -913,7 +919,9 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
   } else if (L.o_sum >= 0) {
     G = (const char*)dagg + esz * L.o_sum;
   }
-  const void* dmax = L.o_max >= 0 ? (const char*)dagg + esz * L.o_max : nullptr;
+  const void* dmax =
+      L.o_max >= 0 ? (prepped ? dagg : (const void*)((const char*)dagg + esz * L.o_max)) : nullptr;
+  if (prepped) ld = H;  // dmax is its own [N][H] buffer
   const int* am = L.o_max >= 0 ? argmax : nullptr;
   int nv = 0, lpn = 0, slabs = 1;
   const bool g_ok = G == nullptr || ldg % 4 == 0;
@@ -1028,7 +1036,7 @@ int gfm_agg_bwd(const void* dagg, const void* agg, const void* stat_mean, const 
   cudaError_t e = agg_bwd(dtype, dagg, agg, stat_mean, argmax, h_in, rowptr, csc_ptr, csc_eid,
                           csc_dst, edge_w, n_nodes, H, parts, dh, gate, out, workspace,
                           flags & GFM_FLAG_SCALAR, (flags & GFM_FLAG_ARGMAX_U8) != 0,
-                          (cudaStream_t)stream);
+                          (cudaStream_t)stream, (flags & GFM_FLAG_AGG_PREPPED) != 0);
   if (e != cudaSuccess) set_error("gfm_agg_bwd: %s", cudaGetErrorString(e));
   return (int)e;
 }

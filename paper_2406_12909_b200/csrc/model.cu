@@ -307,6 +307,20 @@ cudaError_t linear_bwd_data_t(const T* dY, int ldd, int M, const int* M_dev, int
   return launch_simt_gemm<T>(M, M_dev, K1 + K2, N, nullptr, 1, a, b, epi, s);
 }
 
+// U [rows][4H] (part-major columns p*H + c) -> Up [rows][4H] channel-major
+// (4c + p): the B operand of the fused backward-data + aggregation prep
+__global__ void k_permute_parts(const float* __restrict__ U, int rows, int H, int ldu,
+                                float* __restrict__ Up) {
+  pdl_entry();
+  const long long total = (long long)rows * 4 * H;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / (4 * H)), j = (int)(idx % (4 * H));
+    const int c = j >> 2, p = j & 3;
+    Up[idx] = U[(long long)r * ldu + p * H + c];
+  }
+}
+
 template <typename T>
 int wgrad_splits(int M, int N, int Kt) {
   return use_tc<T>() ? tc::splits_for(N, Kt, M) : choose_splits(N, Kt, M);
@@ -682,6 +696,33 @@ int gfm_force_bwd(const void* h, const void* P, int H, int n_nodes, const int* r
                               (const T*)c, (const T*)u, (const T*)df, (const T*)dh_energy,
                               (T*)grad_v, (T*)grad_c, (T*)grad_u, (T*)dz_out, workspace, flags,
                               (cudaStream_t)stream))
+}
+
+size_t gfm_layer_bwd_data_agg_workspace_bytes(int H) {
+  return sizeof(float) * (size_t)H * 4 * H + 256;
+}
+
+int gfm_layer_bwd_data_agg(const void* dz, int M, int H, const void* W, const void* U,
+                           const void* agg, const void* stat_mean, const int* rowptr, void* dh_in,
+                           void* G, void* coef, void* dmax, void* workspace, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!use_tc<float>() || H <= 0 || (H % 4) || !G || !coef || !dmax) {
+    set_error("gfm_layer_bwd_data_agg: needs the tensor-core engine, float32, H %% 4 == 0");
+    return GFM_EINVAL;
+  }
+  float* Up = (float*)workspace;
+  launch_k(k_permute_parts, grid_1d((long long)H * 4 * H), 256, 0, s, (const float*)U, H, H,
+           4 * H, Up);
+  RowsLd<float> a{(const float*)dz, H};
+  Cols2Ld<float> b{(const float*)W, H, H, Up, 4 * H, 4 * H};
+  tc::TcEpiAggPrep epi{(float*)dh_in, H, (float*)G, (float*)coef, (float*)dmax,
+                       (const float*)agg, (const float*)stat_mean, rowptr};
+  cudaError_t e = tc::launch(M, nullptr, 5 * H, H, nullptr, 1, tc_split3(), a, b, epi, s);
+  if (e != cudaSuccess) {
+    set_error("gfm_layer_bwd_data_agg: %s", cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
 }
 
 int gfm_force_bwd_edges(const void* h, const void* P, int H, int n_nodes, const int* rowptr,

@@ -1369,6 +1369,57 @@ __device__ __forceinline__ void TcEpiSplitCols::store4(int m, int n, float4 v, i
   split_cols4(*this, m, n, v, nv);
 }
 
+// Layer backward-data fused with the PNA aggregation-backward prep
+// (model.py:549-558 + 325-341): columns [0, H) are dh_in = dz W; columns
+// [H, 5H) are dz U with U's columns PERMUTED channel-major (4c + p, parts
+// sum | mean | max | std), so every 4-column store holds one channel's four
+// part gradients and the epilogue writes the gather's inputs directly:
+//   G = dsum + dmean / deg - coef * mean,  coef = dstd / (deg * std) (std > 0)
+//   dmax  (read by the argmax-routed gather)
+// -- the [N][4H] dagg never reaches memory and the prep pass disappears.
+struct TcEpiAggPrep {
+  float* dh;  // [M][H] (ld H)
+  int H;
+  float* G;
+  float* coef;
+  float* dmax;
+  const float* agg;    // [M][4H] forward output (std part at column 3H)
+  const float* smean;  // [M][H]
+  const int* rowptr;
+  __device__ void store4(int m, int n, float4 v, int nv, int) const {
+    if (n < H) {
+      const float x[4] = {v.x, v.y, v.z, v.w};
+      put4(dh + (long long)m * H + n, x, nv);
+      return;
+    }
+    const int c = (n - H) >> 2;
+    const int deg = __ldg(rowptr + m + 1) - __ldg(rowptr + m);
+    float g = v.x;
+    if (deg > 0) g += __fdiv_rn(v.y, (float)deg);
+    float cf = 0.f;
+    if (deg > 0) {
+      const float sd = __ldg(agg + (long long)m * 4 * H + 3 * H + c);
+      if (sd > 0.f) {
+        const float k = v.w / ((float)deg * sd);
+        g -= k * __ldg(smean + (long long)m * H + c);
+        cf = k;
+      }
+    }
+    const long long o = (long long)m * H + c;
+    G[o] = g;
+    coef[o] = cf;
+    dmax[o] = v.z;
+  }
+  __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv, int split) const {
+    if (!valid) return;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (4 * q < nv)
+        store4(m, n + 4 * q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]),
+               min(4, nv - 4 * q), split);
+  }
+};
+
 struct TcEpiPartial {  // split-K partial tile ws[split][m][n] (row-major, width N)
   float* ws;
   long long split_stride;

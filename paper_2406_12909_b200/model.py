@@ -18,6 +18,7 @@ call raises ``ExtensionMissingError``.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -845,21 +846,43 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     # message-passing layers (model.py:549-562)
     dz = dzl
     agg_ws = sc.bytes("agg_bwd_ws", query("gfm_agg_bwd_workspace_bytes", N, H, parts, code))
+    # PNA on the float32 tensor-core engine: backward-data GEMM + agg prep
+    # fused (opt-in GFM_FUSED_PREP=1: its per-element epilogue loads measured
+    # slower than the separate float4 prep pass, 70 vs 36 us per layer at C2)
+    fused_prep = (os.environ.get("GFM_FUSED_PREP") == "1" and dt == torch.float32
+                  and parts == 15 and H % 4 == 0 and N > 0
+                  and query("gfm_get_gemm_mode") != 0 and not flags & _lib.FLAG_SCALAR)
+    up_ws = sc.bytes("up_ws", query("gfm_layer_bwd_data_agg_workspace_bytes", H)) \
+        if fused_prep else None
     for l in range(cfg.mpnn_layers - 1, -1, -1):
         lay = cache["layers"][l]
         wgrad(dz, H, H, lay["h_in"], H, H, lay["agg"], K * H, K * H, gp.view(f"layer_{l}.w"),
               gp.view(f"layer_{l}.u"), gp.view(f"layer_{l}.b"), f"layer{l}")
         dh_in = sc.get("dh_in", (N, H), dt)
-        dagg = sc.get("dagg", (N, K * H), dt)
-        call("gfm_linear_bwd_data", ptr(dz), H, N, None, H, ptr(params.view(f"layer_{l}.w")), H, H,
-             ptr(params.view(f"layer_{l}.u")), K * H, K * H, ptr(dh_in), H, ptr(dagg), K * H, None,
-             0, code, s)
         out = sc.get(f"dz_l{l}", (N, H), dt)
-        call("gfm_agg_bwd", ptr(dagg), ptr(lay["agg"]), ptr(lay["smean"]), ptr(lay["argmax"]),
-             ptr(lay["h_in"]), ptr(batch.rowptr), ptr(batch.csc_ptr), ptr(batch.csc_eid),
-             ptr(batch.csc_dst), ptr(batch.edge_w), N, H, parts, ptr(dh_in),
-             ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
-             flags | _argmax_flag(batch), s)
+        if fused_prep:
+            # dh_in = dz W and the gather's inputs (G | coef in agg_ws, dmax)
+            # straight from the GEMM epilogue: no [N][4H] dagg, no prep pass
+            dmax = sc.get("dmax", (N, H), dt)
+            call("gfm_layer_bwd_data_agg", ptr(dz), N, H, ptr(params.view(f"layer_{l}.w")),
+                 ptr(params.view(f"layer_{l}.u")), ptr(lay["agg"]), ptr(lay["smean"]),
+                 ptr(batch.rowptr), ptr(dh_in), agg_ws.data_ptr(),
+                 agg_ws.data_ptr() + 4 * N * H, ptr(dmax), ptr(up_ws), s)
+            call("gfm_agg_bwd", ptr(dmax), ptr(lay["agg"]), ptr(lay["smean"]), ptr(lay["argmax"]),
+                 ptr(lay["h_in"]), ptr(batch.rowptr), ptr(batch.csc_ptr), ptr(batch.csc_eid),
+                 ptr(batch.csc_dst), ptr(batch.edge_w), N, H, parts, ptr(dh_in),
+                 ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
+                 flags | _argmax_flag(batch) | _lib.FLAG_AGG_PREPPED, s)
+        else:
+            dagg = sc.get("dagg", (N, K * H), dt)
+            call("gfm_linear_bwd_data", ptr(dz), H, N, None, H, ptr(params.view(f"layer_{l}.w")),
+                 H, H, ptr(params.view(f"layer_{l}.u")), K * H, K * H, ptr(dh_in), H, ptr(dagg),
+                 K * H, None, 0, code, s)
+            call("gfm_agg_bwd", ptr(dagg), ptr(lay["agg"]), ptr(lay["smean"]), ptr(lay["argmax"]),
+                 ptr(lay["h_in"]), ptr(batch.rowptr), ptr(batch.csc_ptr), ptr(batch.csc_eid),
+                 ptr(batch.csc_dst), ptr(batch.edge_w), N, H, parts, ptr(dh_in),
+                 ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
+                 flags | _argmax_flag(batch), s)
         dz = out
     # the batched reduction follows the weight-gradient GEMMs on the side
     # stream while the embedding gradient runs here; join before returning

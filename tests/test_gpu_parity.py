@@ -573,3 +573,49 @@ def test_deferred_batched_splitk_reduce_bitwise(dtype):
             else:
                 np.testing.assert_allclose(b.cpu().numpy(), a.cpu().numpy(), rtol=1e-12,
                                            atol=1e-12)
+
+
+@pytest.mark.parametrize("H", [64, 512])
+def test_fused_bwd_data_agg_prep_matches_unfused(H):
+    """gfm_layer_bwd_data_agg (GEMM epilogue writes G | coef | dmax) +
+    gfm_agg_bwd(GFM_FLAG_AGG_PREPPED) == gfm_linear_bwd_data + gfm_agg_bwd
+    (prep pass) for a PNA layer on the tensor-core engine."""
+    recs, b = _wide_batch(H, F32, 11)
+    N, parts, K = b.n_nodes, 15, 4
+    rg = np.random.default_rng(H + 3)
+    t = lambda *sh, sc=1.0: torch.as_tensor(rg.normal(size=sh) * sc, dtype=F32, device="cuda")
+    h = torch.tanh(t(N, H))
+    W, U = t(H, H, sc=H ** -0.5), t(H, 4 * H, sc=(4 * H) ** -0.5)
+    dz = t(N, H)
+    s = _lib.stream_handle()
+    agg = torch.empty(N, K * H, device="cuda")
+    am = torch.empty(N, H, dtype=torch.int32, device="cuda")
+    sm = torch.empty(N, H, device="cuda")
+    _lib.call("gfm_agg_fwd", _lib.ptr(h), N, H, _lib.ptr(b.rowptr), _lib.ptr(b.col_src),
+              _lib.ptr(b.edge_w), parts, _lib.ptr(agg), _lib.ptr(am), _lib.ptr(sm), _lib.F32, 0, s)
+    ws_b = _lib.query("gfm_agg_bwd_workspace_bytes", N, H, parts, _lib.F32)
+    outs = []
+    for fused in (False, True):
+        dh_in = torch.empty(N, H, device="cuda")
+        out = torch.empty(N, H, device="cuda")
+        ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+        if fused:
+            dmax = torch.empty(N, H, device="cuda")
+            up = torch.empty(_lib.query("gfm_layer_bwd_data_agg_workspace_bytes", H),
+                             dtype=torch.uint8, device="cuda")
+            _lib.call("gfm_layer_bwd_data_agg", _lib.ptr(dz), N, H, _lib.ptr(W), _lib.ptr(U),
+                      _lib.ptr(agg), _lib.ptr(sm), _lib.ptr(b.rowptr), _lib.ptr(dh_in),
+                      ws.data_ptr(), ws.data_ptr() + 4 * N * H, _lib.ptr(dmax), _lib.ptr(up), s)
+            src, fl = dmax, _lib.FLAG_AGG_PREPPED
+        else:
+            dagg = torch.empty(N, K * H, device="cuda")
+            _lib.call("gfm_linear_bwd_data", _lib.ptr(dz), H, N, None, H, _lib.ptr(W), H, H,
+                      _lib.ptr(U), K * H, K * H, _lib.ptr(dh_in), H, _lib.ptr(dagg), K * H, None,
+                      0, _lib.F32, s)
+            src, fl = dagg, 0
+        _lib.call("gfm_agg_bwd", _lib.ptr(src), _lib.ptr(agg), _lib.ptr(sm), _lib.ptr(am),
+                  _lib.ptr(h), _lib.ptr(b.rowptr), _lib.ptr(b.csc_ptr), _lib.ptr(b.csc_eid),
+                  _lib.ptr(b.csc_dst), _lib.ptr(b.edge_w), N, H, parts, _lib.ptr(dh_in),
+                  _lib.ptr(h), _lib.ptr(out), _lib.ptr(ws), _lib.F32, fl, s)
+        outs.append(out.cpu().numpy())
+    assert_close_scaled(outs[1], outs[0], 1e-5, FP32_FLOOR, what=f"H={H}")
