@@ -186,6 +186,11 @@ GFM_API int gfm_force_bwd_edges(const void* h, const void* P, int H, int n_nodes
                                 const void* V, const void* c, const void* u, const void* df,
                                 void* grad_v, void* grad_c, void* grad_u, void* workspace,
                                 int dtype, int flags, void* stream);
+/* with grad_v == NULL, gfm_force_bwd_edges runs the edge passes only and
+ * gfm_force_bwd_grads(…) then forms grad_V / grad_c / grad_u from the same
+ * workspace (any stream ordered after the edge passes) */
+GFM_API int gfm_force_bwd_grads(const void* h, int H, int n_nodes, void* grad_v, void* grad_c,
+                                void* grad_u, void* workspace, int dtype, void* stream);
 GFM_API int gfm_force_bwd_finish(const void* h, int H, int n_nodes, const void* V,
                                  const void* dh_energy, void* dz_out, void* workspace, int dtype,
                                  void* stream);

@@ -84,6 +84,7 @@ SIGNATURES = {
     "gfm_layer_bwd_data_agg": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "gfm_force_bwd_edges": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                  _P, _P, _P, _I, _I, _P]),
+    "gfm_force_bwd_grads": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),
     "gfm_force_bwd_finish": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),
     "gfm_energy_readout": (_I, [_P, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P]),
     "gfm_loss_workspace_bytes": (_S, []),

@@ -536,9 +536,11 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
                         const int* col_src, const T* dx, const int* csc_ptr, const int* csc_eid,
                         const int* csc_dst, const T* V, const T* c, const T* u, const T* df,
                         const T* dh_e, T* gV, T* gc, T* gu, T* dz_out, void* ws, int flags,
-                        cudaStream_t s, int stage = 3) {
-  // stage bit 1: edge passes + grad_V / grad_c / grad_u (S left in ws);
-  // stage bit 2: dz_out from S in ws (lets the caller overlap dh_energy)
+                        cudaStream_t s, int stage = 7) {
+  // stage bit 1: edge passes (S, D_dst, TU left in ws); bit 4: grad_V /
+  // grad_c / grad_u from ws; bit 2: dz_out from S in ws -- separable so the
+  // caller can overlap dh_energy and run the parameter gradients off the
+  // critical path
   const size_t nh = (size_t)(n > 0 ? n : 1) * H;
   T* Ddst = (T*)ws;
   T* TU = Ddst + nh;
@@ -547,10 +549,12 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
   T* wws = part + (size_t)ceil_div(n > 0 ? n : 1, 128) * H + 64;
   wws = (T*)(((uintptr_t)wws + 255) & ~(uintptr_t)255);
   cudaError_t e;
-  if (!(stage & 1)) goto finish;
-  e = force_bwd_edges<T>(P, n, H, rowptr, col_src, csc_ptr, csc_eid, csc_dst, dx, df, c, u, Ddst,
-                         TU, S, flags, s);
-  if (e != cudaSuccess) return e;
+  if (stage & 1) {
+    e = force_bwd_edges<T>(P, n, H, rowptr, col_src, csc_ptr, csc_eid, csc_dst, dx, df, c, u,
+                           Ddst, TU, S, flags, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (!(stage & 4)) goto finish;
   // grad_V = S^T h   (= sum_e dpre_e pair_e^T, model.py:543)
   e = linear_bwd_weight_t<T>(S, H, n, nullptr, H, h, H, H, nullptr, 0, 0, 0, gV, nullptr, nullptr,
                              wws, s);
@@ -730,12 +734,23 @@ int gfm_force_bwd_edges(const void* h, const void* P, int H, int n_nodes, const 
                         const int* csc_eid, const int* csc_dst, const void* V, const void* c,
                         const void* u, const void* df, void* grad_v, void* grad_c, void* grad_u,
                         void* workspace, int dtype, int flags, void* stream) {
+  // grad pointers NULL: edge passes only (then gfm_force_bwd_grads)
+  const int stage = grad_v ? 1 | 4 : 1;
   GFM_DISPATCH(dtype, "gfm_force_bwd_edges",
                force_bwd_t<T>((const T*)h, (const T*)P, H, n_nodes, rowptr, col_src,
                               (const T*)edge_dx, csc_ptr, csc_eid, csc_dst, (const T*)V,
                               (const T*)c, (const T*)u, (const T*)df, nullptr, (T*)grad_v,
                               (T*)grad_c, (T*)grad_u, nullptr, workspace, flags,
-                              (cudaStream_t)stream, 1))
+                              (cudaStream_t)stream, stage))
+}
+
+int gfm_force_bwd_grads(const void* h, int H, int n_nodes, void* grad_v, void* grad_c,
+                        void* grad_u, void* workspace, int dtype, void* stream) {
+  GFM_DISPATCH(dtype, "gfm_force_bwd_grads",
+               force_bwd_t<T>((const T*)h, nullptr, H, n_nodes, nullptr, nullptr, nullptr,
+                              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                              nullptr, (T*)grad_v, (T*)grad_c, (T*)grad_u, nullptr, workspace, 0,
+                              (cudaStream_t)stream, 4))
 }
 
 int gfm_force_bwd_finish(const void* h, int H, int n_nodes, const void* V, const void* dh_energy,

@@ -837,8 +837,13 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     call("gfm_force_bwd_edges", ptr(cache["h_final"]), ptr(cache["force_P"]), H, N,
          ptr(batch.rowptr), ptr(batch.col_src), ptr(batch.edge_dx), ptr(batch.csc_ptr),
          ptr(batch.csc_eid), ptr(batch.csc_dst), ptr(params.force_v), ptr(params.force_c),
-         ptr(params.force_u), ptr(df), ptr(gp.force_v), ptr(gp.force_c), ptr(gp.force_u),
-         ptr(ws), code, flags, s)
+         ptr(params.force_u), ptr(df), None, None, None, ptr(ws), code, flags, s)
+    # grad_V = S^T h, grad_c, grad_u: off the critical path on the side stream
+    edges_done = torch.cuda.Event()
+    edges_done.record(main)
+    side.wait_event(edges_done)
+    call("gfm_force_bwd_grads", ptr(cache["h_final"]), H, N, ptr(gp.force_v), ptr(gp.force_c),
+         ptr(gp.force_u), ptr(ws), code, ss)
     main.wait_event(head_done)
     call("gfm_force_bwd_finish", ptr(cache["h_final"]), H, N, ptr(params.force_v), ptr(dh_e),
          ptr(dzl), ptr(ws), code, s)
