@@ -1152,7 +1152,15 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
   return cudaGetLastError();
 }
 
-inline int pick_bn(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : 128; }
+inline int bn_cap() {  // GFM_TC_BN_MAX (32 / 64 / 128) caps the column tile (A/B runs)
+  static int v = -1;
+  if (v < 0) v = getenv("GFM_TC_BN_MAX") ? atoi(getenv("GFM_TC_BN_MAX")) : 128;
+  return v;
+}
+inline int pick_bn(int n) {
+  const int bn = n <= 32 ? 32 : n <= 64 ? 64 : 128;
+  return bn < bn_cap() ? bn : (bn_cap() >= 128 ? 128 : bn_cap() >= 64 ? 64 : 32);
+}
 
 // BN from N (32 / 64 / 128; N > 128 is tiled in 128-wide column tiles)
 template <class AL, class BL, class Epi>
