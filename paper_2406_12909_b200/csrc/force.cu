@@ -299,23 +299,24 @@ __global__ void __launch_bounds__(256)
     }
   };
   const int beg = rowptr[i], end = rowptr[i + 1];
-  if constexpr (LPN == 32) {
-    // 32-lane rows: lane k computes (src, dm) of edge c0 + k once; shuffles
-    // broadcast them; two P rows in flight per lane
-    for (int c0 = beg; c0 < end; c0 += 32) {
-      const int cnt = min(32, end - c0);
+  if constexpr (LPN >= 8) {
+    // lane k of the node's group computes (src, dm) of edge c0 + k once;
+    // group shuffles broadcast them; two P rows in flight per lane
+    const unsigned gm = LPN == 32 ? 0xffffffffu : (((1u << LPN) - 1u) << (lane - sub));
+    for (int c0 = beg; c0 < end; c0 += LPN) {
+      const int cnt = min(LPN, end - c0);
       int my_s = 0;
       float my_dm = 0.f;
-      if (lane < cnt) {
-        my_s = __ldg(col_src + c0 + lane);
-        my_dm = dm_of(c0 + lane);
+      if (sub < cnt) {
+        my_s = __ldg(col_src + c0 + sub);
+        my_dm = dm_of(c0 + sub);
       }
       for (int e = 0; e < cnt; e += 2) {
         const bool two = e + 1 < cnt;
-        const int s0 = __shfl_sync(0xffffffffu, my_s, e);
-        const float d0 = __shfl_sync(0xffffffffu, my_dm, e);
-        const int s1 = __shfl_sync(0xffffffffu, my_s, two ? e + 1 : e);
-        const float d1 = __shfl_sync(0xffffffffu, my_dm, two ? e + 1 : e);
+        const int s0 = __shfl_sync(gm, my_s, e, LPN);
+        const float d0 = __shfl_sync(gm, my_dm, e, LPN);
+        const int s1 = __shfl_sync(gm, my_s, two ? e + 1 : e, LPN);
+        const float d1 = __shfl_sync(gm, my_dm, two ? e + 1 : e, LPN);
         float4 r0[NV], r1[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
@@ -382,23 +383,24 @@ __global__ void __launch_bounds__(256)
     }
   };
   const int qb = csc_ptr[j], qe = csc_ptr[j + 1];
-  if constexpr (LPN == 32) {
-    // lane k computes (dst, dm) of CSC slot c0 + k once; shuffles broadcast
-    for (int c0 = qb; c0 < qe; c0 += 32) {
-      const int cnt = min(32, qe - c0);
+  if constexpr (LPN >= 8) {
+    // lane k of the node's group computes (dst, dm) of CSC slot c0 + k once
+    const unsigned gm = LPN == 32 ? 0xffffffffu : (((1u << LPN) - 1u) << (lane - sub));
+    for (int c0 = qb; c0 < qe; c0 += LPN) {
+      const int cnt = min(LPN, qe - c0);
       int my_i = 0;
       float my_dm = 0.f;
-      if (lane < cnt) {
-        const int p = __ldg(csc_eid + c0 + lane);
-        my_i = __ldg(csc_dst + c0 + lane);
+      if (sub < cnt) {
+        const int p = __ldg(csc_eid + c0 + sub);
+        my_i = __ldg(csc_dst + c0 + sub);
         my_dm = dm_of(p, my_i);
       }
       for (int e = 0; e < cnt; e += 2) {
         const bool two = e + 1 < cnt;
-        const int i0 = __shfl_sync(0xffffffffu, my_i, e);
-        const float d0 = __shfl_sync(0xffffffffu, my_dm, e);
-        const int i1 = __shfl_sync(0xffffffffu, my_i, two ? e + 1 : e);
-        const float d1 = __shfl_sync(0xffffffffu, my_dm, two ? e + 1 : e);
+        const int i0 = __shfl_sync(gm, my_i, e, LPN);
+        const float d0 = __shfl_sync(gm, my_dm, e, LPN);
+        const int i1 = __shfl_sync(gm, my_i, two ? e + 1 : e, LPN);
+        const float d1 = __shfl_sync(gm, my_dm, two ? e + 1 : e, LPN);
         float4 r0[NV], r1[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
