@@ -59,6 +59,15 @@ __device__ __forceinline__ float group_sum(float v) {
   return v;
 }
 
+template <int LPN>
+__device__ __forceinline__ double group_sum_d(double v) {
+  const int lane = threadIdx.x & 31;
+  const unsigned mask = LPN == 32 ? 0xffffffffu : (((1u << LPN) - 1u) << (lane / LPN * LPN));
+#pragma unroll
+  for (int o = LPN / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, LPN);
+  return v;
+}
+
 // c / u are views into the flat parameter vector: not 16-byte aligned
 __device__ __forceinline__ float4 ld4u(const float* p, int c4) {
   return make_float4(__ldg(p + 4 * c4), __ldg(p + 4 * c4 + 1), __ldg(p + 4 * c4 + 2),
@@ -119,9 +128,10 @@ __global__ void __launch_bounds__(256)
       d0 += th<FAST>(x0.x) * uu[v].x + th<FAST>(x0.y) * uu[v].y + th<FAST>(x0.z) * uu[v].z + th<FAST>(x0.w) * uu[v].w;
       d1 += th<FAST>(x1.x) * uu[v].x + th<FAST>(x1.y) * uu[v].y + th<FAST>(x1.z) * uu[v].z + th<FAST>(x1.w) * uu[v].w;
     }
-    const float m0 = group_sum<LPN>(d0), m1 = group_sum<LPN>(d1);
-    fx += (double)m0 * dx[3LL * p + 0]; fy += (double)m0 * dx[3LL * p + 1]; fz += (double)m0 * dx[3LL * p + 2];
-    fx += (double)m1 * dx[3LL * p + 3]; fy += (double)m1 * dx[3LL * p + 4]; fz += (double)m1 * dx[3LL * p + 5];
+    // f = sum_e m_e dx_e = sum_lanes sum_e d_lane(e) dx_e: each lane keeps
+    // its partial force, one group reduction per node (not per edge)
+    fx += (double)d0 * dx[3LL * p + 0]; fy += (double)d0 * dx[3LL * p + 1]; fz += (double)d0 * dx[3LL * p + 2];
+    fx += (double)d1 * dx[3LL * p + 3]; fy += (double)d1 * dx[3LL * p + 4]; fz += (double)d1 * dx[3LL * p + 5];
   }
   for (; p < end; ++p) {
     const int s0 = __ldg(col_src + p);
@@ -131,9 +141,11 @@ __global__ void __launch_bounds__(256)
       const float4 x0 = f4add3(pi[v], __ldg(P4 + (long long)s0 * H4 + v * LPN + sub), cu[v]);
       d0 += th<FAST>(x0.x) * uu[v].x + th<FAST>(x0.y) * uu[v].y + th<FAST>(x0.z) * uu[v].z + th<FAST>(x0.w) * uu[v].w;
     }
-    const float m0 = group_sum<LPN>(d0);
-    fx += (double)m0 * dx[3LL * p + 0]; fy += (double)m0 * dx[3LL * p + 1]; fz += (double)m0 * dx[3LL * p + 2];
+    fx += (double)d0 * dx[3LL * p + 0]; fy += (double)d0 * dx[3LL * p + 1]; fz += (double)d0 * dx[3LL * p + 2];
   }
+  fx = group_sum_d<LPN>(fx);
+  fy = group_sum_d<LPN>(fy);
+  fz = group_sum_d<LPN>(fz);
   if (sub == 0) {
     f[3LL * i + 0] = (float)fx;
     f[3LL * i + 1] = (float)fy;
