@@ -26,6 +26,9 @@
 
 #include "common.cuh"
 
+#ifndef GFM_AGG_BWD_U
+#define GFM_AGG_BWD_U 2
+#endif
 #ifndef GFM_AGG_FWD_UF
 #define GFM_AGG_FWD_UF 4
 #endif
@@ -559,7 +562,7 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
     // accumulation, so U x 3 gathers per lane are in flight.  Narrow rows
     // (LPN < 32: several nodes per warp) are issue-bound rather than latency-
     // bound and measure faster unbatched.
-    constexpr int U = LPN == 32 ? 2 : 1;
+    constexpr int U = LPN == 32 ? GFM_AGG_BWD_U : 1;
     // the node's LPN lanes load LPN CSC slots (eid, dst, w[eid]) at once and
     // broadcast them with shuffles
     const int gl = (threadIdx.x & 31) % LPN;
