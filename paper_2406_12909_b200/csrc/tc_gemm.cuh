@@ -32,12 +32,21 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
 
 namespace gfm {
 namespace tc {
+
+// epilogues may define prefetch(m, n) -> state and store4(m, n, v, nv, split,
+// state): the kernel then issues the four rows' prefetches of a chunk before
+// any of their stores (their global loads overlap instead of serialising)
+template <class E, class = void>
+struct HasPrefetch : std::false_type {};
+template <class E>
+struct HasPrefetch<E, std::void_t<decltype(&E::prefetch)>> : std::true_type {};
 
 // GFM_NO_TMA=1 forces the thread-staged (cp.async) engine (debug / A-B runs)
 inline bool tma_disabled() {
@@ -1086,14 +1095,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           *reinterpret_cast<float4*>(stg + lane * 20 + 4 * q) =
               make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         __syncwarp();
+        if constexpr (HasPrefetch<Epi>::value) {
+          decltype(epi.prefetch(0, 0)) pre[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = 8 * j + (lane >> 2), q = lane & 3;
-          const int col = n0 + c + 4 * q;
-          const int rr = quarter * 32 + r;
-          if (rr < m_lim && col < N)
-            epi.store4(m0 + rr, col, *reinterpret_cast<const float4*>(stg + r * 20 + 4 * q),
-                       min(4, N - col), split);
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), q = lane & 3;
+            const int col = n0 + c + 4 * q;
+            const int rr = quarter * 32 + r;
+            if (rr < m_lim && col < N) pre[j] = epi.prefetch(m0 + rr, col);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), q = lane & 3;
+            const int col = n0 + c + 4 * q;
+            const int rr = quarter * 32 + r;
+            if (rr < m_lim && col < N)
+              epi.store4(m0 + rr, col, *reinterpret_cast<const float4*>(stg + r * 20 + 4 * q),
+                         min(4, N - col), split, pre[j]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), q = lane & 3;
+            const int col = n0 + c + 4 * q;
+            const int rr = quarter * 32 + r;
+            if (rr < m_lim && col < N)
+              epi.store4(m0 + rr, col, *reinterpret_cast<const float4*>(stg + r * 20 + 4 * q),
+                         min(4, N - col), split);
+          }
         }
         __syncwarp();
       }
@@ -1394,29 +1423,42 @@ struct TcEpiAggPrep {
   const float* agg;    // [M][4H] forward output (std part at column 3H)
   const float* smean;  // [M][H]
   const int* rowptr;
-  __device__ void store4(int m, int n, float4 v, int nv, int) const {
+  struct Pre {
+    int deg;
+    float sd, mu;
+  };
+  __device__ Pre prefetch(int m, int n) const {
+    Pre p{0, 0.f, 0.f};
+    if (n >= H) {
+      const int c = (n - H) >> 2;
+      p.deg = __ldg(rowptr + m + 1) - __ldg(rowptr + m);
+      p.sd = __ldg(agg + (long long)m * 4 * H + 3 * H + c);
+      p.mu = __ldg(smean + (long long)m * H + c);
+    }
+    return p;
+  }
+  __device__ void store4(int m, int n, float4 v, int nv, int, const Pre& p) const {
     if (n < H) {
       const float x[4] = {v.x, v.y, v.z, v.w};
       put4(dh + (long long)m * H + n, x, nv);
       return;
     }
     const int c = (n - H) >> 2;
-    const int deg = __ldg(rowptr + m + 1) - __ldg(rowptr + m);
     float g = v.x;
-    if (deg > 0) g += __fdiv_rn(v.y, (float)deg);
+    if (p.deg > 0) g += __fdiv_rn(v.y, (float)p.deg);
     float cf = 0.f;
-    if (deg > 0) {
-      const float sd = __ldg(agg + (long long)m * 4 * H + 3 * H + c);
-      if (sd > 0.f) {
-        const float k = v.w / ((float)deg * sd);
-        g -= k * __ldg(smean + (long long)m * H + c);
-        cf = k;
-      }
+    if (p.deg > 0 && p.sd > 0.f) {
+      const float k = v.w / ((float)p.deg * p.sd);
+      g -= k * p.mu;
+      cf = k;
     }
     const long long o = (long long)m * H + c;
     G[o] = g;
     coef[o] = cf;
     dmax[o] = v.z;
+  }
+  __device__ void store4(int m, int n, float4 v, int nv, int split) const {
+    store4(m, n, v, nv, split, prefetch(m, n));
   }
   __device__ void chunk(int m, bool valid, int n, const float (&v)[16], int nv, int split) const {
     if (!valid) return;

@@ -852,8 +852,9 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     dz = dzl
     agg_ws = sc.bytes("agg_bwd_ws", query("gfm_agg_bwd_workspace_bytes", N, H, parts, code))
     # PNA on the float32 tensor-core engine: backward-data GEMM + agg prep
-    # fused (opt-in GFM_FUSED_PREP=1: its per-element epilogue loads measured
-    # slower than the separate float4 prep pass, 70 vs 36 us per layer at C2)
+    # fused (opt-in GFM_FUSED_PREP=1: even with its loads prefetched per chunk
+    # the epilogue measured 6% slower end to end at C2 than the separate
+    # float4 prep pass)
     fused_prep = (os.environ.get("GFM_FUSED_PREP") == "1" and dt == torch.float32
                   and parts == 15 and H % 4 == 0 and N > 0
                   and query("gfm_get_gemm_mode") != 0 and not flags & _lib.FLAG_SCALAR)
