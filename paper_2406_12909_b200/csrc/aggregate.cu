@@ -835,6 +835,11 @@ static bool vec_shape(int H, int& nv, int& lpn, int* slabs = nullptr, bool wide2
 // The shared-memory staged tiles are opt-in (GFM_AGG_TILE=1): measured on
 // B200 they lose to the register gathers at C2 and C3 (the gathers are
 // issue-bound, not L2-bound, and staging adds a serial phase per block).
+static int tile_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 static bool no_tile() {
   const char* e = getenv("GFM_AGG_TILE");
   return !(e && e[0] == '1');
@@ -847,7 +852,8 @@ cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, c
   int nv = 0, lpn = 0, slabs = 1;
   if (dtype == GFM_F32 && !force_scalar && !am_u8 && H % 64 == 0 && !no_tile()) {
     // staged tiles: 16-lane (64-column) slabs, 128 dst nodes, <= 384 rows
-    constexpr int kLpn = 16, kNb = 128, kCap = 384;
+    constexpr int kLpn = 16;
+    const int kNb = tile_env("GFM_AGG_TILE_NB", 128), kCap = tile_env("GFM_AGG_TILE_CAP", 384);
     const size_t smem = (size_t)kCap * kLpn * sizeof(float4);
     cudaFuncSetAttribute(k_agg_fwd_tile<kLpn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
@@ -933,7 +939,8 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
   if (dtype == GFM_F32 && !force_scalar && !am_u8 && H % 32 == 0 && g_ok && ld % 4 == 0 &&
       !no_tile()) {
     // staged tiles: 8-lane (32-column) slabs, 64 CSC nodes, <= 256 dst rows
-    constexpr int kLpn = 8, kNb = 64, kCap = 256;
+    constexpr int kLpn = 8;
+    const int kNb = tile_env("GFM_AGG_TILE_NB", 64), kCap = tile_env("GFM_AGG_TILE_CAP", 256);
     const size_t smem = 3 * (size_t)kCap * kLpn * sizeof(float4);
     cudaFuncSetAttribute(k_agg_bwd_tile<kLpn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
