@@ -110,3 +110,24 @@ def test_early_stopper_eleven():
         if st.update(v):
             break
     assert epochs == 11
+
+
+def test_bench_reference_arm_json_contract():
+    """`bench.py --impl reference` (the CPU oracle port on host cores) prints
+    one JSON line with the contract's keys."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "0", "--cpu-sample-s", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "graphs/s"
+    assert line["value"] > 0 and line["higher_is_better"] is True
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    for k in ("metric", "n_gpus", "steps", "warmup", "scaling", "dtype", "data", "config"):
+        assert k in line
