@@ -262,6 +262,13 @@ GFM_API int gfm_adam_step(const void* grad_sum, int grad_dtype, long long n, dou
  * Adam without host involvement */
 GFM_API int gfm_adam_advance(long long* step, double beta1, double beta2, double* bias_corr,
                              const int* skip_flag, void* stream);
+/* gfm_nonfinite_flag + gfm_adam_advance in one launch: flag points at TWO
+ * ints (flag[0] the non-finite flag, flag[1] a completion ticket that must
+ * start at 0 and is left at 0); step / bias_corr are advanced after the
+ * whole scan unless flag[0] is set (step == NULL: guard only) */
+GFM_API int gfm_nonfinite_advance(const void* v, long long n, int dtype, int* flag,
+                                  long long* step, double beta1, double beta2, double* bias_corr,
+                                  void* stream);
 GFM_API int gfm_sgd_step(const void* grad_sum, int grad_dtype, long long n, double world, double* master,
                  double lr, const int* skip_flag, float* params32, void* stream);
 GFM_API int gfm_cast_f64_to_f32(const double* in, long long n, float* out, void* stream);

@@ -95,6 +95,7 @@ SIGNATURES = {
     "gfm_nonfinite_flag": (_I, [_P, _L, _I, _P, _P]),
     "gfm_adam_step": (_I, [_P, _I, _L, _D, _P, _P, _P, _P, _D, _D, _D, _D, _P, _P, _P]),
     "gfm_adam_advance": (_I, [_P, _D, _D, _P, _P, _P]),
+    "gfm_nonfinite_advance": (_I, [_P, _L, _I, _P, _P, _D, _D, _P, _P]),
     "gfm_sgd_step": (_I, [_P, _I, _L, _D, _P, _D, _P, _P, _P]),
     "gfm_cast_f64_to_f32": (_I, [_P, _L, _P, _P]),
 }

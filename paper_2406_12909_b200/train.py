@@ -194,7 +194,7 @@ class DataParallelTrainer:
         self.v = torch.zeros_like(self.master)
         self.t_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.bc = torch.zeros(2, dtype=torch.float64, device=self.device)
-        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.flag = torch.zeros(2, dtype=torch.int32, device=self.device)  # [non-finite, ticket]
         self.contrib = torch.zeros(P + 2, dtype=dtype, device=self.device)
         if dtype == torch.float32:
             self.work = torch.empty(P, dtype=torch.float32, device=self.device)
@@ -225,12 +225,14 @@ class DataParallelTrainer:
         s = stream_handle()
         self.comm.allreduce_sum_(self.contrib)
         code = _lib.dtype_code(self.dtype)
-        call("gfm_nonfinite_flag", ptr(self.contrib), P + 1, code, ptr(self.flag), s)
+        adam = self.tcfg.optimizer == "adam"
+        # train.py:262-274 guard, fused with Adam's device step counter
+        call("gfm_nonfinite_advance", ptr(self.contrib), P + 1, code, ptr(self.flag),
+             ptr(self.t_dev) if adam else None, float(self.tcfg.beta1), float(self.tcfg.beta2),
+             ptr(self.bc), s)
         out32 = self.work if self.dtype == torch.float32 else None
         world = float(self.comm.size)
-        if self.tcfg.optimizer == "adam":
-            call("gfm_adam_advance", ptr(self.t_dev), float(self.tcfg.beta1),
-                 float(self.tcfg.beta2), ptr(self.bc), ptr(self.flag), s)
+        if adam:
             call("gfm_adam_step", ptr(self.contrib), code, P, world, ptr(self.master), ptr(self.m),
                  ptr(self.v), ptr(self.bc), float(self.tcfg.learning_rate),
                  float(self.tcfg.beta1), float(self.tcfg.beta2), float(self.tcfg.eps),
@@ -247,7 +249,7 @@ class DataParallelTrainer:
 
     @property
     def nan_event(self) -> bool:
-        return bool(self.flag.item())
+        return bool(self.flag[0].item())
 
     def current_params(self) -> ModelParams:
         return ModelParams(self.cfg, self.master.clone())

@@ -495,6 +495,27 @@ def test_trainer_nan_guard_discards_update():
     assert torch.equal(tr.master, before)
 
 
+def test_guard_advance_ticket_counts_each_step_once():
+    """gfm_nonfinite_advance: the last block advances t / bias_corr once per
+    step (multi-block grid), leaves the ticket at 0, and freezes both once
+    the non-finite flag is set."""
+    recs = O.synthetic(4, rc=2.5, seed=1)
+    cfg = cfg_of("pna-agg", 2, 64, 2, 32)
+    tr = T.DataParallelTrainer(cfg, T.TrainConfig(), dtype=F32)
+    assert tr.P > 256 * 4  # several blocks race for the ticket
+    b = M.make_batch(as_records(recs), dtype=F32)
+    for k in range(1, 4):
+        tr.step(b)
+        torch.cuda.synchronize()
+        assert int(tr.t_dev.item()) == k
+        assert int(tr.flag[1].item()) == 0
+        np.testing.assert_allclose(tr.bc.cpu().numpy(), [1.0 - 0.9 ** k, 1.0 - 0.999 ** k],
+                                   rtol=1e-14)
+    b.energy_true = np.full(4, np.nan)
+    tr.step(b)
+    assert tr.nan_event and int(tr.t_dev.item()) == 3 and int(tr.flag[1].item()) == 0
+
+
 @pytest.mark.parametrize("use_graph", [False, True])
 def test_runner_pipelined_step_matches_blocking_step(use_graph):
     """StructureStepRunner.step_pipelined (loss read one call later) produces
