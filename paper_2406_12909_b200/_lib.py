@@ -15,7 +15,8 @@ import threading
 from .errors import GFMError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgfm_b200.so")
+# GFM_LIB_PATH: an alternative in-tree build of the same library (A/B runs)
+LIB_PATH = os.environ.get("GFM_LIB_PATH") or os.path.join(_HERE, "_lib", "libgfm_b200.so")
 
 F32, F64 = 0, 1
 PART_SUM, PART_MEAN, PART_MAX, PART_STD = 1, 2, 4, 8

@@ -882,7 +882,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     tc_gemm_tma_kernel(int M, const int* __restrict__ M_dev, int N, int K, int k_chunk, int splits,
                        int split3, const __grid_constant__ TmaOp ta,
                        const __grid_constant__ TmaOp tb, Epi epi) {
-  pdl_entry();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = SmemT<BN, AT != 0>;
   // TMEM: two BN-column accumulators, then (AT) kL A slots of 32 hi + 32 lo columns
@@ -901,15 +900,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   uint64_t* tempty = tfull + 2;  // accumulator drained [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int m_total = M_dev ? *M_dev : M;
-  const int m_tiles = (m_total + kBM - 1) / kBM;
-  const int n_tiles = (N + BN - 1) / BN;
-  const int n_work = m_tiles * n_tiles * splits;
-  if ((int)blockIdx.x >= n_work) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool split_on = split3 != 0;
   constexpr int kMmaWarp = 1 + kConvWarps;
 
+  // prologue (barriers, descriptor prefetch, TMEM) touches no predecessor
+  // output, so it runs before the programmatic-dependency wait
   if (threadIdx.x == 0) {
     for (int q = 0; q < kR; ++q) {
       mbar_init(&tfl[q], 1);
@@ -932,6 +928,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_entry();
+
+  const int m_total = M_dev ? *M_dev : M;
+  const int m_tiles = (m_total + kBM - 1) / kBM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int n_work = m_tiles * n_tiles * splits;
+  if ((int)blockIdx.x >= n_work) {
+    if (warp == 0) tmem_free<NC>(tmem);
+    return;
+  }
 
   auto tile_of = [&](int w, int& bm, int& bn, int& split) {
     split = w / (m_tiles * n_tiles);
