@@ -382,11 +382,21 @@ def run_native(args):
     except Exception:
         pass
 
+    # L2-resident read throughput measured on a B200 by tools/l2_bw.cu: the
+    # per-edge row gathers are L2 hits, so this is the ceiling they approach
+    l2 = {}
+    try:
+        l2 = json.load(open(os.path.join(ROOT, "profiles", "r01_l2_bw.json")))
+    except Exception:
+        pass
+
     def roof(kernel, nbytes, ms_, key):
         ach = nbytes / (ms_ / 1e3) / 1e9
+        l2p = l2.get("l2_read_gbs")
         return dict(kernel=kernel, bound="hbm", achieved=ach, peak=peak, unit="GB/s",
                     frac=ach / peak, traffic=traffic.get(key), launch_ms=ms_,
-                    algorithmic_bytes=nbytes,
+                    algorithmic_bytes=nbytes, l2_peak=l2p, l2_frac=ach / l2p if l2p else None,
+                    l2_peak_source="profiles/r01_l2_bw.json (tools/l2_bw.cu)" if l2p else None,
                     peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                     note=("algorithmic bytes per SURVEY 8(d) count every per-edge row gather; "
                           "those are mostly L2 hits, so frac can exceed 1 -- traffic is the "

@@ -84,6 +84,18 @@ __device__ __forceinline__ float th(float x) {
     return tanhf(x);
 }
 
+template <bool FAST>
+__device__ __forceinline__ float4 th4(float4 x) {
+  if constexpr (FAST)
+    return tanh4_fast(x);
+  else
+    return make_float4(tanhf(x.x), tanhf(x.y), tanhf(x.z), tanhf(x.w));
+}
+
+__device__ __forceinline__ float dot4(float4 t, float4 u) {
+  return t.x * u.x + t.y * u.y + t.z * u.z + t.w * u.w;
+}
+
 __device__ __forceinline__ float4 f4add3(float4 a, float4 b, float4 c) {
   return make_float4(a.x + b.x + c.x, a.y + b.y + c.y, a.z + b.z + c.z, a.w + b.w + c.w);
 }
@@ -110,6 +122,10 @@ __global__ void __launch_bounds__(256)
     cu[v] = ld4u(c, c4);
     uu[v] = ld4u(u, c4);
   }
+  // f = sum_e m_e dx_e = sum_lanes sum_e d_lane(e) dx_e: each lane keeps its
+  // partial force in fp64 (one fp32 rounding per edge pair, then one
+  // fp32 -> fp64 conversion per pair and component: the conversions share
+  // the SFU pipe with the tanh), one group reduction per node
   double fx = 0.0, fy = 0.0, fz = 0.0;
   const int beg = rowptr[i], end = rowptr[i + 1];
   int p = beg;
@@ -124,24 +140,22 @@ __global__ void __launch_bounds__(256)
     float d0 = 0.f, d1 = 0.f;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const float4 x0 = f4add3(pi[v], r0[v], cu[v]), x1 = f4add3(pi[v], r1[v], cu[v]);
-      d0 += th<FAST>(x0.x) * uu[v].x + th<FAST>(x0.y) * uu[v].y + th<FAST>(x0.z) * uu[v].z + th<FAST>(x0.w) * uu[v].w;
-      d1 += th<FAST>(x1.x) * uu[v].x + th<FAST>(x1.y) * uu[v].y + th<FAST>(x1.z) * uu[v].z + th<FAST>(x1.w) * uu[v].w;
+      d0 += dot4(th4<FAST>(f4add3(pi[v], r0[v], cu[v])), uu[v]);
+      d1 += dot4(th4<FAST>(f4add3(pi[v], r1[v], cu[v])), uu[v]);
     }
-    // f = sum_e m_e dx_e = sum_lanes sum_e d_lane(e) dx_e: each lane keeps
-    // its partial force, one group reduction per node (not per edge)
-    fx += (double)d0 * dx[3LL * p + 0]; fy += (double)d0 * dx[3LL * p + 1]; fz += (double)d0 * dx[3LL * p + 2];
-    fx += (double)d1 * dx[3LL * p + 3]; fy += (double)d1 * dx[3LL * p + 4]; fz += (double)d1 * dx[3LL * p + 5];
+    fx += (double)fmaf(d1, dx[3LL * p + 3], d0 * dx[3LL * p + 0]);
+    fy += (double)fmaf(d1, dx[3LL * p + 4], d0 * dx[3LL * p + 1]);
+    fz += (double)fmaf(d1, dx[3LL * p + 5], d0 * dx[3LL * p + 2]);
   }
   for (; p < end; ++p) {
     const int s0 = __ldg(col_src + p);
     float d0 = 0.f;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const float4 x0 = f4add3(pi[v], __ldg(P4 + (long long)s0 * H4 + v * LPN + sub), cu[v]);
-      d0 += th<FAST>(x0.x) * uu[v].x + th<FAST>(x0.y) * uu[v].y + th<FAST>(x0.z) * uu[v].z + th<FAST>(x0.w) * uu[v].w;
-    }
-    fx += (double)d0 * dx[3LL * p + 0]; fy += (double)d0 * dx[3LL * p + 1]; fz += (double)d0 * dx[3LL * p + 2];
+    for (int v = 0; v < NV; ++v)
+      d0 += dot4(th4<FAST>(f4add3(pi[v], __ldg(P4 + (long long)s0 * H4 + v * LPN + sub), cu[v])), uu[v]);
+    fx += (double)(d0 * dx[3LL * p + 0]);
+    fy += (double)(d0 * dx[3LL * p + 1]);
+    fz += (double)(d0 * dx[3LL * p + 2]);
   }
   fx = group_sum_d<LPN>(fx);
   fy = group_sum_d<LPN>(fy);
@@ -199,8 +213,8 @@ __global__ void __launch_bounds__(256)
       const float4 ra = __ldg(P4 + (long long)sa * H4 + c4);
       const float4 rb = __ldg(P4 + (long long)sb * H4 + c4);
       const float4 xa = f4add3(pi, ra, cu), xb = f4add3(pi, rb, cu);
-      float da = th<FAST>(xa.x) * uu.x + th<FAST>(xa.y) * uu.y + th<FAST>(xa.z) * uu.z + th<FAST>(xa.w) * uu.w;
-      float db = th<FAST>(xb.x) * uu.x + th<FAST>(xb.y) * uu.y + th<FAST>(xb.z) * uu.z + th<FAST>(xb.w) * uu.w;
+      float da = dot4(th4<FAST>(xa), uu);
+      float db = dot4(th4<FAST>(xb), uu);
       da = group_sum<32>(da);
       db = group_sum<32>(db);
       if (lane == 0) {
@@ -268,6 +282,10 @@ __global__ void k_force_fwd_warp(const T* __restrict__ P, int n, int H, const in
 }
 
 // ------------------------------------------------------------------ backward
+#ifndef GFM_FORCE_BWD_U
+#define GFM_FORCE_BWD_U 4
+#endif
+constexpr int kFU = GFM_FORCE_BWD_U;
 // pass 1 (dst rows): D_dst[i] = sum dpre_e, TU[i] = sum t_e dm_e
 template <int NV, int LPN, bool FAST>
 __global__ void __launch_bounds__(256)
@@ -323,20 +341,23 @@ __global__ void __launch_bounds__(256)
         my_s = __ldg(col_src + c0 + sub);
         my_dm = dm_of(c0 + sub);
       }
-      for (int e = 0; e < cnt; e += 2) {
-        const bool two = e + 1 < cnt;
-        const int s0 = __shfl_sync(gm, my_s, e, LPN);
-        const float d0 = __shfl_sync(gm, my_dm, e, LPN);
-        const int s1 = __shfl_sync(gm, my_s, two ? e + 1 : e, LPN);
-        const float d1 = __shfl_sync(gm, my_dm, two ? e + 1 : e, LPN);
-        float4 r0[NV], r1[NV];
+      for (int e = 0; e < cnt; e += kFU) {  // kFU P rows in flight per lane
+        int s[kFU];
+        float d[kFU];
+        float4 r[kFU][NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          r0[v] = __ldg(P4 + (long long)s0 * H4 + v * LPN + cb);
-          r1[v] = __ldg(P4 + (long long)s1 * H4 + v * LPN + cb);
+        for (int q = 0; q < kFU; ++q) {
+          const int src = e + q < cnt ? e + q : e;
+          s[q] = __shfl_sync(gm, my_s, src, LPN);
+          d[q] = __shfl_sync(gm, my_dm, src, LPN);
         }
-        edge(r0, d0);
-        if (two) edge(r1, d1);
+#pragma unroll
+        for (int q = 0; q < kFU; ++q)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) r[q][v] = __ldg(P4 + (long long)s[q] * H4 + v * LPN + cb);
+#pragma unroll
+        for (int q = 0; q < kFU; ++q)
+          if (e + q < cnt) edge(r[q], d[q]);
       }
     }
   } else {
@@ -407,20 +428,23 @@ __global__ void __launch_bounds__(256)
         my_i = __ldg(csc_dst + c0 + sub);
         my_dm = dm_of(p, my_i);
       }
-      for (int e = 0; e < cnt; e += 2) {
-        const bool two = e + 1 < cnt;
-        const int i0 = __shfl_sync(gm, my_i, e, LPN);
-        const float d0 = __shfl_sync(gm, my_dm, e, LPN);
-        const int i1 = __shfl_sync(gm, my_i, two ? e + 1 : e, LPN);
-        const float d1 = __shfl_sync(gm, my_dm, two ? e + 1 : e, LPN);
-        float4 r0[NV], r1[NV];
+      for (int e = 0; e < cnt; e += kFU) {  // kFU P rows in flight per lane
+        int i[kFU];
+        float d[kFU];
+        float4 r[kFU][NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          r0[v] = __ldg(P4 + (long long)i0 * H4 + v * LPN + cb);
-          r1[v] = __ldg(P4 + (long long)i1 * H4 + v * LPN + cb);
+        for (int q = 0; q < kFU; ++q) {
+          const int src = e + q < cnt ? e + q : e;
+          i[q] = __shfl_sync(gm, my_i, src, LPN);
+          d[q] = __shfl_sync(gm, my_dm, src, LPN);
         }
-        edge(r0, d0);
-        if (two) edge(r1, d1);
+#pragma unroll
+        for (int q = 0; q < kFU; ++q)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) r[q][v] = __ldg(P4 + (long long)i[q] * H4 + v * LPN + cb);
+#pragma unroll
+        for (int q = 0; q < kFU; ++q)
+          if (e + q < cnt) edge(r[q], d[q]);
       }
     }
   } else {
