@@ -314,8 +314,17 @@ __device__ __forceinline__ void agg_fwd_node(Ld ld, int node, int cb, int H,
   }
 }
 
+// resident 256-thread CTAs per SM the register allocation must allow: the
+// gather kernels are latency bound (long-scoreboard stalls, L2 far from its
+// throughput cap), so more warps in flight is the lever
+#ifndef GFM_AGG_FWD_MINB
+#define GFM_AGG_FWD_MINB 4
+#endif
+#ifndef GFM_AGG_BWD_MINB
+#define GFM_AGG_BWD_MINB 5
+#endif
 template <int NV, int LPN, bool U8>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NV == 1 ? GFM_AGG_FWD_MINB : 1)
     k_agg_fwd_vec(const float* __restrict__ h, int n_nodes, int H, const int* __restrict__ rowptr,
                   const int* __restrict__ col_src, const float* __restrict__ w, int parts,
                   float* __restrict__ agg, int* __restrict__ argmax, float* __restrict__ stat_mean) {
@@ -698,7 +707,7 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
 }
 
 template <int NV, int LPN, bool U8>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NV == 1 ? (LPN == 32 ? (GFM_AGG_BWD_MINB > 4 ? 4 : GFM_AGG_BWD_MINB) : GFM_AGG_BWD_MINB) : 1)
     k_agg_bwd_vec(const float* __restrict__ G, int ldg, const float* __restrict__ coef,
                   const float* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
                   const float* __restrict__ h_in, const int* __restrict__ csc_ptr,
