@@ -15,8 +15,11 @@ which is exactly the reference's "update discarded, training aborted"
 
 from __future__ import annotations
 
+import json
 import logging
+import struct
 import time
+import zlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -25,7 +28,7 @@ import torch
 from . import _lib
 from ._lib import call, ptr, stream_handle
 from .comm import Comm, LocalComm
-from .errors import ConfigError, ValidationError
+from .errors import ConfigError, CorruptionError, FormatError, UnsupportedVersionError, ValidationError
 from .model import (ModelConfig, ModelParams, _Scratch, count_params, forward_batch, param_layout,
                     init_params_flat, loss_and_grad, make_batch)
 from .schedule import epoch_schedule
@@ -254,6 +257,18 @@ class DataParallelTrainer:
     def current_params(self) -> ModelParams:
         return ModelParams(self.cfg, self.master.clone())
 
+    def optimizer_state(self) -> "OptimizerState":
+        """Adam moments in the reference's flat order plus the applied-step
+        count ``t`` (train.py:100: every applied update, SGD included; a
+        discarded non-finite step does not count)."""
+        lay = self.layout
+        if self.tcfg.optimizer == "adam":
+            t = int(self.t_dev.item())
+        else:
+            t = self.steps - int(self.nan_event)
+        return OptimizerState(lay.compact(self.m).cpu().numpy(), lay.compact(self.v).cpu().numpy(),
+                              t)
+
     def flat_master(self) -> np.ndarray:
         """float64 master parameters in the reference's flat order"""
         return self.layout.compact(self.master).cpu().numpy()
@@ -431,6 +446,91 @@ class StructureStepRunner:
         return tot / cnt if cnt else float("nan")
 
 
+# --------------------------------------------------------------------------
+# GFMP checkpoints (train.py:341-423): the reference's byte format, so a
+# model trained here loads in the reference's ensemble/HPO/uq tooling and
+# vice versa.  Layout (little-endian):
+#   b"GFMP" | u32 version | u64 len(cfg) | cfg json (sort_keys) |
+#   u64 n | u64 t | i64 epoch | i64 base_seed | f64 flat[n] | f64 m[n] |
+#   f64 v[n] | u32 crc32(everything before it)
+# --------------------------------------------------------------------------
+
+CHECKPOINT_MAGIC = b"GFMP"        # train.py:55
+CHECKPOINT_VERSION = 1            # train.py:56
+_CKPT_HEAD = struct.Struct("<IQ")
+_CKPT_COUNTS = struct.Struct("<QQq")
+
+
+@dataclass
+class Checkpoint:
+    """train.py:349-355."""
+    model_config: ModelConfig
+    flat: np.ndarray
+    opt_state: OptimizerState
+    epoch: int
+    base_seed: int
+
+
+def _host_f64(x) -> np.ndarray:
+    if isinstance(x, torch.Tensor):
+        x = x.detach().to("cpu", torch.float64).numpy()
+    return np.ascontiguousarray(x, dtype="<f8")
+
+
+def save_checkpoint(path: str, model_config: ModelConfig, flat, opt_state: OptimizerState,
+                    epoch: int, base_seed: int) -> None:
+    """train.py:358-381.  ``flat``/``m``/``v`` may be numpy or device tensors
+    in the reference's flat order; the file is byte-identical to the
+    reference's for the same values."""
+    flat = _host_f64(flat)
+    m, v = _host_f64(opt_state.m), _host_f64(opt_state.v)
+    n = flat.shape[0]
+    if flat.ndim != 1 or m.shape != (n,) or v.shape != (n,):
+        raise ValidationError(f"checkpoint vectors disagree: flat {flat.shape}, m {m.shape}, "
+                              f"v {v.shape}")
+    cfg = json.dumps(model_config.to_dict(), sort_keys=True).encode()
+    body = b"".join((CHECKPOINT_MAGIC, _CKPT_HEAD.pack(CHECKPOINT_VERSION, len(cfg)), cfg,
+                     _CKPT_COUNTS.pack(n, int(opt_state.t), int(epoch)),
+                     struct.pack("<q", int(base_seed)), flat.tobytes(), m.tobytes(),
+                     v.tobytes()))
+    with open(path, "wb") as fh:
+        fh.write(body + struct.pack("<I", zlib.crc32(body)))
+
+
+def load_checkpoint(path: str) -> Checkpoint:
+    """train.py:384-423, same checks and error classes: bad magic ->
+    FormatError; wrong version -> UnsupportedVersionError; bad crc or
+    length -> CorruptionError.  Returns host (numpy) vectors."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    magic = len(CHECKPOINT_MAGIC)
+    if len(blob) < 4 or blob[:magic] != CHECKPOINT_MAGIC:
+        raise FormatError(f"{path!r} is not a checkpoint (bad magic)")
+    if len(blob) < 8:
+        raise CorruptionError(f"checkpoint {path!r} truncated")
+    body = memoryview(blob)[:-4]
+    if zlib.crc32(body) != struct.unpack("<I", blob[-4:])[0]:
+        raise CorruptionError(f"checkpoint {path!r} failed its checksum")
+    version, cfg_len = _CKPT_HEAD.unpack_from(body, magic)
+    if version != CHECKPOINT_VERSION:
+        raise UnsupportedVersionError(
+            f"checkpoint version {version} not supported (want {CHECKPOINT_VERSION})")
+    off = magic + _CKPT_HEAD.size
+    model_config = ModelConfig.from_dict(json.loads(bytes(body[off:off + cfg_len])))
+    off += cfg_len
+    n, t, epoch = _CKPT_COUNTS.unpack_from(body, off)
+    off += _CKPT_COUNTS.size
+    (base_seed,) = struct.unpack_from("<q", body, off)
+    off += 8
+    if len(body) != off + 24 * n:
+        raise CorruptionError(f"checkpoint {path!r} truncated: {len(body)} bytes, "
+                              f"expected {off + 24 * n}")
+    vecs = np.frombuffer(body, dtype="<f8", count=3 * n, offset=off).reshape(3, n).copy()
+    return Checkpoint(model_config=model_config, flat=vecs[0].copy(),
+                      opt_state=OptimizerState(vecs[1].copy(), vecs[2].copy(), t),
+                      epoch=epoch, base_seed=base_seed)
+
+
 def evaluate(params: ModelParams, store, comm: Comm, group: str = "valset",
              batch_size: int = 64) -> tuple[float, float]:
     """Per-atom energy MAE and force-component MAE over a group
@@ -464,8 +564,6 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
     comm = comm or LocalComm()
     config = config or TrainConfig()
     clock = clock or PhaseClock()
-    if config.checkpoint_path:
-        raise ConfigError("GFMP checkpoint I/O is not part of the GPU hot path (see DESIGN.md)")
     trainer = DataParallelTrainer(model_config, config, comm, device=device, initial=initial,
                                   dtype=dtype)
     ownership = store.ownership.get("trainset")
@@ -478,6 +576,7 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
     stop_reason = "max_epochs"
     nan_event = False
     P = trainer.P
+    epoch = 0
     for epoch in range(1, config.max_epochs + 1):
         t0 = time.perf_counter()
         before = clock.totals()
@@ -529,6 +628,9 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
         if comm.broadcast_obj("budget" if over else None) is not None:
             stop_reason = "budget"
             break
+    if config.checkpoint_path and comm.rank == 0:  # train.py:323-331
+        save_checkpoint(config.checkpoint_path, model_config, trainer.flat_master(),
+                        trainer.optimizer_state(), epoch=epoch, base_seed=config.base_seed)
     return TrainResult(params=trainer.current_params(), metrics=metrics,
                        stop_reason=stop_reason, nan_event=nan_event,
                        epochs_run=len(metrics) + (1 if nan_event else 0))
