@@ -67,6 +67,16 @@ GFM_API int gfm_get_gemm_mode(void);
 /* ---- K1/K2: batch geometry (preprocess.py:90-104, model.py:234-285) --- */
 /* gnode[i] = graph of node i (model.py:243) */
 GFM_API int gfm_graph_of_node(const int* node_offsets, int n_graphs, int* gnode, void* stream);
+/* Device sample store gather, replacing DDStore.fetch_batch + decode_record
+ * + make_batch's host concatenation (ddstore.py:316-490, records.py:154-183,
+ * model.py:237-250): output structure b = resident structure idx[b], its
+ * atoms written at dst_off[b] (caller-computed, e.g. a fixed runner layout).
+ * z int32, pos float64 in and out; energy/forces float64 in, `dtype` out. */
+GFM_API int gfm_gather_structures(const int* idx, int n_out, const int* src_off,
+                                  const int* dst_off, const int* z_in, const double* pos_in,
+                                  const double* energy_in, const double* forces_in, int* z_out,
+                                  double* pos_out, void* energy_out, void* forces_out, int dtype,
+                                  void* stream);
 /* out[0..n] = exclusive prefix sum of in[0..n) (np.cumsum, model.py:238) */
 GFM_API size_t gfm_scan_workspace_bytes(int n);
 GFM_API int gfm_exclusive_scan(const int* in, int n, int* out, void* workspace, void* stream);

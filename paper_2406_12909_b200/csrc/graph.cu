@@ -21,6 +21,31 @@ __global__ void k_graph_of_node(const int* __restrict__ off, int n_graphs, int* 
     for (int i = off[g] + threadIdx.x; i < off[g + 1]; i += blockDim.x) gnode[i] = g;
 }
 
+// Device sample store gather (replaces DDStore fetch + decode_record +
+// make_batch's host concatenation, ddstore.py:316-490 / model.py:237-250):
+// output structure b is resident structure idx[b]; its atoms land at
+// dst_off[b].  One CTA per output structure (grid-strided), coalesced
+// contiguous copies; labels are converted to the compute dtype on the way.
+template <typename T>
+__global__ void k_gather_structures(const int* __restrict__ idx, int n_out,
+                                    const int* __restrict__ src_off, const int* __restrict__ dst_off,
+                                    const int* __restrict__ z_in, const double* __restrict__ pos_in,
+                                    const double* __restrict__ e_in, const double* __restrict__ f_in,
+                                    int* __restrict__ z_out, double* __restrict__ pos_out,
+                                    T* __restrict__ e_out, T* __restrict__ f_out) {
+  pdl_entry();
+  for (int b = blockIdx.x; b < n_out; b += gridDim.x) {
+    const int s = idx[b];
+    const int so = src_off[s], n = src_off[s + 1] - so, d = dst_off[b];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) z_out[d + i] = z_in[so + i];
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) {
+      pos_out[3 * d + i] = pos_in[3 * so + i];
+      f_out[3 * d + i] = (T)f_in[3 * so + i];
+    }
+    if (threadIdx.x == 0) e_out[b] = (T)e_in[s];
+  }
+}
+
 __global__ void k_iota(int* __restrict__ out, int n) {
   pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
@@ -612,6 +637,24 @@ extern "C" {
 int gfm_graph_of_node(const int* node_offsets, int n_graphs, int* gnode, void* stream) {
   if (n_graphs <= 0) return 0;
   launch_k(k_graph_of_node, grid_for(n_graphs, 1), 128, 0, (cudaStream_t)stream, node_offsets, n_graphs, gnode);
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gfm_gather_structures(const int* idx, int n_out, const int* src_off, const int* dst_off,
+                          const int* z_in, const double* pos_in, const double* energy_in,
+                          const double* forces_in, int* z_out, double* pos_out, void* energy_out,
+                          void* forces_out, int dtype, void* stream) {
+  if (n_out <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = n_out < 148 * 16 ? n_out : 148 * 16;
+  if (dtype == GFM_F32)
+    launch_k(k_gather_structures<float>, grid, 128, 0, s, idx, n_out, src_off, dst_off, z_in, pos_in,
+             energy_in, forces_in, z_out, pos_out, (float*)energy_out, (float*)forces_out);
+  else
+    launch_k(k_gather_structures<double>, grid, 128, 0, s, idx, n_out, src_off, dst_off, z_in,
+             pos_in, energy_in, forces_in, z_out, pos_out, (double*)energy_out,
+             (double*)forces_out);
   GFM_TRY(cudaGetLastError());
   return 0;
 }

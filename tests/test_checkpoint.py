@@ -103,14 +103,25 @@ def test_train_loop_matches_oracle_and_checkpoints(tmp_path, optimizer):
     flat = O.init_flat(ocfg, seed=tc.base_seed)
     m, v, t = np.zeros_like(flat), np.zeros_like(flat), 0
     for epoch in (1, 2):
+        losses = []
         for idx in O.schedule(8, 1, mc.batch_size, tc.base_seed, epoch)[0]:
-            _, g, _ = O.loss_and_grad(ocfg, flat, O.pack([dicts[i] for i in idx]))
+            (loss, _, _), g, _ = O.loss_and_grad(ocfg, flat, O.pack([dicts[i] for i in idx]))
+            losses.append(loss)
             if optimizer == "adam":
                 flat, m, v, t = O.adam(flat, g, m, v, t, lr=tc.learning_rate)
             else:
                 flat, t = O.sgd(flat, g, tc.learning_rate), t + 1
     got = res.params.flatten()
     np.testing.assert_allclose(got, flat, rtol=1e-9, atol=1e-12)
+    # epoch metrics: mean step loss (train.py:276-283) and evaluate() on the
+    # valset with the epoch's final parameters (train.py:160-189)
+    last = res.metrics[-1]
+    np.testing.assert_allclose(last.train_loss, np.mean(losses), rtol=1e-10)
+    vb = O.pack(dicts[8:])
+    e, f = O.forward(ocfg, flat, vb)
+    np.testing.assert_allclose(last.val_energy_mae,
+                               np.mean(np.abs((e - vb["e_true"]) / vb["n_per"])), rtol=1e-9)
+    np.testing.assert_allclose(last.val_force_mae, np.mean(np.abs(f - vb["f_true"])), rtol=1e-9)
 
     ck = T.load_checkpoint(path)
     assert ck.model_config == mc and ck.epoch == 2 and ck.base_seed == 2

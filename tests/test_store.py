@@ -1,0 +1,79 @@
+"""HBM-resident sample store: gfm_gather_structures against the host
+concatenation make_batch performs (model.py:237-250) -- bit-exact -- and
+the runner path against the runner's own host-copy path."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gfm_oracle as O
+
+from paper_2406_12909_b200 import model as M, train as T  # noqa: E402
+from paper_2406_12909_b200.errors import ValidationError  # noqa: E402
+from paper_2406_12909_b200.records import GraphRecord  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _records(count, seed, n_range=(4, 12)):
+    dicts = O.synthetic(count, n_atoms_range=n_range, seed=seed)
+    return [GraphRecord(d["z"], d["pos"], d["edges"], d["energy"], d["forces"]) for d in dicts]
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_gather_matches_host_concatenation(dtype):
+    from paper_2406_12909_b200.store import DeviceStructureStore
+    recs = _records(40, 3)
+    store = DeviceStructureStore({"trainset": recs})
+    idx = np.array([7, 0, 39, 7, 12, 5, 33])  # repeats allowed, any order
+    pos, z, e, f, off = store.gather("trainset", idx, dtype=dtype)
+    sel = [recs[i] for i in idx]
+    np.testing.assert_array_equal(off, np.concatenate([[0], np.cumsum([r.n_atoms for r in sel])]))
+    np.testing.assert_array_equal(pos.cpu().numpy(), np.concatenate([r.positions for r in sel]))
+    np.testing.assert_array_equal(z.cpu().numpy(), np.concatenate([r.atomic_numbers for r in sel]))
+    np.testing.assert_array_equal(e.cpu().numpy(),
+                                  np.array([r.energy for r in sel]).astype(e.cpu().numpy().dtype))
+    np.testing.assert_array_equal(
+        f.cpu().numpy(), np.concatenate([r.forces for r in sel]).astype(f.cpu().numpy().dtype))
+    with pytest.raises(ValidationError):
+        store.gather("trainset", [40])
+    with pytest.raises(ValidationError):
+        store.gather("trainset", [])
+
+
+def test_runner_fed_from_store_matches_host_feed():
+    from paper_2406_12909_b200.store import DeviceStructureStore
+    recs = _records(24, 5, n_range=(10, 10))  # fixed size: one runner layout
+    store = DeviceStructureStore({"trainset": recs})
+    mc = M.ModelConfig(mpnn_kind="sum-agg", mpnn_layers=2, mpnn_width=16, fc_width=16)
+    tr = T.DataParallelTrainer(mc, T.TrainConfig())
+    idx = np.array([3, 17, 8, 21])
+    off = store.host_offsets("trainset", idx)
+    run = T.StructureStepRunner(tr, off, rc=2.0, use_graph=False)
+    sel = [recs[i] for i in idx]
+    host = [torch.from_numpy(np.concatenate([r.positions for r in sel])),
+            torch.from_numpy(np.concatenate([r.atomic_numbers for r in sel]).astype(np.int32)),
+            torch.tensor([r.energy for r in sel], dtype=torch.float32),
+            torch.from_numpy(np.concatenate([r.forces for r in sel]).astype(np.float32))]
+    run.load(*host)
+    want = {k: v.clone() for k, v in run.slot.items()}
+    for v in run.slot.values():
+        v.zero_()
+    store.load_runner("trainset", idx, run)
+    for k in want:
+        assert torch.equal(run.slot[k], want[k]), k
+    run.run()
+    torch.cuda.synchronize()
+    assert np.isfinite(tr.contrib[tr.P].item())
+    with pytest.raises(ValidationError):
+        store.load_runner("trainset", idx[:3], run)
+
+
+def test_train_accepts_device_store():
+    from paper_2406_12909_b200.store import DeviceStructureStore
+    recs = _records(10, 8)
+    store = DeviceStructureStore({"trainset": recs[:7], "valset": recs[7:]})
+    mc = M.ModelConfig(mpnn_kind="mean-agg", mpnn_layers=1, mpnn_width=8, fc_width=8,
+                       batch_size=4)
+    res = T.train(mc, store, config=T.TrainConfig(max_epochs=1), dtype=torch.float64)
+    assert res.epochs_run == 1 and np.isfinite(res.metrics[0].val_mae)
