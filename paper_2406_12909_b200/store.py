@@ -30,38 +30,53 @@ class _Ownership:
 
 
 class _Group:
-    def __init__(self, records, device):
-        if not records:
-            raise ValidationError("a store group needs at least one structure")
-        n = np.array([r.atomic_numbers.shape[0] for r in records], np.int64)
-        self.host_off = np.concatenate([[0], np.cumsum(n)]).astype(np.int32)
-        self.records = list(records)
-        cat = np.concatenate
-        self.z = torch.as_tensor(cat([r.atomic_numbers for r in records]).astype(np.int32),
-                                 device=device)
-        self.pos = torch.as_tensor(cat([r.positions for r in records]).astype(np.float64),
-                                   device=device)
-        self.energy = torch.as_tensor(np.array([r.energy for r in records], np.float64),
+    def __init__(self, records, device, arrays=None):
+        if arrays is None:
+            if not records:
+                raise ValidationError("a store group needs at least one structure")
+            cat = np.concatenate
+            n = np.array([r.atomic_numbers.shape[0] for r in records], np.int64)
+            off = np.concatenate([[0], np.cumsum(n)])
+            arrays = (cat([r.atomic_numbers for r in records]), cat([r.positions for r in records]),
+                      np.array([r.energy for r in records]), cat([r.forces for r in records]), off)
+        z, pos, energy, forces, off = arrays
+        self.records = None if records is None else list(records)
+        self.host_off = np.asarray(off, np.int64).astype(np.int32)
+        self.n_samples = self.host_off.shape[0] - 1
+        N = int(self.host_off[-1])
+        self.z = torch.as_tensor(np.asarray(z).reshape(N).astype(np.int32), device=device)
+        self.pos = torch.as_tensor(np.asarray(pos, np.float64).reshape(N, 3), device=device)
+        self.energy = torch.as_tensor(np.asarray(energy, np.float64).reshape(self.n_samples),
                                       device=device)
-        self.forces = torch.as_tensor(cat([r.forces for r in records]).astype(np.float64),
-                                      device=device)
+        self.forces = torch.as_tensor(np.asarray(forces, np.float64).reshape(N, 3), device=device)
         self.off = torch.as_tensor(self.host_off, device=device)
 
 
 class DeviceStructureStore:
     """``{group: [GraphRecord]}`` ingested into HBM once."""
 
-    def __init__(self, groups: dict, device=None):
+    def __init__(self, groups: dict, device=None, _arrays: dict | None = None):
         _lib.load(require_device=True)
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self._groups = {k: _Group(v, self.device) for k, v in groups.items()}
-        self.ownership = {k: _Ownership(len(g.records)) for k, g in self._groups.items()}
+        for k, a in (_arrays or {}).items():
+            self._groups[k] = _Group(None, self.device, a)
+        self.ownership = {k: _Ownership(g.n_samples) for k, g in self._groups.items()}
         self._idx = {}
+
+    @classmethod
+    def from_arrays(cls, groups: dict, device=None) -> "DeviceStructureStore":
+        """``{group: (z (N,), pos (N,3), energy (S,), forces (N,3), offsets
+        (S+1,))}`` -- already-concatenated structures (no host records, so
+        ``fetch_batch`` is unavailable; use ``gather``/``load_runner``)."""
+        return cls({}, device, _arrays=groups)
 
     # ---- DDStore surface (ddstore.py:316-490) ----------------------------
     def fetch_batch(self, group, indices):
         recs = self._groups[group].records
+        if recs is None:
+            raise ValidationError(f"group {group!r} was ingested from arrays; it has no records")
         return [recs[int(i)] for i in indices]
 
     def close(self):
@@ -79,8 +94,8 @@ class DeviceStructureStore:
         idx = np.asarray(indices, np.int64).reshape(-1)
         if idx.size == 0:
             raise ValidationError("cannot build a batch from zero records")
-        if idx.min() < 0 or idx.max() >= len(g.records):
-            raise ValidationError(f"sample index out of range [0, {len(g.records)})")
+        if idx.min() < 0 or idx.max() >= g.n_samples:
+            raise ValidationError(f"sample index out of range [0, {g.n_samples})")
         return idx
 
     def _launch(self, g, idx, dst_off, z, pos, e, f, dtype):

@@ -77,3 +77,21 @@ def test_train_accepts_device_store():
                        batch_size=4)
     res = T.train(mc, store, config=T.TrainConfig(max_epochs=1), dtype=torch.float64)
     assert res.epochs_run == 1 and np.isfinite(res.metrics[0].val_mae)
+
+
+def test_store_from_arrays():
+    from paper_2406_12909_b200.store import DeviceStructureStore
+    recs = _records(9, 6)
+    off = np.concatenate([[0], np.cumsum([r.n_atoms for r in recs])])
+    arrays = (np.concatenate([r.atomic_numbers for r in recs]),
+              np.concatenate([r.positions for r in recs]), np.array([r.energy for r in recs]),
+              np.concatenate([r.forces for r in recs]), off)
+    a = DeviceStructureStore.from_arrays({"trainset": arrays})
+    b = DeviceStructureStore({"trainset": recs})
+    assert a.ownership["trainset"].n_samples == 9
+    idx = [8, 1, 4]
+    for x, y in zip(a.gather("trainset", idx, torch.float64)[:4],
+                    b.gather("trainset", idx, torch.float64)[:4]):
+        assert torch.equal(x, y)
+    with pytest.raises(ValidationError):
+        a.fetch_batch("trainset", idx)
