@@ -450,6 +450,30 @@ def run_native(args):
     roof_bwd = roof("gfm_agg_bwd (pna CSC gather)", bwd_bytes, bwd_ms, "agg_bwd_dram_bytes")
     roof_fwd = roof("gfm_agg_fwd (pna: sum|mean|max|std)", fwd_bytes, fwd_ms, "agg_fwd_dram_bytes")
 
+    # ---- neighbour-list construction per graph, the GPU
+    # radius-graph batch assembly (count + fill + CSR/CSC in one pass) on this
+    # batch vs the oracle's build_cutoff_edges restatement on host structures
+    def nbr_call():
+        M.radius_batch(runner.slot["pos"], runner.slot["z"], runner.off, runner.host_off,
+                       runner.rc, runner.max_nbr, runner.cells, runner.slot["e"],
+                       runner.slot["f"], runner.tr.dtype, e_cap=runner.e_cap, out=runner.bufs)
+
+    nbr_ms = launch_ms(nbr_call)
+    neighbour_list = dict(gpu_ms_per_batch=nbr_ms, gpu_us_per_graph=nbr_ms * 1e3 / B,
+                          note="radius_batch on the step's input slots, L2 flushed per launch")
+    if rank == 0 and world == 1:
+        from oracle import gfm_oracle as O
+        zc, pc, _, _ = make_structures(64, 4242)
+        t0, done = time.perf_counter(), 0
+        while done < 64 and (done < 4 or time.perf_counter() - t0 < 1.0):
+            O.cutoff_edges(pc[done], WORKLOAD["rc"], max_nbr=WORKLOAD["max_nbr"],
+                           cell=(WORKLOAD["box"],) * 3 if WORKLOAD["periodic"] else None)
+            done += 1
+        cpu_ms = (time.perf_counter() - t0) * 1e3 / done
+        neighbour_list.update(cpu_ms_per_graph=cpu_ms, cpu_cores=1,
+                              cpu_sample=f"{done} graphs, oracle cutoff_edges (numpy fp64)",
+                              speedup=cpu_ms / (nbr_ms / B))
+
     # ---- launches per step (one extra untimed step under the profiler)
     launches = None
     try:
@@ -482,6 +506,7 @@ def run_native(args):
                         l2=("step working set (activations, E x H workspaces) > 126 MB L2; "
                             "8-batch input pool cycled")),
             e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
+            neighbour_list=neighbour_list,
             e2e_device_store=dict(value=store_value, unit=UNIT, h2d_bytes_per_step=4 * B,
                                   d2h_bytes_per_step=d2h,
                                   note="dataset resident in HBM (store.DeviceStructureStore); "
