@@ -148,6 +148,32 @@ __global__ void k_node_energy(const T* __restrict__ y, int n, int G, const T* __
   }
 }
 
+// float32, G % 4 == 0, G/4 a power of two <= 32: LPN = G/4 lanes per node,
+// one float4 of y and a per lane, group shuffle reduction (32/LPN nodes per
+// warp, every load a full 16 B)
+__global__ void k_node_energy4(const float* __restrict__ y, int n, int G, int lpn,
+                               const float* __restrict__ a, const float* __restrict__ c,
+                               float* __restrict__ node_e) {
+  pdl_entry();
+  const int lane = threadIdx.x & 31, sub = lane & (lpn - 1);
+  const int per_warp = 32 / lpn;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  const float4 av = reinterpret_cast<const float4*>(a)[sub];
+  const float c0 = c[0];
+  // base is warp-uniform, so every lane runs the group shuffles together
+  for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * per_warp; base < n;
+       base += warps * per_warp) {
+    const int i = base + lane / lpn;
+    float s = 0.f;
+    if (i < n) {
+      const float4 yv = reinterpret_cast<const float4*>(y + (long long)i * G)[sub];
+      s = yv.x * av.x + yv.y * av.y + yv.z * av.z + yv.w * av.w;
+    }
+    for (int o = lpn >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (i < n && sub == 0) node_e[i] = s + c0;
+  }
+}
+
 // e_pred[b] = add.reduceat(node_e, offsets) (model.py:373): x0 + pairwise(x1..)
 template <typename T>
 __global__ void k_graph_pool(const T* __restrict__ node_e, const int* __restrict__ off,
@@ -245,6 +271,30 @@ __global__ void k_energy_seed(const T* __restrict__ de, const int* __restrict__ 
       const T yy = y[row + g];
       dz[row + g] = mul_rn(mul_rn(s, a[g]), sub_rn(T(1), mul_rn(yy, yy)));
     }
+  }
+}
+
+// float32, G % 4 == 0: one float4 of (y, dz) per thread, same per-element
+// rounding as k_energy_seed (bit-identical output)
+__global__ void k_energy_seed4(const float* __restrict__ de, const int* __restrict__ gnode, int n,
+                               int G4, const float* __restrict__ a, const float* __restrict__ y,
+                               float* __restrict__ ds, int ld_ds, float* __restrict__ dz) {
+  pdl_entry();
+  const long long total = (long long)n * G4;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / G4), q = (int)(t - (long long)i * G4);
+    const float s = de[gnode[i]];
+    if (q == 0)
+      for (int k = 0; k < ld_ds; ++k) ds[(long long)i * ld_ds + k] = k == 0 ? s : 0.f;
+    const float4 yv = reinterpret_cast<const float4*>(y)[t];
+    const float4 av = reinterpret_cast<const float4*>(a)[q];
+    float4 o;
+    o.x = mul_rn(mul_rn(s, av.x), sub_rn(1.f, mul_rn(yv.x, yv.x)));
+    o.y = mul_rn(mul_rn(s, av.y), sub_rn(1.f, mul_rn(yv.y, yv.y)));
+    o.z = mul_rn(mul_rn(s, av.z), sub_rn(1.f, mul_rn(yv.z, yv.z)));
+    o.w = mul_rn(mul_rn(s, av.w), sub_rn(1.f, mul_rn(yv.w, yv.w)));
+    reinterpret_cast<float4*>(dz)[t] = o;
   }
 }
 
@@ -600,6 +650,15 @@ reduce:
 
 using namespace gfm;
 
+#define GFM_TRY_CUDA(expr)                                                 \
+  do {                                                                     \
+    cudaError_t _e2 = (expr);                                              \
+    if (_e2 != cudaSuccess) {                                              \
+      set_error("%s: %s", #expr, cudaGetErrorString(_e2));                 \
+      return (int)_e2;                                                     \
+    }                                                                      \
+  } while (0)
+
 #define GFM_DISPATCH(dtype, NAME, ...)                                     \
   cudaError_t _err;                                                        \
   if (dtype == GFM_F32) {                                                  \
@@ -766,6 +825,17 @@ int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const v
                        const int* node_offsets, int n_graphs, void* node_e, void* e_pred,
                        int dtype, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  const int lpn = G / 4;
+  if (dtype == GFM_F32 && G % 4 == 0 && lpn <= 32 && (lpn & (lpn - 1)) == 0 && al16(y) &&
+      al16(a) && n_nodes > 0) {
+    GFM_TRY_CUDA(launch_k(k_node_energy4, grid_1d((long long)n_nodes * lpn), 256, 0, s,
+                          (const float*)y, n_nodes, G, lpn, (const float*)a, (const float*)c,
+                          (float*)node_e));
+    GFM_TRY_CUDA(launch_k(k_graph_pool<float>, grid_1d(n_graphs), 256, 0, s,
+                          (const float*)node_e, node_offsets, n_graphs, (float*)e_pred));
+    GFM_TRY_CUDA(cudaGetLastError());
+    return 0;
+  }
   GFM_DISPATCH(dtype, "gfm_energy_readout",
                (launch_k(k_node_energy<T>, grid_1d((long long)n_nodes * 32), 256, 0, s,
                     (const T*)y, n_nodes, G, (const T*)a, (const T*)c, (T*)node_e),
@@ -795,6 +865,13 @@ int gfm_energy_seed(const void* de, const int* gnode, int n_nodes, int G, const 
                     const void* y, void* ds, int ld_ds, void* dz, int dtype, void* stream) {
   if (ld_ds < 1) return GFM_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GFM_F32 && G % 4 == 0 && al16(y) && al16(a) && al16(dz) && n_nodes > 0) {
+    GFM_TRY_CUDA(launch_k(k_energy_seed4, grid_1d((long long)n_nodes * (G / 4)), 256, 0, s,
+                          (const float*)de, gnode, n_nodes, G / 4, (const float*)a,
+                          (const float*)y, (float*)ds, ld_ds, (float*)dz));
+    GFM_TRY_CUDA(cudaGetLastError());
+    return 0;
+  }
   GFM_DISPATCH(dtype, "gfm_energy_seed",
                (launch_k(k_energy_seed<T>, dim3(1, std::min(ceil_div(std::max(n_nodes, 1), 8), 65535)), dim3(32, 8), 0, s,
                     (const T*)de, gnode, n_nodes, G, (const T*)a, (const T*)y, (T*)ds, ld_ds,
