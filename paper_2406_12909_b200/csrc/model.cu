@@ -831,7 +831,7 @@ int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const v
     GFM_TRY_CUDA(launch_k(k_node_energy4, grid_1d((long long)n_nodes * lpn), 256, 0, s,
                           (const float*)y, n_nodes, G, lpn, (const float*)a, (const float*)c,
                           (float*)node_e));
-    GFM_TRY_CUDA(launch_k(k_graph_pool<float>, grid_1d(n_graphs), 256, 0, s,
+    GFM_TRY_CUDA(launch_k(k_graph_pool<float>, grid_1d(n_graphs, 32), 32, 0, s,
                           (const float*)node_e, node_offsets, n_graphs, (float*)e_pred));
     GFM_TRY_CUDA(cudaGetLastError());
     return 0;
@@ -839,7 +839,7 @@ int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const v
   GFM_DISPATCH(dtype, "gfm_energy_readout",
                (launch_k(k_node_energy<T>, grid_1d((long long)n_nodes * 32), 256, 0, s,
                     (const T*)y, n_nodes, G, (const T*)a, (const T*)c, (T*)node_e),
-                launch_k(k_graph_pool<T>, grid_1d(n_graphs), 256, 0, s, (const T*)node_e, node_offsets,
+                launch_k(k_graph_pool<T>, grid_1d(n_graphs, 32), 32, 0, s, (const T*)node_e, node_offsets,
                                                                  n_graphs, (T*)e_pred),
                 cudaGetLastError()))
 }
