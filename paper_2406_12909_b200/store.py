@@ -72,6 +72,14 @@ class DeviceStructureStore:
         ``fetch_batch`` is unavailable; use ``gather``/``load_runner``)."""
         return cls({}, device, _arrays=groups)
 
+    @classmethod
+    def from_container(cls, path: str, groups=None, device=None) -> "DeviceStructureStore":
+        """Ingest a gfmkit container directory (container.py) into HBM."""
+        from .container import GROUP_NAMES, read_group, read_manifest
+        man = read_manifest(path)
+        return cls({g: read_group(man, g, path) for g in (groups or GROUP_NAMES)
+                    if man.group(g).record_count}, device)
+
     # ---- DDStore surface (ddstore.py:316-490) ----------------------------
     def fetch_batch(self, group, indices):
         recs = self._groups[group].records
