@@ -378,17 +378,22 @@ class StructureStepRunner:
         self._graphs = None
 
     def _capture_stages(self):
-        """One captured step per staging copy, each starting with the device
-        copy stage -> slot.  Capture records without executing, so building
-        these never adds a training step."""
+        """One captured step per staging copy, each reading its staging
+        buffers directly (no stage -> slot copy; the stage stays busy until
+        the step's ``_stage_free`` event).  Capture records without executing,
+        so building these never adds a training step."""
         torch.cuda.synchronize()
         self._graphs = []
-        for k in range(2):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._from_stage(k)
-                self._eager()
-            self._graphs.append(g)
+        slot = self.slot
+        try:
+            for k in range(2):
+                self.slot = self._stage[k]
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._eager()
+                self._graphs.append(g)
+        finally:
+            self.slot = slot
 
     def step_pipelined(self, pos, z, energy, forces):
         """As ``step``, but pipelined: the host->device copy of this step's
