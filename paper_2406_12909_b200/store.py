@@ -64,6 +64,7 @@ class DeviceStructureStore:
             self._groups[k] = _Group(None, self.device, a)
         self.ownership = {k: _Ownership(g.n_samples) for k, g in self._groups.items()}
         self._idx = {}
+        self._copy_stream = None
 
     @classmethod
     def from_arrays(cls, groups: dict, device=None) -> "DeviceStructureStore":
@@ -107,28 +108,39 @@ class DeviceStructureStore:
         return idx
 
     def _launch(self, g, idx, dst_off, z, pos, e, f, dtype):
-        # a ring of pinned index buffers: a slot is refilled only after the
-        # H2D copy that last read it has completed (no whole-stream sync)
+        # indices go host -> device on a copy stream (so the copy overlaps the
+        # step still running on the compute stream) through a ring of pinned /
+        # device buffers; a slot is reused only after its last H2D copy (host
+        # side) and its last gather (device side) have completed
         B = idx.shape[0]
+        main = torch.cuda.current_stream(self.device)
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+        cs = self._copy_stream
         ring = self._idx.get(B)
         if ring is None:
             ring = self._idx[B] = dict(k=0, slots=[
-                (torch.empty(B, dtype=torch.int32).pin_memory(),
-                 torch.empty(B, dtype=torch.int32, device=self.device), None)
+                [torch.empty(B, dtype=torch.int32).pin_memory(),
+                 torch.empty(B, dtype=torch.int32, device=self.device), None, None]
                 for _ in range(4)])
-        k = ring["k"]
-        host, dev, done = ring["slots"][k]
-        if done is not None:
-            done.synchronize()
+        slot = ring["slots"][ring["k"]]
+        ring["k"] = (ring["k"] + 1) % len(ring["slots"])
+        host, dev, copied, used = slot
+        if copied is not None:
+            copied.synchronize()
         host.numpy()[:] = idx
-        dev.copy_(host, non_blocking=True)
-        done = torch.cuda.Event()
-        done.record()
-        ring["slots"][k] = (host, dev, done)
-        ring["k"] = (k + 1) % len(ring["slots"])
+        if used is not None:
+            cs.wait_event(used)
+        with torch.cuda.stream(cs):
+            dev.copy_(host, non_blocking=True)
+        slot[2] = torch.cuda.Event()
+        slot[2].record(cs)
+        main.wait_event(slot[2])
         call("gfm_gather_structures", ptr(dev), int(B), ptr(g.off), ptr(dst_off),
              ptr(g.z), ptr(g.pos), ptr(g.energy), ptr(g.forces), ptr(z), ptr(pos), ptr(e), ptr(f),
              _lib.dtype_code(dtype), stream_handle())
+        slot[3] = torch.cuda.Event()
+        slot[3].record(main)
 
     def gather(self, group, indices, dtype=torch.float32):
         """Assemble structures ``indices`` on the device: returns
