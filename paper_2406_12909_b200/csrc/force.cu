@@ -519,8 +519,12 @@ __global__ void k_force_bwd_src_scalar(const T* __restrict__ P, int n, int H, co
 constexpr int kColChunk = 128;
 template <typename T>
 __global__ void __launch_bounds__(256)
-    k_colsum_partial(const T* __restrict__ X, int n, int H, int chunk, int cw, T* __restrict__ part) {
+    k_colsum_partial(const T* __restrict__ X1, int n, int H, int chunk, int cw, T* __restrict__ part1,
+                     const T* __restrict__ X2, T* __restrict__ part2) {
   pdl_entry();
+  // gridDim.z = 2: a second, independent (X, part) pair in the same launch
+  const T* __restrict__ X = blockIdx.z ? X2 : X1;
+  T* __restrict__ part = blockIdx.z ? part2 : part1;
   // block (ch, cb): rows [ch*chunk, ch*chunk+chunk) x columns [cb*cw, cb*cw+cw);
   // 256/cw row groups stride the rows, then a fixed-order smem combine, so the
   // result depends only on (n, H, chunk, cw) -- deterministic
@@ -545,20 +549,33 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// column sums of one or two (n x H) arrays (X2 may be null); part holds
+// ceil(n / kColChunk) * H partials per array
 template <typename T>
-cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s) {
+cudaError_t colsum2(const T* X1, const T* X2, int n, int H, T* out1, T* out2, T* part,
+                    cudaStream_t s) {
   if (H <= 0) return cudaSuccess;
   const int cw = H < 64 ? H : 64;
+  const int z = X2 ? 2 : 1;
   if (n <= 0) {
-    cudaMemsetAsync(out, 0, sizeof(T) * H, s);
+    cudaMemsetAsync(out1, 0, sizeof(T) * H, s);
+    if (X2) cudaMemsetAsync(out2, 0, sizeof(T) * H, s);
     return cudaGetLastError();
   }
   const int nch = ceil_div(n, kColChunk);
-  launch_k(k_colsum_partial<T>, dim3(nch, ceil_div(H, cw)), 256, 0, s, X, n, H, kColChunk, cw, part);
+  T* part2 = part + (size_t)nch * H;
+  launch_k(k_colsum_partial<T>, dim3(nch, ceil_div(H, cw), z), 256, 0, s, X1, n, H, kColChunk, cw,
+           part, X2, part2);
   // second level: the nch partial rows, one block per column slab
   const int cw2 = H < 32 ? H : 32;
-  launch_k(k_colsum_partial<T>, dim3(1, ceil_div(H, cw2)), 256, 0, s, part, nch, H, nch, cw2, out);
+  launch_k(k_colsum_partial<T>, dim3(1, ceil_div(H, cw2), z), 256, 0, s, (const T*)part, nch, H,
+           nch, cw2, out1, (const T*)part2, out2);
   return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s) {
+  return colsum2<T>(X, nullptr, n, H, out, nullptr, part, s);
 }
 
 #define GFM_FVEC_CASES(M) M(1, 1) M(1, 2) M(1, 4) M(1, 8) M(1, 16) M(1, 32) M(2, 32) M(4, 32)
@@ -656,5 +673,9 @@ template cudaError_t force_bwd_edges<double>(const double*, int, int, const int*
                                              double*, double*, int, cudaStream_t);
 template cudaError_t colsum<float>(const float*, int, int, float*, float*, cudaStream_t);
 template cudaError_t colsum<double>(const double*, int, int, double*, double*, cudaStream_t);
+template cudaError_t colsum2<float>(const float*, const float*, int, int, float*, float*, float*,
+                                    cudaStream_t);
+template cudaError_t colsum2<double>(const double*, const double*, int, int, double*, double*,
+                                     double*, cudaStream_t);
 
 }  // namespace gfm

@@ -393,6 +393,9 @@ __global__ void k_fill_ones(T* __restrict__ ones, int m) {  // ones[i][0] = 1, [
 
 template <typename T>
 cudaError_t colsum(const T* X, int n, int H, T* out, T* part, cudaStream_t s);  // force.cu
+template <typename T>
+cudaError_t colsum2(const T* X1, const T* X2, int n, int H, T* out1, T* out2, T* part,
+                    cudaStream_t s);  // force.cu
 
 // actual number of K splits after rounding the chunk to the engine's K step
 inline int real_splits(int K, int splits, int kstep) {
@@ -577,7 +580,7 @@ cudaError_t force_fwd_t(const T* h, int H, int n, const int* rowptr, const int* 
 template <typename T>
 size_t force_bwd_ws(int H, int n) {
   const size_t nh = (size_t)(n > 0 ? n : 1) * H;
-  const size_t parts = (size_t)ceil_div(n > 0 ? n : 1, 128) * H;  // colsum chunk partials
+  const size_t parts = 2 * (size_t)ceil_div(n > 0 ? n : 1, 128) * H;  // two colsums' partials
   return sizeof(T) * (3 * nh + parts + 64) + linear_bwd_weight_ws<T>(n, H, H, 0, 0) + 4096;
 }
 
@@ -596,7 +599,7 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
   T* TU = Ddst + nh;
   T* S = TU + nh;
   T* part = S + nh;
-  T* wws = part + (size_t)ceil_div(n > 0 ? n : 1, 128) * H + 64;
+  T* wws = part + 2 * (size_t)ceil_div(n > 0 ? n : 1, 128) * H + 64;
   wws = (T*)(((uintptr_t)wws + 255) & ~(uintptr_t)255);
   cudaError_t e;
   if (stage & 1) {
@@ -609,8 +612,8 @@ cudaError_t force_bwd_t(const T* h, const T* P, int H, int n, const int* rowptr,
   e = linear_bwd_weight_t<T>(S, H, n, nullptr, H, h, H, H, nullptr, 0, 0, 0, gV, nullptr, nullptr,
                              wws, s);
   if (e != cudaSuccess) return e;
-  if ((e = colsum<T>(Ddst, n, H, gc, part, s)) != cudaSuccess) return e;  // model.py:544
-  if ((e = colsum<T>(TU, n, H, gu, part, s)) != cudaSuccess) return e;    // model.py:540
+  // grad_c = colsum(D_dst) (model.py:544), grad_u = colsum(TU) (model.py:540): one launch pair
+  if ((e = colsum2<T>(Ddst, TU, n, H, gc, gu, part, s)) != cudaSuccess) return e;
 finish:
   if (!(stage & 2)) return cudaGetLastError();
   // dz_last = (dh_energy + S V) * (1 - h^2)   (model.py:545-547, 553)
