@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define GFM_ABI_VERSION 1
+#define GFM_ABI_VERSION 2
 
 enum { GFM_F32 = 0, GFM_F64 = 1 };
 enum { GFM_EINVAL = -1 };
@@ -112,12 +112,19 @@ GFM_API int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* e
 /* Fused batch assembly (replaces graph_of_node + radius_count + scan +
  * radius_fill + csc_from_csr): one CTA per graph (graphs of up to 256 atoms;
  * GFM_EINVAL otherwise -- use the separate calls), same predicate, cap, order
- * and outputs.  `workspace`: gfm_radius_batch_workspace_bytes (scratch). */
+ * and outputs.  `workspace`: gfm_radius_batch_workspace_bytes (scratch).
+ * Capacity semantics (ragged batches in a fixed-shape captured step): n_nodes
+ * may exceed node_offsets[n_graphs]; the tail nodes get rowptr = csc_ptr = E
+ * (no edges) and gnode = -1.  The edge buffers hold e_cap edges: a batch with
+ * more is emitted edge-free and raises the int overflow flag at index
+ * gfm_radius_batch_overflow_index(n_graphs) of the workspace (no
+ * out-of-bounds writes). */
 GFM_API size_t gfm_radius_batch_workspace_bytes(int n_graphs);
+GFM_API int gfm_radius_batch_overflow_index(int n_graphs);
 GFM_API int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, int n_nodes,
                              int max_atoms, const double* cells, double rc, int max_nbr,
                              int* gnode, int* rowptr, int* col_src, int* edge_dst, void* edge_w,
-                             void* edge_dx, int* csc_ptr, int* csc_eid, int* csc_dst,
+                             void* edge_dx, int* csc_ptr, int* csc_eid, int* csc_dst, int e_cap,
                              void* workspace, int dtype, void* stream);
 
 /* ---- K3/K4/K11: embedding and aggregation (model.py:293-341, 351-356) - */
@@ -219,12 +226,15 @@ GFM_API int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a,
 /* loss = [total, energy_term, force_term]; de, df = backward seeds;
  * contrib (float32, optional) receives [total, 1.0] (train.py:257).
  * workspace (gfm_loss_workspace_bytes) must be ZERO-initialised once; the
- * kernel leaves it ready for the next call. */
+ * kernel leaves it ready for the next call.  counts (device, optional) =
+ * [B, N] true graph / node counts of a ragged batch held in n_graphs /
+ * n_nodes capacity buffers: the means use the true counts and the capacity
+ * tail gets zero seeds. */
 GFM_API size_t gfm_loss_workspace_bytes(void);
 GFM_API int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_per, int n_graphs,
-                   const void* f_pred, const void* f_true, int n_nodes, double alpha_e,
-                   double alpha_f, void* loss, void* de, void* df, float* contrib,
-                   void* workspace, int dtype, void* stream);
+                   const void* f_pred, const void* f_true, int n_nodes, const int* counts,
+                   double alpha_e, double alpha_f, void* loss, void* de, void* df,
+                   float* contrib, void* workspace, int dtype, void* stream);
 /* ds_i = de[g(i)]; dz = (ds_i a) * (1 - y^2)  (model.py:521-529).
  * ds is written as an [n_nodes][ld_ds] row-major column vector (column 0 =
  * ds, columns 1..ld_ds-1 = 0) so ld_ds = 4 keeps rows 16-byte aligned for the
@@ -269,16 +279,20 @@ GFM_API int gfm_adam_step(const void* grad_sum, int grad_dtype, long long n, dou
                   double beta2, double eps, const int* skip_flag, float* params32, void* stream);
 /* device step counter: *step += 1, bias_corr = [1 - b1^step, 1 - b2^step]
  * (skipped when *skip_flag != 0) -- lets a CUDA-graph-captured step advance
- * Adam without host involvement */
+ * Adam without host involvement.  bc_table (device, optional, [table_len][2])
+ * holds the host-computed 1 - beta^t values (the reference's libm pow,
+ * train.py:104-105); device pow is used only past its end.  bias_corr ==
+ * NULL (SGD) advances the applied-step count only. */
 GFM_API int gfm_adam_advance(long long* step, double beta1, double beta2, double* bias_corr,
-                             const int* skip_flag, void* stream);
+                             const double* bc_table, long long table_len, const int* skip_flag,
+                             void* stream);
 /* gfm_nonfinite_flag + gfm_adam_advance in one launch: flag points at TWO
  * ints (flag[0] the non-finite flag, flag[1] a completion ticket that must
  * start at 0 and is left at 0); step / bias_corr are advanced after the
  * whole scan unless flag[0] is set (step == NULL: guard only) */
 GFM_API int gfm_nonfinite_advance(const void* v, long long n, int dtype, int* flag,
                                   long long* step, double beta1, double beta2, double* bias_corr,
-                                  void* stream);
+                                  const double* bc_table, long long table_len, void* stream);
 GFM_API int gfm_sgd_step(const void* grad_sum, int grad_dtype, long long n, double world, double* master,
                  double lr, const int* skip_flag, float* params32, void* stream);
 GFM_API int gfm_cast_f64_to_f32(const double* in, long long n, float* out, void* stream);

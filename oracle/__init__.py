@@ -12,7 +12,10 @@ schedule, ordered allreduce and uncapped non-periodic neighbour lists are
 PINNED against golden vectors produced by the reference itself
 (``oracle/make_golden.py`` -> ``tests/golden/``).  The extensions the
 reference lacks (std / pna aggregation, neighbour cap, periodic images) are
-restatements whose parity is UNPINNED (no reference implementation exists);
-they follow the reference's conventions and are checked by finite
-differences instead.
+restatements: no reference implementation exists to pin them against, so
+they follow the reference's conventions and are pinned by finite
+differences with the reference's own FD harness (tests/test_oracle_fd.py,
+port of test_gradients.py:27-108) and by forward identities (std-agg ==
+numpy.std per destination; pna-agg == [sum | mean | max | std] of the
+golden-pinned kinds).
 """

@@ -23,7 +23,7 @@ PART_SUM, PART_MEAN, PART_MAX, PART_STD = 1, 2, 4, 8
 FLAG_SCALAR = 1
 FLAG_ARGMAX_U8 = 2
 FLAG_AGG_PREPPED = 4
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -60,8 +60,9 @@ SIGNATURES = {
                            _P, _I, _P, _P]),
     "gfm_csc_from_csr": (_I, [_P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P]),
     "gfm_radius_batch_workspace_bytes": (_S, [_I]),
+    "gfm_radius_batch_overflow_index": (_I, [_I]),
     "gfm_radius_batch": (_I, [_P, _P, _I, _I, _I, _P, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P,
-                              _P, _P, _I, _P]),
+                              _P, _I, _P, _I, _P]),
     "gfm_embed": (_I, [_P, _I, _P, _I, _P, _I, _P]),
     "gfm_agg_parts_count": (_I, [_I]),
     "gfm_agg_fwd": (_I, [_P, _I, _I, _P, _P, _P, _I, _P, _P, _P, _I, _I, _P]),
@@ -90,14 +91,14 @@ SIGNATURES = {
     "gfm_force_bwd_finish": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, _P]),
     "gfm_energy_readout": (_I, [_P, _I, _I, _P, _P, _P, _I, _P, _P, _I, _P]),
     "gfm_loss_workspace_bytes": (_S, []),
-    "gfm_loss_seeds": (_I, [_P, _P, _P, _I, _P, _P, _I, _D, _D, _P, _P, _P, _P, _P, _I, _P]),
+    "gfm_loss_seeds": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _D, _D, _P, _P, _P, _P, _P, _I, _P]),
     "gfm_energy_seed": (_I, [_P, _P, _I, _I, _P, _P, _P, _I, _P, _I, _P]),
     "gfm_embedding_grad_workspace_bytes": (_S, [_I, _I, _I]),
     "gfm_embedding_grad": (_I, [_P, _I, _P, _I, _P, _P, _I, _P]),
     "gfm_nonfinite_flag": (_I, [_P, _L, _I, _P, _P]),
     "gfm_adam_step": (_I, [_P, _I, _L, _D, _P, _P, _P, _P, _D, _D, _D, _D, _P, _P, _P]),
-    "gfm_adam_advance": (_I, [_P, _D, _D, _P, _P, _P]),
-    "gfm_nonfinite_advance": (_I, [_P, _L, _I, _P, _P, _D, _D, _P, _P]),
+    "gfm_adam_advance": (_I, [_P, _D, _D, _P, _P, _L, _P, _P]),
+    "gfm_nonfinite_advance": (_I, [_P, _L, _I, _P, _P, _D, _D, _P, _P, _L, _P]),
     "gfm_sgd_step": (_I, [_P, _I, _L, _D, _P, _D, _P, _P, _P]),
     "gfm_cast_f64_to_f32": (_I, [_P, _L, _P, _P]),
 }

@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
                    int stride, int* __restrict__ gnode, int* __restrict__ rowptr,
                    int* __restrict__ col_src, int* __restrict__ edge_dst, T* __restrict__ edge_w,
                    T* __restrict__ edge_dx, int* __restrict__ csc_ptr, int* __restrict__ csc_eid,
-                   int* __restrict__ csc_dst, int* __restrict__ gcount, int A) {
+                   int* __restrict__ csc_dst, int* __restrict__ gcount, int A, int e_cap) {
   pdl_entry();
   extern __shared__ __align__(16) unsigned char fsm[];
   double* s_pos = reinterpret_cast<double*>(fsm);
@@ -535,6 +535,25 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
   __syncthreads();
   if (!kFill) {  // count pass: the graph's edge total (scanned between the passes)
     if (threadIdx.x == 0) gcount[g] = s_rp[n];
+    if (g == 0 && threadIdx.x == 0) gcount[n_graphs + 1] = 0;  // overflow flag of this call
+    return;
+  }
+  // edge buffers hold e_cap edges: a batch with more raises the overflow flag
+  // (read by the host, gfm_radius_batch_overflow) and is emitted edge-free
+  // instead of writing out of bounds
+  const int total = gcount[n_graphs];
+  if (total > e_cap) {
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      rowptr[lo + t] = 0;
+      csc_ptr[lo + t] = 0;
+    }
+    if (g == n_graphs - 1)
+      for (int t = node_off[n_graphs] + threadIdx.x; t <= n_nodes; t += blockDim.x) {
+        rowptr[t] = 0;
+        csc_ptr[t] = 0;
+        if (t < n_nodes) gnode[t] = -1;
+      }
+    if (g == 0 && threadIdx.x == 0) gcount[n_graphs + 1] = 1;
     return;
   }
   for (int i = wib; i < n; i += kFusedWarps)
@@ -566,10 +585,14 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
     rowptr[lo + t] = base + s_rp[t];
     csc_ptr[lo + t] = base + s_cs[t];
   }
-  if (g == n_graphs - 1 && threadIdx.x == 0) {
-    rowptr[n_nodes] = base + s_rp[n];
-    csc_ptr[n_nodes] = base + s_rp[n];
-  }
+  // capacity tail (ragged batches in a fixed-capacity runner): nodes past the
+  // last graph are edge-free and belong to no graph
+  if (g == n_graphs - 1)
+    for (int t = node_off[n_graphs] + threadIdx.x; t <= n_nodes; t += blockDim.x) {
+      rowptr[t] = total;
+      csc_ptr[t] = total;
+      if (t < n_nodes) gnode[t] = -1;
+    }
   for (int i = wib; i < n; i += kFusedWarps) {
     const int r0 = s_rp[i], deg = s_rp[i + 1] - r0;
     for (int k = lane; k < deg; k += 32) {
@@ -782,14 +805,16 @@ int gfm_csc_from_csr(const int* rowptr, const int* col_src, const int* edge_dst,
 }
 
 size_t gfm_radius_batch_workspace_bytes(int n_graphs) {
-  return sizeof(int) * (size_t)((n_graphs > 0 ? n_graphs : 1) + 1) + 256;
+  return sizeof(int) * (size_t)((n_graphs > 0 ? n_graphs : 1) + 2) + 256;
 }
+
+int gfm_radius_batch_overflow_index(int n_graphs) { return n_graphs + 1; }
 
 int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, int n_nodes,
                      int max_atoms, const double* cells, double rc, int max_nbr, int* gnode,
                      int* rowptr, int* col_src, int* edge_dst, void* edge_w, void* edge_dx,
-                     int* csc_ptr, int* csc_eid, int* csc_dst, void* workspace, int dtype,
-                     void* stream) {
+                     int* csc_ptr, int* csc_eid, int* csc_dst, int e_cap, void* workspace,
+                     int dtype, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (max_atoms > kFusedMaxAtoms || max_atoms < 0 || n_graphs <= 0) {
     set_error("gfm_radius_batch: graphs of up to %d atoms (got %d), n_graphs >= 1",
@@ -814,11 +839,11 @@ int gfm_radius_batch(const double* pos, const int* node_offsets, int n_graphs, i
     if (e != cudaSuccess) return e;
     launch_k(k_radius_batch<T, false>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
              n_graphs, n_nodes, cells, rc, max_nbr, stride, gnode, rowptr, col_src, edge_dst,
-             (T*)edge_w, (T*)edge_dx, csc_ptr, csc_eid, csc_dst, gcount, A);
+             (T*)edge_w, (T*)edge_dx, csc_ptr, csc_eid, csc_dst, gcount, A, e_cap);
     launch_k(k_scan_totals, 1, kScanThreads, 0, s, gcount, n_graphs);
     launch_k(k_radius_batch<T, true>, n_graphs, kFusedWarps * 32, smem, s, pos, node_offsets,
              n_graphs, n_nodes, cells, rc, max_nbr, stride, gnode, rowptr, col_src, edge_dst,
-             (T*)edge_w, (T*)edge_dx, csc_ptr, csc_eid, csc_dst, gcount, A);
+             (T*)edge_w, (T*)edge_dx, csc_ptr, csc_eid, csc_dst, gcount, A, e_cap);
     return cudaGetLastError();
   };
   if (dtype == GFM_F32)

@@ -193,16 +193,24 @@ constexpr int kLossBlocks = 64;
 template <typename T>
 __global__ void __launch_bounds__(256)
     k_loss_seeds(const T* __restrict__ e_pred, const T* __restrict__ e_true,
-                 const int* __restrict__ n_per, int B, const T* __restrict__ f_pred,
-                 const T* __restrict__ f_true, int N, T aE, T aF, T* __restrict__ loss,
-                 T* __restrict__ de, T* __restrict__ df, float* __restrict__ contrib,
-                 double* __restrict__ partial, unsigned* __restrict__ ticket) {
+                 const int* __restrict__ n_per, int B_cap, const T* __restrict__ f_pred,
+                 const T* __restrict__ f_true, int N_cap, const int* __restrict__ counts, T aE,
+                 T aF, T* __restrict__ loss, T* __restrict__ de, T* __restrict__ df,
+                 float* __restrict__ contrib, double* __restrict__ partial,
+                 unsigned* __restrict__ ticket) {
   pdl_entry();
   __shared__ double red[2][8];
   __shared__ bool last;
+  // ragged batches in a fixed-capacity step: the true graph / node counts
+  // come from the device ([B, N]); the capacity tail gets zero seeds
+  const int B = counts ? counts[0] : B_cap, N = counts ? counts[1] : N_cap;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
   double se = 0.0, sf = 0.0;
-  for (int b = tid; b < B; b += nth) {
+  for (int b = tid; b < B_cap; b += nth) {
+    if (b >= B) {
+      de[b] = T(0);
+      continue;
+    }
     const T r = div_rn(sub_rn(e_pred[b], e_true[b]), (T)n_per[b]);
     se += (double)fabs(r);
     de[b] = div_rn(mul_rn(aE, sign_t(r)), (T)n_per[b] * (T)B);
@@ -215,6 +223,7 @@ __global__ void __launch_bounds__(256)
     sf += (double)fabs(d);
     df[k] = d > T(0) ? q : (d < T(0) ? -q : T(0));
   }
+  for (int k = 3 * N + tid; k < 3 * N_cap; k += nth) df[k] = T(0);
   se = warp_sum(se);
   sf = warp_sum(sf);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -264,7 +273,8 @@ __global__ void k_energy_seed(const T* __restrict__ de, const int* __restrict__ 
   pdl_entry();
   // 2D: y over nodes, x over the G columns (no 64-bit divides)
   for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
-    const T s = de[gnode[i]];
+    const int gi = gnode[i];  // -1: capacity-tail node of a ragged batch
+    const T s = gi >= 0 ? de[gi] : T(0);
     if (threadIdx.x < ld_ds) ds[(long long)i * ld_ds + threadIdx.x] = threadIdx.x == 0 ? s : T(0);
     const long long row = (long long)i * G;
     for (int g = threadIdx.x; g < G; g += blockDim.x) {
@@ -284,7 +294,8 @@ __global__ void k_energy_seed4(const float* __restrict__ de, const int* __restri
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t / G4), q = (int)(t - (long long)i * G4);
-    const float s = de[gnode[i]];
+    const int gi = gnode[i];
+    const float s = gi >= 0 ? de[gi] : 0.f;
     if (q == 0)
       for (int k = 0; k < ld_ds; ++k) ds[(long long)i * ld_ds + k] = k == 0 ? s : 0.f;
     const float4 yv = reinterpret_cast<const float4*>(y)[t];
@@ -850,16 +861,17 @@ int gfm_energy_readout(const void* y, int n_nodes, int G, const void* a, const v
 size_t gfm_loss_workspace_bytes(void) { return sizeof(double) * 2 * kLossBlocks + 256; }
 
 int gfm_loss_seeds(const void* e_pred, const void* e_true, const int* n_per, int n_graphs,
-                   const void* f_pred, const void* f_true, int n_nodes, double alpha_e,
-                   double alpha_f, void* loss, void* de, void* df, float* contrib,
-                   void* workspace, int dtype, void* stream) {
+                   const void* f_pred, const void* f_true, int n_nodes, const int* counts,
+                   double alpha_e, double alpha_f, void* loss, void* de, void* df,
+                   float* contrib, void* workspace, int dtype, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   double* partial = (double*)workspace;
   unsigned* ticket = (unsigned*)(partial + 2 * kLossBlocks);
   GFM_DISPATCH(dtype, "gfm_loss_seeds",
                (launch_k(k_loss_seeds<T>, kLossBlocks, 256, 0, s,
                     (const T*)e_pred, (const T*)e_true, n_per, n_graphs, (const T*)f_pred,
-                    (const T*)f_true, n_nodes, (T)alpha_e, (T)alpha_f, (T*)loss, (T*)de, (T*)df,
+                    (const T*)f_true, n_nodes, counts, (T)alpha_e, (T)alpha_f, (T*)loss, (T*)de,
+                    (T*)df,
                     contrib, partial, ticket),
                 cudaGetLastError()))
 }

@@ -68,16 +68,32 @@ __global__ void k_cast_f64_f32(const double* __restrict__ in, long long n, float
     out[i] = (float)in[i];
 }
 
+// bias corrections for step t.  The reference evaluates 1.0 - beta ** t on
+// the host (train.py:104-105, libm pow); CUDA's double pow may differ by an
+// ulp, so the host precomputes the values into ``table`` ([len][2]) and the
+// device only looks them up; pow is the fallback past the table's end.
+__device__ __forceinline__ void bias_corr_at(long long tt, double b1, double b2, double* bc,
+                                             const double* table, long long table_len) {
+  if (table != nullptr && tt < table_len) {
+    bc[0] = table[2 * tt];
+    bc[1] = table[2 * tt + 1];
+  } else {
+    bc[0] = 1.0 - pow(b1, (double)tt);
+    bc[1] = 1.0 - pow(b2, (double)tt);
+  }
+}
+
 // t += 1; bc = [1 - b1^t, 1 - b2^t] on the device so a captured step needs
-// no host round trip; frozen once the non-finite flag is set.
+// no host round trip; frozen once the non-finite flag is set.  bc == NULL
+// (SGD) advances the applied-step count only.
 __global__ void k_adam_advance(long long* t, double b1, double b2, double* bc,
+                               const double* table, long long table_len,
                                const int* __restrict__ skip) {
   pdl_entry();
   if (skip && *skip) return;
   const long long tt = *t + 1;
   *t = tt;
-  bc[0] = 1.0 - pow(b1, (double)tt);
-  bc[1] = 1.0 - pow(b2, (double)tt);
+  if (bc) bias_corr_at(tt, b1, b2, bc, table, table_len);
 }
 
 // Guard and Adam advance in one launch: every block ORs its verdict into
@@ -86,7 +102,8 @@ __global__ void k_adam_advance(long long* t, double b1, double b2, double* bc,
 // flag is set.  Saves one dependent launch on the step's critical path.
 template <typename G>
 __global__ void k_nonfinite_advance(const G* __restrict__ v, long long n, int* flag,
-                                    long long* t, double b1, double b2, double* bc) {
+                                    long long* t, double b1, double b2, double* bc,
+                                    const double* table, long long table_len) {
   pdl_entry();
   int bad = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -102,8 +119,7 @@ __global__ void k_nonfinite_advance(const G* __restrict__ v, long long n, int* f
   if (t == nullptr || *(volatile int*)flag) return;
   const long long tt = *t + 1;
   *t = tt;
-  bc[0] = 1.0 - pow(b1, (double)tt);
-  bc[1] = 1.0 - pow(b2, (double)tt);
+  if (bc) bias_corr_at(tt, b1, b2, bc, table, table_len);
 }
 
 static inline int grid_for(long long n) {
@@ -136,15 +152,16 @@ int gfm_nonfinite_flag(const void* v, long long n, int dtype, int* flag, void* s
 }
 
 int gfm_nonfinite_advance(const void* v, long long n, int dtype, int* flag, long long* step,
-                          double beta1, double beta2, double* bias_corr, void* stream) {
+                          double beta1, double beta2, double* bias_corr, const double* bc_table,
+                          long long table_len, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = grid_for(n > 0 ? n : 1);
   if (dtype == GFM_F32)
     launch_k(k_nonfinite_advance<float>, grid, 256, 0, s, (const float*)v, n, flag, step, beta1,
-             beta2, bias_corr);
+             beta2, bias_corr, bc_table, table_len);
   else if (dtype == GFM_F64)
     launch_k(k_nonfinite_advance<double>, grid, 256, 0, s, (const double*)v, n, flag, step, beta1,
-             beta2, bias_corr);
+             beta2, bias_corr, bc_table, table_len);
   else {
     set_error("gfm_nonfinite_advance: bad dtype %d", dtype);
     return GFM_EINVAL;
@@ -197,8 +214,10 @@ int gfm_sgd_step(const void* grad_sum, int grad_dtype, long long n, double world
 }
 
 int gfm_adam_advance(long long* step, double beta1, double beta2, double* bias_corr,
-                     const int* skip_flag, void* stream) {
-  launch_k(k_adam_advance, 1, 1, 0, (cudaStream_t)stream, step, beta1, beta2, bias_corr, skip_flag);
+                     const double* bc_table, long long table_len, const int* skip_flag,
+                     void* stream) {
+  launch_k(k_adam_advance, 1, 1, 0, (cudaStream_t)stream, step, beta1, beta2, bias_corr, bc_table,
+           table_len, skip_flag);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) set_error("gfm_adam_advance: %s", cudaGetErrorString(e));
   return (int)e;

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -287,6 +288,8 @@ class Batch:
     CSR position to the record edge index (the reference's stable argsort).
     Labels are mutable and read at loss time, as in the reference."""
 
+    counts = None  # device [B, N] of a ragged batch in capacity buffers (else None)
+
     def __init__(self, **kw):
         self.dtype = kw.pop("dtype")
         self._e_true = None
@@ -409,7 +412,8 @@ def make_batch(records, device=None, dtype=torch.float32) -> Batch:
 def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
                  host_offsets: np.ndarray, rc: float, max_nbr: int = 0, cells=None,
                  energy_true=None, forces_true=None, dtype=torch.float32, e_cap=None,
-                 out: dict | None = None, fused: bool | None = None) -> Batch:
+                 out: dict | None = None, fused: bool | None = None,
+                 max_atoms: int | None = None) -> Batch:
     """Batch assembly from device-resident raw structures: the radius graph
     (build_cutoff_edges, preprocess.py:90-104, plus cap / minimum-image
     extensions) is built on the GPU directly as the dst-sorted CSR.
@@ -417,7 +421,15 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
     ``e_cap`` bounds the edge buffers (default: exact count, one host sync);
     pass ``n_nodes * max_nbr`` to stay sync-free (CUDA-graph capture).
     ``fused`` (default: when ``e_cap`` is given and the graphs are small
-    enough) builds everything in one per-graph kernel (gfm_radius_batch)."""
+    enough) builds everything in one per-graph kernel (gfm_radius_batch).
+
+    Capacity mode (ragged batches, fused path only): ``node_offsets`` is a
+    device array whose contents change per step, ``host_offsets`` only fixes
+    the graph capacity B (its length) and ``max_atoms`` bounds any graph's
+    size; ``pos`` may hold more rows than ``node_offsets[B]`` (the tail is
+    edge-free and graph-less).  ``out["n_per_graph"]`` / ``out["counts"]``
+    (device [B, N]) preset by the caller are used as the batch's per-graph
+    sizes and true counts."""
     dev = pos.device
     code = _lib.dtype_code(dtype)
     N = int(pos.shape[0])
@@ -434,11 +446,15 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
 
     gnode = buf("gnode", (max(N, 1),), torch.int32)
     n_per = np.diff(host_offsets)
-    max_atoms = int(n_per.max()) if n_per.size else 0
+    if max_atoms is None:
+        max_atoms = int(n_per.max()) if n_per.size else 0
     can_fuse = e_cap is not None and B > 0 and max_atoms <= _FUSED_MAX_ATOMS and (
         bool(max_nbr) or max_atoms <= _FUSED_UNCAPPED_ATOMS)
     if fused and not can_fuse:
         raise ValidationError("fused batch assembly needs e_cap and graphs of <= 256 atoms")
+    if o.get("counts") is not None and not (can_fuse and fused is not False):
+        raise ValidationError("ragged (capacity) batches need the fused assembly: e_cap given, "
+                              "graphs of <= 256 atoms")
     if can_fuse and fused is not False:
         # one fused kernel: neighbour search + CSR + CSC + graph_of_node
         Ec = max(int(e_cap), 1)
@@ -453,7 +469,8 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
         ws = buf("rb_ws", (query("gfm_radius_batch_workspace_bytes", B),), torch.uint8)
         call("gfm_radius_batch", ptr(pos), ptr(node_offsets), B, N, max_atoms, ptr(cells),
              float(rc), int(max_nbr or 0), ptr(gnode), ptr(rowptr), ptr(col_src), ptr(edge_dst),
-             ptr(edge_w), ptr(edge_dx), ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), ptr(ws), code, s)
+             ptr(edge_w), ptr(edge_dx), ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), Ec, ptr(ws),
+             code, s)
         return _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets,
                                     energy_true, forces_true, rowptr, col_src, edge_dst, edge_w,
                                     edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, None,
@@ -491,6 +508,16 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
                                 _deg_bound(max_atoms, max_nbr))
 
 
+def radius_batch_overflowed(out: dict, n_graphs: int) -> bool:
+    """True when the last fused radius_batch into ``out`` found more edges
+    than its e_cap (the batch was emitted edge-free; reads one int, syncs)"""
+    ws = out.get("rb_ws")
+    if ws is None:
+        return False
+    k = query("gfm_radius_batch_overflow_index", int(n_graphs))
+    return bool(ws[4 * k:4 * k + 4].view(torch.int32).item())
+
+
 # fused batch assembly limits (gfm_radius_batch: <= 256 atoms per graph; the
 # uncapped neighbour lists must fit in shared memory)
 _FUSED_MAX_ATOMS = 256
@@ -522,7 +549,8 @@ def _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offset
                  forces_true=forces_true, rowptr=rowptr, col_src=col_src, edge_dst=edge_dst,
                  edge_w=edge_w, edge_dx=edge_dx, csc_ptr=csc_ptr, csc_eid=csc_eid,
                  csc_dst=csc_dst, order=None, n_nodes=N, e_cap=int(e_cap), _n_edges=n_edges,
-                 host_offsets=np.asarray(host_offsets), host_n_per=n_per, max_deg=max_deg)
+                 host_offsets=np.asarray(host_offsets), host_n_per=n_per, max_deg=max_deg,
+                 counts=o.get("counts"))
 
 
 # --------------------------------------------------------------------------
@@ -551,10 +579,19 @@ class _Scratch:
         return self.get(name, (max(int(n), 1),), torch.uint8)
 
     def side_stream(self):
-        """second stream for work with no consumer until a later join"""
+        """second stream for work with no consumer until a later join (one
+        per device and thread, shared by every scratch: API calls without a
+        scratch object do not create a stream per call)"""
         if getattr(self, "_side", None) is None:
-            self._side = torch.cuda.Stream(device=self.device)
+            key = (str(self.device), threading.get_ident())
+            st = _SIDE_STREAMS.get(key)
+            if st is None:
+                st = _SIDE_STREAMS[key] = torch.cuda.Stream(device=self.device)
+            self._side = st
         return self._side
+
+
+_SIDE_STREAMS: dict = {}
 
 
 def _scratch_for(owner, device):
@@ -695,7 +732,7 @@ class LossBreakdown:
 
 
 def _loss_kernel(e_pred, f_pred, e_true, f_true, n_per, alpha_e, alpha_f, scratch=None,
-                 contrib=None):
+                 contrib=None, counts=None):
     dt = e_pred.dtype
     code = _lib.dtype_code(dt)
     sc = _scratch_for(scratch, e_pred.device)
@@ -708,8 +745,8 @@ def _loss_kernel(e_pred, f_pred, e_true, f_true, n_per, alpha_e, alpha_f, scratc
         ws = torch.zeros(query("gfm_loss_workspace_bytes"), dtype=torch.uint8, device=e_pred.device)
         sc.bufs["loss_ws"] = ws
     call("gfm_loss_seeds", ptr(e_pred), ptr(e_true), ptr(n_per), B, ptr(f_pred), ptr(f_true), N,
-         float(alpha_e), float(alpha_f), ptr(vals), ptr(de), ptr(df), ptr(contrib), ptr(ws), code,
-         stream_handle())
+         ptr(counts), float(alpha_e), float(alpha_f), ptr(vals), ptr(de), ptr(df), ptr(contrib),
+         ptr(ws), code, stream_handle())
     return vals, de, df
 
 
@@ -769,7 +806,7 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     F = cfg.fc_layers
     vals, de, df = _loss_kernel(e_pred, f_pred, batch.energy_true, batch.forces_true,
                                 batch.n_per_graph, cfg.alpha_energy, cfg.alpha_forces,
-                                scratch=sc, contrib=contrib)
+                                scratch=sc, contrib=contrib, counts=batch.counts)
     grad = grad_out if grad_out is not None else torch.zeros(params.layout.Pp, dtype=dt,
                                                              device=batch.device)
     gp = ModelParams(cfg, grad)

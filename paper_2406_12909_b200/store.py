@@ -22,6 +22,7 @@ import torch
 from . import _lib
 from ._lib import call, ptr, stream_handle
 from .errors import ValidationError
+from .records import MAX_Z
 
 
 @dataclass
@@ -44,6 +45,11 @@ class _Group:
         self.host_off = np.asarray(off, np.int64).astype(np.int32)
         self.n_samples = self.host_off.shape[0] - 1
         N = int(self.host_off[-1])
+        zz = np.asarray(z).reshape(-1)
+        if zz.size != N or (N and (zz.min() < 1 or zz.max() > MAX_Z)):
+            raise ValidationError(f"store ingest: {zz.size} atomic numbers for {N} atoms, "
+                                  f"each must lie in [1, {MAX_Z}]")
+        self.max_atoms = int(np.diff(self.host_off).max()) if self.n_samples else 0
         self.z = torch.as_tensor(np.asarray(z).reshape(N).astype(np.int32), device=device)
         self.pos = torch.as_tensor(np.asarray(pos, np.float64).reshape(N, 3), device=device)
         self.energy = torch.as_tensor(np.asarray(energy, np.float64).reshape(self.n_samples),
@@ -159,11 +165,11 @@ class DeviceStructureStore:
 
     def load_runner(self, group, indices, runner) -> None:
         """Write structures ``indices`` straight into a StructureStepRunner's
-        input slots (its fixed layout must match the structures' sizes);
-        follow with ``runner.run()``."""
+        input slots (a fixed-layout runner needs matching structure sizes; a
+        ragged runner takes any batch within its capacity); follow with
+        ``runner.run()``."""
         g = self._groups[group]
         idx = self._check(g, indices)
-        if not np.array_equal(self.host_offsets(group, idx), runner.host_off):
-            raise ValidationError("batch structure sizes do not match the runner's layout")
+        runner.set_layout(self.host_offsets(group, idx))
         s = runner.slot
         self._launch(g, idx, runner.off, s["z"], s["pos"], s["e"], s["f"], runner.tr.dtype)

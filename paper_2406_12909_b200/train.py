@@ -15,6 +15,7 @@ which is exactly the reference's "update discarded, training aborted"
 
 from __future__ import annotations
 
+import contextlib
 import json
 import logging
 import struct
@@ -31,12 +32,14 @@ from .comm import Comm, LocalComm
 from .errors import ConfigError, CorruptionError, FormatError, UnsupportedVersionError, ValidationError
 from .model import (ModelConfig, ModelParams, _Scratch, count_params, forward_batch, param_layout,
                     init_params_flat, loss_and_grad, make_batch)
+from .records import MAX_Z
 from .schedule import epoch_schedule
 from .telemetry import PhaseClock
 
 log = logging.getLogger(__name__)
 
 OPTIMIZERS = ("adam", "sgd")
+BC_TABLE_LEN = 1 << 20  # steps with host-exact Adam bias corrections (16 MB)
 
 
 @dataclass
@@ -197,6 +200,13 @@ class DataParallelTrainer:
         self.v = torch.zeros_like(self.master)
         self.t_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.bc = torch.zeros(2, dtype=torch.float64, device=self.device)
+        # host-computed bias corrections 1 - beta ** t (train.py:104-105, the
+        # reference's libm pow), looked up by the device step counter; filled
+        # ahead of the host's step count in chunks (fixed address: captured
+        # steps keep reading the same table)
+        self.bc_table = torch.zeros(2 * BC_TABLE_LEN, dtype=torch.float64, device=self.device)
+        self._bc_filled = 0
+        self._ensure_bc(1024)
         self.flag = torch.zeros(2, dtype=torch.int32, device=self.device)  # [non-finite, ticket]
         self.contrib = torch.zeros(P + 2, dtype=dtype, device=self.device)
         if dtype == torch.float32:
@@ -208,17 +218,33 @@ class DataParallelTrainer:
         self.scratch = _Scratch(self.device)
         self.steps = 0
 
-    def compute(self, batch):
-        """forward + backward into ``contrib`` (or zeros when no batch)."""
+    def _ensure_bc(self, steps_ahead: int):
+        """make the bias-correction table cover step counts < steps_ahead"""
+        want = min(int(steps_ahead), BC_TABLE_LEN)
+        if want <= self._bc_filled or self.tcfg.optimizer != "adam":
+            return
+        hi = min(BC_TABLE_LEN, max(want, 2 * self._bc_filled, 1024))
+        b1, b2 = self.tcfg.beta1, self.tcfg.beta2
+        vals = [x for t in range(self._bc_filled, hi)
+                for x in ((1.0 - b1 ** t, 1.0 - b2 ** t) if t else (0.0, 0.0))]
+        self.bc_table[2 * self._bc_filled:2 * hi].copy_(
+            torch.tensor(vals, dtype=torch.float64))
+        self._bc_filled = hi
+
+    def compute(self, batch, scratch=None):
+        """forward + backward into ``contrib`` (or zeros when no batch).
+        ``scratch``: activation buffers to use (default: the trainer's own;
+        a runner keeps one per captured shape)."""
         P = self.P
         if batch is None:
             self.contrib.zero_()
             return
+        sc = scratch if scratch is not None else self.scratch
         if self.dtype == torch.float32:
-            loss_and_grad(self.params, batch, scratch=self.scratch, grad_out=self.contrib[:P],
+            loss_and_grad(self.params, batch, scratch=sc, grad_out=self.contrib[:P],
                           contrib=self.contrib[P:], flags=self.flags)
         else:
-            lb, _ = loss_and_grad(self.params, batch, scratch=self.scratch,
+            lb, _ = loss_and_grad(self.params, batch, scratch=sc,
                                   grad_out=self.contrib[:P], flags=self.flags)
             self.contrib[P:P + 1].copy_(lb.values[:1])
             self.contrib[P + 1].fill_(1.0)
@@ -226,13 +252,17 @@ class DataParallelTrainer:
     def reduce_and_update(self):
         P = self.P
         s = stream_handle()
-        self.comm.allreduce_sum_(self.contrib)
+        _allreduce(self.comm, self.contrib)
         code = _lib.dtype_code(self.dtype)
         adam = self.tcfg.optimizer == "adam"
-        # train.py:262-274 guard, fused with Adam's device step counter
+        capturing = torch.cuda.is_current_stream_capturing()
+        if not capturing:  # a captured replay's caller advances the count
+            self._ensure_bc(self.steps + 2)
+        # train.py:262-274 guard, fused with the device's applied-step counter
+        # (and Adam's bias corrections)
         call("gfm_nonfinite_advance", ptr(self.contrib), P + 1, code, ptr(self.flag),
-             ptr(self.t_dev) if adam else None, float(self.tcfg.beta1), float(self.tcfg.beta2),
-             ptr(self.bc), s)
+             ptr(self.t_dev), float(self.tcfg.beta1), float(self.tcfg.beta2),
+             ptr(self.bc) if adam else None, ptr(self.bc_table), self._bc_filled, s)
         out32 = self.work if self.dtype == torch.float32 else None
         world = float(self.comm.size)
         if adam:
@@ -243,12 +273,33 @@ class DataParallelTrainer:
         else:
             call("gfm_sgd_step", ptr(self.contrib), code, P, world, ptr(self.master),
                  float(self.tcfg.learning_rate), ptr(self.flag), ptr(out32), s)
-        self.steps += 1
+        if not capturing:
+            self.steps += 1
 
-    def step(self, batch):
-        self.compute(batch)
+    def step(self, batch, scratch=None):
+        self.compute(batch, scratch)
         self.reduce_and_update()
         return self.contrib[self.P:self.P + 2]
+
+    def state_tensors(self):
+        """every device tensor a step mutates (for snapshot / restore)"""
+        ts = [self.master, self.m, self.v, self.t_dev, self.bc, self.flag, self.contrib]
+        if self.work is not self.master:
+            ts.append(self.work)
+        return ts
+
+    @contextlib.contextmanager
+    def preserved(self):
+        """run steps (e.g. capture warm-ups) without changing the training
+        state: parameters, moments, counters and flags are restored after"""
+        saved = [t.clone() for t in self.state_tensors()]
+        steps = self.steps
+        try:
+            yield self
+        finally:
+            for t, c in zip(self.state_tensors(), saved):
+                t.copy_(c)
+            self.steps = steps
 
     @property
     def nan_event(self) -> bool:
@@ -262,10 +313,7 @@ class DataParallelTrainer:
         count ``t`` (train.py:100: every applied update, SGD included; a
         discarded non-finite step does not count)."""
         lay = self.layout
-        if self.tcfg.optimizer == "adam":
-            t = int(self.t_dev.item())
-        else:
-            t = self.steps - int(self.nan_event)
+        t = int(self.t_dev.item())  # applied updates only (device counter)
         return OptimizerState(lay.compact(self.m).cpu().numpy(), lay.compact(self.v).cpu().numpy(),
                               t)
 
@@ -278,124 +326,283 @@ class DataParallelTrainer:
         return self.layout.compact(self.contrib[:self.P]).to(torch.float64).cpu().numpy()
 
 
+def _allreduce(comm, contrib: torch.Tensor):
+    """In-place sum of the step payload across ranks.  Comm objects of this
+    package reduce the device tensor directly (NCCL); any other object with
+    the reference's Comm contract (comm.py:55-77, e.g. gfmkit's StarComm)
+    goes through the host: float64 allreduce_sum of the payload, copied back."""
+    fn = getattr(comm, "allreduce_sum_", None)
+    if fn is not None:
+        fn(contrib)
+        return
+    if getattr(comm, "size", 1) == 1:
+        return
+    out = comm.allreduce_sum(contrib.detach().to("cpu", torch.float64).numpy())
+    contrib.copy_(torch.as_tensor(np.asarray(out), dtype=contrib.dtype))
+
+
+class _Shape:
+    """One captured step shape of a runner: node capacity N, edge capacity,
+    its own activation scratch and batch buffers (so graphs captured for
+    different shapes never share a reallocated buffer) and its CUDA graphs."""
+
+    def __init__(self, n_nodes: int, e_cap: int, device):
+        self.N = int(n_nodes)
+        self.e_cap = int(e_cap)
+        self.bufs: dict = {}
+        self.scratch = _Scratch(device)
+        self.graph = None
+        self.stage_graphs = None
+        self.batch = None
+
+
 class StructureStepRunner:
-    """Fixed-shape training step on raw structures: device batch assembly
-    (radius graph -> CSR/CSC) + forward + backward + allreduce + update,
-    optionally captured once into a CUDA graph and replayed.
+    """Training step on raw structures: device batch assembly (radius graph
+    -> CSR/CSC) + forward + backward + allreduce + update, captured into a
+    CUDA graph and replayed.
+
+    Fixed layout: ``host_offsets`` gives the per-graph atom counts of every
+    batch.  Ragged layout (``host_offsets=None``, ``max_graphs``,
+    ``max_atoms``): each batch has its own sizes (up to ``max_graphs``
+    structures of up to ``max_atoms`` atoms, as generate_synthetic's
+    ``n_atoms_range`` produces, preprocess.py:107-153; model.py:234-285
+    batches any sizes).  The step is captured once per node capacity in
+    ``node_caps`` (default: one, ``max_graphs * max_atoms``); a batch runs in
+    the smallest capacity holding it, its true graph / node counts read from
+    the device ([B, N] ``counts``), the tail nodes edge-free and seedless.
 
     ``load(...)`` copies a batch's raw inputs (host pinned or device tensors)
     into stable device slots; ``run()`` executes one step; ``step(...)`` =
     load + run + loss read-back (the end-to-end public call)."""
 
-    def __init__(self, trainer: DataParallelTrainer, host_offsets, rc: float, max_nbr: int = 0,
-                 cells=None, use_graph: bool = True, e_cap: int | None = None):
-        from .model import radius_batch  # noqa: F401  (kept local: avoids import cycle)
-
+    def __init__(self, trainer: DataParallelTrainer, host_offsets=None, rc: float = 5.0,
+                 max_nbr: int = 0, cells=None, use_graph: bool = True, e_cap: int | None = None,
+                 *, max_graphs: int | None = None, max_atoms: int | None = None,
+                 node_caps=None):
         self.tr = trainer
         dev = trainer.device
-        self.host_off = np.asarray(host_offsets, np.int32)
-        self.N = int(self.host_off[-1])
-        self.B = int(self.host_off.shape[0] - 1)
-        self.off = torch.as_tensor(self.host_off, device=dev)
         self.rc = float(rc)
         self.max_nbr = int(max_nbr or 0)
+        self.ragged = host_offsets is None
+        if self.ragged:
+            if not max_graphs or not max_atoms:
+                raise ValidationError("a ragged runner needs max_graphs and max_atoms")
+            self.B = int(max_graphs)
+            self.max_atoms = int(max_atoms)
+            caps = sorted({int(c) for c in (node_caps or [self.B * self.max_atoms])})
+            if caps[-1] > self.B * self.max_atoms or caps[0] < 1:
+                raise ValidationError("node capacities must lie in [1, max_graphs * max_atoms]")
+            # the graph-capacity layout handed to radius_batch: B graphs
+            self.host_off = np.zeros(self.B + 1, np.int32)
+        else:
+            self.host_off = np.asarray(host_offsets, np.int32)
+            self.B = int(self.host_off.shape[0] - 1)
+            n = np.diff(self.host_off)
+            self.max_atoms = int(n.max()) if n.size else 0
+            caps = [int(self.host_off[-1])]
+        self.N = caps[-1]
+        # per-step layout words: [counts (2) | node offsets (B+1) | n_per (B)]
+        self.meta = torch.zeros(2 + 2 * self.B + 1, dtype=torch.int32, device=dev)
+        self.counts = self.meta[0:2] if self.ragged else None
+        self.off = self.meta[2:self.B + 3]
+        self.npg = self.meta[self.B + 3:]
+        if not self.ragged:
+            self._write_meta(self.host_off, sync=True)
+        self._meta_ring = [[torch.empty_like(self.meta, device="cpu").pin_memory(), None]
+                           for _ in range(3)]
+        self._meta_k = 0
         self.cells = None if cells is None else torch.as_tensor(
             np.asarray(cells, np.float64).reshape(self.B, 3), device=dev)
-        if e_cap is None:
-            if not self.max_nbr:
-                n = np.diff(self.host_off).astype(np.int64)
-                e_cap = int((n * (n - 1)).sum())
-            else:
-                e_cap = self.N * self.max_nbr
-        self.e_cap = int(e_cap)
+
+        def edge_cap(n_nodes):
+            if e_cap is not None:
+                return int(e_cap)
+            if self.max_nbr:
+                return n_nodes * self.max_nbr
+            if self.ragged:
+                return (n_nodes // max(self.max_atoms, 1) + 1) * self.max_atoms * \
+                    max(self.max_atoms - 1, 0)
+            n = np.diff(self.host_off).astype(np.int64)
+            return int((n * (n - 1)).sum())
+
+        self.shapes = [_Shape(c, edge_cap(c), dev) for c in caps]
+        self.e_cap = self.shapes[-1].e_cap
         dt = trainer.dtype
-        self.slot = dict(pos=torch.empty(self.N, 3, dtype=torch.float64, device=dev),
-                         z=torch.empty(self.N, dtype=torch.int32, device=dev),
-                         e=torch.empty(self.B, dtype=dt, device=dev),
-                         f=torch.empty(self.N, 3, dtype=dt, device=dev))
-        self.bufs = {}
+        self.slot = dict(pos=torch.zeros(self.N, 3, dtype=torch.float64, device=dev),
+                         z=torch.ones(self.N, dtype=torch.int32, device=dev),
+                         e=torch.zeros(self.B, dtype=dt, device=dev),
+                         f=torch.zeros(self.N, 3, dtype=dt, device=dev))
+        self.cur = self.shapes[-1]
         self.use_graph = use_graph
-        self.graph = None
-        self.batch = None
         self.loss_host = torch.empty(2, dtype=torch.float32).pin_memory()
         # pipelined stepping: two pinned loss slots, each with its copy event
         self._loss_slots = [torch.empty(2, dtype=torch.float32).pin_memory() for _ in range(2)]
         self._loss_events = [None, None]
         self._slot = 0
+        self._stage = None
 
-    def load(self, pos, z, energy, forces):
-        for key, v in (("pos", pos), ("z", z), ("e", energy), ("f", forces)):
-            dst = self.slot[key]
-            dst.copy_(v.reshape(dst.shape), non_blocking=True)
+    # ---- compatibility views ---------------------------------------------
+    @property
+    def graph(self):
+        return self.cur.graph
 
-    def _eager(self):
+    @graph.setter
+    def graph(self, g):
+        self.cur.graph = g
+
+    @property
+    def batch(self):
+        return self.cur.batch
+
+    @property
+    def bufs(self):
+        return self.cur.bufs
+
+    # ---- layout --------------------------------------------------------------
+    def _write_meta(self, offsets, sync=False):
+        off = np.asarray(offsets, np.int64)
+        B_true = off.shape[0] - 1
+        host = np.zeros(self.meta.shape[0], np.int32)
+        host[0], host[1] = B_true, off[-1]
+        host[2:2 + B_true + 1] = off
+        host[2 + B_true + 1:self.B + 3] = off[-1]  # empty capacity graphs
+        host[self.B + 3:self.B + 3 + B_true] = np.diff(off)
+        if sync:
+            self.meta.copy_(torch.from_numpy(host))
+            return
+        buf = self._meta_ring[self._meta_k]
+        self._meta_k = (self._meta_k + 1) % len(self._meta_ring)
+        if buf[1] is not None:
+            buf[1].synchronize()  # that staging buffer's last copy is done
+        buf[0].numpy()[:] = host
+        self.meta.copy_(buf[0], non_blocking=True)
+        buf[1] = torch.cuda.Event()
+        buf[1].record()
+
+    def set_layout(self, offsets) -> _Shape:
+        """Ragged: the next batch's node offsets (host, B_true + 1 entries)
+        -> device layout words; selects the smallest capacity holding it."""
+        off = np.asarray(offsets, np.int64).reshape(-1)
+        if not self.ragged:
+            if not np.array_equal(off, self.host_off):
+                raise ValidationError("batch structure sizes do not match the runner's layout")
+            return self.cur
+        n = np.diff(off)
+        if off.shape[0] - 1 > self.B or off.shape[0] < 2:
+            raise ValidationError(f"a batch holds 1..{self.B} structures, got {off.shape[0] - 1}")
+        if n.size and (n.max() > self.max_atoms or n.min() < 0):
+            raise ValidationError(f"structures hold 0..{self.max_atoms} atoms")
+        N = int(off[-1])
+        for sh in self.shapes:
+            if N <= sh.N:
+                self.cur = sh
+                break
+        else:
+            raise ValidationError(f"batch of {N} atoms exceeds the runner's capacity {self.N}")
+        self._write_meta(off)
+        return self.cur
+
+    def load(self, pos, z, energy, forces, offsets=None):
+        """copy one batch's inputs into the device slots (ragged: with its
+        node ``offsets``; tensors may be pinned host or device memory)"""
+        if self.ragged:
+            if offsets is None:
+                raise ValidationError("a ragged runner needs each batch's node offsets")
+            self.set_layout(offsets)
+        N = int(pos.reshape(-1, 3).shape[0])
+        Bt = int(energy.reshape(-1).shape[0])
+        if not isinstance(z, torch.Tensor) or not z.is_cuda:
+            zz = np.asarray(z.numpy() if isinstance(z, torch.Tensor) else z)
+            if zz.size and (zz.min() < 1 or zz.max() > MAX_Z):
+                raise ValidationError(f"atomic numbers must lie in [1, {MAX_Z}]")
+        for key, v, n in (("pos", pos, N), ("z", z, N), ("e", energy, Bt), ("f", forces, N)):
+            dst = self.slot[key][:n]
+            dst.copy_(torch.as_tensor(v).reshape(dst.shape), non_blocking=True)
+
+    # ---- the step ------------------------------------------------------------
+    def _eager(self, sh: _Shape | None = None, slot=None):
         from .model import radius_batch
 
-        self.batch = radius_batch(self.slot["pos"], self.slot["z"], self.off, self.host_off,
-                                  self.rc, self.max_nbr, self.cells, self.slot["e"],
-                                  self.slot["f"], self.tr.dtype, e_cap=self.e_cap, out=self.bufs)
-        self.tr.step(self.batch)
+        sh = sh or self.cur
+        sl = slot or self.slot
+        sh.bufs["n_per_graph"] = self.npg
+        sh.bufs["counts"] = self.counts
+        sh.batch = radius_batch(sl["pos"][:sh.N], sl["z"][:sh.N], self.off, self.host_off,
+                                self.rc, self.max_nbr, self.cells, sl["e"], sl["f"][:sh.N],
+                                self.tr.dtype, e_cap=sh.e_cap, out=sh.bufs,
+                                max_atoms=self.max_atoms)
+        self.tr.step(sh.batch, scratch=sh.scratch)
 
     def capture(self, warmup: int = 2):
-        """Warm up eagerly (allocates every buffer), then record one step."""
-        for _ in range(warmup):
-            self._eager()
-        torch.cuda.synchronize()
-        if self.use_graph:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._eager()
-            self.graph = g
+        """Warm up eagerly (allocates every buffer) and record one step per
+        capacity.  The training state is restored afterwards: capturing adds
+        no training step."""
+        with self.tr.preserved():
+            for sh in self.shapes:
+                for _ in range(warmup):
+                    self._eager(sh)
+                torch.cuda.synchronize()
+                self._check_overflow(sh)
+            if self.use_graph:
+                for sh in self.shapes:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        self._eager(sh)
+                    sh.graph = g
+            torch.cuda.synchronize()
         return self
 
+    def _check_overflow(self, sh):
+        from .model import radius_batch_overflowed
+
+        if radius_batch_overflowed(sh.bufs, self.B):
+            raise ValidationError(f"a batch had more than e_cap={sh.e_cap} edges; raise e_cap")
+
     def run(self):
-        if self.graph is not None:
-            self.graph.replay()
+        self.tr.steps += 1
+        self.tr._ensure_bc(self.tr.steps + 2)
+        if self.cur.graph is not None:
+            self.cur.graph.replay()
         else:
             self._eager()
+            self.tr.steps -= 1  # tr.step counted it
 
-    def step(self, pos, z, energy, forces) -> float:
+    def step(self, pos, z, energy, forces, offsets=None) -> float:
         """End to end: inputs (host or device) -> step -> mean loss on host."""
-        self.load(pos, z, energy, forces)
+        self.load(pos, z, energy, forces, offsets)
         self.run()
         P = self.tr.P
         self.loss_host.copy_(self.tr.contrib[P:P + 2].float(), non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        self._check_overflow(self.cur)
         tot, cnt = float(self.loss_host[0]), float(self.loss_host[1])
         return tot / cnt if cnt else float("nan")
-
-    def _from_stage(self, k):
-        for key, dst in self.slot.items():
-            dst.copy_(self._stage[k][key])
 
     def _build_stages(self):
         """Two device staging copies of the input slots (+ the copy stream)."""
         dev = self.tr.device
         self._stage = [{k: torch.empty_like(v) for k, v in self.slot.items()} for _ in range(2)]
+        for st in self._stage:
+            st["z"].fill_(1)
         self._copy_stream = torch.cuda.Stream(device=dev)
         self._stage_free = [None, None]
         self._stage_i = 0
-        self._graphs = None
 
-    def _capture_stages(self):
+    def _capture_stages(self, sh):
         """One captured step per staging copy, each reading its staging
         buffers directly (no stage -> slot copy; the stage stays busy until
         the step's ``_stage_free`` event).  Capture records without executing,
         so building these never adds a training step."""
         torch.cuda.synchronize()
-        self._graphs = []
-        slot = self.slot
-        try:
-            for k in range(2):
-                self.slot = self._stage[k]
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._eager()
-                self._graphs.append(g)
-        finally:
-            self.slot = slot
+        graphs = []
+        for k in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._eager(sh, self._stage[k])
+            graphs.append(g)
+        sh.stage_graphs = graphs
 
-    def step_pipelined(self, pos, z, energy, forces):
+    def step_pipelined(self, pos, z, energy, forces, offsets=None):
         """As ``step``, but pipelined: the host->device copy of this step's
         inputs runs on a copy stream into one of two staging buffers while the
         previous step computes, and the host reads this step's loss one call
@@ -403,27 +610,42 @@ class StructureStepRunner:
         (pinned) input buffer until two calls later.  Returns the previous
         step's mean loss (None on the first call); call ``drain()`` after the
         last step for its loss."""
-        if getattr(self, "_stage", None) is None:
+        if self._stage is None:
             self._build_stages()
         main = torch.cuda.current_stream(self.tr.device)
+        if self.ragged:
+            if offsets is None:
+                raise ValidationError("a ragged runner needs each batch's node offsets")
+            self.set_layout(offsets)
+        sh = self.cur
         k = self._stage_i
         cs = self._copy_stream
         if self._stage_free[k] is not None:
             cs.wait_event(self._stage_free[k])  # the step that last read stage k is done
+        ins = (("pos", pos), ("z", z), ("e", energy), ("f", forces))
+        if any(isinstance(v, torch.Tensor) and v.is_cuda for _, v in ins):
+            cs.wait_stream(main)  # device inputs produced on the compute stream
+        N = int(pos.reshape(-1, 3).shape[0])
+        Bt = int(energy.reshape(-1).shape[0])
         with torch.cuda.stream(cs):
-            for key, v in (("pos", pos), ("z", z), ("e", energy), ("f", forces)):
-                dst = self._stage[k][key]
-                dst.copy_(v.reshape(dst.shape), non_blocking=True)
+            for key, v in ins:
+                n = Bt if key == "e" else N
+                dst = self._stage[k][key][:n]
+                dst.copy_(torch.as_tensor(v).reshape(dst.shape), non_blocking=True)
+                if isinstance(v, torch.Tensor) and v.is_cuda:
+                    v.record_stream(cs)
         copied = torch.cuda.Event()
         copied.record(cs)
         main.wait_event(copied)
-        if self.use_graph and self._graphs is None and self.batch is not None:
-            self._capture_stages()  # buffers exist (an earlier eager step allocated them)
-        if self._graphs is not None:
-            self._graphs[k].replay()
+        if self.use_graph and sh.stage_graphs is None and sh.batch is not None:
+            self._capture_stages(sh)  # buffers exist (an earlier eager step allocated them)
+        self.tr.steps += 1
+        self.tr._ensure_bc(self.tr.steps + 2)
+        if sh.stage_graphs is not None:
+            sh.stage_graphs[k].replay()
         else:
-            self._from_stage(k)
-            self._eager()
+            self._eager(sh, self._stage[k])
+            self.tr.steps -= 1
         free = torch.cuda.Event()
         free.record(main)
         self._stage_free[k] = free

@@ -1,0 +1,132 @@
+"""GPU parity at the GFM-scale model shape, and finite-difference checks of
+the GPU's own float64 gradients for the restated aggregations.
+
+* ``test_c3_shape_*``: pna-agg, 6 layers, hidden 512, fc 2 x 512, 84
+  periodic 100-atom crystals (12 A cell, rc 5 A, cap 32): N = 8,400 nodes,
+  ~243k edges.  Inputs are built by the benched path (device radius graph,
+  ``radius_batch``) and the step by ``DataParallelTrainer.compute`` -- the
+  same calls ``bench.py`` times -- against ``tests/golden/c3_shape.npz``
+  (``oracle/make_c3_golden.py``: the float64 oracle at this shape, kink-free
+  targets).  N > 8,192 puts several 128-row tiles on each GEMM CTA and splits
+  the weight-gradient K dimension.  Bars: float64 1e-10; float32 with the
+  default 3xTF32 tensor-core GEMMs, the stated 5e-4 (both relative,
+  elementwise, denominator floored at 1e-3 / 1e-2 of the array's max).
+* ``test_gpu_fp64_gradient_matches_fd``: the reference's FD harness
+  (test_gradients.py:27-108: kink-free targets, step 1e-4, rel 1e-5, floor
+  1e-4) run on the GPU's float64 path for std-agg / pna-agg, capped and
+  periodic.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, golden
+from oracle import gfm_oracle as O
+from oracle.make_c3_golden import SPEC, checksum, inputs
+
+pytestmark = pytest.mark.gpu
+
+from paper_2406_12909_b200 import model as M, train as T  # noqa: E402
+from test_gpu_parity import as_records, assert_close_scaled, cfg_of  # noqa: E402
+from test_oracle_fd import _kinks  # noqa: E402
+
+F64, F32 = torch.float64, torch.float32
+
+
+@pytest.fixture(scope="module")
+def c3():
+    if not os.path.exists(os.path.join(GOLDEN, "c3_shape.npz")):
+        pytest.fail("tests/golden/c3_shape.npz missing: run oracle/make_c3_golden.py")
+    g = golden("c3_shape.npz")
+    recs = inputs()
+    np.testing.assert_array_equal(checksum(recs), g["checksum"])
+    return g, recs
+
+
+def _c3_step(g, recs, dtype):
+    s = SPEC
+    cfg = cfg_of(s["kind"], s["layers"], s["hidden"], s["fc_layers"], s["fc_width"])
+    flat = O.init_flat(O.config(s["kind"], s["layers"], s["hidden"], s["fc_layers"],
+                                s["fc_width"]), s["param_seed"])
+    dev = torch.device("cuda")
+    n = s["n_atoms"]
+    B = len(recs)
+    off = (np.arange(B + 1) * n).astype(np.int32)
+    pos = torch.as_tensor(np.concatenate([r["pos"] for r in recs]), device=dev)
+    z = torch.as_tensor(np.concatenate([r["z"] for r in recs]).astype(np.int32), device=dev)
+    cells = torch.full((B, 3), s["box"], dtype=torch.float64, device=dev)
+    b = M.radius_batch(pos, z, torch.as_tensor(off, device=dev), off, s["rc"], s["max_nbr"],
+                       cells, g["e_true"], g["f_true"], dtype=dtype, e_cap=B * n * s["max_nbr"])
+    assert b.n_edges == int(g["n_edges"])
+    tr = T.DataParallelTrainer(cfg, T.TrainConfig(), initial=flat, dtype=dtype)
+    assert tr.layout.P == int(g["n_params"])
+    tr.compute(b)
+    torch.cuda.synchronize()
+    loss = float(tr.contrib[tr.P].item())
+    grad = tr.flat_grad()
+    e, f = M.forward_batch(tr.params, b)
+    return loss, grad, e.cpu().numpy(), f.cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype,rel,floor", [(F64, 1e-10, 1e-3), (F32, 5e-4, 1e-2)],
+                         ids=["f64", "f32_tc3"])
+def test_c3_shape_vs_oracle(c3, dtype, rel, floor):
+    g, recs = c3
+    loss, grad, e, f = _c3_step(g, recs, dtype)
+    assert_close_scaled(e, g["e_pred"], rel, floor, what="e_pred")
+    assert_close_scaled(f, g["f_pred"], rel, floor, what="f_pred")
+    assert abs(loss - g["loss"][0]) <= rel * abs(g["loss"][0]), (loss, g["loss"][0])
+    idx = g["grad_idx"]
+    want = g["grad_val"]
+    got = grad[idx]
+    # per parameter array: the floor is relative to that array's scale
+    s = SPEC
+    cfg = cfg_of(s["kind"], s["layers"], s["hidden"], s["fc_layers"], s["fc_width"])
+    off = 0
+    for name, shape in M.param_shapes(cfg):
+        n = int(np.prod(shape))
+        sel = (idx >= off) & (idx < off + n)
+        assert_close_scaled(got[sel], want[sel], rel, floor, what=f"grad {name}")
+        off += n
+
+
+def _kink_free(params, b, rng):
+    e, f = M.forward_batch(params, b)
+    e, f = e.cpu().numpy(), f.cpu().numpy()
+    sign = lambda shape: np.where(rng.uniform(size=shape) < 0.5, -1.0, 1.0)
+    b.energy_true = e + (0.5 + rng.uniform(0, 0.5, e.shape)) * sign(e.shape) * b.host_n_per
+    b.forces_true = f + (0.3 + rng.uniform(0, 0.5, f.shape)) * sign(f.shape)
+
+
+@pytest.mark.parametrize("kind,max_nbr,periodic", [("std-agg", None, False),
+                                                   ("pna-agg", None, False),
+                                                   ("pna-agg", 3, True)])
+def test_gpu_fp64_gradient_matches_fd(kind, max_nbr, periodic):
+    cfg = cfg_of(kind, 2, 3, 2, 2)
+    ocfg = O.config(kind, 2, 3, 2, 2)
+    rng = np.random.default_rng(7)
+    recs = O.synthetic(3, n_atoms_range=(3, 6), rc=2.5, box_length=5.5, seed=25,
+                       max_nbr=max_nbr, periodic=periodic)
+    flat = O.init_flat(ocfg, 3)
+    var_gap, max_gap = _kinks(ocfg, flat, O.pack(recs))  # std clamp / max ties
+    assert var_gap > 0.05 and max_gap > 3e-3, (var_gap, max_gap)
+    b = M.make_batch(as_records(recs), dtype=F64)
+    params = M.ModelParams.from_flat(cfg, flat, dtype=F64)
+    _kink_free(params, b, rng)
+    _, analytic = M.loss_and_grad(params, b)
+    analytic = analytic.cpu().numpy()
+    step = 1e-4
+    numeric = np.zeros_like(flat)
+    for k in range(flat.size):
+        p, m = flat.copy(), flat.copy()
+        p[k] += step
+        m[k] -= step
+        lp = M.batch_loss(M.ModelParams.from_flat(cfg, p, dtype=F64), b).total
+        lm = M.batch_loss(M.ModelParams.from_flat(cfg, m, dtype=F64), b).total
+        numeric[k] = (lp - lm) / (2 * step)
+    rel = np.abs(analytic - numeric) / np.maximum(np.maximum(np.abs(analytic), np.abs(numeric)),
+                                                  1e-4)
+    assert rel.max() < 1e-5, f"{kind}: worst rel err {rel.max():.3e} at {int(rel.argmax())}"
