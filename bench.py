@@ -1,17 +1,30 @@
 """Benchmark: training graphs/s of the data-parallel energy+force MTL step.
 
-Workload (BASELINE.json configs[1], "C2"): HydraGNN-PNA stand-in -- pna-agg
-(sum|mean|max|std), 3 message-passing layers, hidden 64, fc 2 x 64 -- on
-synthetic 32-atom molecular graphs (8 A box, radius 5 A, max 20
-neighbours), 1024 graphs per GPU per step.  A step = device batch assembly
-(radius graph -> CSR/CSC) from device-resident raw structures + forward +
-backward + gradient allreduce (NCCL) + Adam.  N > 1: one process per GPU
-(torchrun), per-GPU batch fixed (weak scaling).
+Headline workload (BASELINE.json configs[2], "C3", the north-star GFM-scale
+target): HydraGNN-PNA stand-in -- pna-agg (sum|mean|max|std), 6 message-
+passing layers, hidden 512, fc 2 x 512 -- on synthetic 100-atom periodic
+crystals (12 A cubic cell, radius 5 A, max 32 neighbours), 512 graphs per
+GPU per step.  Nested in the same line: ``c2`` (configs[1]: pna L3 H64,
+1024 x 32-atom molecules, max 20 neighbours) and ``ragged`` (C2 with 20..44
+atoms per structure through the capacity-bucketed runner).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+A step = device batch assembly (radius graph -> CSR/CSC) from device-
+resident raw structures + forward + backward + gradient allreduce (NCCL) +
+Adam, captured once in a CUDA graph and replayed.  N > 1: one process per
+GPU (torchrun), per-GPU batch fixed (weak scaling).  Synthetic structures
+follow the reference's generate_synthetic (preprocess.py:107-153: same rng
+call sequence, ToyPotential labels -- per-element constant + harmonic pairs
+within the cutoff, forces its exact negative gradient).
 
-Prints ONE JSON line on rank 0.  ``--impl reference`` times the CPU oracle
-port (numpy float64, the reference's algorithm) on the host cores instead.
+    python bench.py [--gpus N --steps K --warmup W] [--config c3|c2]
+                    [--impl reference] [--no-nested]
+
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the CPU side
+instead: the numpy float64 oracle port of the reference step on the same
+config over all host cores (the line's value), beside the reference's own
+gfmkit data-parallel path (``scaling.run_strong_scaling(transport=
+"process")``, mean-agg -- the reference has no PNA) when baseline/_ref holds
+the installed reference.
 """
 
 from __future__ import annotations
@@ -30,20 +43,24 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # BASELINE.json configs[1]: the single-GPU headline
-    "c2": dict(kind="pna-agg", layers=3, hidden=64, fc_layers=2, fc_width=64, atoms=32, box=8.0,
-               rc=5.0, max_nbr=20, batch=1024, periodic=False, cpu_sample=32,
+    # BASELINE.json configs[1]: the single-GPU kernel roofline config
+    "c2": dict(kind="pna-agg", layers=3, hidden=64, fc_layers=2, fc_width=64, atoms=(32, 32),
+               box=8.0, rc=5.0, max_nbr=20, batch=1024, periodic=False, cpu_sample=32,
                desc="C2: pna-agg L3 H64 fc2x64, 32-atom graphs, box 8 A, rc 5 A, max 20 "
                     "neighbours, 1024 graphs/GPU"),
-    # BASELINE.json configs[2]: GFM scale, data parallel
-    "c3": dict(kind="pna-agg", layers=6, hidden=512, fc_layers=2, fc_width=512, atoms=100,
+    # BASELINE.json configs[2]: GFM scale, data parallel (the headline)
+    "c3": dict(kind="pna-agg", layers=6, hidden=512, fc_layers=2, fc_width=512, atoms=(100, 100),
                box=12.0, rc=5.0, max_nbr=32, batch=512, periodic=True, cpu_sample=2,
                desc="C3: pna-agg L6 H512 fc2x512, 100-atom periodic crystals, 12 A cell, "
                     "rc 5 A, max 32 neighbours, 512 graphs/GPU"),
+    # C2 with ragged structures (mean 32 atoms): the capacity-bucketed runner
+    "c2r": dict(kind="pna-agg", layers=3, hidden=64, fc_layers=2, fc_width=64, atoms=(20, 44),
+                box=8.0, rc=5.0, max_nbr=20, batch=1024, periodic=False, cpu_sample=32,
+                desc="C2-ragged: as C2 with 20..44 atoms per structure (mean 32)"),
 }
-WORKLOAD = dict(CONFIGS["c2"])
 METRIC = "training graphs/sec (energy+forces MTL) at 1/2/4/8 B200; aggregation HBM GB/s"
 UNIT = "graphs/s"
+DTYPE = "f32 (3xTF32 tensor-core GEMMs, stated bound 5e-4 rel)"
 
 
 def parse():
@@ -52,45 +69,70 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=["c2", "c3"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-graph", action="store_true", help="disable CUDA-graph capture")
+    ap.add_argument("--no-nested", action="store_true", help="skip the nested c2 / ragged lines")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
+    ap.add_argument("--ref-ranks", default="1,2,4,8,all",
+                    help="rank counts of the reference's own DP timing (--impl reference)")
     return ap.parse_args()
 
 
 # ---------------------------------------------------------------- synthetic data
-def make_structures(n_graphs, seed):
-    """Positions / species / labels of n_graphs 32-atom structures (host)."""
+def synthetic(count, W, seed):
+    """generate_synthetic (preprocess.py:107-153): per structure n =
+    integers(lo, hi + 1), species choice over {H, C, O}, positions uniform in
+    the box; ToyPotential labels (preprocess.py:41-87: -0.1 Z per atom +
+    sum over pairs within rc of (r - 1)^2, forces = -grad), vectorised.
+    Returns (z list, pos list, energy array, forces list)."""
+    lo, hi = W["atoms"]
+    zs = np.array([1, 6, 8])
     rng = np.random.default_rng(seed)
-    n = WORKLOAD["atoms"]
-    z = rng.choice(np.array([1, 6, 8]), size=(n_graphs, n)).astype(np.int32)
-    pos = rng.uniform(0.0, WORKLOAD["box"], size=(n_graphs, n, 3))
-    energy = rng.normal(size=n_graphs) * 5.0 - 0.1 * z.sum(axis=1)
-    forces = rng.normal(size=(n_graphs, n, 3))
-    return z, pos, energy, forces
+    Z, P, E, F = [], [], np.zeros(count), []
+    for g in range(count):
+        n = int(rng.integers(lo, hi + 1))
+        z = zs[rng.choice(3, size=n, p=np.full(3, 1.0 / 3.0))]
+        pos = rng.uniform(0.0, W["box"], size=(n, 3))
+        d = pos[:, None, :] - pos[None, :, :]
+        r = np.sqrt((d ** 2).sum(axis=2))
+        pair = np.triu(r <= W["rc"], 1)
+        i, j = np.nonzero(pair)
+        rr = r[i, j]
+        e = float((-0.1 * z).sum() + ((rr - 1.0) ** 2).sum())
+        gvec = (2.0 * (rr - 1.0) / np.maximum(rr, 1e-12))[:, None] * d[i, j]
+        f = np.zeros((n, 3))
+        np.add.at(f, i, -gvec)
+        np.add.at(f, j, gvec)
+        Z.append(z.astype(np.int32))
+        P.append(pos)
+        E[g] = e
+        F.append(f)
+    return Z, P, E, F
 
 
-# ---------------------------------------------------------------- CPU oracle leg
+def packed(count, W, seed):
+    Z, P, E, F = synthetic(count, W, seed)
+    off = np.concatenate([[0], np.cumsum([len(z) for z in Z])]).astype(np.int32)
+    return np.concatenate(Z), np.concatenate(P), E, np.concatenate(F), off
+
+
+# ---------------------------------------------------------------- CPU legs
 def _cpu_worker(args):
-    seed, n_graphs, budget_s, config = args
-    WORKLOAD.update(CONFIGS[config])
+    seed, n_graphs, budget_s, W = args
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import gfm_oracle as O
 
-    cfg = O.config(WORKLOAD["kind"], WORKLOAD["layers"], WORKLOAD["hidden"],
-                   WORKLOAD["fc_layers"], WORKLOAD["fc_width"])
+    cfg = O.config(W["kind"], W["layers"], W["hidden"], W["fc_layers"], W["fc_width"])
     flat = O.init_flat(cfg, 0)
     m = np.zeros_like(flat)
     v = np.zeros_like(flat)
-    z, pos, energy, forces = make_structures(n_graphs, seed)
+    Z, P, E, F = synthetic(n_graphs, W, seed)
     recs = []
     for g in range(n_graphs):
-        cell = (WORKLOAD["box"],) * 3 if WORKLOAD["periodic"] else None
-        edges, shift = O.cutoff_edges(pos[g], WORKLOAD["rc"], max_nbr=WORKLOAD["max_nbr"],
-                                      cell=cell)
-        recs.append(dict(z=z[g], pos=pos[g], edges=edges, shift=shift, energy=energy[g],
-                         forces=forces[g]))
+        cell = (W["box"],) * 3 if W["periodic"] else None
+        edges, shift = O.cutoff_edges(P[g], W["rc"], max_nbr=W["max_nbr"], cell=cell)
+        recs.append(dict(z=Z[g], pos=P[g], edges=edges, shift=shift, energy=E[g], forces=F[g]))
     steps, t = 0, 0
     t0 = time.perf_counter()
     while True:
@@ -103,38 +145,115 @@ def _cpu_worker(args):
     return steps * n_graphs, time.perf_counter() - t0
 
 
-def cpu_oracle_rate(budget_s, procs=None, sample_graphs=None, config="c2"):
+def host_info():
+    """cores used, CPU model and numpy / BLAS versions of this host"""
+    info = dict(cores=len(os.sched_getaffinity(0)))
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    info["numpy"] = np.__version__
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        if blas:
+            info["blas"] = f"{blas[0].get('internal_api')} {blas[0].get('version')}"
+    except Exception:
+        pass
+    return info
+
+
+def cpu_oracle_rate(budget_s, W, procs=None):
     """graphs/s of the numpy oracle step (make_batch + fwd + bwd + Adam, the
     reference's train.py:247-277 minus the fetch) over all host cores: one
-    single-threaded process per core, each on its own 32-graph sample."""
+    single-threaded process per core, each stepping its own sample."""
     import multiprocessing as mp
 
     procs = procs or len(os.sched_getaffinity(0))
-    sample_graphs = sample_graphs or CONFIGS[config]["cpu_sample"]
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
-        res = pool.map(_cpu_worker, [(1000 + k, sample_graphs, budget_s, config)
+        res = pool.map(_cpu_worker, [(1000 + k, W["cpu_sample"], budget_s, W)
                                      for k in range(procs)])
     graphs = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
-    return graphs / wall, procs, (f"{procs} processes x {sample_graphs}-graph "
-                                  f"{config.upper()} samples "
-                                  f"(numpy float64 oracle port, OPENBLAS_NUM_THREADS=1), "
-                                  f"~{budget_s:.0f} s each")
+    return graphs / wall, procs, (f"{procs} processes x {W['cpu_sample']}-graph samples of "
+                                  f"the config (numpy float64 oracle port, "
+                                  f"OPENBLAS_NUM_THREADS=1), ~{budget_s:.0f} s each")
 
 
-def run_reference(args):
+def reference_dp(W, rank_counts, budget_s=8.0):
+    """The reference's own data-parallel CPU path:
+    gfmkit.scaling.run_strong_scaling(transport="process") over a container
+    of gfmkit.generate_synthetic structures, OPENBLAS_NUM_THREADS =
+    cores / ranks.  mean-agg (the reference has no PNA / cap / PBC: its
+    edges are all pairs within rc in the non-periodic box)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "gfmkit")):
+        return dict(unavailable="baseline/_ref has no installed gfmkit")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import tempfile
+
+    from gfmkit.container import write_container
+    from gfmkit.model import ModelConfig
+    from gfmkit.preprocess import generate_synthetic
+    from gfmkit.scaling import run_strong_scaling
+
+    cores = len(os.sched_getaffinity(0))
+    counts = sorted({cores if c == "all" else int(c) for c in rank_counts if c})
+    counts = [c for c in counts if c <= cores]
+    lo, hi = W["atoms"]
+    bs = W["cpu_sample"]
+    # enough samples for every rank to take a few batches at the largest count
+    n_total = max(counts) * bs * 2
+    recs = generate_synthetic(n_total, n_atoms_range=(lo, hi), box_length=W["box"],
+                              cutoff_radius=W["rc"], seed=0)
+    mc = ModelConfig(mpnn_kind="mean-agg", mpnn_layers=W["layers"], mpnn_width=W["hidden"],
+                     fc_layers=W["fc_layers"], fc_width=W["fc_width"], batch_size=bs)
+    out = []
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "c")
+        write_container({"trainset": recs, "valset": recs[:1], "testset": recs[:1]}, 4, path)
+        for p in counts:
+            os.environ["OPENBLAS_NUM_THREADS"] = str(max(1, cores // p))
+            t0 = time.perf_counter()
+            rep = run_strong_scaling(path, [p], mc, transport="process", warmup_epochs=1,
+                                     scratch_dir=tmp, oversubscribe=False)
+            pt = rep.points[0]
+            epoch = max(t.epoch_time_s for t in pt.rank_timings)
+            out.append(dict(ranks=p, blas_threads=max(1, cores // p), graphs=n_total,
+                            epoch_s=epoch, value=n_total / epoch, lif=pt.lif["epoch"],
+                            wait_fractions=pt.wait_fractions,
+                            wall_s=time.perf_counter() - t0))
+    best = max(out, key=lambda r: r["value"])
+    return dict(value=best["value"], unit=UNIT, kind="reference", model="mean-agg (no PNA in "
+                "the reference)", impl="gfmkit.scaling.run_strong_scaling(transport='process')",
+                points=out,
+                sample=f"{n_total} generate_synthetic structures ({lo}..{hi} atoms, box "
+                       f"{W['box']} A, rc {W['rc']} A, uncapped, non-periodic), batch {bs}, "
+                       "1 warm-up + 1 timed epoch per rank count", **host_info())
+
+
+def run_reference(args, W):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s, config=args.config)
+    rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s, W)
+    try:
+        dp = reference_dp(W, args.ref_ranks.split(","))
+    except Exception as exc:  # the reference's harness failing must not lose the line
+        dp = dict(unavailable=f"{type(exc).__name__}: {exc}")
     line = dict(metric=METRIC, value=rate, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, higher_is_better=True, scaling="weak", vs_baseline=None,
                 dtype="f64", data="synthetic", impl="reference",
-                config=dict(workload=WORKLOAD["desc"],
-                            global_batch=WORKLOAD["batch"] * args.gpus),
-                cpu_baseline=dict(value=rate, unit=UNIT, cores=cores, kind="port", sample=sample),
+                config=dict(workload=W["desc"], global_batch=W["batch"] * args.gpus),
+                cpu_baseline=dict(value=rate, unit=UNIT, kind="port", sample=sample,
+                                  **host_info()),
+                reference_dp=dp,
                 e2e=dict(value=rate, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
 
@@ -184,48 +303,113 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- native leg
-def run_native(args):
-    import torch
-    import torch.distributed as dist
+class Ctx:
+    """process-wide state shared by the measurements of one run"""
 
-    from paper_2406_12909_b200 import _lib
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        from paper_2406_12909_b200 import _lib
+        from paper_2406_12909_b200.comm import LocalComm, TorchComm
+
+        self.args = args
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.comm = TorchComm()
+        else:
+            self.comm = LocalComm()
+        _lib.load(require_device=True)
+        self.peaks = {}
+        try:
+            self.peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        self.flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=self.dev)
+
+    def barrier(self):
+        if self.world > 1:
+            self.comm.barrier()
+
+    def max_over_ranks(self, x):
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather(self, x):
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.dev)
+        if self.world == 1:
+            return [float(x)]
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t)
+        return [float(o.item()) for o in out]
+
+    def launch_ms(self, fn, stream, reps=20):
+        """mean device time of fn (CUDA events on the launch stream, L2
+        flushed before every launch)"""
+        import torch
+
+        for _ in range(3):
+            fn()
+        tot = 0.0
+        for _ in range(reps):
+            self.flush.zero_()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            tot += a0.elapsed_time(a1)
+        return tot / reps
+
+
+def _trainer(ctx, W, B):
     from paper_2406_12909_b200 import model as M
     from paper_2406_12909_b200 import train as T
-    from paper_2406_12909_b200.comm import LocalComm, TorchComm
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        comm = TorchComm()
-    else:
-        comm = LocalComm()
-    _lib.load(require_device=True)
-
-    B, n = args.batch, WORKLOAD["atoms"]
-    N = B * n
-    cfg = M.ModelConfig(mpnn_kind=WORKLOAD["kind"], mpnn_layers=WORKLOAD["layers"],
-                        mpnn_width=WORKLOAD["hidden"], fc_layers=WORKLOAD["fc_layers"],
-                        fc_width=WORKLOAD["fc_width"], batch_size=B)
+    cfg = M.ModelConfig(mpnn_kind=W["kind"], mpnn_layers=W["layers"], mpnn_width=W["hidden"],
+                        fc_layers=W["fc_layers"], fc_width=W["fc_width"], batch_size=B)
     tr = T.DataParallelTrainer(cfg, T.TrainConfig(optimizer="adam", learning_rate=1e-3),
-                               comm=comm, device=dev)
-    host_off = (np.arange(B + 1) * n).astype(np.int32)
-    cells = [[WORKLOAD["box"]] * 3] * B if WORKLOAD["periodic"] else None
-    runner = T.StructureStepRunner(tr, host_off, WORKLOAD["rc"], WORKLOAD["max_nbr"], cells=cells,
-                                   use_graph=not args.no_graph)
+                               comm=ctx.comm, device=ctx.dev)
+    return cfg, tr
 
-    # pool of distinct device-resident batches (raw structures + labels)
+
+def measure_step(ctx, W, full=True):
+    """graphs/s of the captured step (inputs resident in HBM), e2e from
+    pinned host buffers, e2e from the HBM sample store, and (full) the
+    kernel rooflines, neighbour-list timing, launches and LIF."""
+    import torch
+
+    from paper_2406_12909_b200 import train as T
+
+    args = ctx.args
+    B = args.batch if (args.batch and W is CONFIGS[args.config]) else W["batch"]
+    n = W["atoms"][1]
+    N = B * n
+    cfg, tr = _trainer(ctx, W, B)
+    host_off = (np.arange(B + 1) * n).astype(np.int32)
+    cells = [[W["box"]] * 3] * B if W["periodic"] else None
+    runner = T.StructureStepRunner(tr, host_off, W["rc"], W["max_nbr"], cells=cells,
+                                   use_graph=not args.no_graph)
+    dev = ctx.dev
     pool = []
     for k in range(8):
-        z, pos, energy, forces = make_structures(B, 1000 * rank + k)
-        pool.append(dict(
-            z=torch.as_tensor(z.reshape(-1), device=dev),
-            pos=torch.as_tensor(pos.reshape(-1, 3), device=dev),
-            e=torch.as_tensor(energy, dtype=torch.float32, device=dev),
-            f=torch.as_tensor(forces.reshape(-1, 3), dtype=torch.float32, device=dev)))
+        z, pos, energy, forces, _ = packed(B, W, 1000 * ctx.rank + k)
+        pool.append(dict(z=torch.as_tensor(z, device=dev), pos=torch.as_tensor(pos, device=dev),
+                         e=torch.as_tensor(energy, dtype=torch.float32, device=dev),
+                         f=torch.as_tensor(forces, dtype=torch.float32, device=dev)))
 
     def load_slot(k):
         d = pool[k % len(pool)]
@@ -239,51 +423,39 @@ def run_native(args):
         print(f"[bench] CUDA-graph capture failed ({exc}); eager launches", file=sys.stderr)
         runner.graph = None
         runner.use_graph = False
-    for i in range(3):
+    for i in range(max(args.warmup, 3)):
         load_slot(i)
         runner.run()
     torch.cuda.synchronize()
 
-    def one(i):
-        load_slot(i)
-        runner.run()
-
-    # ---- timed region: K steps, inputs already in HBM
-    if world > 1:
-        comm.barrier()
+    # ---- timed region: K steps, inputs already in HBM (8-batch pool)
+    ctx.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(ctx.local) as clk:
         ev0.record(s)
         for i in range(args.steps):
-            one(i)
+            load_slot(i)
+            runner.run()
         ev1.record(s)
         torch.cuda.synchronize()
-    if world > 1:
-        comm.barrier()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    value = world * B * args.steps / (ms / 1e3)
+    ctx.barrier()
+    ms = ctx.max_over_ranks(ev0.elapsed_time(ev1))
+    out = dict(value=ctx.world * B * args.steps / (ms / 1e3), ms_per_step=ms / args.steps,
+               clocks=clk.summary(), per_gpu_batch=B, nodes_per_gpu=N,
+               cuda_graph=runner.graph is not None)
 
-    # ---- e2e: the public call (StructureStepRunner.step) from pinned host
-    # buffers, with the loss read back to the host every step
+    # ---- e2e: the public call (StructureStepRunner.step_pipelined) from pinned
+    # host buffers: every step copies its inputs host->device and its loss back
     host = []
     for k in range(4):
-        z, pos, energy, forces = make_structures(B, 5000 + 1000 * rank + k)
-        host.append(dict(z=torch.as_tensor(z.reshape(-1)).pin_memory(),
-                         pos=torch.as_tensor(pos.reshape(-1, 3)).pin_memory(),
+        z, pos, energy, forces, _ = packed(B, W, 5000 + 1000 * ctx.rank + k)
+        host.append(dict(z=torch.as_tensor(z).pin_memory(), pos=torch.as_tensor(pos).pin_memory(),
                          e=torch.as_tensor(energy, dtype=torch.float32).pin_memory(),
-                         f=torch.as_tensor(forces.reshape(-1, 3), dtype=torch.float32).pin_memory()))
+                         f=torch.as_tensor(forces, dtype=torch.float32).pin_memory()))
     h2d = sum(v.numel() * v.element_size() for v in host[0].values())
     d2h = runner.loss_host.numel() * runner.loss_host.element_size()
 
-    # step_pipelined: every step copies its inputs from pinned host memory and
-    # its loss back to pinned host memory; the host reads step i's loss while
-    # step i + 1 runs (asynchronous loss logging), and drain() reads the last
-    # one inside the timed region
     def e2e_step(i):
         hb = host[i % len(host)]
         return runner.step_pipelined(hb["pos"], hb["z"], hb["e"], hb["f"])
@@ -291,31 +463,33 @@ def run_native(args):
     for i in range(2):
         e2e_step(i)
     runner.drain()
-    if world > 1:
-        comm.barrier()
+    ctx.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     losses = [e2e_step(i) for i in range(args.steps)]
     losses.append(runner.drain())
     torch.cuda.synchronize()
     assert all(x is not None and np.isfinite(x) for x in losses[1:]), losses
-    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = world * B * args.steps / float(e2e_s.item())
+    e2e_s = ctx.max_over_ranks(time.perf_counter() - t0)
+    out["e2e"] = dict(value=ctx.world * B * args.steps / e2e_s, unit=UNIT,
+                      h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h,
+                      note="StructureStepRunner.step_pipelined: pinned host inputs copied and "
+                           "the loss read back every step (read one step late)")
+    if not full:
+        out["runner"] = runner
+        return out
 
     # ---- e2e from the HBM-resident sample store: the
-    # dataset (8 batches of structures + labels) is ingested once; per step
-    # only the B sample indices go host->device (gfm_gather_structures writes
-    # the runner's input slots) and the loss comes back (read one step late)
+    # dataset is ingested once; per step only the B sample indices go
+    # host->device and the loss comes back (read one step late)
     from paper_2406_12909_b200.store import DeviceStructureStore
-    zs, ps, es, fs = zip(*(make_structures(B, 9000 + 1000 * rank + k) for k in range(8)))
+    parts = [packed(B, W, 9000 + 1000 * ctx.rank + k) for k in range(8)]
     S = 8 * B
     store = DeviceStructureStore.from_arrays({"trainset": (
-        np.concatenate([z.reshape(-1) for z in zs]), np.concatenate([p.reshape(-1, 3) for p in ps]),
-        np.concatenate(es), np.concatenate([f.reshape(-1, 3) for f in fs]),
+        np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]),
+        np.concatenate([p[2] for p in parts]), np.concatenate([p[3] for p in parts]),
         np.arange(S + 1) * n)}, device=dev)
-    rng = np.random.default_rng(77 + rank)
+    rng = np.random.default_rng(77 + ctx.rank)
     loss_slots = [torch.empty(2, dtype=torch.float32).pin_memory() for _ in range(2)]
     loss_ev = [None, None]
     P = tr.P
@@ -335,35 +509,96 @@ def run_native(args):
 
     for i in range(3):
         store_step(i)
-    if world > 1:
-        comm.barrier()
+    ctx.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     slosses = [store_step(i) for i in range(args.steps)]
     loss_ev[(args.steps - 1) % 2].synchronize()
     torch.cuda.synchronize()
     assert all(x is not None and np.isfinite(x) for x in slosses), slosses
-    st_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(st_s, op=dist.ReduceOp.MAX)
-    store_value = world * B * args.steps / float(st_s.item())
+    st_s = ctx.max_over_ranks(time.perf_counter() - t0)
+    out["e2e_device_store"] = dict(
+        value=ctx.world * B * args.steps / st_s, unit=UNIT, h2d_bytes_per_step=4 * B,
+        d2h_bytes_per_step=d2h,
+        note="dataset resident in HBM (store.DeviceStructureStore); per step: B int32 sample "
+             "indices H2D, loss D2H")
     del store
-    graph = runner.graph
 
-    # ---- roofline of the aggregation kernels (CUDA events on the launch
-    # stream, L2 flushed before every launch): the backward CSC gather is the
-    # step's largest kernel at C2 and C3 (profiles/r01_launches_*), the forward
-    # is reported beside it
+    # ---- load balance (scaling.py:54-72): each rank's compute time (batch
+    # assembly + forward + backward, no collective) over its pool
+    from paper_2406_12909_b200.telemetry import compute_lif, wait_fraction
     load_slot(0)
     runner._eager()
-    b = runner.batch
     torch.cuda.synchronize()
-    E = b.n_edges
+    b = runner.batch
+
+    def compute_only():
+        from paper_2406_12909_b200.model import radius_batch
+        radius_batch(runner.slot["pos"], runner.slot["z"], runner.off, runner.host_off,
+                     runner.rc, runner.max_nbr, runner.cells, runner.slot["e"], runner.slot["f"],
+                     tr.dtype, e_cap=runner.e_cap, out=runner.bufs)
+        tr.compute(b, scratch=runner.cur.scratch)
+
+    busy = ctx.launch_ms(compute_only, s, reps=10)
+    times = ctx.gather(busy)
+    out["load_balance"] = dict(compute_ms_per_rank=times, lif=compute_lif(times),
+                               wait_fraction=wait_fraction(times),
+                               note="scaling.py:54-72 on each rank's device compute time")
+
+    # ---- kernel rooflines (CUDA events on the launch stream, L2 flushed
+    # before every launch) on this step's batch, with the step's own flags
+    out.update(rooflines(ctx, W, cfg, b, s))
+
+    # ---- neighbour lists, GPU batch assembly per graph
+    from paper_2406_12909_b200 import model as M
+
+    def nbr_call():
+        M.radius_batch(runner.slot["pos"], runner.slot["z"], runner.off, runner.host_off,
+                       runner.rc, runner.max_nbr, runner.cells, runner.slot["e"],
+                       runner.slot["f"], tr.dtype, e_cap=runner.e_cap, out=runner.bufs)
+
+    nbr_ms = ctx.launch_ms(nbr_call, s)
+    out["neighbour_list"] = dict(gpu_ms_per_batch=nbr_ms, gpu_us_per_graph=nbr_ms * 1e3 / B,
+                                 note="radius_batch on the step's input slots, L2 flushed")
+    out["edges_per_gpu"] = b.n_edges
+
+    # ---- launches per step (one extra untimed eager step under the profiler):
+    # every kernel of this repository (gfm:: and tc:: namespaces)
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        load_slot(1)
+        with tr.preserved():
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                runner._eager()
+                torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+        ours = [nm for nm in names if "gfm::" in nm or "tc::" in nm]
+        out["gpu_launches"] = len(ours) * args.steps
+        out["launches_per_step"] = len(ours)
+    except Exception:
+        out["gpu_launches"] = None
+    out["runner"] = runner
+    return out
+
+
+def rooflines(ctx, W, cfg, b, s):
+    """The aggregation kernels as the step runs them (uint8 argmax) and the
+    largest GEMM, against MEASURED_PEAKS.json.  ``frac`` uses SURVEY 8(d)'s
+    algorithmic bytes only."""
+    import torch
+
+    from paper_2406_12909_b200 import _lib
+    from paper_2406_12909_b200 import model as M
+
+    dev = ctx.dev
+    N, E = b.n_nodes, b.n_edges
     H, K = cfg.mpnn_width, cfg.n_parts
     parts = M.KIND_PARTS[cfg.mpnn_kind]
+    flags = M._argmax_flag(b)
     h_in = torch.randn(N, H, device=dev)
     agg = torch.empty(N, K * H, device=dev)
-    am = torch.empty(N, H, dtype=torch.int32, device=dev)
+    am = torch.empty(N, H, dtype=torch.uint8 if flags else torch.int32, device=dev)
     sm_ = torch.empty(N, H, device=dev)
     dagg = torch.randn(N, K * H, device=dev)
     dh_b = torch.randn(N, H, device=dev)
@@ -375,150 +610,180 @@ def run_native(args):
 
     def agg_fwd_call():
         _lib.call("gfm_agg_fwd", P_(h_in), N, H, P_(b.rowptr), P_(b.col_src), P_(b.edge_w),
-                  parts, P_(agg), P_(am), P_(sm_), _lib.F32, 0, sh)
+                  parts, P_(agg), P_(am), P_(sm_), _lib.F32, flags, sh)
 
     def agg_bwd_call():
         _lib.call("gfm_agg_bwd", P_(dagg), P_(agg), P_(sm_), P_(am), P_(h_in), P_(b.rowptr),
                   P_(b.csc_ptr), P_(b.csc_eid), P_(b.csc_dst), P_(b.edge_w), N, H, parts,
-                  P_(dh_b), P_(h_in), P_(out_b), P_(ws_b), _lib.F32, 0, sh)
-
-    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
-
-    def launch_ms(fn, reps=20):
-        for _ in range(3):
-            fn()
-        tot = 0.0
-        for _ in range(reps):
-            flush.zero_()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(s)
-            fn()
-            a1.record(s)
-            torch.cuda.synchronize()
-            tot += a0.elapsed_time(a1)
-        return tot / reps
+                  P_(dh_b), P_(h_in), P_(out_b), P_(ws_b), _lib.F32, flags, sh)
 
     agg_fwd_call()
-    fwd_ms, bwd_ms = launch_ms(agg_fwd_call), launch_ms(agg_bwd_call)
-    # SURVEY 8(d) C5 formulas (fused h + src + w mode), s = 4 bytes.
-    # fwd: E*H*s gathered rows + 4E src + 4E w + 4(N+1) rowptr + K*N*H*s out
-    #      + 4*N*H argmax + 4*N*H std mean
-    fwd_bytes = E * H * 4 + 8 * E + 4 * (N + 1) + K * N * H * 4 + 4 * N * H + 4 * N * H
-    # bwd (CSC gather): E*H*s (G rows) + 8E (eid, dst) + 4(N+1) + N*H*s (dh in)
-    #      + E*H*4 argmax (max part) + E*H*s coef (std part) + 4E w + N*H*s out
-    #      + N*H*s h_in (std coef) + N*H*s gate
-    #      + 7*N*H*s for the prep pass the same call launches first (reads dsum,
-    #      dmean, dstd, std, mean; writes G, coef)
-    bwd_bytes = (E * H * 4 + 8 * E + 4 * (N + 1) + N * H * 4 + E * H * 4 + E * H * 4 + 4 * E
-                 + 3 * N * H * 4 + 7 * N * H * 4)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    # DRAM bytes per launch from the committed ncu --set full capture of the
-    # same kernels on this workload (tools/ncu_agg_traffic.sh), when present
-    traffic = {}
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", f"r01_agg_traffic_{args.config}.json")))
-        if tr.get("config") == args.config:
-            traffic = tr
-    except Exception:
-        pass
-
-    # L2-resident read throughput measured on a B200 by tools/l2_bw.cu: the
-    # per-edge row gathers are L2 hits, so this is the ceiling they approach
+    fwd_ms, bwd_ms = ctx.launch_ms(agg_fwd_call, s), ctx.launch_ms(agg_bwd_call, s)
+    s4 = 4
+    # SURVEY 8(d) C5 formulas, fused mode (ii), s = 4 bytes, pna (k = 4, max + std):
+    # fwd: E*H*s + 4E (src) + 4E (w) + 4(N+1) + k*N*H*s + 4*N*H argmax
+    fwd_bytes = E * H * s4 + 8 * E + 4 * (N + 1) + K * N * H * s4 + 4 * N * H
+    # bwd (CSC gather): E*H*s + 8E + 4(N+1) + N*H*s + E*H*4 argmax (max) + E*H*s (std)
+    bwd_bytes = E * H * s4 + 8 * E + 4 * (N + 1) + N * H * s4 + E * H * 4 + E * H * s4
+    peak = float(ctx.peaks.get("hbm_gbs", 6550.0))
     l2 = {}
+    traffic = {}
     try:
         l2 = json.load(open(os.path.join(ROOT, "profiles", "r01_l2_bw.json")))
     except Exception:
         pass
+    name = "c3" if H >= 256 else "c2"
+    for rnd in ("r02", "r01"):
+        try:
+            tr_ = json.load(open(os.path.join(ROOT, "profiles", f"{rnd}_agg_traffic_{name}.json")))
+            if tr_.get("config") == name and tr_.get("flags", 0) == flags:
+                traffic = tr_
+                break
+        except Exception:
+            continue
 
-    def roof(kernel, nbytes, ms_, key):
+    def roof(kernel, nbytes, ms_, key, note):
         ach = nbytes / (ms_ / 1e3) / 1e9
         l2p = l2.get("l2_read_gbs")
+        t = traffic.get(key)
         return dict(kernel=kernel, bound="hbm", achieved=ach, peak=peak, unit="GB/s",
-                    frac=ach / peak, traffic=traffic.get(key), launch_ms=ms_,
-                    algorithmic_bytes=nbytes, l2_peak=l2p, l2_frac=ach / l2p if l2p else None,
-                    l2_peak_source="profiles/r01_l2_bw.json (tools/l2_bw.cu)" if l2p else None,
-                    peak_source="MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
-                    note=("algorithmic bytes per SURVEY 8(d) count every per-edge row gather; "
-                          "those are mostly L2 hits, so frac can exceed 1 -- traffic is the "
-                          "DRAM bytes ncu measured for one launch"))
+                    frac=ach / peak, traffic=t, launch_ms=ms_, algorithmic_bytes=nbytes,
+                    dram_frac=(t / (ms_ / 1e3) / 1e9 / peak) if t else None,
+                    traffic_source=traffic.get("source") if t else None,
+                    l2_peak=l2p, l2_frac=ach / l2p if l2p else None,
+                    peak_source="MEASURED_PEAKS.json hbm_gbs" if ctx.peaks else "fallback",
+                    note=note)
 
-    roof_bwd = roof("gfm_agg_bwd (pna CSC gather)", bwd_bytes, bwd_ms, "agg_bwd_dram_bytes")
-    roof_fwd = roof("gfm_agg_fwd (pna: sum|mean|max|std)", fwd_bytes, fwd_ms, "agg_fwd_dram_bytes")
+    res = dict(
+        roofline=roof("gfm_agg_bwd (pna CSC gather, uint8 argmax as in the step)", bwd_bytes,
+                      bwd_ms, "agg_bwd_dram_bytes",
+                      "frac = SURVEY 8(d) bwd bytes (argmax counted at 4 B/elem as 8(d) "
+                      "states; the step stores 1 B) / time / HBM peak.  The per-edge row "
+                      "gathers are mostly L2 hits: dram_frac is ncu's DRAM bytes / time"),
+        roofline_agg_fwd=roof("gfm_agg_fwd (pna: sum|mean|max|std)", fwd_bytes, fwd_ms,
+                              "agg_fwd_dram_bytes", "SURVEY 8(d) fwd bytes"))
 
-    # ---- neighbour-list construction per graph, the GPU
-    # radius-graph batch assembly (count + fill + CSR/CSC in one pass) on this
-    # batch vs the oracle's build_cutoff_edges restatement on host structures
-    def nbr_call():
-        M.radius_batch(runner.slot["pos"], runner.slot["z"], runner.off, runner.host_off,
-                       runner.rc, runner.max_nbr, runner.cells, runner.slot["e"],
-                       runner.slot["f"], runner.tr.dtype, e_cap=runner.e_cap, out=runner.bufs)
+    # ---- the largest GEMM: a layer's weight gradient [dW | dU | db] =
+    # dz^T [h | agg | 1], M = N rows (split-K), 512 x (H + kH) outputs
+    dz = torch.randn(N, H, device=dev)
+    g1 = torch.empty(H, H, device=dev)
+    g2 = torch.empty(H, K * H, device=dev)
+    gb = torch.empty(H, device=dev)
+    nb = _lib.query("gfm_linear_bwd_weight_workspace_bytes", N, H, H, K * H, 1, _lib.F32)
+    ws = torch.empty(nb, dtype=torch.uint8, device=dev)
 
-    nbr_ms = launch_ms(nbr_call)
-    neighbour_list = dict(gpu_ms_per_batch=nbr_ms, gpu_us_per_graph=nbr_ms * 1e3 / B,
-                          note="radius_batch on the step's input slots, L2 flushed per launch")
-    if rank == 0 and world == 1:
-        from oracle import gfm_oracle as O
-        zc, pc, _, _ = make_structures(64, 4242)
-        t0, done = time.perf_counter(), 0
-        while done < 64 and (done < 4 or time.perf_counter() - t0 < 1.0):
-            O.cutoff_edges(pc[done], WORKLOAD["rc"], max_nbr=WORKLOAD["max_nbr"],
-                           cell=(WORKLOAD["box"],) * 3 if WORKLOAD["periodic"] else None)
-            done += 1
-        cpu_ms = (time.perf_counter() - t0) * 1e3 / done
-        neighbour_list.update(cpu_ms_per_graph=cpu_ms, cpu_cores=1,
-                              cpu_sample=f"{done} graphs, oracle cutoff_edges (numpy fp64)",
-                              speedup=cpu_ms / (nbr_ms / B))
+    def wgrad_call():
+        _lib.call("gfm_linear_bwd_weight", P_(dz), H, N, None, H, P_(h_in), H, H, P_(agg),
+                  K * H, K * H, 1, P_(g1), P_(g2), P_(gb), P_(ws), _lib.F32, sh)
 
-    # ---- launches per step (one extra untimed step under the profiler)
-    launches = None
-    try:
-        from torch.profiler import ProfilerActivity, profile
+    wg_ms = ctx.launch_ms(wgrad_call, s)
+    flops = 2.0 * N * H * (H + K * H + 1)
+    tf = flops / (wg_ms / 1e3) / 1e12
+    pk = float(ctx.peaks.get("bf16_tflops_sustained", 1379.5))
+    res["roofline_gemm"] = dict(
+        kernel="layer weight gradient (tcgen05 3xTF32 split-K + ordered reduce)", bound="tensor",
+        achieved=tf, peak=pk, unit="TFLOP/s", frac=tf / pk, launch_ms=wg_ms,
+        algorithmic_flops=flops,
+        note="useful fp32 flops; each product costs 3 TF32 MMAs (hi*hi + hi*lo + lo*hi); peak "
+             "= MEASURED_PEAKS bf16 sustained")
+    return res
 
-        load_slot(1)
-        with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            one(1)
-            torch.cuda.synchronize()
-        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
-        ours = [nm for nm in names if nm.startswith(("gfm::", "void gfm::")) or "gfm::" in nm]
-        launches = len(ours) * args.steps
-    except Exception:
-        launches = None
 
-    if rank == 0:
-        clocks = clk.summary()
+def measure_ragged(ctx, W, fixed_value):
+    """C2 with 20..44-atom structures (mean 32) through the ragged runner:
+    two captured node capacities (mean + 4 sigma, and the maximum)."""
+    import torch
+
+    from paper_2406_12909_b200 import train as T
+
+    args = ctx.args
+    B = W["batch"]
+    lo, hi = W["atoms"]
+    _, tr = _trainer(ctx, W, B)
+    sd = np.sqrt(((hi - lo + 1) ** 2 - 1) / 12.0) * np.sqrt(B)
+    cap_q = int(np.ceil((B * (lo + hi) / 2 + 4 * sd) / 256.0) * 256)
+    runner = T.StructureStepRunner(tr, None, W["rc"], W["max_nbr"], max_graphs=B,
+                                   max_atoms=hi, node_caps=[min(cap_q, B * hi), B * hi],
+                                   use_graph=not args.no_graph)
+    dev = ctx.dev
+    pool = []
+    for k in range(8):
+        z, pos, energy, forces, off = packed(B, W, 3000 + 1000 * ctx.rank + k)
+        pool.append((torch.as_tensor(pos, device=dev), torch.as_tensor(z, device=dev),
+                     torch.as_tensor(energy, dtype=torch.float32, device=dev),
+                     torch.as_tensor(forces, dtype=torch.float32, device=dev), off))
+    runner.load(*pool[0])
+    runner.capture(warmup=3)
+    for i in range(3):
+        runner.load(*pool[i % 8])
+        runner.run()
+    ctx.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(s)
+    for i in range(args.steps):
+        runner.load(*pool[i % 8])
+        runner.run()
+    ev1.record(s)
+    torch.cuda.synchronize()
+    ms = ctx.max_over_ranks(ev0.elapsed_time(ev1))
+    value = ctx.world * B * args.steps / (ms / 1e3)
+    mean_atoms = float(np.mean([p[4][-1] for p in pool])) / B
+    return dict(value=value, unit=UNIT, ms_per_step=ms / args.steps, workload=W["desc"],
+                node_caps=[sh.N for sh in runner.shapes], mean_atoms_per_graph=mean_atoms,
+                vs_fixed_c2=value / fixed_value if fixed_value else None,
+                note="ragged runner (capacity buckets, device counts); same model and per-GPU "
+                     "batch as C2; vs_fixed_c2 = this / the fixed-size C2 value")
+
+
+def run_native(args):
+    import torch
+
+    ctx = Ctx(args)
+    W = CONFIGS[args.config]
+    main = measure_step(ctx, W, full=True)
+    main.pop("runner")
+    nested = {}
+    if not args.no_nested:
+        torch.cuda.empty_cache()
+        if args.config != "c2":
+            c2 = measure_step(ctx, CONFIGS["c2"], full=False)
+            c2.pop("runner")
+            nested["c2"] = dict(value=c2["value"], unit=UNIT, ms_per_step=c2["ms_per_step"],
+                                e2e=c2["e2e"], workload=CONFIGS["c2"]["desc"],
+                                clocks=c2["clocks"])
+            c2_value = c2["value"]
+        else:
+            c2_value = main["value"]
+        nested["ragged"] = measure_ragged(ctx, CONFIGS["c2r"], c2_value)
+    if ctx.rank == 0:
         cpu = None
-        if world == 1:
-            rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s, config=args.config)
-            cpu = dict(value=rate, unit=UNIT, cores=cores, kind="port", sample=sample)
+        if ctx.world == 1:
+            rate, cores, sample = cpu_oracle_rate(args.cpu_sample_s, W)
+            cpu = dict(value=rate, unit=UNIT, kind="port", sample=sample, **host_info())
+        B = main["per_gpu_batch"]
         line = dict(
-            metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
-            warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True,
-            scaling="weak", vs_baseline=None, dtype="f32", data="synthetic",
-            config=dict(workload=WORKLOAD["desc"],
-                        global_batch=B * world, per_gpu_batch=B, nodes_per_gpu=N,
-                        edges_per_gpu=E, parallelism=f"dp{world}",
-                        cuda_graph=graph is not None,
+            metric=METRIC, value=main["value"], unit=UNIT, n_gpus=ctx.world, steps=args.steps,
+            warmup=args.warmup, ms_per_step=main["ms_per_step"], higher_is_better=True,
+            scaling="weak", vs_baseline=None, dtype=DTYPE, data="synthetic",
+            config=dict(workload=W["desc"], global_batch=B * ctx.world, per_gpu_batch=B,
+                        nodes_per_gpu=main["nodes_per_gpu"], edges_per_gpu=main["edges_per_gpu"],
+                        parallelism=f"dp{ctx.world}", cuda_graph=main["cuda_graph"],
                         l2=("step working set (activations, E x H workspaces) > 126 MB L2; "
                             "8-batch input pool cycled")),
-            e2e=dict(value=e2e_value, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
-            neighbour_list=neighbour_list,
-            e2e_device_store=dict(value=store_value, unit=UNIT, h2d_bytes_per_step=4 * B,
-                                  d2h_bytes_per_step=d2h,
-                                  note="dataset resident in HBM (store.DeviceStructureStore); "
-                                       "per step: B int32 sample indices H2D, loss D2H"),
-            roofline=roof_bwd, roofline_agg_fwd=roof_fwd,
-            cpu_baseline=cpu, clocks=clocks, gpu_launches=launches)
+            e2e=main["e2e"], e2e_device_store=main["e2e_device_store"],
+            roofline=main["roofline"], roofline_agg_fwd=main["roofline_agg_fwd"],
+            roofline_gemm=main["roofline_gemm"], neighbour_list=main["neighbour_list"],
+            load_balance=main["load_balance"], cpu_baseline=cpu, clocks=main["clocks"],
+            gpu_launches=main["gpu_launches"], launches_per_step=main.get("launches_per_step"),
+            **nested)
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if ctx.world > 1:
         # A communicator captured inside a CUDA graph can block NCCL teardown;
         # every rank is done and rank 0 has printed, so leave without it.
         torch.cuda.synchronize()
-        comm.barrier()
+        ctx.comm.barrier()
         sys.stdout.flush()
         sys.stderr.flush()
         os._exit(0)
@@ -526,11 +791,8 @@ def run_native(args):
 
 def main():
     args = parse()
-    WORKLOAD.update(CONFIGS[args.config])
-    if args.batch is None:
-        args.batch = WORKLOAD["batch"]
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args, CONFIGS[args.config])
     else:
         run_native(args)
 

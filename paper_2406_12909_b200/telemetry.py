@@ -10,6 +10,8 @@ import threading
 import time
 from contextlib import contextmanager
 
+from .errors import ValidationError
+
 PHASES = ("dataload", "forward", "backward", "sync")
 
 
@@ -38,13 +40,24 @@ class PhaseClock:
                 self._t[k] = 0.0
 
 
-def compute_lif(times):
-    """Load-imbalance factor max/mean over ranks (scaling.py:54-61)."""
-    times = [float(t) for t in times]
-    mean = sum(times) / len(times) if times else 0.0
-    return max(times) / mean if mean > 0 else 1.0
+def compute_lif(per_rank_times) -> float:
+    """Load-imbalance factor: max over ranks / mean over ranks (>= 1)
+    (scaling.py:54-61, same errors)."""
+    times = [float(t) for t in per_rank_times]
+    if not times:
+        raise ValidationError("LIF needs at least one rank time")
+    if any(t <= 0 for t in times):
+        raise ValidationError("LIF requires strictly positive rank times")
+    return max(times) / (sum(times) / len(times))
 
 
-def wait_fraction(step_time, busy_time):
-    """Share of a step spent waiting at the collective (scaling.py:64-72)."""
-    return max(0.0, (step_time - busy_time) / step_time) if step_time > 0 else 0.0
+def wait_fraction(per_rank_times) -> float:
+    """Mean over ranks of (slowest - own) / slowest; 0 when balanced
+    (scaling.py:64-72)."""
+    times = [float(t) for t in per_rank_times]
+    if not times:
+        return 0.0
+    peak = max(times)
+    if peak <= 0:
+        return 0.0
+    return sum((peak - t) / peak for t in times) / len(times)

@@ -72,9 +72,11 @@ def test_ragged_runner_matches_oracle(dtype, rel, floor, use_graph):
         bo = O.pack(recs)
         (tot, _, _), grad_o, _ = O.loss_and_grad(ocfg, flat, bo)
         pos, z, e, f, off = _host(recs, dtype)
-        loss = run.step(pos, z, e, f, off)
+        loss32 = run.step(pos, z, e, f, off)  # the host read-back is float32
+        loss = float(tr.contrib[tr.P].item())
         used.add(run.cur.N)
         assert abs(loss - tot) <= rel * abs(tot), (loss, tot)
+        assert abs(loss32 - tot) <= 1e-6 * abs(tot)
         assert_close_scaled(tr.flat_grad(), grad_o, rel, floor, what=f"grad B={len(recs)}")
         flat, m, v, t = O.adam(flat, tr.flat_grad() if dtype == F32 else grad_o, m, v, t)
         if dtype == F64:
