@@ -62,6 +62,20 @@ inline bool at_disabled() {
   return v != 0;
 }
 
+// Accumulation flush depth in 32-wide k-blocks (TMA engine).  The tensor
+// core's fp32 accumulator rounds toward zero, so its error grows linearly
+// with the accumulation depth (tools/tf32_probe.py k: 1.0e-7 rms relative at
+// K = 32, 6.0e-6 at 2,560, 1.9e-5 at 8,192, almost all of it a bias toward
+// zero; IEEE FFMA chains: 9e-7 at 2,560).  Every kFlushKB k-blocks the
+// epilogue warps fold the TMEM partial into fp32 registers (IEEE adds) while
+// the MMAs fill the other accumulator, which bounds the biased run at
+// kFlushKB * 32 products.  GFM_TC_FLUSH_KB overrides (0 = never flush).
+inline int flush_kb() {
+  static int v = -1;
+  if (v < 0) v = getenv("GFM_TC_FLUSH_KB") ? atoi(getenv("GFM_TC_FLUSH_KB")) : 8;
+  return v > 0 ? v : (1 << 30);
+}
+
 constexpr int kBM = 128;       // MMA M (cta_group::1)
 constexpr int kBK = 32;        // fp32 elements per 128-byte swizzle row
 constexpr int kThreads = 256;  // 8 warps: staging + epilogue; thread 0 issues MMAs
@@ -191,7 +205,9 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory");
 }
 
-constexpr int tmem_cols(int cols) { return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256; }
+constexpr int tmem_cols(int cols) {
+  return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+}
 
 // ring depth by BN (192 KB of ring + lo buffers, one CTA per SM)
 template <int BN>
@@ -880,7 +896,7 @@ __device__ __forceinline__ void kb_ss1(uint32_t d, uint64_t ah, uint64_t ainc, u
 template <int BN, class Epi, int AT>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     tc_gemm_tma_kernel(int M, const int* __restrict__ M_dev, int N, int K, int k_chunk, int splits,
-                       int split3, const __grid_constant__ TmaOp ta,
+                       int split3, int fkb, const __grid_constant__ TmaOp ta,
                        const __grid_constant__ TmaOp tb, Epi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = SmemT<BN, AT != 0>;
@@ -945,6 +961,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     bm = (w % (m_tiles * n_tiles)) / n_tiles;
   };
   auto nkb_of = [&](int w) { return item_nkb(w, m_tiles * n_tiles, k_chunk, K); };
+  // accumulation chunks of a work item (>= 1: an empty item still completes once)
+  auto nch_of = [&](int nkb) { return nkb > 0 ? (nkb + fkb - 1) / fkb : 1; };
 
   if (warp == 0) {
     // ============================================================ TMA producer
@@ -1030,20 +1048,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     };
     const uint64_t ainc = a_mn ? 1024 >> 4 : 32 >> 4, binc = b_mn ? 1024 >> 4 : 32 >> 4;
     int q = 0, t = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
-      const int nkb = nkb_of(w);
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+     const int nkb = nkb_of(w), nch = nch_of(nkb);
+     for (int ch = 0; ch < nch; ++ch, ++t) {  // one accumulator per chunk
       const int acc = t & 1;
       if (t >= 2) mbar_wait(&tempty[acc], ((t >> 1) - 1) & 1);
       tc_fence_after();
       const uint32_t d = tmem + (uint32_t)(acc * BN);
-      for (int kb = 0; kb < nkb; ++kb, ++q) {
+      const int kb_end = min(nkb, (ch + 1) * fkb);
+      for (int kb = ch * fkb; kb < kb_end; ++kb, ++q) {
         const int s = q % kR, l = q % kL;
         mbar_wait(&tfl[s], (q / kR) & 1);
         if (split_on) mbar_wait(&cvt[l], (q / kL) & 1);
         tc_fence_after();
         const uint32_t ah = smem_u32(base + s * S::kRaw), bh = ah + S::kA;
         const uint32_t al = smem_u32(lo_base + l * S::kLo), bl = AT != 0 ? al : al + S::kA;
-        const uint32_t acc0 = kb > 0 ? 1u : 0u;
+        const uint32_t acc0 = kb > ch * fkb ? 1u : 0u;
         const uint32_t e_bar = smem_u32(&empty[s]), l_bar = smem_u32(&lofree[l]);
         if constexpr (AT != 0) {
           kb_at3(d, tmem + (uint32_t)(kACol + l * 64), desc0(b_mn, bh), desc0(b_mn, bl), binc,
@@ -1063,6 +1083,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tfull[acc])) : "memory");
       }
       __syncwarp();
+     }
     }
   } else {
     // ============================================================ epilogue
@@ -1073,10 +1094,45 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
       int bm, bn, split;
       tile_of(w, bm, bn, split);
-      const int nkb = nkb_of(w);
+      const int nkb = nkb_of(w), nch = nch_of(nkb);
+      // chunks before the last: fold each TMEM partial into fp32 registers
+      // (IEEE adds, in chunk order) and hand the accumulator back at once
+      constexpr int kRegs = (BN / 2 >= 16 ? BN / 2 : 16);
+      float racc[kRegs];
+      const int c_lo = half * kHalf, c_hi = min(BN, (half + 1) * kHalf);
+      for (int ch = 0; ch + 1 < nch; ++ch, ++t) {
+        const int acc = t & 1;
+        mbar_wait(&tfull[acc], (t >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int j = 0; j < kRegs / 16; ++j) {
+          if (c_lo + 16 * j >= c_hi) continue;
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c_lo + 16 * j), v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) racc[16 * j + i] = ch == 0 ? v[i] : racc[16 * j + i] + v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[acc])) : "memory");
+      }
       const int acc = t & 1;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
+      if (nch > 1) {  // last chunk: add the folded sum back into TMEM (racc dies here)
+#pragma unroll
+        for (int j = 0; j < kRegs / 16; ++j) {
+          if (c_lo + 16 * j >= c_hi) continue;
+          const uint32_t ta_ = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c_lo + 16 * j);
+          float v[16];
+          uint32_t u[16];
+          tmem_ld16(ta_, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(racc[16 * j + i] + v[i]);
+          tmem_st16(ta_, u);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
       const int m0 = bm * kBM, n0 = bn * BN;
       const int row = quarter * 32 + lane;
       const int m = m0 + row;
@@ -1087,7 +1143,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       float* stg = epi_stage + (warp - (kMmaWarp + 1)) * (32 * 20);
       const int m_lim = min(kBM, m_total - m0);
 #pragma unroll 1
-      for (int c = half * kHalf; c < min(BN, (half + 1) * kHalf); c += 16) {
+      for (int c = c_lo; c < c_hi; c += 16) {
         float v[16];
         if (nkb > 0) {
           tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
@@ -1171,7 +1227,8 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
       const int smem = at ? SmemT<BN, true>::kBytes : SmemT<BN, false>::kBytes;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      launch_k(kern, grid, kTmaThreads, smem, s, M, M_dev, N, K, k_chunk, splits, split3, ta, tb, epi);
+      launch_k(kern, grid, kTmaThreads, smem, s, M, M_dev, N, K, k_chunk, splits, split3,
+               flush_kb(), ta, tb, epi);
       return cudaGetLastError();
     }
   }
