@@ -297,6 +297,56 @@ GFM_API int gfm_sgd_step(const void* grad_sum, int grad_dtype, long long n, doub
                  double lr, const int* skip_flag, float* params32, void* stream);
 GFM_API int gfm_cast_f64_to_f32(const double* in, long long n, float* out, void* stream);
 
+/* ---- C4: EGNN-style variant with autograd forces (oracle/egnn_oracle.py;
+ * no reference implementation: SPEC.md:8, 352).  Reverse-over-forward
+ * training: every "d" (tangent) pointer may be NULL for a primal-only call.
+ * AB = h [wa; wb]^T ([n][2H] rows of stride ldab: A | B); x (n x 3).
+ * Edge e = j -> i in CSR row i: m = tanh(A_i + B_j + wd |x_j - x_i|^2 + c),
+ * agg_i = sum m, x'_i = x_i - sum (x_j - x_i)(m . ux) / max(deg_i, 1)
+ * (coord_update != 0).  H in {32, 64, 128, 256, 512}. */
+GFM_API int gfm_egnn_edge_fwd(const void* AB, int ldab, const void* ABd, const void* x,
+                              const void* xd, int n_nodes, int H, const int* rowptr,
+                              const int* col_src, const void* wd, const void* c, const void* ux,
+                              int coord_update, void* agg, int ldg, void* aggd, void* x_out,
+                              void* xd_out, int dtype, void* stream);
+/* Edge adjoints: aggb/aggdb = dL/d agg (and tangent), xb_out/xdb_out =
+ * dL/d x' (read when coord_update).  Writes dA at dAB and dB at dAB + H
+ * (row stride ldd; tangent rows at dABd), per-edge dpre / dpredot (E x H,
+ * CSR positions) and dr / drdot (E x 3) scratch, xb_in / xdb_in = dL/dx of
+ * the layer input, part = per-node [d wd | d ux] partials (n x 2H).
+ * Deterministic: dst sums in CSR order, src sums in CSC order. */
+GFM_API int gfm_egnn_edge_bwd(const void* AB, int ldab, const void* ABd, const void* x,
+                              const void* xd, int n_nodes, int H, const int* rowptr,
+                              const int* col_src, const int* csc_ptr, const int* csc_eid,
+                              const void* wd, const void* c, const void* ux, int coord_update,
+                              const void* aggb, int ldgb, const void* aggdb, const void* xb_out,
+                              const void* xdb_out, void* dAB, int ldd, void* dABd, void* preb,
+                              void* predb, void* rb, void* rdb, void* xb_in, void* xdb_in,
+                              void* part, int dtype, void* stream);
+/* h = tanh(z + bias) (primal rows), hd = (1 - h^2) zd (tangent rows);
+ * z == NULL: h is an input (tangent only) */
+GFM_API int gfm_egnn_tanh_fwd(const void* z, const void* zd, int ldz, const void* bias, int n,
+                              int H, void* h, void* hd, int ldh, int dtype, void* stream);
+/* zb = (1 - h^2)(hb - 2 h zd hdb), zdb = (1 - h^2) hdb */
+GFM_API int gfm_egnn_tanh_bwd(const void* h, int ldh, const void* zd, int ldzd, const void* hb,
+                              const void* hdb, int ldhb, int n, int H, void* zb, void* zdb,
+                              int ldzb, int dtype, void* stream);
+/* node_e = y a + c (node_ed = yd a); e_pred / e_dot = per-graph sums */
+GFM_API int gfm_egnn_energy(const void* y, const void* yd, int ldy, int n, int G, const void* a,
+                            const void* c, const int* node_offsets, int n_graphs, void* node_e,
+                            void* node_ed, void* e_pred, void* e_dot, int dtype, void* stream);
+/* head seeds over `rows` (= n primal, or 2n with tangent) rows: s = de[g(i)]
+ * (primal) or edot_seed (tangent), 0 for gnode < 0; ds = [s 0 0 0] rows,
+ * yb = s a (row stride ldyb) */
+GFM_API int gfm_egnn_head_seed(const void* de, const int* gnode, int n, int rows,
+                               double edot_seed, const void* a, int G, void* ds, void* yb,
+                               int ldyb, int dtype, void* stream);
+/* out[c] (+)= sum_{r < rows} X[r][c] (row stride ld), fixed order */
+GFM_API int gfm_colsum(const void* X, int rows, int cols, int ld, void* out, int accumulate,
+                       int dtype, void* stream);
+/* y = alpha x */
+GFM_API int gfm_scale(const void* x, long long n, double alpha, void* y, int dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

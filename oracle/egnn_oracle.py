@@ -53,14 +53,17 @@ def config(layers=3, hidden=64, fc_layers=2, fc_width=64, alpha_energy=1.0,
 
 
 def param_shapes(cfg):
-    """flat order: embedding; per layer wa, wb, wd, c (edge MLP), ux
-    (coordinate weight), w, u, b (node update); energy head as the MPNN."""
+    """flat order: embedding; per layer w (node update, on h), wa, wb (edge
+    MLP on h_dst / h_src), u (node update, on agg), wd, c (edge MLP distance
+    weight and bias), ux (coordinate weight), b (node update bias); energy
+    head as the MPNN.  [w; wa; wb] are adjacent so the backward's
+    dh = [dz | dA | dB] [w; wa; wb] is one GEMM."""
     H, G = cfg["H"], cfg["G"]
     out = [("embedding", (MAX_Z, H))]
     for l in range(cfg["L"]):
-        out += [(f"egnn_{l}.wa", (H, H)), (f"egnn_{l}.wb", (H, H)), (f"egnn_{l}.wd", (H,)),
-                (f"egnn_{l}.c", (H,)), (f"egnn_{l}.ux", (H,)), (f"egnn_{l}.w", (H, H)),
-                (f"egnn_{l}.u", (H, H)), (f"egnn_{l}.b", (H,))]
+        out += [(f"egnn_{l}.w", (H, H)), (f"egnn_{l}.wa", (H, H)), (f"egnn_{l}.wb", (H, H)),
+                (f"egnn_{l}.u", (H, H)), (f"egnn_{l}.wd", (H,)), (f"egnn_{l}.c", (H,)),
+                (f"egnn_{l}.ux", (H,)), (f"egnn_{l}.b", (H,))]
     ws = [(G, H)] + [(G, G)] * (cfg["F"] - 2) + [(1, G)]
     bs = [(G,)] * (cfg["F"] - 1) + [(1,)]
     for f in range(cfg["F"]):

@@ -101,6 +101,16 @@ SIGNATURES = {
     "gfm_nonfinite_advance": (_I, [_P, _L, _I, _P, _P, _D, _D, _P, _P, _L, _P]),
     "gfm_sgd_step": (_I, [_P, _I, _L, _D, _P, _D, _P, _P, _P]),
     "gfm_cast_f64_to_f32": (_I, [_P, _L, _P, _P]),
+    "gfm_egnn_edge_fwd": (_I, [_P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P,
+                               _P, _I, _P]),
+    "gfm_egnn_edge_bwd": (_I, [_P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I,
+                               _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P]),
+    "gfm_egnn_tanh_fwd": (_I, [_P, _P, _I, _P, _I, _I, _P, _P, _I, _I, _P]),
+    "gfm_egnn_tanh_bwd": (_I, [_P, _I, _P, _I, _P, _P, _I, _I, _I, _P, _P, _I, _I, _P]),
+    "gfm_egnn_energy": (_I, [_P, _P, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _I, _P]),
+    "gfm_egnn_head_seed": (_I, [_P, _P, _I, _I, _D, _P, _I, _P, _P, _I, _I, _P]),
+    "gfm_colsum": (_I, [_P, _I, _I, _I, _P, _I, _I, _P]),
+    "gfm_scale": (_I, [_P, _L, _D, _P, _I, _P]),
 }
 
 

@@ -23,6 +23,15 @@
 
 namespace gfm {
 
+// SFU tanh (tanh4_fast, |err| <= 5e-7) in the float32 edge kernels of the
+// tensor-core modes; GFM_EXACT_TANH=1 (or the SIMT engine) keeps tanhf.
+inline bool fast_tanh_on() {
+  static int v = -1;
+  if (v < 0) v = getenv("GFM_EXACT_TANH") ? (atoi(getenv("GFM_EXACT_TANH")) == 0) : 1;
+  return v && gemm_mode() != GFM_GEMM_SIMT;
+}
+
+
 // choose (NV float4 per lane, LPN lanes per node) for the float32 path
 static bool force_vec_shape(int H, int& nv, int& lpn, int* slabs = nullptr) {
   if (H % 4) return false;
@@ -590,7 +599,7 @@ cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const i
     if (!(flags & GFM_FLAG_SCALAR) && force_vec_shape(H, nv, lpn, &slabs)) {
       if (slabs == 2 || slabs == 4 || slabs == 8) {
         const int grid = ceil_div(n, 8 / slabs);
-        const bool fast = gemm_mode() != GFM_GEMM_SIMT;
+        const bool fast = fast_tanh_on();
 #define GFM_FS(SL_)                                                                                 \
   if (slabs == SL_) {                                                                               \
     if (fast)                                                                                       \
@@ -605,7 +614,7 @@ cudaError_t force_fwd_edges(const T* P, int n, int H, const int* rowptr, const i
       const int grid = ceil_div(n, 8 * (32 / lpn));
 #define GFM_FF(NV_, LPN_)                                                                    \
   if (nv == NV_ && lpn == LPN_) {                                                            \
-    if (gemm_mode() != GFM_GEMM_SIMT)                                                        \
+    if (fast_tanh_on())                                                        \
       launch_k(k_force_fwd_vec<NV_, LPN_, true>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, c, u, f); \
     else                                                                                     \
       launch_k(k_force_fwd_vec<NV_, LPN_, false>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, c, u, f); \
@@ -632,7 +641,7 @@ cudaError_t force_bwd_edges(const T* P, int n, int H, const int* rowptr, const i
       const dim3 grid(ceil_div(n, 8 * (32 / lpn)), slabs);
 #define GFM_FB(NV_, LPN_)                                                                         \
   if (nv == NV_ && lpn == LPN_) {                                                                 \
-    if (gemm_mode() != GFM_GEMM_SIMT) {                                                           \
+    if (fast_tanh_on()) {                                                           \
       launch_k(k_force_bwd_dst_vec<NV_, LPN_, true>, grid, 256, 0, s, P, n, H, rowptr, col_src, dx, df, \
                                                                 c, u, Ddst, TU);                  \
       launch_k(k_force_bwd_src_vec<NV_, LPN_, true>, grid, 256, 0, s, P, n, H, csc_ptr, csc_eid,        \

@@ -66,13 +66,17 @@ inline bool at_disabled() {
 // core's fp32 accumulator rounds toward zero, so its error grows linearly
 // with the accumulation depth (tools/tf32_probe.py k: 1.0e-7 rms relative at
 // K = 32, 6.0e-6 at 2,560, 1.9e-5 at 8,192, almost all of it a bias toward
-// zero; IEEE FFMA chains: 9e-7 at 2,560).  Every kFlushKB k-blocks the
-// epilogue warps fold the TMEM partial into fp32 registers (IEEE adds) while
-// the MMAs fill the other accumulator, which bounds the biased run at
-// kFlushKB * 32 products.  GFM_TC_FLUSH_KB overrides (0 = never flush).
+// zero; IEEE FFMA chains: 9e-7 at 2,560).  Every 16 k-blocks (512 products)
+// the epilogue warps fold the TMEM partial into fp32 registers (IEEE adds)
+// while the MMAs fill the other accumulator, which bounds the biased run:
+// 1.2e-6 rms at any K.  The last chunk is folded too and its accumulator
+// released before the stores, so the next tile's MMAs do not wait on them.
+// Measured at the C3 shapes (tools/gemm_time.py): every 16 k-blocks costs
+// +5% forward, +0% backward-data, +4% weight gradient; every 8 costs up to
+// +70% (register spills).  GFM_TC_FLUSH_KB overrides (0 = never flush).
 inline int flush_kb() {
   static int v = -1;
-  if (v < 0) v = getenv("GFM_TC_FLUSH_KB") ? atoi(getenv("GFM_TC_FLUSH_KB")) : 8;
+  if (v < 0) v = getenv("GFM_TC_FLUSH_KB") ? atoi(getenv("GFM_TC_FLUSH_KB")) : 16;
   return v > 0 ? v : (1 << 30);
 }
 
@@ -1119,39 +1123,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       const int acc = t & 1;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
-      if (nch > 1) {  // last chunk: add the folded sum back into TMEM (racc dies here)
-#pragma unroll
-        for (int j = 0; j < kRegs / 16; ++j) {
-          if (c_lo + 16 * j >= c_hi) continue;
-          const uint32_t ta_ = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c_lo + 16 * j);
-          float v[16];
-          uint32_t u[16];
-          tmem_ld16(ta_, v);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(racc[16 * j + i] + v[i]);
-          tmem_st16(ta_, u);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      }
       const int m0 = bm * kBM, n0 = bn * BN;
-      const int row = quarter * 32 + lane;
-      const int m = m0 + row;
-      const bool valid = row < min(kBM, m_total - m0);
-      // per 16-column chunk: TMEM -> registers (row = lane) -> this warp's smem
-      // stage -> read back transposed so each store instruction writes 8 rows
-      // x 64 contiguous bytes (full sectors) instead of 32 rows x 16 bytes
+      // per 16-column chunk: registers (row = lane) -> this warp's smem stage
+      // -> read back transposed so each store instruction writes 8 rows x 64
+      // contiguous bytes (full sectors) instead of 32 rows x 16 bytes
       float* stg = epi_stage + (warp - (kMmaWarp + 1)) * (32 * 20);
       const int m_lim = min(kBM, m_total - m0);
-#pragma unroll 1
-      for (int c = c_lo; c < c_hi; c += 16) {
-        float v[16];
-        if (nkb > 0) {
-          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        }
-        if (n0 + c >= N) continue;
+      auto store16 = [&](int c, const float (&v)[16]) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           *reinterpret_cast<float4*>(stg + lane * 20 + 4 * q) =
@@ -1187,9 +1165,44 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           }
         }
         __syncwarp();
+      };
+      if (nch > 1) {
+        // last chunk: fold it too and hand the accumulator back BEFORE the
+        // stores, so the next tile's MMAs are not held up by this epilogue
+#pragma unroll
+        for (int j = 0; j < kRegs / 16; ++j) {
+          if (c_lo + 16 * j >= c_hi) continue;
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c_lo + 16 * j), v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) racc[16 * j + i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[acc])) : "memory");
+#pragma unroll
+        for (int j = 0; j < kRegs / 16; ++j) {
+          const int c = c_lo + 16 * j;
+          if (c >= c_hi || n0 + c >= N) continue;
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = racc[16 * j + i];
+          store16(c, v);
+        }
+        continue;
       }
-      (void)m;
-      (void)valid;
+#pragma unroll 1
+      for (int c = c_lo; c < c_hi; c += 16) {
+        float v[16];
+        if (nkb > 0) {
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (n0 + c >= N) continue;
+        store16(c, v);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[acc])) : "memory");

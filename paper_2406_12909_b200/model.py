@@ -85,9 +85,17 @@ class ModelConfig:
         return cls(**doc)
 
 
+def _is_egnn(config) -> bool:
+    return getattr(config, "model_type", "mpnn") == "egnn"
+
+
 def param_shapes(config: ModelConfig):
     """(name, shape) in the canonical flat order (ModelParams.arrays,
-    model.py:120-132); U is (H, k*H) for k aggregation parts."""
+    model.py:120-132); U is (H, k*H) for k aggregation parts.  An
+    EGNNConfig has its own order (egnn.egnn_param_shapes)."""
+    if _is_egnn(config):
+        from .egnn import egnn_param_shapes
+        return egnn_param_shapes(config)
     h, g, k = config.mpnn_width, config.fc_width, config.n_parts
     out = [("embedding", (MAX_Z, h))]
     for l in range(config.mpnn_layers):
@@ -103,6 +111,9 @@ def param_shapes(config: ModelConfig):
 def count_params(config: ModelConfig) -> int:
     """Closed form (model.py:89-97) with U widened to k*H:
     118H + L(H^2 + kH^2 + H) + [HG + G + (F-2)(G^2 + G) + G + 1] + H^2 + 2H."""
+    if _is_egnn(config):
+        from .egnn import egnn_count_params
+        return egnn_count_params(config)
     h, l, k = config.mpnn_width, config.mpnn_layers, config.n_parts
     f, g = config.fc_layers, config.fc_width
     head = h * g + g + max(0, f - 2) * (g * g + g) + (g + 1)
@@ -259,6 +270,9 @@ class ModelParams:
 def init_params_flat(config: ModelConfig, seed: int = 0) -> np.ndarray:
     """init_params (model.py:178-187) on the host, float64: uniform(+-1/sqrt(H))
     drawn from default_rng(seed) in flat order, biases (.b/.c) zero."""
+    if _is_egnn(config):
+        from .egnn import egnn_init_flat
+        return egnn_init_flat(config, seed)
     rng = np.random.default_rng(seed)
     bound = 1.0 / np.sqrt(config.mpnn_width)
     parts = []
@@ -289,6 +303,7 @@ class Batch:
     Labels are mutable and read at loss time, as in the reference."""
 
     counts = None  # device [B, N] of a ragged batch in capacity buffers (else None)
+    periodic = False  # edges carry periodic image shifts
 
     def __init__(self, **kw):
         self.dtype = kw.pop("dtype")
@@ -404,7 +419,8 @@ def make_batch(records, device=None, dtype=torch.float32) -> Batch:
               edge_w=edge_w, edge_dx=edge_dx, csc_ptr=csc_ptr, csc_eid=csc_eid,
               csc_dst=csc_dst, order=order, n_nodes=N, e_cap=E, _n_edges=E,
               host_offsets=offsets, host_n_per=n_per,
-              max_deg=int(np.bincount(dst, minlength=1).max()) if E else 0)
+              max_deg=int(np.bincount(dst, minlength=1).max()) if E else 0,
+              periodic=shift is not None)
     b._keep = (t_src, t_dst, t_eoff, t_shift, ws)
     return b
 
@@ -474,7 +490,7 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
         return _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets,
                                     energy_true, forces_true, rowptr, col_src, edge_dst, edge_w,
                                     edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, None,
-                                    _deg_bound(max_atoms, max_nbr))
+                                    _deg_bound(max_atoms, max_nbr), cells is not None)
     call("gfm_graph_of_node", ptr(node_offsets), B, ptr(gnode), s)
     deg = buf("deg", (max(N, 1),), torch.int32)
     cells_t = None if cells is None else cells
@@ -505,7 +521,7 @@ def radius_batch(pos: torch.Tensor, z: torch.Tensor, node_offsets: torch.Tensor,
     return _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets,
                                 energy_true, forces_true, rowptr, col_src, edge_dst, edge_w,
                                 edge_dx, csc_ptr, csc_eid, csc_dst, e_cap, n_edges,
-                                _deg_bound(max_atoms, max_nbr))
+                                _deg_bound(max_atoms, max_nbr), cells is not None)
 
 
 def radius_batch_overflowed(out: dict, n_graphs: int) -> bool:
@@ -532,7 +548,7 @@ def _deg_bound(max_atoms: int, max_nbr: int) -> int:
 
 def _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offsets, energy_true,
                          forces_true, rowptr, col_src, edge_dst, edge_w, edge_dx, csc_ptr,
-                         csc_eid, csc_dst, e_cap, n_edges, max_deg):
+                         csc_eid, csc_dst, e_cap, n_edges, max_deg, periodic=False):
     B = int(host_offsets.shape[0] - 1)
     N = int(pos.shape[0])
     n_per = np.diff(host_offsets)
@@ -550,7 +566,7 @@ def _radius_batch_result(o, dev, dtype, z, pos, node_offsets, gnode, host_offset
                  edge_w=edge_w, edge_dx=edge_dx, csc_ptr=csc_ptr, csc_eid=csc_eid,
                  csc_dst=csc_dst, order=None, n_nodes=N, e_cap=int(e_cap), _n_edges=n_edges,
                  host_offsets=np.asarray(host_offsets), host_n_per=n_per, max_deg=max_deg,
-                 counts=o.get("counts"))
+                 counts=o.get("counts"), periodic=periodic)
 
 
 # --------------------------------------------------------------------------
@@ -607,8 +623,15 @@ def _argmax_flag(batch) -> int:
 def forward_batch(params: ModelParams, batch: Batch, cache: dict | None = None,
                   scratch: _Scratch | None = None, flags: int = 0):
     """forward_batch (model.py:344-400): returns (e_pred (B,), f_pred (N, 3))
-    as device tensors; fills ``cache`` with what the backward needs."""
+    as device tensors; fills ``cache`` with what the backward needs.  For an
+    EGNNConfig, f_pred = -dE/dx0 (egnn.forces)."""
     cfg = params.config
+    if _is_egnn(cfg):
+        from . import egnn
+        _, e_pred, f_pred = egnn.forces(params, batch, scratch)
+        if scratch is None:
+            return e_pred[:batch.n_graphs].clone(), f_pred[:batch.n_nodes].clone()
+        return e_pred, f_pred
     dt = params.dtype
     if batch.dtype != dt:
         raise ValidationError(f"batch dtype {batch.dtype} != params dtype {dt}")
@@ -792,6 +815,10 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     ``grad_out`` (length P, params dtype) receives the gradient in place;
     ``contrib`` (float32) receives [loss.total, 1.0] for the DP allreduce."""
     cfg = params.config
+    if _is_egnn(cfg):
+        from . import egnn
+        return egnn.loss_and_grad(params, batch, scratch=scratch, grad_out=grad_out,
+                                  contrib=contrib)
     dt = params.dtype
     code = _lib.dtype_code(dt)
     sc = _scratch_for(scratch, batch.device)

@@ -743,7 +743,12 @@ def load_checkpoint(path: str) -> Checkpoint:
         raise UnsupportedVersionError(
             f"checkpoint version {version} not supported (want {CHECKPOINT_VERSION})")
     off = magic + _CKPT_HEAD.size
-    model_config = ModelConfig.from_dict(json.loads(bytes(body[off:off + cfg_len])))
+    doc = json.loads(bytes(body[off:off + cfg_len]))
+    if doc.get("model_type") == "egnn":
+        from .egnn import EGNNConfig
+        model_config = EGNNConfig.from_dict(doc)
+    else:
+        model_config = ModelConfig.from_dict(doc)
     off += cfg_len
     n, t, epoch = _CKPT_COUNTS.unpack_from(body, off)
     off += _CKPT_COUNTS.size
