@@ -809,11 +809,15 @@ def batch_loss(params: ModelParams, batch: Batch) -> LossBreakdown:
 
 def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
                   scratch: _Scratch | None = None, grad_out: torch.Tensor | None = None,
-                  contrib: torch.Tensor | None = None, flags: int = 0):
+                  contrib: torch.Tensor | None = None, flags: int = 0, grad_ready=None):
     """Loss plus exact analytic gradient as a flat vector (model.py:483-565).
 
     ``grad_out`` (length P, params dtype) receives the gradient in place;
-    ``contrib`` (float32) receives [loss.total, 1.0] for the DP allreduce."""
+    ``contrib`` (float32) receives [loss.total, 1.0] for the DP allreduce.
+    ``grad_ready(group, stream)``, when given, is called as soon as a group of
+    gradient entries is final on ``stream`` -- "loss", "head", "force",
+    "layer{L-1}" ... "layer0", "embedding", in that order of production -- so
+    the trainer can allreduce finished buckets while the backward runs."""
     cfg = params.config
     if _is_egnn(cfg):
         from . import egnn
@@ -834,6 +838,9 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     vals, de, df = _loss_kernel(e_pred, f_pred, batch.energy_true, batch.forces_true,
                                 batch.n_per_graph, cfg.alpha_energy, cfg.alpha_forces,
                                 scratch=sc, contrib=contrib, counts=batch.counts)
+    main_s = torch.cuda.current_stream(batch.device)
+    if grad_ready is not None:
+        grad_ready("loss", main_s)
     grad = grad_out if grad_out is not None else torch.zeros(params.layout.Pp, dtype=dt,
                                                              device=batch.device)
     gp = ModelParams(cfg, grad)
@@ -846,6 +853,13 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     jobs = []
     main = torch.cuda.current_stream(batch.device)
     side = sc.side_stream()
+
+    def flush_jobs():
+        """reduce the weight-gradient partials issued so far (side stream)"""
+        if jobs:
+            arr = (_lib.ReduceJob * len(jobs))(*jobs)
+            call("gfm_splitk_reduce_batch", arr, len(jobs), code, side.cuda_stream)
+            jobs.clear()
 
     def wgrad(dY, ldd, n_out, X1, ld1, K1, X2, ld2, K2, g1, g2, gb, tag, inputs_on_side=False):
         nb = query("gfm_linear_bwd_weight_workspace_bytes", N, n_out, K1, K2, 1, code)
@@ -892,6 +906,9 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
         else:
             call("gfm_linear_bwd_data", ptr(dz), G, N, None, G, ptr(params.view(f"head_{f}.w")),
                  kin, kin, None, 0, 0, ptr(dh_e), H, None, 0, None, 0, code, ss)
+    if grad_ready is not None:  # bucketed allreduce: reduce the head's partials now
+        flush_jobs()
+        grad_ready("head", side)
     head_done = torch.cuda.Event()
     head_done.record(side)
 
@@ -908,6 +925,8 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     side.wait_event(edges_done)
     call("gfm_force_bwd_grads", ptr(cache["h_final"]), H, N, ptr(gp.force_v), ptr(gp.force_c),
          ptr(gp.force_u), ptr(ws), code, ss)
+    if grad_ready is not None:
+        grad_ready("force", side)
     main.wait_event(head_done)
     call("gfm_force_bwd_finish", ptr(cache["h_final"]), H, N, ptr(params.force_v), ptr(dh_e),
          ptr(dzl), ptr(ws), code, s)
@@ -928,6 +947,9 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
         lay = cache["layers"][l]
         wgrad(dz, H, H, lay["h_in"], H, H, lay["agg"], K * H, K * H, gp.view(f"layer_{l}.w"),
               gp.view(f"layer_{l}.u"), gp.view(f"layer_{l}.b"), f"layer{l}")
+        if grad_ready is not None:
+            flush_jobs()
+            grad_ready(f"layer{l}", side)
         dh_in = sc.get("dh_in", (N, H), dt)
         out = sc.get(f"dz_l{l}", (N, H), dt)
         if fused_prep:
@@ -956,10 +978,11 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
         dz = out
     # the batched reduction follows the weight-gradient GEMMs on the side
     # stream while the embedding gradient runs here; join before returning
-    arr = (_lib.ReduceJob * len(jobs))(*jobs)
-    call("gfm_splitk_reduce_batch", arr, len(jobs), code, side.cuda_stream)
+    flush_jobs()
     ews = sc.bytes("emb_ws", query("gfm_embedding_grad_workspace_bytes", N, H, code))
     call("gfm_embedding_grad", ptr(batch.z), N, ptr(dz), H, ptr(gp.embedding), ptr(ews), code, s)
+    if grad_ready is not None:
+        grad_ready("embedding", main_s)
     done = torch.cuda.Event()
     done.record(side)
     main.wait_event(done)

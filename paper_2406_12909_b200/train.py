@@ -174,7 +174,7 @@ class DataParallelTrainer:
 
     def __init__(self, model_config: ModelConfig, train_config: TrainConfig | None = None,
                  comm: Comm | None = None, device=None, initial=None,
-                 dtype=torch.float32, flags: int = 0):
+                 dtype=torch.float32, flags: int = 0, bucket_bytes: int = 4 << 20):
         _lib.load(require_device=True)
         self.cfg = model_config
         self.tcfg = train_config or TrainConfig()
@@ -217,6 +217,15 @@ class DataParallelTrainer:
         self.params = ModelParams(model_config, self.work)
         self.scratch = _Scratch(self.device)
         self.steps = 0
+        # bucketed, backward-overlapped gradient allreduce (N > 1, MPNN): each
+        # bucket is summed on a comm stream as soon as its gradients are final
+        self.buckets = plan_buckets(self.layout, model_config, bucket_bytes,
+                                    self.contrib.element_size())
+        self.bucketed = (self.comm.size > 1 and len(self.buckets) > 1
+                         and getattr(model_config, "model_type", "mpnn") == "mpnn"
+                         and hasattr(self.comm, "allreduce_sum_"))
+        self._comm_stream = torch.cuda.Stream(device=self.device) if self.bucketed else None
+        self._reduced = False
 
     def _ensure_bc(self, steps_ahead: int):
         """make the bias-correction table cover step counts < steps_ahead"""
@@ -236,23 +245,63 @@ class DataParallelTrainer:
         ``scratch``: activation buffers to use (default: the trainer's own;
         a runner keeps one per captured shape)."""
         P = self.P
+        self._reduced = False
         if batch is None:
             self.contrib.zero_()
             return
         sc = scratch if scratch is not None else self.scratch
         if self.dtype == torch.float32:
+            hook = self._bucket_hook() if self.bucketed else None
             loss_and_grad(self.params, batch, scratch=sc, grad_out=self.contrib[:P],
-                          contrib=self.contrib[P:], flags=self.flags)
+                          contrib=self.contrib[P:], flags=self.flags, grad_ready=hook)
+            if hook is not None:
+                self._join_buckets()
         else:
             lb, _ = loss_and_grad(self.params, batch, scratch=sc,
                                   grad_out=self.contrib[:P], flags=self.flags)
             self.contrib[P:P + 1].copy_(lb.values[:1])
             self.contrib[P + 1].fill_(1.0)
 
+    def _bucket_hook(self):
+        """grad_ready callback: launch each bucket's allreduce on the comm
+        stream once all its groups are final (same order on every rank)"""
+        waiting = [set(b.groups) for b in self.buckets]
+        events = [[] for _ in self.buckets]
+        cs = self._comm_stream
+
+        def ready(group, stream):
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            for k, b in enumerate(self.buckets):
+                if group in waiting[k]:
+                    waiting[k].discard(group)
+                    events[k].append(ev)
+                    if not waiting[k]:
+                        for e in events[k]:
+                            cs.wait_event(e)
+                        with torch.cuda.stream(cs):
+                            self.comm.allreduce_sum_(self.contrib[b.lo:b.hi])
+        self._reduced = True
+        return ready
+
+    def _join_buckets(self):
+        torch.cuda.current_stream(self.device).wait_stream(self._comm_stream)
+
     def reduce_and_update(self):
         P = self.P
         s = stream_handle()
-        _allreduce(self.comm, self.contrib)
+        if self.bucketed and not self._reduced:
+            # an idle rank (or a caller that bypassed compute) runs the same
+            # bucket sequence so the collectives line up across ranks
+            cs = self._comm_stream
+            cs.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(cs):
+                for b in sorted(self.buckets, key=lambda b: b.order):
+                    self.comm.allreduce_sum_(self.contrib[b.lo:b.hi])
+            self._join_buckets()
+        elif not self.bucketed:
+            _allreduce(self.comm, self.contrib)
+        self._reduced = False
         code = _lib.dtype_code(self.dtype)
         adam = self.tcfg.optimizer == "adam"
         capturing = torch.cuda.is_current_stream_capturing()
@@ -324,6 +373,59 @@ class DataParallelTrainer:
     def flat_grad(self) -> np.ndarray:
         """last step's (summed) gradient in the reference's flat order"""
         return self.layout.compact(self.contrib[:self.P]).to(torch.float64).cpu().numpy()
+
+
+@dataclass
+class Bucket:
+    """a contiguous slice [lo, hi) of the [grad | loss | 1] payload and the
+    gradient groups whose completion it waits for; ``order`` = its launch
+    position (buckets complete in the backward's production order)"""
+    lo: int
+    hi: int
+    groups: tuple
+    order: int
+
+
+def plan_buckets(layout, config, bucket_bytes: int, elem_bytes: int = 4):
+    """Gradient buckets in reverse layer order: the payload
+    [embedding | layer_0 .. layer_{L-1} | head | force | loss, 1] is cut, from
+    the end, into contiguous buckets of >= bucket_bytes made of whole groups,
+    so each bucket's allreduce can start when the backward has finished its
+    groups ("loss"/"head"/"force" first, "embedding" last)."""
+    ent = {name: (off, size) for name, _, off, size in layout.entries}
+    if getattr(config, "model_type", "mpnn") != "mpnn":
+        return [Bucket(0, layout.Pp + 2, ("all",), 0)]
+    L = config.mpnn_layers
+    names = [n for n, _, _, _ in layout.entries]
+    groups = [("embedding", ["embedding"])]
+    groups += [(f"layer{l}", [n for n in names if n.startswith(f"layer_{l}.")]) for l in range(L)]
+    groups += [("head", [n for n in names if n.startswith("head_")]),
+               ("force", [n for n in names if n.startswith("force.")])]
+    starts = [ent[g[1][0]][0] for g in groups] + [layout.Pp]
+    spans = [(g[0], starts[k], starts[k + 1]) for k, g in enumerate(groups)]
+    spans.append(("loss", layout.Pp, layout.Pp + 2))
+    # production order of the groups in loss_and_grad
+    produced = ["loss", "head", "force"] + [f"layer{l}" for l in range(L - 1, -1, -1)] +         ["embedding"]
+    buckets, cur = [], []
+    for name, lo, hi in reversed(spans):  # from the end of the payload
+        cur.append((name, lo, hi))
+        if sum(h - l for _, l, h in cur) * elem_bytes >= bucket_bytes:
+            buckets.append(cur)
+            cur = []
+    if cur:
+        if buckets and sum(h - l for _, l, h in cur) * elem_bytes < bucket_bytes // 4:
+            buckets[-1].extend(cur)  # a small remainder joins the last bucket
+        else:
+            buckets.append(cur)
+    out = []
+    for grp in buckets:
+        gs = tuple(n for n, _, _ in grp)
+        done = max(produced.index(n) for n in gs)
+        out.append(Bucket(min(l for _, l, _ in grp), max(h for _, _, h in grp), gs, done))
+    order = sorted(range(len(out)), key=lambda k: out[k].order)
+    for pos, k in enumerate(order):
+        out[k].order = pos
+    return out
 
 
 def _allreduce(comm, contrib: torch.Tensor):
