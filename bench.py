@@ -5,8 +5,9 @@ target): HydraGNN-PNA stand-in -- pna-agg (sum|mean|max|std), 6 message-
 passing layers, hidden 512, fc 2 x 512 -- on synthetic 100-atom periodic
 crystals (12 A cubic cell, radius 5 A, max 32 neighbours), 512 graphs per
 GPU per step.  Nested in the same line: ``c2`` (configs[1]: pna L3 H64,
-1024 x 32-atom molecules, max 20 neighbours) and ``ragged`` (C2 with 20..44
-atoms per structure through the capacity-bucketed runner).
+1024 x 32-atom molecules, max 20 neighbours), ``ragged`` (C2 with 20..44
+atoms per structure through the capacity-bucketed runner) and ``c4_egnn``
+(configs[3]: the EGNN variant with autograd forces, 256 graphs).
 
 A step = device batch assembly (radius graph -> CSR/CSC) from device-
 resident raw structures + forward + backward + gradient allreduce (NCCL) +
@@ -53,6 +54,12 @@ CONFIGS = {
                box=12.0, rc=5.0, max_nbr=32, batch=512, periodic=True, cpu_sample=2,
                desc="C3: pna-agg L6 H512 fc2x512, 100-atom periodic crystals, 12 A cell, "
                     "rc 5 A, max 32 neighbours, 512 graphs/GPU"),
+    # BASELINE.json configs[3]: EGNN variant, coordinate updates, autograd forces
+    "c4": dict(kind="egnn", layers=3, hidden=64, fc_layers=2, fc_width=64, atoms=(32, 32),
+               box=8.0, rc=5.0, max_nbr=20, batch=256, periodic=False, cpu_sample=8,
+               desc="C4: EGNN L3 H64 fc2x64 (coordinate updates, forces = -dE/dx by "
+                    "reverse-over-forward), 32-atom molecules, box 8 A, rc 5 A, max 20 "
+                    "neighbours, 256 graphs/GPU"),
     # C2 with ragged structures (mean 32 atoms): the capacity-bucketed runner
     "c2r": dict(kind="pna-agg", layers=3, hidden=64, fc_layers=2, fc_width=64, atoms=(20, 44),
                 box=8.0, rc=5.0, max_nbr=20, batch=1024, periodic=False, cpu_sample=32,
@@ -689,6 +696,53 @@ def rooflines(ctx, W, cfg, b, s):
     return res
 
 
+def measure_egnn(ctx, W):
+    """C4: the EGNN variant's full training step (forward, forces by the
+    reverse pass, loss, tangent forward, reverse over primal + tangent,
+    allreduce, Adam) through the same captured runner."""
+    import torch
+
+    from paper_2406_12909_b200 import train as T
+    from paper_2406_12909_b200.egnn import EGNNConfig
+
+    args = ctx.args
+    B, n = W["batch"], W["atoms"][1]
+    cfg = EGNNConfig(egnn_layers=W["layers"], egnn_width=W["hidden"], fc_layers=W["fc_layers"],
+                     fc_width=W["fc_width"], batch_size=B)
+    tr = T.DataParallelTrainer(cfg, T.TrainConfig(optimizer="adam", learning_rate=1e-3),
+                               comm=ctx.comm, device=ctx.dev)
+    runner = T.StructureStepRunner(tr, (np.arange(B + 1) * n).astype(np.int32), W["rc"],
+                                   W["max_nbr"], use_graph=not args.no_graph)
+    dev = ctx.dev
+    pool = []
+    for k in range(4):
+        z, pos, energy, forces, _ = packed(B, W, 7000 + 1000 * ctx.rank + k)
+        pool.append((torch.as_tensor(pos, device=dev), torch.as_tensor(z, device=dev),
+                     torch.as_tensor(energy, dtype=torch.float32, device=dev),
+                     torch.as_tensor(forces, dtype=torch.float32, device=dev)))
+    runner.load(*pool[0])
+    runner.capture(warmup=3)
+    for i in range(3):
+        runner.load(*pool[i % 4])
+        runner.run()
+    ctx.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(s)
+    for i in range(args.steps):
+        runner.load(*pool[i % 4])
+        runner.run()
+    ev1.record(s)
+    torch.cuda.synchronize()
+    ms = ctx.max_over_ranks(ev0.elapsed_time(ev1))
+    loss = float(tr.contrib[tr.P].item())
+    assert np.isfinite(loss)
+    return dict(value=ctx.world * B * args.steps / (ms / 1e3), unit=UNIT,
+                ms_per_step=ms / args.steps, workload=W["desc"], params=tr.layout.P,
+                note="EGNNConfig through DataParallelTrainer + StructureStepRunner (CUDA graph)")
+
+
 def measure_ragged(ctx, W, fixed_value):
     """C2 with 20..44-atom structures (mean 32) through the ragged runner:
     two captured node capacities (mean + 4 sigma, and the maximum)."""
@@ -757,6 +811,8 @@ def run_native(args):
         else:
             c2_value = main["value"]
         nested["ragged"] = measure_ragged(ctx, CONFIGS["c2r"], c2_value)
+        torch.cuda.empty_cache()
+        nested["c4_egnn"] = measure_egnn(ctx, CONFIGS["c4"])
     if ctx.rank == 0:
         cpu = None
         if ctx.world == 1:

@@ -78,6 +78,24 @@ GFM_API int gfm_gather_structures(const int* idx, int n_out, const int* src_off,
                                   double* pos_out, void* energy_out, void* forces_out, int dtype,
                                   void* stream);
 /* out[0..n] = exclusive prefix sum of in[0..n) (np.cumsum, model.py:238) */
+/* Device batch assembly from a store group's per-structure CSR blocks
+ * (replaces make_batch's host concatenation + CSR/CSC build for records
+ * that keep their own edges, model.py:234-285).  The group (n_s structures)
+ * was packed once by gfm_csr_build in float64: s_off [n_s+1], s_z, s_pos,
+ * s_e, s_f, s_rowptr / s_col / s_w / s_dx / s_cscptr / s_cscid / s_cscdst.
+ * Output graph b = structure idx[b]; meta (device) = [B_true, N_true |
+ * node offsets (n_cap_graphs+1) | n_per (n_cap_graphs) | edge offsets
+ * (n_cap_graphs+1)].  Writes the batch's inputs and its CSR / CSC in the
+ * compute dtype; nodes past N_true up to n_nodes are edge-free with gnode -1.
+ * Capture-safe: every size is read from `meta`. */
+GFM_API int gfm_gather_batch(const int* idx, const int* meta, int n_cap_graphs, int n_nodes,
+                             const int* s_off, const int* s_z, const double* s_pos,
+                             const double* s_e, const double* s_f, const int* s_rowptr,
+                             const int* s_col, const double* s_w, const double* s_dx,
+                             const int* s_cscptr, const int* s_cscid, const int* s_cscdst, int* z,
+                             double* pos, void* e, void* f, int* gnode, int* rowptr, int* col_src,
+                             int* edge_dst, void* w, void* dx, int* csc_ptr, int* csc_eid,
+                             int* csc_dst, int dtype, void* stream);
 GFM_API size_t gfm_scan_workspace_bytes(int n);
 GFM_API int gfm_exclusive_scan(const int* in, int n, int* out, void* workspace, void* stream);
 /* Radius graph replacing build_cutoff_edges (preprocess.py:90-104), emitted

@@ -46,6 +46,79 @@ __global__ void k_gather_structures(const int* __restrict__ idx, int n_out,
   }
 }
 
+// Batch assembly from a store's per-structure CSR blocks (records keep their
+// own edges, as make_batch does: model.py:234-285).  The group was packed
+// once at ingest (gfm_csr_build over all its structures, float64 w / dx),
+// so structure s owns nodes [so, so + n) and CSR / CSC positions
+// [eo, eo + m): output graph b copies both blocks to its node / edge bases
+// with the ids shifted -- the batch's stable dst / src sorts are exactly
+// the concatenation of the per-structure ones (block-diagonal batches).
+// meta = [counts (2) | node offsets (B+1) | n_per (B) | edge offsets (B+1)]
+// of the B_true structures (host-computed); the last CTA fills the capacity
+// tail (rowptr = csc_ptr = E, gnode = -1).
+template <typename T>
+__global__ void k_gather_batch(const int* __restrict__ idx, const int* __restrict__ meta,
+                               int n_cap_graphs, int n_nodes,
+                               const int* __restrict__ s_off, const int* __restrict__ s_z,
+                               const double* __restrict__ s_pos, const double* __restrict__ s_e,
+                               const double* __restrict__ s_f, const int* __restrict__ s_rowptr,
+                               const int* __restrict__ s_col, const double* __restrict__ s_w,
+                               const double* __restrict__ s_dx, const int* __restrict__ s_cscptr,
+                               const int* __restrict__ s_cscid, const int* __restrict__ s_cscdst,
+                               int* __restrict__ z, double* __restrict__ pos, T* __restrict__ e,
+                               T* __restrict__ f, int* __restrict__ gnode,
+                               int* __restrict__ rowptr, int* __restrict__ col_src,
+                               int* __restrict__ edge_dst, T* __restrict__ w, T* __restrict__ dx,
+                               int* __restrict__ csc_ptr, int* __restrict__ csc_eid,
+                               int* __restrict__ csc_dst) {
+  pdl_entry();
+  const int B = meta[0];
+  const int* noff = meta + 2;
+  const int* eoff = meta + 2 + 2 * n_cap_graphs + 1;
+  const int b = blockIdx.x;
+  if (b < B) {
+    const int s = idx[b];
+    const int so = s_off[s], n = s_off[s + 1] - so, d = noff[b];
+    const int eo = s_rowptr[so], m = s_rowptr[so + n] - eo, eb = eoff[b];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      z[d + t] = s_z[so + t];
+      gnode[d + t] = b;
+      rowptr[d + t] = eb + (s_rowptr[so + t] - eo);
+      csc_ptr[d + t] = eb + (s_cscptr[so + t] - eo);
+    }
+    for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) {
+      pos[3LL * d + t] = s_pos[3LL * so + t];
+      f[3LL * d + t] = (T)s_f[3LL * so + t];
+    }
+    for (int q = threadIdx.x; q < m; q += blockDim.x) {
+      const long long sp = (long long)eo + q, dp = (long long)eb + q;
+      col_src[dp] = s_col[sp] - so + d;
+      // the edge's dst: the CSR row holding position sp (binary search)
+      int lo = so, hi = so + n;  // rows [lo, hi): s_rowptr[lo] <= sp < s_rowptr[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_rowptr[mid] <= sp) lo = mid; else hi = mid;
+      }
+      edge_dst[dp] = lo - so + d;
+      w[dp] = (T)s_w[sp];
+      dx[3 * dp] = (T)s_dx[3 * sp];
+      dx[3 * dp + 1] = (T)s_dx[3 * sp + 1];
+      dx[3 * dp + 2] = (T)s_dx[3 * sp + 2];
+      csc_eid[dp] = s_cscid[sp] - eo + eb;
+      csc_dst[dp] = s_cscdst[sp] - so + d;
+    }
+    if (threadIdx.x == 0) e[b] = (T)s_e[s];
+  }
+  if (b == n_cap_graphs - 1) {  // capacity tail: edge-free, graph-less nodes
+    const int N = meta[1], E = eoff[B];
+    for (int t = N + threadIdx.x; t <= n_nodes; t += blockDim.x) {
+      rowptr[t] = E;
+      csc_ptr[t] = E;
+      if (t < n_nodes) gnode[t] = -1;
+    }
+  }
+}
+
 __global__ void k_iota(int* __restrict__ out, int n) {
   pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
@@ -678,6 +751,33 @@ int gfm_gather_structures(const int* idx, int n_out, const int* src_off, const i
     launch_k(k_gather_structures<double>, grid, 128, 0, s, idx, n_out, src_off, dst_off, z_in,
              pos_in, energy_in, forces_in, z_out, pos_out, (double*)energy_out,
              (double*)forces_out);
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gfm_gather_batch(const int* idx, const int* meta, int n_cap_graphs, int n_nodes,
+                     const int* s_off, const int* s_z, const double* s_pos, const double* s_e,
+                     const double* s_f, const int* s_rowptr, const int* s_col, const double* s_w,
+                     const double* s_dx, const int* s_cscptr, const int* s_cscid,
+                     const int* s_cscdst, int* z, double* pos, void* e, void* f, int* gnode,
+                     int* rowptr, int* col_src, int* edge_dst, void* w, void* dx, int* csc_ptr,
+                     int* csc_eid, int* csc_dst, int dtype, void* stream) {
+  if (n_cap_graphs <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == GFM_F32)
+    launch_k(k_gather_batch<float>, n_cap_graphs, 128, 0, s, idx, meta, n_cap_graphs, n_nodes,
+             s_off, s_z, s_pos, s_e, s_f, s_rowptr, s_col, s_w, s_dx, s_cscptr, s_cscid, s_cscdst,
+             z, pos, (float*)e, (float*)f, gnode, rowptr, col_src, edge_dst, (float*)w, (float*)dx,
+             csc_ptr, csc_eid, csc_dst);
+  else if (dtype == GFM_F64)
+    launch_k(k_gather_batch<double>, n_cap_graphs, 128, 0, s, idx, meta, n_cap_graphs, n_nodes,
+             s_off, s_z, s_pos, s_e, s_f, s_rowptr, s_col, s_w, s_dx, s_cscptr, s_cscid,
+             s_cscdst, z, pos, (double*)e, (double*)f, gnode, rowptr, col_src, edge_dst,
+             (double*)w, (double*)dx, csc_ptr, csc_eid, csc_dst);
+  else {
+    set_error("gfm_gather_batch: bad dtype %d", dtype);
+    return GFM_EINVAL;
+  }
   GFM_TRY(cudaGetLastError());
   return 0;
 }

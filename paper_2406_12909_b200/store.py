@@ -50,12 +50,32 @@ class _Group:
             raise ValidationError(f"store ingest: {zz.size} atomic numbers for {N} atoms, "
                                   f"each must lie in [1, {MAX_Z}]")
         self.max_atoms = int(np.diff(self.host_off).max()) if self.n_samples else 0
+        self.host_m = None
         self.z = torch.as_tensor(np.asarray(z).reshape(N).astype(np.int32), device=device)
         self.pos = torch.as_tensor(np.asarray(pos, np.float64).reshape(N, 3), device=device)
         self.energy = torch.as_tensor(np.asarray(energy, np.float64).reshape(self.n_samples),
                                       device=device)
         self.forces = torch.as_tensor(np.asarray(forces, np.float64).reshape(N, 3), device=device)
         self.off = torch.as_tensor(self.host_off, device=device)
+        self.csr = None
+        if self.records is not None:
+            self._pack_edges(device)
+
+    def _pack_edges(self, device):
+        """the records' own edges (make_batch semantics, model.py:234-285)
+        as one float64 CSR / CSC over the whole group, built once on the
+        device; a batch is then a gather of per-structure blocks"""
+        from .model import make_batch
+
+        b = make_batch(self.records, device=device, dtype=torch.float64)
+        m = np.array([int(np.asarray(r.edge_index).reshape(-1, 2).shape[0]) for r in self.records],
+                     np.int64)
+        self.host_m = m
+        self.max_edges = int(m.max()) if m.size else 0
+        self.max_deg = int(b.max_deg)
+        self.csr = dict(rowptr=b.rowptr, col_src=b.col_src, edge_w=b.edge_w, edge_dx=b.edge_dx,
+                        csc_ptr=b.csc_ptr, csc_eid=b.csc_eid, csc_dst=b.csc_dst)
+        self.periodic = bool(b.periodic)
 
 
 class DeviceStructureStore:
@@ -148,6 +168,19 @@ class DeviceStructureStore:
         slot[3] = torch.cuda.Event()
         slot[3].record(main)
 
+    def group(self, name) -> "_Group":
+        return self._groups[name]
+
+    def batch_layout(self, group, indices):
+        """host layout words of a stored-edge batch: (node offsets, edge
+        offsets) of structures ``indices``"""
+        g = self._groups[group]
+        idx = self._check(g, indices)
+        n = g.host_off[idx + 1] - g.host_off[idx]
+        m = g.host_m[idx]
+        return (np.concatenate([[0], np.cumsum(n)]).astype(np.int64),
+                np.concatenate([[0], np.cumsum(m)]).astype(np.int64))
+
     def gather(self, group, indices, dtype=torch.float32):
         """Assemble structures ``indices`` on the device: returns
         (pos f64 (N,3), z i32 (N,), energy (B,), forces (N,3), host_offsets)."""
@@ -173,3 +206,47 @@ class DeviceStructureStore:
         runner.set_layout(self.host_offsets(group, idx))
         s = runner.slot
         self._launch(g, idx, runner.off, s["z"], s["pos"], s["e"], s["f"], runner.tr.dtype)
+
+
+def gather_batch(g: "_Group", idx_dev, meta_dev, n_cap_graphs: int, n_nodes: int, e_cap: int,
+                 dtype, out: dict, slot: dict, off_view, npg_view, counts_view, host_off_cap):
+    """Assemble a training Batch of stored-edge structures on the device
+    (gfm_gather_batch) into the buffers of ``out`` / ``slot``; every size is
+    read from ``meta_dev``, so the call is CUDA-graph capturable."""
+    from .model import Batch
+
+    dev = g.z.device
+    Ec = max(int(e_cap), 1)
+
+    def buf(name, shape, dt):
+        t = out.get(name)
+        if t is None or t.dtype != dt or tuple(t.shape) != tuple(shape):
+            t = torch.empty(shape, dtype=dt, device=dev)
+            out[name] = t
+        return t
+
+    N = int(n_nodes)
+    gnode = buf("gnode", (max(N, 1),), torch.int32)
+    rowptr = buf("rowptr", (N + 1,), torch.int32)
+    csc_ptr = buf("csc_ptr", (N + 1,), torch.int32)
+    col_src = buf("col_src", (Ec,), torch.int32)
+    edge_dst = buf("edge_dst", (Ec,), torch.int32)
+    csc_eid = buf("csc_eid", (Ec,), torch.int32)
+    csc_dst = buf("csc_dst", (Ec,), torch.int32)
+    edge_w = buf("edge_w", (Ec,), dtype)
+    edge_dx = buf("edge_dx", (Ec, 3), dtype)
+    c = g.csr
+    call("gfm_gather_batch", ptr(idx_dev), ptr(meta_dev), int(n_cap_graphs), N, ptr(g.off),
+         ptr(g.z), ptr(g.pos), ptr(g.energy), ptr(g.forces), ptr(c["rowptr"]), ptr(c["col_src"]),
+         ptr(c["edge_w"]), ptr(c["edge_dx"]), ptr(c["csc_ptr"]), ptr(c["csc_eid"]),
+         ptr(c["csc_dst"]), ptr(slot["z"]), ptr(slot["pos"]), ptr(slot["e"]), ptr(slot["f"]),
+         ptr(gnode), ptr(rowptr), ptr(col_src), ptr(edge_dst), ptr(edge_w), ptr(edge_dx),
+         ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), _lib.dtype_code(dtype), stream_handle())
+    b = Batch(dtype=dtype, device=dev, z=slot["z"][:N], pos=slot["pos"][:N],
+              node_offsets=off_view, n_per_graph=npg_view, graph_of_node=gnode,
+              energy_true=slot["e"], forces_true=slot["f"][:N], rowptr=rowptr, col_src=col_src,
+              edge_dst=edge_dst, edge_w=edge_w, edge_dx=edge_dx, csc_ptr=csc_ptr,
+              csc_eid=csc_eid, csc_dst=csc_dst, order=None, n_nodes=N, e_cap=Ec, _n_edges=None,
+              host_offsets=host_off_cap, host_n_per=np.diff(host_off_cap), max_deg=g.max_deg,
+              counts=counts_view, periodic=g.periodic)
+    return b

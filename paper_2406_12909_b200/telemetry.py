@@ -1,7 +1,11 @@
 """Phase accounting inside the step (PhaseClock, telemetry.py:41-86).
 
-Host wall-clock per phase, as the reference reports it; for device time the
-trainer also records CUDA events per phase (``DeviceClock``).
+``PhaseClock``: host wall-clock per phase, as the reference reports it --
+around asynchronous launches that is enqueue time.  ``DeviceClock``: the
+same phases timed on the device with CUDA events on the launching stream
+(``train(device_clock=...)``), read once per epoch.  ``compute_lif`` /
+``wait_fraction``: the scaling report's load-balance measures
+(scaling.py:54-72).
 """
 
 from __future__ import annotations
@@ -38,6 +42,36 @@ class PhaseClock:
         with self._lock:
             for k in self._t:
                 self._t[k] = 0.0
+
+
+class DeviceClock:
+    """Device time per phase: a CUDA event pair per phase occurrence on the
+    current stream; ``totals()`` synchronises once and sums the elapsed
+    times (seconds), cumulative like PhaseClock.totals()."""
+
+    def __init__(self):
+        self._pending = []  # (name, start event, end event)
+        self._t = {}
+
+    @contextmanager
+    def phase(self, name):
+        import torch
+
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        try:
+            yield
+        finally:
+            b.record()
+            self._pending.append((name, a, b))
+
+    def totals(self) -> dict:
+        for name, a, b in self._pending:
+            b.synchronize()
+            self._t[name] = self._t.get(name, 0.0) + a.elapsed_time(b) / 1e3
+        self._pending.clear()
+        return dict(self._t)
 
 
 def compute_lif(per_rank_times) -> float:

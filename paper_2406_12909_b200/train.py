@@ -34,7 +34,7 @@ from .model import (ModelConfig, ModelParams, _Scratch, count_params, forward_ba
                     init_params_flat, loss_and_grad, make_batch)
 from .records import MAX_Z
 from .schedule import epoch_schedule
-from .telemetry import PhaseClock
+from .telemetry import DeviceClock, PhaseClock
 
 log = logging.getLogger(__name__)
 
@@ -150,11 +150,13 @@ class EpochMetrics:
     val_force_mae: float
     epoch_time_s: float
     phase_seconds: dict = field(default_factory=dict)
+    device_phase_seconds: dict = field(default_factory=dict)  # DeviceClock (CUDA events)
 
     def to_dict(self) -> dict:
         return dict(epoch=self.epoch, train_loss=self.train_loss, val_mae=self.val_mae,
                     val_energy_mae=self.val_energy_mae, val_force_mae=self.val_force_mae,
-                    epoch_time_s=self.epoch_time_s, phase_seconds=dict(self.phase_seconds))
+                    epoch_time_s=self.epoch_time_s, phase_seconds=dict(self.phase_seconds),
+                    device_phase_seconds=dict(self.device_phase_seconds))
 
 
 @dataclass
@@ -240,10 +242,11 @@ class DataParallelTrainer:
             torch.tensor(vals, dtype=torch.float64))
         self._bc_filled = hi
 
-    def compute(self, batch, scratch=None):
+    def compute(self, batch, scratch=None, precomputed=None):
         """forward + backward into ``contrib`` (or zeros when no batch).
         ``scratch``: activation buffers to use (default: the trainer's own;
-        a runner keeps one per captured shape)."""
+        a runner keeps one per captured shape); ``precomputed``: a forward
+        already run into that scratch (cache, e_pred, f_pred)."""
         P = self.P
         self._reduced = False
         if batch is None:
@@ -252,12 +255,13 @@ class DataParallelTrainer:
         sc = scratch if scratch is not None else self.scratch
         if self.dtype == torch.float32:
             hook = self._bucket_hook() if self.bucketed else None
-            loss_and_grad(self.params, batch, scratch=sc, grad_out=self.contrib[:P],
-                          contrib=self.contrib[P:], flags=self.flags, grad_ready=hook)
+            loss_and_grad(self.params, batch, precomputed=precomputed, scratch=sc,
+                          grad_out=self.contrib[:P], contrib=self.contrib[P:], flags=self.flags,
+                          grad_ready=hook)
             if hook is not None:
                 self._join_buckets()
         else:
-            lb, _ = loss_and_grad(self.params, batch, scratch=sc,
+            lb, _ = loss_and_grad(self.params, batch, precomputed=precomputed, scratch=sc,
                                   grad_out=self.contrib[:P], flags=self.flags)
             self.contrib[P:P + 1].copy_(lb.values[:1])
             self.contrib[P + 1].fill_(1.0)
@@ -428,6 +432,15 @@ def plan_buckets(layout, config, bucket_bytes: int, elem_bytes: int = 4):
     return out
 
 
+@contextlib.contextmanager
+def _dphase(dclk, name):
+    if dclk is None:
+        yield
+    else:
+        with dclk.phase(name):
+            yield
+
+
 def _allreduce(comm, contrib: torch.Tensor):
     """In-place sum of the step payload across ranks.  Comm objects of this
     package reduce the device tensor directly (NCCL); any other object with
@@ -480,11 +493,23 @@ class StructureStepRunner:
     def __init__(self, trainer: DataParallelTrainer, host_offsets=None, rc: float = 5.0,
                  max_nbr: int = 0, cells=None, use_graph: bool = True, e_cap: int | None = None,
                  *, max_graphs: int | None = None, max_atoms: int | None = None,
-                 node_caps=None):
+                 node_caps=None, store=None, group: str = "trainset"):
         self.tr = trainer
         dev = trainer.device
         self.rc = float(rc)
         self.max_nbr = int(max_nbr or 0)
+        # store mode: batches are gathered from a DeviceStructureStore's
+        # per-structure CSR blocks (the records' own edges) inside the graph
+        self.store = store
+        self.group = group
+        if store is not None:
+            g = store.group(group)
+            if g.csr is None:
+                raise ValidationError(f"store group {group!r} holds no edges (ingest records)")
+            host_offsets = None
+            max_atoms = max_atoms or g.max_atoms
+            if e_cap is None:
+                e_cap = int(max_graphs) * max(g.max_edges, 1)
         self.ragged = host_offsets is None
         if self.ragged:
             if not max_graphs or not max_atoms:
@@ -503,15 +528,17 @@ class StructureStepRunner:
             self.max_atoms = int(n.max()) if n.size else 0
             caps = [int(self.host_off[-1])]
         self.N = caps[-1]
-        # per-step layout words: [counts (2) | node offsets (B+1) | n_per (B)]
-        self.meta = torch.zeros(2 + 2 * self.B + 1, dtype=torch.int32, device=dev)
+        # per-step layout words: [counts (2) | node offsets (B+1) | n_per (B) |
+        # edge offsets (B+1), store mode]
+        self.meta = torch.zeros(3 * self.B + 4, dtype=torch.int32, device=dev)
         self.counts = self.meta[0:2] if self.ragged else None
         self.off = self.meta[2:self.B + 3]
-        self.npg = self.meta[self.B + 3:]
+        self.npg = self.meta[self.B + 3:2 * self.B + 3]
+        self.idx = torch.zeros(self.B, dtype=torch.int32, device=dev)
         if not self.ragged:
             self._write_meta(self.host_off, sync=True)
-        self._meta_ring = [[torch.empty_like(self.meta, device="cpu").pin_memory(), None]
-                           for _ in range(3)]
+        self._meta_ring = [[torch.empty(self.meta.shape[0] + self.B, dtype=torch.int32)
+                            .pin_memory(), None] for _ in range(3)]
         self._meta_k = 0
         self.cells = None if cells is None else torch.as_tensor(
             np.asarray(cells, np.float64).reshape(self.B, 3), device=dev)
@@ -561,27 +588,47 @@ class StructureStepRunner:
         return self.cur.bufs
 
     # ---- layout --------------------------------------------------------------
-    def _write_meta(self, offsets, sync=False):
+    def _write_meta(self, offsets, sync=False, eoffsets=None, idx=None):
         off = np.asarray(offsets, np.int64)
         B_true = off.shape[0] - 1
-        host = np.zeros(self.meta.shape[0], np.int32)
+        host = np.zeros(self.meta.shape[0] + self.B, np.int32)  # meta | idx
         host[0], host[1] = B_true, off[-1]
         host[2:2 + B_true + 1] = off
         host[2 + B_true + 1:self.B + 3] = off[-1]  # empty capacity graphs
         host[self.B + 3:self.B + 3 + B_true] = np.diff(off)
+        if eoffsets is not None:
+            eo = np.asarray(eoffsets, np.int64)
+            e0 = 2 * self.B + 3
+            host[e0:e0 + B_true + 1] = eo
+            host[e0 + B_true + 1:e0 + self.B + 1] = eo[-1]
+        nm = self.meta.shape[0]
+        if idx is not None:
+            host[nm:nm + B_true] = idx
         if sync:
-            self.meta.copy_(torch.from_numpy(host))
+            self.meta.copy_(torch.from_numpy(host[:nm]))
             return
         buf = self._meta_ring[self._meta_k]
         self._meta_k = (self._meta_k + 1) % len(self._meta_ring)
         if buf[1] is not None:
             buf[1].synchronize()  # that staging buffer's last copy is done
         buf[0].numpy()[:] = host
-        self.meta.copy_(buf[0], non_blocking=True)
+        self.meta.copy_(buf[0][:nm], non_blocking=True)
+        if idx is not None:
+            self.idx.copy_(buf[0][nm:], non_blocking=True)
         buf[1] = torch.cuda.Event()
         buf[1].record()
 
-    def set_layout(self, offsets) -> _Shape:
+    def set_indices(self, indices) -> _Shape:
+        """Store mode: the next batch = store structures ``indices`` (host
+        ints).  Their layout words and the indices go to the device (one
+        small copy); the captured step gathers the structures itself."""
+        if self.store is None:
+            raise ValidationError("set_indices needs a runner built with store=")
+        idx = np.asarray(indices, np.int64).reshape(-1)
+        off, eoff = self.store.batch_layout(self.group, idx)
+        return self.set_layout(off, eoffsets=eoff, idx=idx)
+
+    def set_layout(self, offsets, eoffsets=None, idx=None) -> _Shape:
         """Ragged: the next batch's node offsets (host, B_true + 1 entries)
         -> device layout words; selects the smallest capacity holding it."""
         off = np.asarray(offsets, np.int64).reshape(-1)
@@ -601,7 +648,10 @@ class StructureStepRunner:
                 break
         else:
             raise ValidationError(f"batch of {N} atoms exceeds the runner's capacity {self.N}")
-        self._write_meta(off)
+        if eoffsets is not None and int(np.asarray(eoffsets)[-1]) > self.cur.e_cap:
+            raise ValidationError(f"batch of {int(np.asarray(eoffsets)[-1])} edges exceeds "
+                                  f"e_cap={self.cur.e_cap}")
+        self._write_meta(off, eoffsets=eoffsets, idx=idx)
         return self.cur
 
     def load(self, pos, z, energy, forces, offsets=None):
@@ -627,6 +677,13 @@ class StructureStepRunner:
 
         sh = sh or self.cur
         sl = slot or self.slot
+        if self.store is not None:
+            from .store import gather_batch
+            sh.batch = gather_batch(self.store.group(self.group), self.idx, self.meta, self.B,
+                                    sh.N, sh.e_cap, self.tr.dtype, sh.bufs, sl, self.off,
+                                    self.npg, self.counts, self.host_off)
+            self.tr.step(sh.batch, scratch=sh.scratch)
+            return
         sh.bufs["n_per_graph"] = self.npg
         sh.bufs["counts"] = self.counts
         sh.batch = radius_batch(sl["pos"][:sh.N], sl["z"][:sh.N], self.off, self.host_off,
@@ -657,7 +714,7 @@ class StructureStepRunner:
     def _check_overflow(self, sh):
         from .model import radius_batch_overflowed
 
-        if radius_batch_overflowed(sh.bufs, self.B):
+        if self.store is None and radius_batch_overflowed(sh.bufs, self.B):
             raise ValidationError(f"a batch had more than e_cap={sh.e_cap} edges; raise e_cap")
 
     def run(self):
@@ -893,8 +950,21 @@ def evaluate(params: ModelParams, store, comm: Comm, group: str = "valset",
 def train(model_config: ModelConfig, store, comm: Comm | None = None,
           config: TrainConfig | None = None, clock: PhaseClock | None = None,
           initial: ModelParams | None = None, schedule_fn=None, device=None,
-          dtype=torch.float32) -> TrainResult:
-    """The data-parallel training loop on this rank (train.py:192-338)."""
+          dtype=torch.float32, nan_check_every: int = 16,
+          device_clock: "DeviceClock | None" = None) -> TrainResult:
+    """The data-parallel training loop on this rank (train.py:192-338).
+
+    With a ``store.DeviceStructureStore`` holding records, every batch is
+    assembled on the device from the store's per-structure CSR blocks inside
+    one captured step (StructureStepRunner store mode): per step only the
+    batch's indices and layout words cross PCIe.  Otherwise batches are
+    packed from fetched records (``make_batch``).  The sticky non-finite
+    guard (train.py:264-274) freezes parameters on the device at once; the
+    host reads it every ``nan_check_every`` steps and at each epoch end.
+    ``device_clock`` (telemetry.DeviceClock) records CUDA-event device time
+    per phase beside ``clock``'s host wall time."""
+    from .store import DeviceStructureStore
+
     comm = comm or LocalComm()
     config = config or TrainConfig()
     clock = clock or PhaseClock()
@@ -903,6 +973,12 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
     ownership = store.ownership.get("trainset")
     if ownership is None:
         raise ValidationError(f"trainset not loaded on rank {comm.rank}")
+    runner = None
+    if isinstance(store, DeviceStructureStore) and store.group("trainset").csr is not None:
+        runner = StructureStepRunner(trainer, None, store=store, group="trainset",
+                                     max_graphs=model_config.batch_size)
+    captured = False
+    dclk = device_clock
     n_train = ownership.n_samples
     start = time.monotonic()
     stopper = EarlyStopper(config.patience)
@@ -914,6 +990,7 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
     for epoch in range(1, config.max_epochs + 1):
         t0 = time.perf_counter()
         before = clock.totals()
+        dbefore = dclk.totals() if dclk is not None else {}
         if schedule_fn is not None:
             per_rank = schedule_fn(epoch)
             mine = per_rank[comm.rank]
@@ -925,35 +1002,54 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
             steps = sched.max_batches()
         acc = torch.zeros(2, dtype=torch.float64, device=trainer.device)
         for step in range(steps):
-            batch = None
-            if step < len(mine) and len(mine[step]):
+            has = step < len(mine) and len(mine[step])
+            if has and runner is not None:
+                # device assembly + forward + backward + allreduce + update:
+                # one captured graph (device time under "step")
                 with clock.phase("dataload"):
+                    runner.set_indices(mine[step])
+                if not captured:
+                    runner.capture(warmup=1)
+                    captured = True
+                with clock.phase("step"), _dphase(dclk, "step"):
+                    runner.run()
+            elif has:
+                with clock.phase("dataload"), _dphase(dclk, "dataload"):
                     batch = make_batch(store.fetch_batch("trainset", mine[step]),
                                        device=trainer.device, dtype=dtype)
-                with clock.phase("forward"):
-                    trainer.compute(batch)
-            else:
-                trainer.contrib.zero_()
-            with clock.phase("sync"):
-                trainer.reduce_and_update()
-            if trainer.nan_event:  # train.py:264-274
-                log.warning("rank %d: non-finite loss at epoch %d step %d; update discarded, "
-                            "training aborted", comm.rank, epoch, step)
-                nan_event = True
-                stop_reason = "nan"
-                break
+                with clock.phase("forward"), _dphase(dclk, "forward"):
+                    cache: dict = {}
+                    e_pred, f_pred = forward_batch(trainer.params, batch, cache,
+                                                   scratch=trainer.scratch)
+                with clock.phase("backward"), _dphase(dclk, "backward"):
+                    trainer.compute(batch, precomputed=(cache, e_pred, f_pred))
+                with clock.phase("sync"), _dphase(dclk, "sync"):
+                    trainer.reduce_and_update()
+            else:  # no batch for this rank: zero contribution (train.py:257-259)
+                with clock.phase("sync"), _dphase(dclk, "sync"):
+                    trainer.compute(None)
+                    trainer.reduce_and_update()
             acc += trainer.contrib[P:P + 2].to(torch.float64)
+            if (step + 1) % max(1, nan_check_every) == 0 or step == steps - 1:
+                if trainer.nan_event:  # train.py:264-274 (the device skipped the update)
+                    log.warning("rank %d: non-finite loss at epoch %d (by step %d); update "
+                                "discarded, training aborted", comm.rank, epoch, step)
+                    nan_event = True
+                    stop_reason = "nan"
+                    break
         if nan_event:
             break
         params = ModelParams(model_config, trainer.work)
         ve, vf = evaluate(params, store, comm)
         after = clock.totals()
+        dafter = dclk.totals() if dclk is not None else {}
         loss_sum, loss_count = acc.cpu().numpy()
         metrics.append(EpochMetrics(
             epoch=epoch, train_loss=loss_sum / loss_count if loss_count else float("nan"),
             val_mae=ve + vf, val_energy_mae=ve, val_force_mae=vf,
             epoch_time_s=time.perf_counter() - t0,
-            phase_seconds={k: after[k] - before.get(k, 0.0) for k in after}))
+            phase_seconds={k: after[k] - before.get(k, 0.0) for k in after},
+            device_phase_seconds={k: dafter[k] - dbefore.get(k, 0.0) for k in dafter}))
         if stopper.update(ve + vf):
             stop_reason = "early_stop"
             break

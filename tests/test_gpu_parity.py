@@ -460,6 +460,34 @@ def test_adam_bitwise_vs_reference():
         np.testing.assert_array_equal(flat, g["adam_traj"][k])
 
 
+def test_trainer_adam_trajectory_bitwise_vs_reference():
+    """DataParallelTrainer's fused guard + Adam (device step counter, host
+    1 - beta^t table: train.py:104-105) over 5 steps == the reference's
+    apply_update trajectory bit for bit, given the same float64 gradients"""
+    g = golden("misc.npz")
+    flat = g["adam_init"]
+    n = flat.shape[0]
+    # any config with n parameters' worth of padded slots: drive the trainer's
+    # update on a flat vector by placing it in a one-array layout
+    cfg = cfg_of("sum-agg", 1, 2, 2, 1)  # 259 parameters >= the 257 of the golden
+    tr = T.DataParallelTrainer(cfg, T.TrainConfig(optimizer="adam", learning_rate=1e-3),
+                               dtype=F64)
+    lay = tr.layout
+    m = n
+    assert lay.P >= n
+    idx = lay.index(tr.device)[:m]
+    master0 = torch.zeros_like(tr.master)
+    master0[idx] = torch.as_tensor(flat[:m], device=tr.device)
+    tr.master.copy_(master0)
+    for k in range(5):
+        tr.contrib.zero_()
+        tr.contrib[idx] = torch.as_tensor(g["adam_grads"][k][:m], device=tr.device)
+        tr.contrib[tr.P + 1] = 1.0
+        tr.reduce_and_update()
+        np.testing.assert_array_equal(tr.master[idx].cpu().numpy(), g["adam_traj"][k][:m])
+    assert int(tr.t_dev.item()) == 5 and tr.optimizer_state().t == 5
+
+
 def test_c1_adam_first_step_matches_golden():
     g = golden("c1_model.npz")
     flat = g["mean-agg_flat"]
