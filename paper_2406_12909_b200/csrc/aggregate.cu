@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(256)
     k_agg_bwd_prep_vec(const float* __restrict__ dagg, const int* __restrict__ rowptr, int n_nodes,
                        int H, int parts, const float* __restrict__ agg,
                        const float* __restrict__ stat_mean, float* __restrict__ G,
-                       float* __restrict__ coef) {
+                       float* __restrict__ coef, int interleave) {
   pdl_entry();
   const AggLayout L = agg_layout(parts, H);
   const int H4 = H >> 2, ld4 = (L.K * H) >> 2;
@@ -499,8 +499,13 @@ __global__ void __launch_bounds__(256)
       cf.x = one(sd.x, ds.x, mu.x, g.x); cf.y = one(sd.y, ds.y, mu.y, g.y);
       cf.z = one(sd.z, ds.z, mu.z, g.z); cf.w = one(sd.w, ds.w, mu.w, g.w);
     }
-    reinterpret_cast<float4*>(G)[idx] = g;
-    if (coef) reinterpret_cast<float4*>(coef)[idx] = cf;
+    if (interleave) {  // [G | coef] per 4 columns: one 32-byte row slice per (node, c4)
+      reinterpret_cast<float4*>(G)[2 * idx] = g;
+      reinterpret_cast<float4*>(G)[2 * idx + 1] = cf;
+    } else {
+      reinterpret_cast<float4*>(G)[idx] = g;
+      if (coef) reinterpret_cast<float4*>(coef)[idx] = cf;
+    }
   }
 }
 
@@ -545,7 +550,21 @@ __global__ void k_agg_bwd_scalar(const T* __restrict__ G, int ldg, const T* __re
 // One CSC node j over float4 columns v*LPN + cb: ldG/ldC/ldA(i, v) return the
 // dst row i slice of G / coef / argmax (global or staged); hasG/hasC/hasA say
 // which are present.
-template <int NV, int LPN, typename LG, typename LC, typename LA>
+struct f4x2 {
+  float4 a, b;
+};
+// 32-byte load (sm_100 LDG.E.ENL2.256): G and coef of one (node, c4) at once
+__device__ __forceinline__ f4x2 ldg256(const float* p) {
+  f4x2 r;
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
+        "=f"(r.b.z), "=f"(r.b.w)
+      : "l"(p));
+  return r;
+}
+
+// GC: ldG returns f4x2 {G, coef} (interleaved workspace), ldC is unused
+template <int NV, int LPN, bool GC = false, typename LG, typename LC, typename LA>
 __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, bool hasC,
                                              bool hasA, int j, int cb, int H,
                                              const float* __restrict__ dmax, int ldm,
@@ -610,8 +629,16 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
             g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
             cf[u][v] = g[u][v];
             a[u][v] = make_int4(-1, -1, -1, -1);
-            if (ok && hasG) g[u][v] = ldG(i[u], v);
-            if (ok && hasC) cf[u][v] = ldC(i[u], v);
+            if constexpr (GC) {
+              if (ok) {
+                const f4x2 t = ldG(i[u], v);
+                g[u][v] = t.a;
+                cf[u][v] = t.b;
+              }
+            } else {
+              if (ok && hasG) g[u][v] = ldG(i[u], v);
+              if (ok && hasC) cf[u][v] = ldC(i[u], v);
+            }
             if (ok && hasA) a[u][v] = ldA(i[u], v);
           }
 #pragma unroll
@@ -665,8 +692,16 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
           g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
           cf[u][v] = g[u][v];
           a[u][v] = make_int4(-1, -1, -1, -1);
-          if (ok && hasG) g[u][v] = ldG(i[u], v);
-          if (ok && hasC) cf[u][v] = ldC(i[u], v);
+          if constexpr (GC) {
+            if (ok) {
+              const f4x2 t = ldG(i[u], v);
+              g[u][v] = t.a;
+              cf[u][v] = t.b;
+            }
+          } else {
+            if (ok && hasG) g[u][v] = ldG(i[u], v);
+            if (ok && hasC) cf[u][v] = ldC(i[u], v);
+          }
           if (ok && hasA) a[u][v] = ldA(i[u], v);
         }
 #pragma unroll
@@ -706,7 +741,7 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
   }
 }
 
-template <int NV, int LPN, bool U8>
+template <int NV, int LPN, bool U8, bool GC = false>
 __global__ void __launch_bounds__(256, NV == 1 ? (LPN == 32 ? (GFM_AGG_BWD_MINB > 4 ? 4 : GFM_AGG_BWD_MINB) : GFM_AGG_BWD_MINB) : 1)
     k_agg_bwd_vec(const float* __restrict__ G, int ldg, const float* __restrict__ coef,
                   const float* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
@@ -721,9 +756,13 @@ __global__ void __launch_bounds__(256, NV == 1 ? (LPN == 32 ? (GFM_AGG_BWD_MINB 
   const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
   if (j >= n_nodes) return;
   const int cb = blockIdx.y * (NV * LPN) + sub;  // column slab (see k_agg_fwd_vec)
-  agg_bwd_node<NV, LPN>(
+  agg_bwd_node<NV, LPN, GC>(
       [&](int i, int v) {
-        return __ldg(reinterpret_cast<const float4*>(G + (long long)i * ldg) + v * LPN + cb);
+        if constexpr (GC) {
+          return ldg256(G + ((long long)i * (H >> 2) + v * LPN + cb) * 8);
+        } else {
+          return __ldg(reinterpret_cast<const float4*>(G + (long long)i * ldg) + v * LPN + cb);
+        }
       },
       [&](int i, int v) {
         return __ldg(reinterpret_cast<const float4*>(coef + (long long)i * H) + v * LPN + cb);
@@ -849,6 +888,16 @@ static int tile_env(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+// A/B knob of the backward gather: GFM_AGG_GC=1 interleaved [G | coef]
+// workspace read with one 32-byte load per (edge, lane) (default off: equal
+// time at C2 / C3).  A node-chunked block mapping (consecutive CSC nodes per
+// block, for L1 reuse of their graphs' dst rows) measured 1-25% slower.
+static bool gc_env() {
+  static int v = -1;
+  if (v < 0) v = getenv("GFM_AGG_GC") ? atoi(getenv("GFM_AGG_GC")) : 0;
+  return v != 0;
+}
+
 static bool no_tile() {
   const char* e = getenv("GFM_AGG_TILE");
   return !(e && e[0] == '1');
@@ -908,6 +957,7 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
   const AggLayout L = agg_layout(parts, H);
   int ld = L.K * H;
   const size_t esz = dtype == GFM_F32 ? 4 : 8;
+  bool gc = false;  // interleaved [G | coef] workspace, read with 32-byte loads
   // G: dsum alone needs no prep (read dagg in place); mean/std need G/coef
   const void* G = nullptr;
   int ldg = ld;
@@ -919,12 +969,15 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
     ldg = H;
     coef = L.o_std >= 0 ? (const void*)((const char*)ws + esz * (size_t)n * H) : nullptr;
   } else if (L.o_mean >= 0 || L.o_std >= 0) {
+    int nv0 = 0, lpn0 = 0;
+    gc = gc_env() && dtype == GFM_F32 && H % 4 == 0 && !force_scalar && L.o_std >= 0 &&
+         vec_shape(H, nv0, lpn0) && no_tile();
     void* Gw = ws;
     void* Cw = L.o_std >= 0 ? (void*)((char*)ws + esz * (size_t)n * H) : nullptr;
     if (dtype == GFM_F32 && H % 4 == 0 && !force_scalar)
       launch_k(k_agg_bwd_prep_vec, grid_1d((long long)n * (H / 4)), 256, 0, s,
           (const float*)dagg, rowptr, n, H, parts, (const float*)agg, (const float*)stat_mean,
-          (float*)Gw, (float*)Cw);
+          (float*)Gw, (float*)Cw, gc ? 1 : 0);
     else if (dtype == GFM_F32)
       launch_k(k_agg_bwd_prep<float>, grid_1d((long long)n * H), 256, 0, s,
           (const float*)dagg, rowptr, n, H, parts, (const float*)agg, (const float*)stat_mean,
@@ -963,22 +1016,25 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
   if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn, &slabs)) {
     const int nodes_per_block = 8 * (32 / lpn);
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);
+#define GFM_BWD_LAUNCH(NV_, LPN_, U8_, GC_)                                                  \
+  launch_k(k_agg_bwd_vec<NV_, LPN_, U8_, GC_>, grid, 256, 0, s, (const float*)G, ldg,          \
+           (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in, csc_ptr,        \
+           csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,            \
+           (float*)out)
 #define GFM_BWD_CASE(NV_, LPN_)                                                              \
   if (nv == NV_ && lpn == LPN_) {                                                            \
-    if (am_u8)                                                                               \
-      launch_k(k_agg_bwd_vec<NV_, LPN_, true>, grid, 256, 0, s, (const float*)G, ldg,          \
-               (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in, csc_ptr,    \
-               csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,        \
-               (float*)out);                                                                  \
-    else                                                                                     \
-      launch_k(k_agg_bwd_vec<NV_, LPN_, false>, grid, 256, 0, s, (const float*)G, ldg,         \
-               (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in, csc_ptr,    \
-               csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,        \
-               (float*)out);                                                                  \
+    if (gc) {                                                                                \
+      if (am_u8) GFM_BWD_LAUNCH(NV_, LPN_, true, true);                                      \
+      else GFM_BWD_LAUNCH(NV_, LPN_, false, true);                                           \
+    } else {                                                                                 \
+      if (am_u8) GFM_BWD_LAUNCH(NV_, LPN_, true, false);                                     \
+      else GFM_BWD_LAUNCH(NV_, LPN_, false, false);                                          \
+    }                                                                                        \
     return cudaGetLastError();                                                               \
   }
     GFM_VEC_CASES(GFM_BWD_CASE)
 #undef GFM_BWD_CASE
+#undef GFM_BWD_LAUNCH
   }
   if (dtype == GFM_F32)
     launch_k(k_agg_bwd_scalar<float>, grid_1d((long long)n * H), 256, 0, s,

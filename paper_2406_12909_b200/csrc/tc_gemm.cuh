@@ -785,7 +785,9 @@ struct SmemT {
   static constexpr int kRaw = kA + kB;
   static constexpr int kLo = AT ? kB : kRaw;  // lo slot: B only when A lives in TMEM
   // lo slots: conversion of k-block q + kL waits for the MMAs of q, so kL
-  // bounds how far the converters run ahead of the tensor pipe
+  // bounds how far the converters run ahead of the tensor pipe (with A in
+  // TMEM each slot also takes 64 TMEM columns; kL = 2 for 64-wide tiles, to
+  // stay within 256 columns, measured 2% slower at C2)
   static constexpr int kL = AT ? 4 : 3;
   // epilogue transpose staging: 8 warps x 32 rows x (16 + 4 pad) floats
   static constexpr int kEpi = 8 * 32 * 20 * 4;
@@ -897,7 +899,9 @@ __device__ __forceinline__ void kb_ss1(uint32_t d, uint64_t ah, uint64_t ainc, u
 // AT: 0 = A in smem; 1 = A in TMEM, staged K-major SWIZZLE_128B; 2 = A in
 // TMEM, staged MN-major without swizzle ([32-row atom][k][32], so converter
 // lane r reads its row down the k column conflict-free)
-template <int BN, class Epi, int AT>
+// FLUSH: work items deeper than the flush depth (see flush_kb) accumulate in
+// chunks folded into registers; shallow GEMMs take the plain instantiation
+template <int BN, class Epi, int AT, bool FLUSH>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     tc_gemm_tma_kernel(int M, const int* __restrict__ M_dev, int N, int K, int k_chunk, int splits,
                        int split3, int fkb, const __grid_constant__ TmaOp ta,
@@ -966,7 +970,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   };
   auto nkb_of = [&](int w) { return item_nkb(w, m_tiles * n_tiles, k_chunk, K); };
   // accumulation chunks of a work item (>= 1: an empty item still completes once)
-  auto nch_of = [&](int nkb) { return nkb > 0 ? (nkb + fkb - 1) / fkb : 1; };
+  auto nch_of = [&](int nkb) {
+    if constexpr (!FLUSH) return 1;
+    return nkb > 0 ? (nkb + fkb - 1) / fkb : 1;
+  };
 
   if (warp == 0) {
     // ============================================================ TMA producer
@@ -1234,9 +1241,13 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
         else
           build_tma(a, &ta, kBM, M, K);
       }
-      auto kern = at == 1   ? tc_gemm_tma_kernel<BN, Epi, 1>
-                  : at == 2 ? tc_gemm_tma_kernel<BN, Epi, 2>
-                            : tc_gemm_tma_kernel<BN, Epi, 0>;
+      const bool flush = ceil_div(k_chunk, kBK) > flush_kb();
+      auto kern = flush ? (at == 1   ? tc_gemm_tma_kernel<BN, Epi, 1, true>
+                           : at == 2 ? tc_gemm_tma_kernel<BN, Epi, 2, true>
+                                     : tc_gemm_tma_kernel<BN, Epi, 0, true>)
+                        : (at == 1   ? tc_gemm_tma_kernel<BN, Epi, 1, false>
+                           : at == 2 ? tc_gemm_tma_kernel<BN, Epi, 2, false>
+                                     : tc_gemm_tma_kernel<BN, Epi, 0, false>);
       const int smem = at ? SmemT<BN, true>::kBytes : SmemT<BN, false>::kBytes;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;

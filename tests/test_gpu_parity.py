@@ -668,3 +668,34 @@ def test_fused_bwd_data_agg_prep_matches_unfused(H):
                   _lib.ptr(h), _lib.ptr(out), _lib.ptr(ws), _lib.F32, fl, s)
         outs.append(out.cpu().numpy())
     assert_close_scaled(outs[1], outs[0], 1e-5, FP32_FLOOR, what=f"H={H}")
+
+
+class _HostOnlyComm:
+    """a gfmkit-style Comm (comm.py:55-77): host float64 allreduce_sum only,
+    no device method -- here two identical ranks (sum = 2 x)"""
+    rank, size = 0, 2
+
+    def allreduce_sum(self, vec):
+        return np.asarray(vec, np.float64) * 2.0
+
+    def broadcast_obj(self, obj, root=0):
+        return obj
+
+    def barrier(self):
+        pass
+
+
+def test_trainer_accepts_reference_style_comm():
+    """train.py's allreduce contract through a Comm without allreduce_sum_
+    (host path) == two identical ranks == one rank, bitwise"""
+    recs = O.synthetic(6, rc=2.5, seed=2)
+    cfg = cfg_of("pna-agg", 2, 16, 2, 8)
+    flat = O.init_flat(O.config("pna-agg", 2, 16, 2, 8), 3)
+    outs = []
+    for comm in (_HostOnlyComm(), None):
+        tr = T.DataParallelTrainer(cfg, T.TrainConfig(), comm=comm, initial=flat, dtype=F32)
+        b = M.make_batch(as_records(recs), dtype=F32)
+        for _ in range(2):
+            tr.step(b)
+        outs.append(tr.flat_master())
+    np.testing.assert_array_equal(outs[0], outs[1])

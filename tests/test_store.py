@@ -95,3 +95,72 @@ def test_store_from_arrays():
         assert torch.equal(x, y)
     with pytest.raises(ValidationError):
         a.fetch_batch("trainset", idx)
+
+
+def _gather_runner_batch(store, idx, dtype):
+    """run the store-mode gather once (eagerly) and return its Batch"""
+    mc = M.ModelConfig(mpnn_kind="sum-agg", mpnn_layers=1, mpnn_width=8, fc_width=8)
+    tr = T.DataParallelTrainer(mc, T.TrainConfig(), dtype=dtype)
+    run = T.StructureStepRunner(tr, None, store=store, max_graphs=len(idx) + 2, use_graph=False)
+    run.set_indices(idx)
+    with tr.preserved():
+        run._eager()
+    torch.cuda.synchronize()
+    return run.batch
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_store_gather_batch_matches_make_batch(dtype):
+    """gfm_gather_batch (per-structure CSR blocks copied with shifted ids)
+    == make_batch's CSR / CSC of the same records, bitwise; capacity tail
+    nodes edge-free with gnode -1"""
+    from paper_2406_12909_b200.store import DeviceStructureStore
+    recs = _records(30, 11, n_range=(2, 14))
+    store = DeviceStructureStore({"trainset": recs})
+    idx = np.array([4, 29, 0, 4, 17, 9])
+    b = _gather_runner_batch(store, idx, dtype)
+    ref = M.make_batch([recs[i] for i in idx], dtype=dtype)
+    N, E = ref.n_nodes, ref.n_edges
+    assert int(b.rowptr[N].item()) == E and int(b.rowptr[-1].item()) == E
+    for k in ("rowptr", "csc_ptr"):
+        np.testing.assert_array_equal(getattr(b, k).cpu().numpy()[:N + 1],
+                                      getattr(ref, k).cpu().numpy(), err_msg=k)
+    for k in ("col_src", "edge_dst", "csc_eid", "csc_dst", "edge_w", "edge_dx"):
+        np.testing.assert_array_equal(getattr(b, k).cpu().numpy()[:E],
+                                      getattr(ref, k).cpu().numpy()[:E], err_msg=k)
+    np.testing.assert_array_equal(b.graph_of_node.cpu().numpy()[:N],
+                                  ref.graph_of_node.cpu().numpy()[:N])
+    assert (b.graph_of_node.cpu().numpy()[N:] == -1).all()
+    np.testing.assert_array_equal(b.counts.cpu().numpy(), [len(idx), N])
+
+
+class _HostStore:
+    """the reference DDStore surface only (ownership + fetch_batch): train()
+    then packs every batch with make_batch on the host"""
+
+    def __init__(self, groups):
+        self._g = groups
+        self.ownership = {k: type("O", (), {"n_samples": len(v)})() for k, v in groups.items()}
+
+    def fetch_batch(self, group, indices):
+        return [self._g[group][int(i)] for i in indices]
+
+
+def test_train_device_store_matches_host_packing():
+    """train() with a DeviceStructureStore (batches gathered on the device
+    inside one captured step, ragged, short last batch) == train() packing
+    the same batches on the host, float64, 2 epochs"""
+    from paper_2406_12909_b200.store import DeviceStructureStore
+    recs = _records(23, 12, n_range=(3, 11))
+    groups = {"trainset": recs[:19], "valset": recs[19:]}
+    mc = M.ModelConfig(mpnn_kind="pna-agg", mpnn_layers=2, mpnn_width=16, fc_width=16,
+                       batch_size=4)
+    cfg = T.TrainConfig(max_epochs=2, patience=5)
+    dev = T.train(mc, DeviceStructureStore(groups), config=cfg, dtype=torch.float64)
+    host = T.train(mc, _HostStore(groups), config=cfg, dtype=torch.float64)
+    assert dev.epochs_run == host.epochs_run == 2
+    for a, b in zip(dev.metrics, host.metrics):
+        assert abs(a.train_loss - b.train_loss) <= 1e-10 * abs(b.train_loss)
+        assert abs(a.val_mae - b.val_mae) <= 1e-10 * abs(b.val_mae)
+        assert "step" in a.phase_seconds and "forward" in b.phase_seconds
+    np.testing.assert_allclose(dev.params.flatten(), host.params.flatten(), rtol=0, atol=1e-10)
