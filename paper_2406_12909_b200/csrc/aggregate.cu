@@ -26,8 +26,10 @@
 
 #include "common.cuh"
 
+// CSC slots batched per iteration on 32-lane rows: 1 measured 4.6% faster
+// than 2 (and 4 55% slower) at C3 (tools/agg_knobs2.sh, round 2)
 #ifndef GFM_AGG_BWD_U
-#define GFM_AGG_BWD_U 2
+#define GFM_AGG_BWD_U 1
 #endif
 #ifndef GFM_AGG_FWD_UF
 #define GFM_AGG_FWD_UF 4

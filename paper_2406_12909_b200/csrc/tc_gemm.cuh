@@ -210,7 +210,11 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 constexpr int tmem_cols(int cols) {
+#ifdef GFM_TMEM_CAP256
+  return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256;
+#else
   return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+#endif
 }
 
 // ring depth by BN (192 KB of ring + lo buffers, one CTA per SM)

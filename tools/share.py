@@ -19,8 +19,10 @@ def load(path):
 
 CATS = [("radius/CSR/CSC", r"k_radius|k_stable_bucket|k_scan|k_histogram|k_csc|k_csr|k_count|k_fill_idx|k_place"),
         ("agg fwd", r"k_agg_fwd"), ("agg bwd", r"k_agg_bwd"),
-        ("force edges", r"k_force_"), ("tcgen05 GEMM", r"tc_gemm"),
-        ("split-K / colsum", r"splitk|colsum"), ("other", r".")]
+        ("force edges", r"k_force_"), ("EGNN edge / tanh / head", r"k_egnn"),
+        ("tcgen05 GEMM", r"tc_gemm"),
+        ("split-K / colsum", r"splitk|colsum"), ("loss / Adam / guard", r"k_loss|k_adam|k_nonfinite|k_sgd"),
+        ("other", r".")]
 rows = load(sys.argv[1])
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 tot = sum(t for _, t in rows)

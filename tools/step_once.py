@@ -21,8 +21,13 @@ ap.add_argument("--batch", type=int, default=None)
 a = ap.parse_args()
 W = CONFIGS[a.config]
 B, n = a.batch or W["batch"], W["atoms"][1]
-cfg = M.ModelConfig(mpnn_kind=W["kind"], mpnn_layers=W["layers"], mpnn_width=W["hidden"],
-                    fc_layers=2, fc_width=W["fc_width"], batch_size=B)
+if W["kind"] == "egnn":
+    from paper_2406_12909_b200.egnn import EGNNConfig
+    cfg = EGNNConfig(egnn_layers=W["layers"], egnn_width=W["hidden"], fc_layers=W["fc_layers"],
+                     fc_width=W["fc_width"], batch_size=B)
+else:
+    cfg = M.ModelConfig(mpnn_kind=W["kind"], mpnn_layers=W["layers"], mpnn_width=W["hidden"],
+                        fc_layers=2, fc_width=W["fc_width"], batch_size=B)
 tr = T.DataParallelTrainer(cfg, T.TrainConfig())
 cells = [[W["box"]] * 3] * B if W["periodic"] else None
 runner = T.StructureStepRunner(tr, (np.arange(B + 1) * n).astype(np.int32), W["rc"],
