@@ -359,9 +359,11 @@ GFM_API int gfm_egnn_energy(const void* y, const void* yd, int ldy, int n, int G
 GFM_API int gfm_egnn_head_seed(const void* de, const int* gnode, int n, int rows,
                                double edot_seed, const void* a, int G, void* ds, void* yb,
                                int ldyb, int dtype, void* stream);
-/* out[c] (+)= sum_{r < rows} X[r][c] (row stride ld), fixed order */
+/* out[c] (+)= sum_{r < rows} X[r][c] (row stride ld), fixed order (two
+ * levels through a float64 workspace of gfm_colsum_workspace_bytes) */
+GFM_API size_t gfm_colsum_workspace_bytes(int rows, int cols);
 GFM_API int gfm_colsum(const void* X, int rows, int cols, int ld, void* out, int accumulate,
-                       int dtype, void* stream);
+                       void* workspace, int dtype, void* stream);
 /* y = alpha x */
 GFM_API int gfm_scale(const void* x, long long n, double alpha, void* y, int dtype, void* stream);
 

@@ -110,7 +110,8 @@ SIGNATURES = {
     "gfm_egnn_tanh_bwd": (_I, [_P, _I, _P, _I, _P, _P, _I, _I, _I, _P, _P, _I, _I, _P]),
     "gfm_egnn_energy": (_I, [_P, _P, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _I, _P]),
     "gfm_egnn_head_seed": (_I, [_P, _P, _I, _I, _D, _P, _I, _P, _P, _I, _I, _P]),
-    "gfm_colsum": (_I, [_P, _I, _I, _I, _P, _I, _I, _P]),
+    "gfm_colsum_workspace_bytes": (_S, [_I, _I]),
+    "gfm_colsum": (_I, [_P, _I, _I, _I, _P, _I, _P, _I, _P]),
     "gfm_scale": (_I, [_P, _L, _D, _P, _I, _P]),
 }
 

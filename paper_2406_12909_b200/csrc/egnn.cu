@@ -26,7 +26,7 @@
 //   k_egnn_tanh_fwd/bwd  h = tanh(z + b), hdot = (1 - h^2) zdot and adjoints
 //   k_egnn_head_out      node energies (and tangents) + per-graph pool
 //   k_egnn_head_seed     dL/d node energy (primal de[g], tangent -1) rows
-//   k_colsum_ld          deterministic column sums (bias / vector grads)
+//   k_colsum_part/final  deterministic two-level column sums (bias / vector grads)
 #include <cstdio>
 
 #include "common.cuh"
@@ -469,23 +469,40 @@ __global__ void k_egnn_head_seed(const T* __restrict__ de, const int* __restrict
   }
 }
 
-// deterministic column sums of rows [0, rows) of X (ld): block per 32-column
-// slab, 8 row groups strided, fixed-order combine (double accumulation)
+// deterministic column sums of rows [0, rows) of X (ld), two levels: block
+// (chunk c, slab s) sums rows [c*kColRows, +kColRows) of 32 columns (8 row
+// groups, fixed-order combine, double) into part[c][cols]; a second launch
+// sums the chunk partials in chunk order.  Result depends only on the shape.
+constexpr int kColRows = 256;
 template <typename T>
-__global__ void k_colsum_ld(const T* __restrict__ X, int rows, int cols, int ld,
-                            T* __restrict__ out, int accumulate) {
+__global__ void k_colsum_part(const T* __restrict__ X, int rows, int cols, int ld,
+                              double* __restrict__ part) {
   pdl_entry();
   __shared__ double red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + tx;
+  const int c = blockIdx.y * 32 + tx;
+  const int r0 = blockIdx.x * kColRows, r1 = min(rows, r0 + kColRows);
   double s = 0.0;
-  if (c < cols)
-    for (int r = ty; r < rows; r += 8) s += (double)X[(long long)r * ld + c];
+  if (c < cols) {
+#pragma unroll 4
+    for (int r = r0 + ty; r < r1; r += 8) s += (double)X[(long long)r * ld + c];
+  }
   red[ty][tx] = s;
   __syncthreads();
   if (ty == 0 && c < cols) {
     double t = 0.0;
     for (int q = 0; q < 8; ++q) t += red[q][tx];
+    part[(long long)blockIdx.x * cols + c] = t;
+  }
+}
+
+template <typename T>
+__global__ void k_colsum_final(const double* __restrict__ part, int chunks, int cols,
+                               T* __restrict__ out, int accumulate) {
+  pdl_entry();
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int k = 0; k < chunks; ++k) t += part[(long long)k * cols + c];
     out[c] = accumulate ? (T)((double)out[c] + t) : (T)t;
   }
 }
@@ -666,12 +683,23 @@ int gfm_egnn_head_seed(const void* de, const int* gnode, int n, int rows, double
                          (const T*)a, G, (T*)ds, (T*)yb, ldyb))
 }
 
-int gfm_colsum(const void* X, int rows, int cols, int ld, void* out, int accumulate, int dtype,
-               void* stream) {
+size_t gfm_colsum_workspace_bytes(int rows, int cols) {
+  const int chunks = rows > 0 ? (rows + kColRows - 1) / kColRows : 1;
+  return sizeof(double) * (size_t)chunks * (size_t)(cols > 0 ? cols : 1);
+}
+
+int gfm_colsum(const void* X, int rows, int cols, int ld, void* out, int accumulate,
+               void* workspace, int dtype, void* stream) {
   if (cols <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int chunks = rows > 0 ? (rows + kColRows - 1) / kColRows : 1;
+  double* part = (double*)workspace;
   GFM_EDISPATCH(dtype, "gfm_colsum",
-                launch_k(k_colsum_ld<T>, (cols + 31) / 32, 256, 0, (cudaStream_t)stream,
-                         (const T*)X, rows, cols, ld, (T*)out, accumulate))
+                (rows > 0 ? launch_k(k_colsum_part<T>, dim3(chunks, (cols + 31) / 32), 256, 0, s,
+                                     (const T*)X, rows, cols, ld, part)
+                          : cudaMemsetAsync(part, 0, sizeof(double) * cols, s),
+                 launch_k(k_colsum_final<T>, (cols + 255) / 256, 256, 0, s, (const double*)part,
+                          chunks, cols, (T*)out, accumulate)))
 }
 
 int gfm_scale(const void* x, long long n, double alpha, void* y, int dtype, void* stream) {
