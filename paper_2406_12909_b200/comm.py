@@ -118,10 +118,12 @@ class TorchComm(Comm):
         if self.deterministic:
             parts = [torch.empty_like(t) for _ in range(self.size)]
             dist.all_gather(parts, t, group=self.group)
-            out = parts[0].clone()
-            for p in parts[1:]:  # ascending rank order, always (comm.py:143-147)
-                out += p
-            t.copy_(out)
+            # ascending rank order, always, accumulated in float64 like the
+            # reference's float64 vectors (comm.py:143-147)
+            out = parts[0].to(torch.float64)
+            for p in parts[1:]:
+                out += p.to(torch.float64)
+            t.copy_(out.to(t.dtype))
             return t
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t

@@ -121,7 +121,8 @@ def test_bench_reference_arm_json_contract():
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
-                          "--steps", "1", "--warmup", "0", "--cpu-sample-s", "1"],
+                          "--config", "c2", "--steps", "1", "--warmup", "0", "--cpu-sample-s",
+                          "1", "--ref-ranks", "1"],
                          capture_output=True, text=True, timeout=300, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -131,3 +132,7 @@ def test_bench_reference_arm_json_contract():
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     for k in ("metric", "n_gpus", "steps", "warmup", "scaling", "dtype", "data", "config"):
         assert k in line
+    dp = line["reference_dp"]  # the reference's own DP path, when baseline/_ref holds it
+    if "unavailable" not in dp:
+        assert dp["kind"] == "reference" and dp["value"] > 0
+        assert dp["points"][0]["ranks"] == 1 and "cpu_model" in dp

@@ -9,10 +9,10 @@ formulas (algorithmic bytes) against MEASURED_PEAKS.json's HBM copy rate.
 
 Two modes:
  (ii) fused  -- h[N, H] + src + w: the step's kernels gather h[src] rows;
- (i)  materialised -- msg[E, H] already formed (PyG scatter style): the same
-      kernels with every edge its own source row (col_src = identity, w = 1),
-      so the forward streams msg once in CSR order and the backward writes
-      dmsg[E, H] (one row per edge).
+ (i)  materialised -- msg[E, H] already formed (PyG scatter style, sum): the
+      same kernels with every edge its own source row (col_src = identity,
+      w = 1), so the forward streams msg once in CSR order and the backward
+      writes dmsg[E, H] (one row per edge).
 Configurations whose buffers would exceed --mem-gb are skipped (e.g. mode
 (i) at 100M x 512: msg alone is 205 GB).
 """
@@ -149,7 +149,10 @@ for Em in [m for m in (1, 4, 16, 64, 100) if m <= a.max_e]:
                 u8 = _lib.FLAG_ARGMAX_U8 if g["max_deg"] <= 256 else 0
                 # footprint: h, agg, dagg, dh, out, argmax, std mean, G + coef
                 fp = 4 * N * H * (1 + K + K + 2 + 1 + 2) + N * H
-                if "materialised" in modes and pattern == "random" and \
+                # (i) is the PyG scatter-sum baseline: one message row per edge,
+                # sum only (the kernels' node count is the source count, so the
+                # dst-side prep of mean/std/max needs the fused layout)
+                if "materialised" in modes and pattern == "random" and kind == "sum" and \
                         E * H * 4 * 3 + 4 * N * H * (2 * K + 3) < a.mem_gb * 1e9:
                     rows.append(materialised(E, H, g, kind, parts, K, u8))
                 if "fused" not in modes or fp > a.mem_gb * 1e9:
