@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import contextlib
 import json
+import os
 import logging
 import struct
 import time
@@ -221,6 +222,9 @@ class DataParallelTrainer:
         self.steps = 0
         # bucketed, backward-overlapped gradient allreduce (N > 1, MPNN): each
         # bucket is summed on a comm stream as soon as its gradients are final
+        if os.environ.get("GFM_BUCKET_MB"):  # A/B knob: bucket size in MB (0 = one bucket)
+            mb = float(os.environ["GFM_BUCKET_MB"])
+            bucket_bytes = int(mb * (1 << 20)) if mb > 0 else 1 << 62
         self.buckets = plan_buckets(self.layout, model_config, bucket_bytes,
                                     self.contrib.element_size())
         self.bucketed = (self.comm.size > 1 and len(self.buckets) > 1
