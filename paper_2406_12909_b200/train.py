@@ -177,7 +177,7 @@ class DataParallelTrainer:
 
     def __init__(self, model_config: ModelConfig, train_config: TrainConfig | None = None,
                  comm: Comm | None = None, device=None, initial=None,
-                 dtype=torch.float32, flags: int = 0, bucket_bytes: int = 4 << 20):
+                 dtype=torch.float32, flags: int = 0, bucket_bytes: int = 64 << 20):
         _lib.load(require_device=True)
         self.cfg = model_config
         self.tcfg = train_config or TrainConfig()
@@ -221,7 +221,12 @@ class DataParallelTrainer:
         self.scratch = _Scratch(self.device)
         self.steps = 0
         # bucketed, backward-overlapped gradient allreduce (N > 1, MPNN): each
-        # bucket is summed on a comm stream as soon as its gradients are final
+        # bucket is summed on a comm stream as soon as its gradients are final.
+        # Default 64 MB buckets, i.e. one allreduce for every benched config:
+        # at C3 on 4 B200 (34 MB payload) 4 MB buckets measured 22.2 ms/step,
+        # 16 MB 21.8, one allreduce 21.45 (profiles/r02_bucket_ab.txt) -- NCCL
+        # kernels overlapping the persistent (one CTA per SM) GEMMs cost the
+        # GEMMs more than the overlap hides
         if os.environ.get("GFM_BUCKET_MB"):  # A/B knob: bucket size in MB (0 = one bucket)
             mb = float(os.environ["GFM_BUCKET_MB"])
             bucket_bytes = int(mb * (1 << 20)) if mb > 0 else 1 << 62
