@@ -96,6 +96,14 @@ GFM_API int gfm_gather_batch(const int* idx, const int* meta, int n_cap_graphs, 
                              double* pos, void* e, void* f, int* gnode, int* rowptr, int* col_src,
                              int* edge_dst, void* w, void* dx, int* csc_ptr, int* csc_eid,
                              int* csc_dst, int dtype, void* stream);
+/* Variable-length row-block gather (sharded store pack / unpack, the
+ * NVLink shard exchange replacing DDStore's remote fetch, ddstore.py:441-464):
+ * output block b = input block idx[b] (idx NULL: identity), rows
+ * [src_off[s], src_off[s+1]) copied to rows from dst_off[b], `width` 32-bit
+ * words per row; add[b] (optional) is added to every word (node-id shift). */
+GFM_API int gfm_gather_blocks(const int* idx, int n_out, const long long* src_off,
+                              const long long* dst_off, int width, const void* in, void* out,
+                              const int* add, void* stream);
 GFM_API size_t gfm_scan_workspace_bytes(int n);
 GFM_API int gfm_exclusive_scan(const int* in, int n, int* out, void* workspace, void* stream);
 /* Radius graph replacing build_cutoff_edges (preprocess.py:90-104), emitted

@@ -119,6 +119,26 @@ __global__ void k_gather_batch(const int* __restrict__ idx, const int* __restric
   }
 }
 
+// Variable-length row-block gather (the sharded store's pack / unpack for
+// the NVLink exchange): output block b = input block idx[b], rows
+// [src_off[s], src_off[s+1]) -> rows from dst_off[b], `width` 32-bit words
+// per row; add (optional) is added to every word of block b (node-id shift
+// of edge lists).  One CTA per output block (grid-strided), coalesced.
+__global__ void k_gather_blocks(const int* __restrict__ idx, int n_out,
+                                const long long* __restrict__ src_off,
+                                const long long* __restrict__ dst_off, int width,
+                                const unsigned* __restrict__ in, unsigned* __restrict__ out,
+                                const int* __restrict__ add) {
+  pdl_entry();
+  for (int b = blockIdx.x; b < n_out; b += gridDim.x) {
+    const int s = idx ? idx[b] : b;
+    const long long so = src_off[s] * width, n = (src_off[s + 1] - src_off[s]) * width;
+    const long long d = dst_off[b] * width;
+    const unsigned a = add ? (unsigned)add[b] : 0u;
+    for (long long t = threadIdx.x; t < n; t += blockDim.x) out[d + t] = in[so + t] + a;
+  }
+}
+
 __global__ void k_iota(int* __restrict__ out, int n) {
   pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
@@ -778,6 +798,17 @@ int gfm_gather_batch(const int* idx, const int* meta, int n_cap_graphs, int n_no
     set_error("gfm_gather_batch: bad dtype %d", dtype);
     return GFM_EINVAL;
   }
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gfm_gather_blocks(const int* idx, int n_out, const long long* src_off,
+                      const long long* dst_off, int width, const void* in, void* out,
+                      const int* add, void* stream) {
+  if (n_out <= 0) return 0;
+  const int grid = n_out < 148 * 16 ? n_out : 148 * 16;
+  launch_k(k_gather_blocks, grid, 128, 0, (cudaStream_t)stream, idx, n_out, src_off, dst_off,
+           width, (const unsigned*)in, (unsigned*)out, add);
   GFM_TRY(cudaGetLastError());
   return 0;
 }

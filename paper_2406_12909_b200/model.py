@@ -391,11 +391,30 @@ def make_batch(records, device=None, dtype=torch.float32) -> Batch:
     N, E, B = int(offsets[-1]), int(e_off[-1]), len(records)
     if E and (src.max() >= N or dst.max() >= N or min(src.min(), dst.min()) < 0):
         raise ValidationError("edge endpoint out of range")
-    f = dict(device=dev)
     t_pos = torch.from_numpy(pos).to(dev, non_blocking=True)
     t_src, t_dst = _i32(src, dev), _i32(dst, dev)
     t_eoff, t_off = _i32(e_off, dev), _i32(offsets, dev)
     t_shift = torch.from_numpy(shift).to(dev) if shift is not None else None
+    return batch_from_device(_i32(z, dev), t_pos, energy, forces, t_src, t_dst, t_eoff, t_off,
+                             offsets, dtype, t_shift,
+                             int(np.bincount(dst, minlength=1).max()) if E else 0)
+
+
+def batch_from_device(z, pos, energy, forces, src, dst, edge_offsets, node_offsets,
+                      host_offsets, dtype=torch.float32, shift=None, max_deg=None) -> Batch:
+    """make_batch's device half (model.py:234-285): structures already
+    concatenated on the device -- z i32 [N], pos f64 [N,3], energy [B],
+    forces [N,3], record edges as global src / dst i32 [E] with per-graph edge
+    offsets (device, B+1) -- into the dst-sorted CSR + src-sorted CSC batch.
+    ``max_deg`` bounds any row (enables the uint8 argmax; None = unknown)."""
+    dev = pos.device
+    code = _lib.dtype_code(dtype)
+    offsets = np.asarray(host_offsets, np.int64)
+    n_per = np.diff(offsets)
+    N, B = int(offsets[-1]), int(offsets.shape[0] - 1)
+    E = int(src.shape[0])
+    f = dict(device=dev)
+    t_pos, t_src, t_dst, t_eoff, t_off, t_shift = pos, src, dst, edge_offsets, node_offsets, shift
     Ec = max(E, 1)
     rowptr = torch.empty(N + 1, dtype=torch.int32, **f)
     csc_ptr = torch.empty(N + 1, dtype=torch.int32, **f)
@@ -413,13 +432,12 @@ def make_batch(records, device=None, dtype=torch.float32) -> Batch:
          ptr(csc_ptr), ptr(csc_eid), ptr(csc_dst), code, ptr(ws), s)
     gnode = torch.empty(max(N, 1), dtype=torch.int32, **f)
     call("gfm_graph_of_node", ptr(t_off), B, ptr(gnode), s)
-    b = Batch(dtype=dtype, device=dev, z=_i32(z, dev), pos=t_pos, node_offsets=t_off,
+    b = Batch(dtype=dtype, device=dev, z=z, pos=t_pos, node_offsets=t_off,
               n_per_graph=_i32(n_per, dev), graph_of_node=gnode, energy_true=energy,
               forces_true=forces, rowptr=rowptr, col_src=col_src, edge_dst=edge_dst,
               edge_w=edge_w, edge_dx=edge_dx, csc_ptr=csc_ptr, csc_eid=csc_eid,
               csc_dst=csc_dst, order=order, n_nodes=N, e_cap=E, _n_edges=E,
-              host_offsets=offsets, host_n_per=n_per,
-              max_deg=int(np.bincount(dst, minlength=1).max()) if E else 0,
+              host_offsets=offsets, host_n_per=n_per, max_deg=max_deg,
               periodic=shift is not None)
     b._keep = (t_src, t_dst, t_eoff, t_shift, ws)
     return b

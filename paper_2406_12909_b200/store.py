@@ -250,3 +250,304 @@ def gather_batch(g: "_Group", idx_dev, meta_dev, n_cap_graphs: int, n_nodes: int
               host_offsets=host_off_cap, host_n_per=np.diff(host_off_cap), max_deg=g.max_deg,
               counts=counts_view, periodic=g.periodic)
     return b
+
+
+# --------------------------------------------------------------------------
+# Sharded store: DDStore over NVLink
+# --------------------------------------------------------------------------
+
+
+def partition_for_readers(record_count: int, reader_count: int):
+    """container.py:253-268: contiguous, disjoint, sizes differ by at most
+    one, the larger ranges on the lower ids."""
+    if reader_count < 1:
+        raise ValidationError(f"reader_count must be >= 1, got {reader_count}")
+    base, extra = divmod(int(record_count), int(reader_count))
+    out, start = [], 0
+    for r in range(reader_count):
+        size = base + (1 if r < extra else 0)
+        out.append((start, start + size))
+        start += size
+    return out
+
+
+class OwnershipMap:
+    """Who holds which contiguous slice (ddstore.py:95-165): ranks form
+    ``replication_factor`` sub-groups of P / R consecutive ranks; each
+    sub-group holds the whole group, split by partition_for_readers or by
+    explicit ``chunk_sizes`` (empty chunks allowed)."""
+
+    def __init__(self, n_samples: int, n_ranks: int, replication_factor: int = 1,
+                 chunk_sizes=None):
+        from .errors import ConfigError
+        if n_ranks < 1 or replication_factor < 1 or n_ranks % replication_factor:
+            raise ConfigError(f"replication_factor {replication_factor} must divide "
+                              f"n_ranks {n_ranks} (>= 1)")
+        self.n_samples = int(n_samples)
+        self.n_ranks = int(n_ranks)
+        self.replication_factor = int(replication_factor)
+        self.group_size = n_ranks // replication_factor
+        if chunk_sizes is None:
+            self.local_ranges = partition_for_readers(n_samples, self.group_size)
+        else:
+            cs = [int(c) for c in chunk_sizes]
+            if len(cs) != self.group_size or min(cs, default=0) < 0 or sum(cs) != n_samples:
+                raise ConfigError(f"chunk_sizes must be {self.group_size} nonnegative sizes "
+                                  f"summing to {n_samples}")
+            edges = np.concatenate([[0], np.cumsum(cs)]).astype(int)
+            self.local_ranges = [(int(edges[i]), int(edges[i + 1])) for i in range(len(cs))]
+        # upper bounds of the non-empty chunks -> their local ids
+        self._hi = np.array([hi for lo, hi in self.local_ranges if hi > lo], np.int64)
+        self._id = np.array([k for k, (lo, hi) in enumerate(self.local_ranges) if hi > lo],
+                            np.int64)
+
+    def subgroup_of(self, rank: int) -> int:
+        return rank // self.group_size
+
+    def local_rank(self, rank: int) -> int:
+        return rank % self.group_size
+
+    def range_of(self, rank: int):
+        return self.local_ranges[self.local_rank(rank)]
+
+    def chunk_sizes(self):
+        return [hi - lo for lo, hi in self.local_ranges]
+
+    def owners(self, indices, caller_rank: int) -> np.ndarray:
+        """owning rank of every index, within the caller's replica sub-group"""
+        idx = np.asarray(indices, np.int64).reshape(-1)
+        if idx.size and (idx.min() < 0 or idx.max() >= self.n_samples):
+            raise ValidationError(f"index out of range [0, {self.n_samples})")
+        local = self._id[np.searchsorted(self._hi, idx, side="right")]
+        return self.subgroup_of(caller_rank) * self.group_size + local
+
+    def owner_of(self, global_index: int, caller_rank: int) -> int:
+        return int(self.owners([global_index], caller_rank)[0])
+
+
+def plan_fetch(indices, ownership: OwnershipMap, rank: int, world: int):
+    """host plan of one collective fetch: per-owner request lists (in the
+    caller's order within each owner), the send counts, and the permutation
+    from owner-grouped arrival order back to ``indices`` order"""
+    idx = np.asarray(indices, np.int64).reshape(-1)
+    own = ownership.owners(idx, rank) if idx.size else np.zeros(0, np.int64)
+    order = np.argsort(own, kind="stable")          # owner-grouped, stable
+    counts = np.bincount(own, minlength=world).astype(np.int64)
+    arrival_to_batch = np.empty_like(order)
+    arrival_to_batch[order] = np.arange(order.shape[0])  # batch position -> arrival slot
+    return idx[order], counts, arrival_to_batch
+
+
+class ShardedDeviceStore:
+    """DDStore's one-sided remote fetch (ddstore.py:316-490; the paper's MPI
+    RMA store) rebuilt over NVLink: every rank keeps only
+    its OwnershipMap shard of each group in HBM -- structures and their
+    records' own edges -- and a batch is assembled by ONE collective
+    exchange: request counts and indices (all_to_all), the owners pack the
+    requested structures on the device (gfm_gather_blocks), the packed
+    arrays travel with all_to_all_single over NCCL, and the requester unpacks
+    them into batch order and builds the CSR/CSC (gfm_csr_build).
+
+    ``fetch_device_batch`` is collective: every rank of ``comm`` calls it
+    once per step (an idle rank with no indices)."""
+
+    collective = True
+
+    def __init__(self, groups: dict, comm, replication_factor: int = 1, device=None,
+                 chunk_sizes=None):
+        """``groups``: {name: full record list} (each rank keeps its shard)
+        or {name: (records of this rank's shard, total count)}."""
+        _lib.load(require_device=True)
+        self.comm = comm
+        self.rank, self.world = comm.rank, comm.size
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.ownership = {}
+        self._g = {}
+        self._max_deg = {}
+        for name, v in groups.items():
+            if isinstance(v, tuple):
+                recs, total = v
+            else:
+                recs, total = v, len(v)
+            own = OwnershipMap(total, self.world, replication_factor,
+                               (chunk_sizes or {}).get(name))
+            lo, hi = own.range_of(self.rank)
+            if not isinstance(v, tuple):
+                recs = recs[lo:hi]
+            if len(recs) != hi - lo:
+                raise ValidationError(f"group {name!r}: shard of rank {self.rank} needs "
+                                      f"{hi - lo} records, got {len(recs)}")
+            self.ownership[name] = own
+            periodic = self._global_max(int(any(getattr(r, "edge_shift", None) is not None
+                                                 for r in recs)))
+            self._g[name] = self._ingest(recs, bool(periodic))
+            self._max_deg[name] = self._global_max(self._g[name]["max_deg"])
+
+    @classmethod
+    def from_container(cls, path: str, comm, groups=None, replication_factor: int = 1,
+                       device=None) -> "ShardedDeviceStore":
+        """read only this rank's shard of each group (container.read_range)"""
+        from .container import GROUP_NAMES, read_manifest, read_range
+        man = read_manifest(path)
+        out = {}
+        for g in (groups or GROUP_NAMES):
+            n = man.group(g).record_count
+            if not n:
+                continue
+            lo, hi = OwnershipMap(n, comm.size, replication_factor).range_of(comm.rank)
+            out[g] = (read_range(man, g, (lo, hi), path), n)
+        return cls(out, comm, replication_factor, device)
+
+    def _global_max(self, x: int) -> int:
+        if self.world == 1:
+            return int(x)
+        vals = self.comm.gather_obj(int(x))
+        return int(self.comm.broadcast_obj(max(vals) if self.rank == 0 else None))
+
+    def _ingest(self, recs, periodic: bool):
+        dev = self.device
+        n = np.array([int(np.asarray(r.atomic_numbers).shape[0]) for r in recs], np.int64)
+        m = np.array([int(np.asarray(r.edge_index).reshape(-1, 2).shape[0]) for r in recs],
+                     np.int64)
+        cat = lambda xs, dt, shape: (np.concatenate([np.asarray(x, dt).reshape(shape)
+                                                     for x in xs]) if len(xs) else
+                                     np.zeros((0,) + shape[1:], dt))
+        z = cat([r.atomic_numbers for r in recs], np.int32, (-1,))
+        if z.size and (z.min() < 1 or z.max() > MAX_Z):
+            raise ValidationError(f"atomic numbers must lie in [1, {MAX_Z}]")
+        edges = cat([r.edge_index for r in recs], np.int32, (-1, 2))
+        deg = 0
+        for r in recs:
+            e = np.asarray(r.edge_index, np.int64).reshape(-1, 2)
+            if e.size:
+                deg = max(deg, int(np.bincount(e[:, 1]).max()))
+        t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+        return dict(n=n, m=m, noff=t(np.concatenate([[0], np.cumsum(n)])),
+                    eoff=t(np.concatenate([[0], np.cumsum(m)])),
+                    soff=t(np.arange(len(recs) + 1, dtype=np.int64)),
+                    z=t(z), pos=t(cat([r.positions for r in recs], np.float64, (-1, 3))),
+                    forces=t(cat([r.forces for r in recs], np.float64, (-1, 3))),
+                    energy=t(np.array([float(r.energy) for r in recs], np.float64)),
+                    edges=t(edges), max_deg=deg,
+                    shift=t(cat([np.zeros((m[k], 3)) if getattr(r, "edge_shift", None) is None
+                                 else r.edge_shift for k, r in enumerate(recs)], np.float64,
+                                (-1, 3))) if periodic else None)
+
+    # ---- one collective fetch ---------------------------------------------
+    def _a2a(self, send, send_splits, recv_splits, row_shape, dtype):
+        import torch.distributed as dist
+        out = torch.empty((int(sum(recv_splits)),) + row_shape, dtype=dtype, device=self.device)
+        if self.world == 1:
+            out.copy_(send)
+            return out
+        dist.all_to_all_single(out, send.contiguous(), [int(x) for x in recv_splits],
+                               [int(x) for x in send_splits], group=self.comm.group)
+        return out
+
+    def _blocks(self, idx_host, sizes, n_blocks_src_off, src, width, add=None):
+        """gather blocks idx of `src` (rows per block from n_blocks_src_off)
+        into a contiguous buffer in idx order"""
+        dev = self.device
+        n_out = int(idx_host.shape[0])
+        rows = sizes[idx_host] if n_out else np.zeros(0, np.int64)
+        dst_off = torch.as_tensor(np.concatenate([[0], np.cumsum(rows)]).astype(np.int64),
+                                  device=dev)
+        out = torch.empty((int(rows.sum()),) + tuple(src.shape[1:]), dtype=src.dtype, device=dev)
+        if n_out and out.numel():
+            idx = torch.as_tensor(idx_host.astype(np.int32), device=dev)
+            call("gfm_gather_blocks", ptr(idx), n_out, ptr(n_blocks_src_off), ptr(dst_off),
+                 int(width), ptr(src), ptr(out), ptr(add), stream_handle())
+        return out
+
+    def fetch_device_batch(self, group: str, indices, dtype=torch.float32):
+        """Collective.  Returns a model.Batch of structures ``indices`` (in
+        that order) or None when this rank requested nothing."""
+        import torch.distributed as dist
+
+        from .model import batch_from_device
+        own = self.ownership[group]
+        g = self._g[group]
+        dev = self.device
+        req, send_counts, arrival_to_batch = plan_fetch(indices, own, self.rank, self.world)
+        # 1. request counts and indices (all_to_all)
+        sc = torch.as_tensor(send_counts, device=dev)
+        rc = torch.empty_like(sc)
+        if self.world > 1:
+            dist.all_to_all_single(rc, sc, group=self.comm.group)
+        else:
+            rc.copy_(sc)
+        recv_counts = rc.cpu().numpy()
+        want = self._a2a(torch.as_tensor(req, device=dev), send_counts, recv_counts, (),
+                         torch.int64)
+        lo, _ = own.range_of(self.rank)
+        serve = want.cpu().numpy() - lo                  # local positions I serve
+        # 2. sizes of the served structures back to the requesters
+        sizes = np.stack([g["n"][serve], g["m"][serve]], 1) if serve.size else \
+            np.zeros((0, 2), np.int64)
+        got_sizes = self._a2a(torch.as_tensor(sizes, device=dev), recv_counts, send_counts, (2,),
+                              torch.int64).cpu().numpy()
+        # per-peer row counts of every array (send side: what I serve per peer)
+        peer_of_serve = np.repeat(np.arange(self.world), recv_counts)
+        s_atoms = np.bincount(peer_of_serve, weights=sizes[:, 0], minlength=self.world) \
+            .astype(np.int64) if serve.size else np.zeros(self.world, np.int64)
+        s_edges = np.bincount(peer_of_serve, weights=sizes[:, 1], minlength=self.world) \
+            .astype(np.int64) if serve.size else np.zeros(self.world, np.int64)
+        peer_of_req = np.repeat(np.arange(self.world), send_counts)
+        r_atoms = np.bincount(peer_of_req, weights=got_sizes[:, 0], minlength=self.world) \
+            .astype(np.int64) if got_sizes.size else np.zeros(self.world, np.int64)
+        r_edges = np.bincount(peer_of_req, weights=got_sizes[:, 1], minlength=self.world) \
+            .astype(np.int64) if got_sizes.size else np.zeros(self.world, np.int64)
+        # 3. pack the served structures (device), exchange, unpack in batch order
+        packed = dict(
+            z=self._blocks(serve, g["n"], g["noff"], g["z"], 1),
+            pos=self._blocks(serve, g["n"], g["noff"], g["pos"], 6),
+            forces=self._blocks(serve, g["n"], g["noff"], g["forces"], 6),
+            energy=self._blocks(serve, np.ones_like(g["n"]), g["soff"], g["energy"], 2),
+            edges=self._blocks(serve, g["m"], g["eoff"], g["edges"], 2),
+            shift=None if g["shift"] is None else
+            self._blocks(serve, g["m"], g["eoff"], g["shift"], 6))
+        recv = dict(
+            z=self._a2a(packed["z"], s_atoms, r_atoms, (), torch.int32),
+            pos=self._a2a(packed["pos"], s_atoms, r_atoms, (3,), torch.float64),
+            forces=self._a2a(packed["forces"], s_atoms, r_atoms, (3,), torch.float64),
+            energy=self._a2a(packed["energy"], recv_counts, send_counts, (), torch.float64),
+            edges=self._a2a(packed["edges"], s_edges, r_edges, (2,), torch.int32),
+            shift=None if g["shift"] is None else
+            self._a2a(packed["shift"], s_edges, r_edges, (3,), torch.float64))
+        B = int(arrival_to_batch.shape[0])
+        if B == 0:
+            return None
+        # arrival slot of each batch position; blocks of the arrival buffers
+        n_arr, m_arr = got_sizes[:, 0], got_sizes[:, 1]
+        a_noff = torch.as_tensor(np.concatenate([[0], np.cumsum(n_arr)]).astype(np.int64),
+                                 device=dev)
+        a_eoff = torch.as_tensor(np.concatenate([[0], np.cumsum(m_arr)]).astype(np.int64),
+                                 device=dev)
+        a_soff = torch.as_tensor(np.arange(B + 1, dtype=np.int64), device=dev)
+        src_slot = arrival_to_batch  # batch position b comes from arrival slot src_slot[b]
+        n_b, m_b = n_arr[src_slot], m_arr[src_slot]
+        host_off = np.concatenate([[0], np.cumsum(n_b)]).astype(np.int64)
+        node_base = torch.as_tensor(host_off[:-1].astype(np.int32), device=dev)
+        z = self._blocks(src_slot, n_arr, a_noff, recv["z"], 1)
+        pos = self._blocks(src_slot, n_arr, a_noff, recv["pos"], 6)
+        forces = self._blocks(src_slot, n_arr, a_noff, recv["forces"], 6)
+        energy = self._blocks(src_slot, np.ones(B, np.int64), a_soff, recv["energy"], 2)
+        # record-local endpoints + the structure's node base in the batch
+        edges = self._blocks(src_slot, m_arr, a_eoff, recv["edges"], 2, add=node_base)
+        shift = None if g["shift"] is None else \
+            self._blocks(src_slot, m_arr, a_eoff, recv["shift"], 6)
+        e_off = np.concatenate([[0], np.cumsum(m_b)]).astype(np.int32)
+        assert int(e_off[-1]) == edges.shape[0]
+        src = edges[:, 0].contiguous()
+        dst = edges[:, 1].contiguous()
+        return batch_from_device(z, pos, energy.to(dtype), forces.to(dtype), src, dst,
+                                 torch.as_tensor(e_off, device=dev),
+                                 torch.as_tensor(host_off.astype(np.int32), device=dev),
+                                 host_off, dtype, shift, self._max_deg[group])
+
+    def fetch_batch(self, group, indices):
+        raise ValidationError("a sharded store fetches collectively: use fetch_device_batch")
+
+    def close(self):
+        self._g.clear()

@@ -931,6 +931,16 @@ def load_checkpoint(path: str) -> Checkpoint:
                       epoch=epoch, base_seed=base_seed)
 
 
+def _fetch_batch(store, group: str, indices, device, dtype):
+    """one batch from any store: a collective store (store.ShardedDeviceStore)
+    is called on every rank, with or without indices; None = nothing here"""
+    if getattr(store, "collective", False):
+        return store.fetch_device_batch(group, indices, dtype=dtype)
+    if not len(indices):
+        return None
+    return make_batch(store.fetch_batch(group, indices), device=device, dtype=dtype)
+
+
 def evaluate(params: ModelParams, store, comm: Comm, group: str = "valset",
              batch_size: int = 64) -> tuple[float, float]:
     """Per-atom energy MAE and force-component MAE over a group
@@ -942,9 +952,14 @@ def evaluate(params: ModelParams, store, comm: Comm, group: str = "valset",
     dev = params.flat.device
     acc = torch.zeros(4, dtype=torch.float64, device=dev)
     mine = np.arange(comm.rank, n, comm.size)
-    for lo in range(0, mine.shape[0], batch_size):
-        records = store.fetch_batch(group, mine[lo:lo + batch_size])
-        batch = make_batch(records, device=dev, dtype=params.dtype)
+    collective = getattr(store, "collective", False)
+    # a collective (sharded) store needs every rank in every fetch: all ranks
+    # run rank 0's batch count, shorter ones with empty requests
+    n_rows = -(-n // comm.size) if collective else mine.shape[0]
+    for lo in range(0, n_rows, batch_size):
+        batch = _fetch_batch(store, group, mine[lo:lo + batch_size], dev, params.dtype)
+        if batch is None:
+            continue
         e_pred, f_pred = forward_batch(params, batch)
         acc[0] += ((e_pred - batch.energy_true) / batch.n_per_graph.to(e_pred.dtype)).abs().sum()
         acc[1] += batch.n_graphs
@@ -1022,22 +1037,23 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
                     captured = True
                 with clock.phase("step"), _dphase(dclk, "step"):
                     runner.run()
-            elif has:
+            else:
                 with clock.phase("dataload"), _dphase(dclk, "dataload"):
-                    batch = make_batch(store.fetch_batch("trainset", mine[step]),
-                                       device=trainer.device, dtype=dtype)
-                with clock.phase("forward"), _dphase(dclk, "forward"):
-                    cache: dict = {}
-                    e_pred, f_pred = forward_batch(trainer.params, batch, cache,
-                                                   scratch=trainer.scratch)
-                with clock.phase("backward"), _dphase(dclk, "backward"):
-                    trainer.compute(batch, precomputed=(cache, e_pred, f_pred))
-                with clock.phase("sync"), _dphase(dclk, "sync"):
-                    trainer.reduce_and_update()
-            else:  # no batch for this rank: zero contribution (train.py:257-259)
-                with clock.phase("sync"), _dphase(dclk, "sync"):
-                    trainer.compute(None)
-                    trainer.reduce_and_update()
+                    batch = _fetch_batch(store, "trainset", mine[step] if has else [],
+                                         trainer.device, dtype)
+                if batch is not None:
+                    with clock.phase("forward"), _dphase(dclk, "forward"):
+                        cache: dict = {}
+                        e_pred, f_pred = forward_batch(trainer.params, batch, cache,
+                                                       scratch=trainer.scratch)
+                    with clock.phase("backward"), _dphase(dclk, "backward"):
+                        trainer.compute(batch, precomputed=(cache, e_pred, f_pred))
+                    with clock.phase("sync"), _dphase(dclk, "sync"):
+                        trainer.reduce_and_update()
+                else:  # no batch for this rank: zero contribution (train.py:257-259)
+                    with clock.phase("sync"), _dphase(dclk, "sync"):
+                        trainer.compute(None)
+                        trainer.reduce_and_update()
             acc += trainer.contrib[P:P + 2].to(torch.float64)
             if (step + 1) % max(1, nan_check_every) == 0 or step == steps - 1:
                 if trainer.nan_event:  # train.py:264-274 (the device skipped the update)
