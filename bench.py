@@ -68,6 +68,14 @@ CONFIGS = {
 METRIC = "training graphs/sec (energy+forces MTL) at 1/2/4/8 B200; aggregation HBM GB/s"
 UNIT = "graphs/s"
 DTYPE = "f32 (3xTF32 tensor-core GEMMs, stated bound 5e-4 rel)"
+# --gemm: engine code and the dtype label it puts on the line
+GEMM_MODES = {
+    "tc3": (1, DTYPE),
+    "mixed": (3, "f32 (3xTF32 tensor-core GEMMs; weight-gradient GEMMs 1xTF32, bounds in "
+                 "DESIGN.md section 4)"),
+    "tc1": (2, "f32 storage, 1xTF32 tensor-core GEMMs (~1e-3 rel)"),
+    "simt": (0, "f32 (IEEE fp32 FFMA GEMMs)"),
+}
 
 
 def parse():
@@ -78,6 +86,8 @@ def parse():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="c3", choices=["c2", "c3"])
     ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--gemm", default="tc3", choices=list(GEMM_MODES),
+                    help="float32 GEMM engine (gfm_set_gemm_mode)")
     ap.add_argument("--no-graph", action="store_true", help="disable CUDA-graph capture")
     ap.add_argument("--no-nested", action="store_true", help="skip the nested c2 / ragged lines")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
@@ -795,6 +805,8 @@ def run_native(args):
     import torch
 
     ctx = Ctx(args)
+    from paper_2406_12909_b200 import _lib
+    _lib.call("gfm_set_gemm_mode", GEMM_MODES[args.gemm][0])
     W = CONFIGS[args.config]
     main = measure_step(ctx, W, full=True)
     main.pop("runner")
@@ -822,10 +834,11 @@ def run_native(args):
         line = dict(
             metric=METRIC, value=main["value"], unit=UNIT, n_gpus=ctx.world, steps=args.steps,
             warmup=args.warmup, ms_per_step=main["ms_per_step"], higher_is_better=True,
-            scaling="weak", vs_baseline=None, dtype=DTYPE, data="synthetic",
+            scaling="weak", vs_baseline=None, dtype=GEMM_MODES[args.gemm][1], data="synthetic",
             config=dict(workload=W["desc"], global_batch=B * ctx.world, per_gpu_batch=B,
                         nodes_per_gpu=main["nodes_per_gpu"], edges_per_gpu=main["edges_per_gpu"],
                         parallelism=f"dp{ctx.world}", cuda_graph=main["cuda_graph"],
+                        gemm_engine=args.gemm,
                         l2=("step working set (activations, E x H workspaces) > 126 MB L2; "
                             "8-batch input pool cycled")),
             e2e=main["e2e"], e2e_device_store=main["e2e_device_store"],

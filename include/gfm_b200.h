@@ -53,8 +53,10 @@ enum { GFM_FLAG_ARGMAX_U8 = 2 };
  * gradient [N][H] (as written by gfm_layer_bwd_data_agg) -- no prep pass */
 enum { GFM_FLAG_AGG_PREPPED = 4 };
 /* float32 GEMM engine: tcgen05 3xTF32 (default, fp32-level accuracy),
- * tcgen05 1xTF32 (faster, ~1e-3 relative), or the SIMT fp32 engine */
-enum { GFM_GEMM_SIMT = 0, GFM_GEMM_TC3 = 1, GFM_GEMM_TC1 = 2 };
+ * tcgen05 1xTF32 (faster, ~1e-3 relative), the SIMT fp32 engine, or MIXED:
+ * 3xTF32 everywhere except the weight-gradient GEMMs (gfm_linear_bwd_weight*,
+ * gfm_embedding_grad), which run 1xTF32 */
+enum { GFM_GEMM_SIMT = 0, GFM_GEMM_TC3 = 1, GFM_GEMM_TC1 = 2, GFM_GEMM_MIXED = 3 };
 
 /* ---- housekeeping ---------------------------------------------------- */
 GFM_API int gfm_abi_version(void);

@@ -35,7 +35,8 @@ const char* gfm_last_error(void) { return gfm::g_err; }
 int gfm_device_sm_count(void) { return gfm::num_sms(); }
 
 int gfm_set_gemm_mode(int mode) {
-  if (mode != GFM_GEMM_SIMT && mode != GFM_GEMM_TC3 && mode != GFM_GEMM_TC1) {
+  if (mode != GFM_GEMM_SIMT && mode != GFM_GEMM_TC3 && mode != GFM_GEMM_TC1 &&
+      mode != GFM_GEMM_MIXED) {
     gfm::set_error("gfm_set_gemm_mode: unknown mode %d", mode);
     return GFM_EINVAL;
   }

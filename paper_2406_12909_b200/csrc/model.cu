@@ -334,6 +334,10 @@ inline bool use_tc() {
   return std::is_same<T, float>::value && gemm_mode() != GFM_GEMM_SIMT;
 }
 inline int tc_split3() { return gemm_mode() == GFM_GEMM_TC1 ? 0 : 1; }
+// weight-gradient GEMMs (dW = X^T dY, embedding one-hot^T dh): 1xTF32 in MIXED
+inline int tc_split3_wgrad() {
+  return gemm_mode() == GFM_GEMM_TC1 || gemm_mode() == GFM_GEMM_MIXED ? 0 : 1;
+}
 
 template <typename T>
 cudaError_t linear_fwd_t(const T* X1, int ld1, int K1, const T* X2, int ld2, int K2, const T* W1,
@@ -440,7 +444,7 @@ cudaError_t linear_bwd_weight_t(const T* dY, int ldd, int M, const int* M_dev, i
       }
       ColsLd<T> b{dY, ldd};
       tc::TcEpiPartial epi{ws, (long long)N * Kt, Kt, N};
-      e = tc::launch(Kt, nullptr, N, M, M_dev, splits, tc_split3(), a, b, epi, s);
+      e = tc::launch(Kt, nullptr, N, M, M_dev, splits, tc_split3_wgrad(), a, b, epi, s);
       real = real_splits(M, splits, tc::kBK);
       trans = 1;
       goto reduce;
@@ -644,7 +648,7 @@ cudaError_t embedding_grad_t(const int* z, int n_nodes, const T* dh, int H, T* g
   if constexpr (std::is_same<T, float>::value) {
     if (use_tc<T>()) {
       tc::TcEpiPartial epi{ws, (long long)E * H, E, H};
-      e = tc::launch(E, nullptr, H, n_nodes, nullptr, splits, tc_split3(), a, b, epi, s);
+      e = tc::launch(E, nullptr, H, n_nodes, nullptr, splits, tc_split3_wgrad(), a, b, epi, s);
       real = real_splits(n_nodes, splits, tc::kBK);
       goto reduce;
     }
