@@ -629,10 +629,15 @@ def rooflines(ctx, W, cfg, b, s):
         _lib.call("gfm_agg_fwd", P_(h_in), N, H, P_(b.rowptr), P_(b.col_src), P_(b.edge_w),
                   parts, P_(agg), P_(am), P_(sm_), _lib.F32, flags, sh)
 
+    # the step's backward reads the edge weights in CSC order (GFM_FLAG_W_CSC)
+    w_csc = torch.empty_like(b.edge_w)
+    _lib.call("gfm_permute", P_(b.csc_eid), int(b.edge_w.shape[0]), P_(b.rowptr) + 4 * N,
+              P_(b.edge_w), P_(w_csc), _lib.F32, sh)
+
     def agg_bwd_call():
         _lib.call("gfm_agg_bwd", P_(dagg), P_(agg), P_(sm_), P_(am), P_(h_in), P_(b.rowptr),
-                  P_(b.csc_ptr), P_(b.csc_eid), P_(b.csc_dst), P_(b.edge_w), N, H, parts,
-                  P_(dh_b), P_(h_in), P_(out_b), P_(ws_b), _lib.F32, flags, sh)
+                  P_(b.csc_ptr), P_(b.csc_eid), P_(b.csc_dst), P_(w_csc), N, H, parts,
+                  P_(dh_b), P_(h_in), P_(out_b), P_(ws_b), _lib.F32, flags | _lib.FLAG_W_CSC, sh)
 
     agg_fwd_call()
     fwd_ms, bwd_ms = ctx.launch_ms(agg_fwd_call, s), ctx.launch_ms(agg_bwd_call, s)

@@ -52,6 +52,9 @@ enum { GFM_FLAG_ARGMAX_U8 = 2 };
 /* gfm_agg_bwd: G | coef already in `workspace` and `dagg` is the max part's
  * gradient [N][H] (as written by gfm_layer_bwd_data_agg) -- no prep pass */
 enum { GFM_FLAG_AGG_PREPPED = 4 };
+/* gfm_agg_bwd: edge_w is in CSC order (w[q] for CSC slot q, e.g. from
+ * gfm_permute) -- a coalesced load instead of a dependent gather w[eid] */
+enum { GFM_FLAG_W_CSC = 8 };
 /* float32 GEMM engine: tcgen05 3xTF32 (default, fp32-level accuracy),
  * tcgen05 1xTF32 (faster, ~1e-3 relative), the SIMT fp32 engine, or MIXED:
  * 3xTF32 everywhere except the weight-gradient GEMMs (gfm_linear_bwd_weight*,
@@ -106,6 +109,10 @@ GFM_API int gfm_gather_batch(const int* idx, const int* meta, int n_cap_graphs, 
 GFM_API int gfm_gather_blocks(const int* idx, int n_out, const long long* src_off,
                               const long long* dst_off, int width, const void* in, void* out,
                               const int* add, void* stream);
+/* out[q] = in[idx[q]] for q < min(n, *n_dev) (n_dev may be NULL): e.g. the
+ * edge weights in CSC order, w_csc = edge_w[csc_eid] (GFM_FLAG_W_CSC) */
+GFM_API int gfm_permute(const int* idx, int n, const int* n_dev, const void* in, void* out,
+                        int dtype, void* stream);
 GFM_API size_t gfm_scan_workspace_bytes(int n);
 GFM_API int gfm_exclusive_scan(const int* in, int n, int* out, void* workspace, void* stream);
 /* Radius graph replacing build_cutoff_edges (preprocess.py:90-104), emitted

@@ -23,6 +23,7 @@ PART_SUM, PART_MEAN, PART_MAX, PART_STD = 1, 2, 4, 8
 FLAG_SCALAR = 1
 FLAG_ARGMAX_U8 = 2
 FLAG_AGG_PREPPED = 4
+FLAG_W_CSC = 8
 ABI_VERSION = 2
 
 _P = ctypes.c_void_p
@@ -53,6 +54,7 @@ SIGNATURES = {
     "gfm_gather_structures": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P]),
     "gfm_gather_batch": (_I, [_P, _P, _I, _I] + [_P] * 25 + [_I, _P]),
     "gfm_gather_blocks": (_I, [_P, _I, _P, _P, _I, _P, _P, _P, _P]),
+    "gfm_permute": (_I, [_P, _I, _P, _P, _P, _I, _P]),
     "gfm_scan_workspace_bytes": (_S, [_I]),
     "gfm_exclusive_scan": (_I, [_P, _I, _P, _P, _P]),
     "gfm_radius_count": (_I, [_P, _P, _P, _I, _P, _D, _I, _P, _P]),

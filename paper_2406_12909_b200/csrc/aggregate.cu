@@ -26,10 +26,19 @@
 
 #include "common.cuh"
 
-// CSC slots batched per iteration on 32-lane rows: 1 measured 4.6% faster
-// than 2 (and 4 55% slower) at C3 (tools/agg_knobs2.sh, round 2)
+// CSC slots batched per iteration on 32-lane rows, with a max part (3-4
+// rows per slot) / without: 1 / 2 (C3 pna: 1 is 4% faster than 2; C5 random
+// sum at E = 16M: 2 reaches 0.67 of HBM, 1 0.53; tools/agg_knobs3.sh)
 #ifndef GFM_AGG_BWD_U
 #define GFM_AGG_BWD_U 1
+#endif
+#ifndef GFM_AGG_BWD_U_DEEP
+#define GFM_AGG_BWD_U_DEEP 2
+#endif
+// dmax rows loaded with G / coef / argmax (1) or after the argmax compare
+// (0): the dependent load cost 19% at C3 (tools/agg_knobs3.sh, round 2)
+#ifndef GFM_AGG_BWD_PFMAX
+#define GFM_AGG_BWD_PFMAX 1
 #endif
 #ifndef GFM_AGG_FWD_UF
 #define GFM_AGG_FWD_UF 4
@@ -521,7 +530,8 @@ __global__ void k_agg_bwd_scalar(const T* __restrict__ G, int ldg, const T* __re
                                  const T* __restrict__ h_in, const int* __restrict__ csc_ptr,
                                  const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
                                  const T* __restrict__ w, int n_nodes, int H, T* __restrict__ dh,
-                                 const T* __restrict__ gate, T* __restrict__ out, int am_u8) {
+                                 const T* __restrict__ gate, T* __restrict__ out, int am_u8,
+                                 int w_csc) {
   pdl_entry();
   const long long total = (long long)n_nodes * H;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -531,7 +541,7 @@ __global__ void k_agg_bwd_scalar(const T* __restrict__ G, int ldg, const T* __re
     const T hj = coef ? h_in[idx] : T(0);
     for (int q = csc_ptr[j]; q < csc_ptr[j + 1]; ++q) {
       const int p = csc_eid[q], i = csc_dst[q];
-      const T ww = w[p];
+      const T ww = w[w_csc ? q : p];
       T dm = G ? G[(long long)i * ldg + c] : T(0);
       if (coef) dm = dm + coef[(long long)i * H + c] * (hj * ww);
       if (argmax) {
@@ -566,7 +576,7 @@ __device__ __forceinline__ f4x2 ldg256(const float* p) {
 }
 
 // GC: ldG returns f4x2 {G, coef} (interleaved workspace), ldC is unused
-template <int NV, int LPN, bool GC = false, typename LG, typename LC, typename LA>
+template <int NV, int LPN, bool GC = false, int U = 1, typename LG, typename LC, typename LA>
 __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, bool hasC,
                                              bool hasA, int j, int cb, int H,
                                              const float* __restrict__ dmax, int ldm,
@@ -577,7 +587,8 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
                                              const float* __restrict__ w,
                                              const float* __restrict__ dh,
                                              const float* __restrict__ gate,
-                                             float* __restrict__ out, bool am_u8 = false) {
+                                             float* __restrict__ out, bool am_u8 = false,
+                                             bool w_csc = false) {
   const int H4 = H >> 2;
   float4 acc[NV], hj[NV];
 #pragma unroll
@@ -587,148 +598,104 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
     hj[v] = hasC ? reinterpret_cast<const float4*>(h_in)[o] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int qb = csc_ptr[j], qe = csc_ptr[j + 1];
+  // PF: the max part's dmax row is loaded with the others instead of after
+  // the argmax compare (no dependent load; +4 B per channel and edge)
+  constexpr bool PF = GFM_AGG_BWD_PFMAX != 0;
+  struct Rows {
+    float4 g[NV], cf[NV], d[NV];
+    int4 a[NV];
+  };
+  auto load = [&](int i, Rows& r) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      r.g[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      r.cf[v] = r.g[v];
+      r.d[v] = r.g[v];
+      r.a[v] = make_int4(-1, -1, -1, -1);
+      if constexpr (GC) {
+        const f4x2 t = ldG(i, v);
+        r.g[v] = t.a;
+        r.cf[v] = t.b;
+      } else {
+        if (hasG) r.g[v] = ldG(i, v);
+        if (hasC) r.cf[v] = ldC(i, v);
+      }
+      if (hasA) {
+        r.a[v] = ldA(i, v);
+        if constexpr (PF)
+          r.d[v] = __ldg(reinterpret_cast<const float4*>(dmax + (long long)i * ldm) + v * LPN + cb);
+      }
+    }
+  };
+  auto consume = [&](int p, int i, float wv, const Rows& r) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c4 = v * LPN + cb;
+      float4 dm = r.g[v];
+      if (hasC) dm = fma4(r.cf[v], mul4(hj[v], bcast4(wv)), dm);
+      if (hasA) {
+        const int4 am = r.a[v];
+        const int pp = am_u8 ? (p & 0xFF) : p;
+        if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
+          const float4 d = PF ? r.d[v]
+                              : __ldg(reinterpret_cast<const float4*>(dmax + (long long)i * ldm) + c4);
+          if (am.x == pp) dm.x += d.x;
+          if (am.y == pp) dm.y += d.y;
+          if (am.z == pp) dm.z += d.z;
+          if (am.w == pp) dm.w += d.w;
+        }
+      }
+      acc[v] = fma4(dm, bcast4(wv), acc[v]);
+    }
+  };
   if constexpr (LPN == 32) {
-    // U CSC slots per batch: all their row loads issue before the (in-order)
-    // accumulation, so U x 3 gathers per lane are in flight.  Narrow rows
-    // (LPN < 32: several nodes per warp) are issue-bound rather than latency-
-    // bound and measure faster unbatched.
-    constexpr int U = LPN == 32 ? GFM_AGG_BWD_U : 1;
-    // the node's LPN lanes load LPN CSC slots (eid, dst, w[eid]) at once and
-    // broadcast them with shuffles
-    const int gl = (threadIdx.x & 31) % LPN;
-    const unsigned gmask =
-        LPN == 32 ? 0xffffffffu : (((1u << LPN) - 1u) << ((threadIdx.x & 31) - gl));
-    for (int c0 = qb; c0 < qe; c0 += LPN) {
-      const int cnt = min(LPN, qe - c0);
-      int my_p = -2, my_i = 0;
+    // the node's 32 lanes load 32 CSC slots (eid, dst, w) at once and
+    // broadcast them with shuffles; U slots per batch: all their row loads
+    // issue before the (in-order) accumulation (full batches unpredicated,
+    // then a one-slot tail)
+    const int gl = threadIdx.x & 31;
+    for (int c0 = qb; c0 < qe; c0 += 32) {
+      const int cnt = min(32, qe - c0);
+      int my_p = 0, my_i = 0;
       float my_w = 0.f;
       if (gl < cnt) {
         my_p = __ldg(csc_eid + c0 + gl);
         my_i = __ldg(csc_dst + c0 + gl);
-        my_w = __ldg(w + my_p);
+        my_w = __ldg(w + (w_csc ? c0 + gl : my_p));
       }
-      for (int e = 0; e < cnt; e += U) {
+      int e = 0;
+      for (; e + U <= cnt; e += U) {
         int p[U], i[U];
         float ww[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const bool ok = e + u < cnt;
-          const int src = ok ? e + u : 0;
-          const int pp = __shfl_sync(gmask, my_p, src, LPN);
-          const int ii = __shfl_sync(gmask, my_i, src, LPN);
-          const float wv = __shfl_sync(gmask, my_w, src, LPN);
-          p[u] = ok ? pp : -2;
-          i[u] = ok ? ii : 0;
-          ww[u] = ok ? wv : 0.f;
+          p[u] = __shfl_sync(0xffffffffu, my_p, e + u);
+          i[u] = __shfl_sync(0xffffffffu, my_i, e + u);
+          ww[u] = __shfl_sync(0xffffffffu, my_w, e + u);
         }
-        float4 g[U][NV], cf[U][NV];
-        int4 a[U][NV];
+        Rows r[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u) load(i[u], r[u]);
 #pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const bool ok = e + u < cnt;
-            g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-            cf[u][v] = g[u][v];
-            a[u][v] = make_int4(-1, -1, -1, -1);
-            if constexpr (GC) {
-              if (ok) {
-                const f4x2 t = ldG(i[u], v);
-                g[u][v] = t.a;
-                cf[u][v] = t.b;
-              }
-            } else {
-              if (ok && hasG) g[u][v] = ldG(i[u], v);
-              if (ok && hasC) cf[u][v] = ldC(i[u], v);
-            }
-            if (ok && hasA) a[u][v] = ldA(i[u], v);
-          }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (e + u >= cnt) break;
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const int c4 = v * LPN + cb;
-            float4 dm = g[u][v];
-            if (hasC) dm = fma4(cf[u][v], mul4(hj[v], bcast4(ww[u])), dm);
-            if (hasA) {
-              const int4 am = a[u][v];
-              const int pp = am_u8 ? (p[u] & 0xFF) : p[u];
-              if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
-                const float4 d =
-                    __ldg(reinterpret_cast<const float4*>(dmax + (long long)i[u] * ldm) + c4);
-                if (am.x == pp) dm.x += d.x;
-                if (am.y == pp) dm.y += d.y;
-                if (am.z == pp) dm.z += d.z;
-                if (am.w == pp) dm.w += d.w;
-              }
-            }
-            acc[v] = fma4(dm, bcast4(ww[u]), acc[v]);
-          }
-        }
+        for (int u = 0; u < U; ++u) consume(p[u], i[u], ww[u], r[u]);
+      }
+      for (; e < cnt; ++e) {
+        const int p = __shfl_sync(0xffffffffu, my_p, e);
+        const int i = __shfl_sync(0xffffffffu, my_i, e);
+        const float wv = __shfl_sync(0xffffffffu, my_w, e);
+        Rows r;
+        load(i, r);
+        consume(p, i, wv, r);
       }
     }
   } else {
-    // U CSC slots per batch: all their row loads issue before the (in-order)
-    // accumulation, so U x 3 gathers per lane are in flight.  Narrow rows
-    // (LPN < 32: several nodes per warp) are issue-bound rather than latency-
-    // bound and measure faster unbatched.
-    constexpr int U = LPN == 32 ? 2 : 1;
-    for (int q = qb; q < qe; q += U) {
-      int p[U], i[U];
-      float ww[U];
-      float4 g[U][NV], cf[U][NV];
-      int4 a[U][NV];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool ok = q + u < qe;
-        p[u] = ok ? __ldg(csc_eid + q + u) : -2;
-        i[u] = ok ? __ldg(csc_dst + q + u) : 0;
-        ww[u] = ok ? __ldg(w + p[u]) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const bool ok = q + u < qe;
-          g[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-          cf[u][v] = g[u][v];
-          a[u][v] = make_int4(-1, -1, -1, -1);
-          if constexpr (GC) {
-            if (ok) {
-              const f4x2 t = ldG(i[u], v);
-              g[u][v] = t.a;
-              cf[u][v] = t.b;
-            }
-          } else {
-            if (ok && hasG) g[u][v] = ldG(i[u], v);
-            if (ok && hasC) cf[u][v] = ldC(i[u], v);
-          }
-          if (ok && hasA) a[u][v] = ldA(i[u], v);
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (q + u >= qe) break;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int c4 = v * LPN + cb;
-          float4 dm = g[u][v];
-          if (hasC) dm = fma4(cf[u][v], mul4(hj[v], bcast4(ww[u])), dm);
-          if (hasA) {
-            const int4 am = a[u][v];
-            const int pp = am_u8 ? (p[u] & 0xFF) : p[u];
-            if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
-              const float4 d =
-                  __ldg(reinterpret_cast<const float4*>(dmax + (long long)i[u] * ldm) + c4);
-              if (am.x == pp) dm.x += d.x;
-              if (am.y == pp) dm.y += d.y;
-              if (am.z == pp) dm.z += d.z;
-              if (am.w == pp) dm.w += d.w;
-            }
-          }
-          acc[v] = fma4(dm, bcast4(ww[u]), acc[v]);
-        }
-      }
+    // narrow rows (several nodes per warp): issue-bound, one slot at a time
+    for (int q = qb; q < qe; ++q) {
+      const int p = __ldg(csc_eid + q), i = __ldg(csc_dst + q);
+      const float wv = __ldg(w + (w_csc ? q : p));
+      Rows r;
+      load(i, r);
+      consume(p, i, wv, r);
     }
   }
 #pragma unroll
@@ -743,14 +710,14 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
   }
 }
 
-template <int NV, int LPN, bool U8, bool GC = false>
+template <int NV, int LPN, bool U8, bool GC = false, int U = 1>
 __global__ void __launch_bounds__(256, NV == 1 ? (LPN == 32 ? (GFM_AGG_BWD_MINB > 4 ? 4 : GFM_AGG_BWD_MINB) : GFM_AGG_BWD_MINB) : 1)
     k_agg_bwd_vec(const float* __restrict__ G, int ldg, const float* __restrict__ coef,
                   const float* __restrict__ dmax, int ldm, const int* __restrict__ argmax,
                   const float* __restrict__ h_in, const int* __restrict__ csc_ptr,
                   const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
                   const float* __restrict__ w, int n_nodes, int H, float* __restrict__ dh,
-                  const float* __restrict__ gate, float* __restrict__ out) {
+                  const float* __restrict__ gate, float* __restrict__ out, int w_csc) {
   pdl_entry();
   constexpr int NPW = 32 / LPN;
   const int lane = threadIdx.x & 31;
@@ -758,7 +725,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? (LPN == 32 ? (GFM_AGG_BWD_MINB 
   const int j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NPW + lane / LPN;
   if (j >= n_nodes) return;
   const int cb = blockIdx.y * (NV * LPN) + sub;  // column slab (see k_agg_fwd_vec)
-  agg_bwd_node<NV, LPN, GC>(
+  agg_bwd_node<NV, LPN, GC, U>(
       [&](int i, int v) {
         if constexpr (GC) {
           return ldg256(G + ((long long)i * (H >> 2) + v * LPN + cb) * 8);
@@ -779,7 +746,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? (LPN == 32 ? (GFM_AGG_BWD_MINB 
         return __ldg(reinterpret_cast<const int4*>(argmax + (long long)i * H) + v * LPN + cb);
       },
       G != nullptr, coef != nullptr, argmax != nullptr, j, cb, H, dmax, ldm, h_in, csc_ptr,
-      csc_eid, csc_dst, w, dh, gate, out, U8);
+      csc_eid, csc_dst, w, dh, gate, out, U8, w_csc != 0);
 }
 
 // Shared-memory staged backward (see k_agg_fwd_tile): a block owns nb
@@ -793,7 +760,7 @@ __global__ void __launch_bounds__(256)
                    const int* __restrict__ csc_eid, const int* __restrict__ csc_dst,
                    const float* __restrict__ w, int n_nodes, int H, float* __restrict__ dh,
                    const float* __restrict__ gate, float* __restrict__ out, int nb,
-                   int cap_rows) {
+                   int cap_rows, int w_csc) {
   pdl_entry();
   extern __shared__ float4 stage[];  // [G | coef | argmax] each [cap_rows][LPN]
   const int a0 = blockIdx.x * nb, b0 = min(n_nodes, a0 + nb);
@@ -825,7 +792,7 @@ __global__ void __launch_bounds__(256)
                            [&](int i, int) { return sC[(i - lo) * LPN + sub]; },
                            [&](int i, int) { return sA[(i - lo) * LPN + sub]; }, hasG, hasC,
                            hasA, j, cb, H, dmax, ldm, h_in, csc_ptr, csc_eid, csc_dst, w, dh,
-                           gate, out);
+                           gate, out, false, w_csc != 0);
     else
       agg_bwd_node<1, LPN>(
           [&](int i, int) {
@@ -838,7 +805,7 @@ __global__ void __launch_bounds__(256)
             return __ldg(reinterpret_cast<const int4*>(argmax + (long long)i * H) + cb);
           },
           hasG, hasC, hasA, j, cb, H, dmax, ldm, h_in, csc_ptr, csc_eid, csc_dst, w, dh, gate,
-          out);
+          out, false, w_csc != 0);
   }
 }
 
@@ -954,7 +921,7 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
                     const int* argmax, const void* h_in, const int* rowptr, const int* csc_ptr,
                     const int* csc_eid, const int* csc_dst, const void* w, int n, int H, int parts,
                     void* dh, const void* gate, void* out, void* ws, int force_scalar, int am_u8,
-                    cudaStream_t s, int prepped = 0) {
+                    cudaStream_t s, int prepped = 0, int w_csc = 0) {
   if (n <= 0) return cudaSuccess;
   const AggLayout L = agg_layout(parts, H);
   int ld = L.K * H;
@@ -1012,17 +979,30 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
     launch_k(k_agg_bwd_tile<kLpn>, grid, 256, smem, s,
         (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in,
         csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,
-        (float*)out, kNb, kCap);
+        (float*)out, kNb, kCap, w_csc);
     return cudaGetLastError();
   }
   if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn, &slabs)) {
+    // without a max part (no argmax / dmax rows) the gather carries one or
+    // two rows per slot: batch more slots
+    const bool deep = am == nullptr;
     const int nodes_per_block = 8 * (32 / lpn);
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);
-#define GFM_BWD_LAUNCH(NV_, LPN_, U8_, GC_)                                                  \
-  launch_k(k_agg_bwd_vec<NV_, LPN_, U8_, GC_>, grid, 256, 0, s, (const float*)G, ldg,          \
+#define GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, U_)                                            \
+  launch_k(k_agg_bwd_vec<NV_, LPN_, U8_, GC_, U_>, grid, 256, 0, s, (const float*)G, ldg,      \
            (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in, csc_ptr,        \
            csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,            \
-           (float*)out)
+           (float*)out, w_csc)
+#define GFM_BWD_LAUNCH(NV_, LPN_, U8_, GC_)                                                  \
+  do {                                                                                       \
+    if constexpr (LPN_ == 32) {                                                              \
+      if (deep) {                                                                            \
+        GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U_DEEP);                           \
+        break;                                                                               \
+      }                                                                                      \
+    }                                                                                        \
+    GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U);                                    \
+  } while (0)
 #define GFM_BWD_CASE(NV_, LPN_)                                                              \
   if (nv == NV_ && lpn == LPN_) {                                                            \
     if (gc) {                                                                                \
@@ -1037,17 +1017,18 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
     GFM_VEC_CASES(GFM_BWD_CASE)
 #undef GFM_BWD_CASE
 #undef GFM_BWD_LAUNCH
+#undef GFM_BWD_LAUNCH_U
   }
   if (dtype == GFM_F32)
     launch_k(k_agg_bwd_scalar<float>, grid_1d((long long)n * H), 256, 0, s,
         (const float*)G, ldg, (const float*)coef, (const float*)dmax, ld, am, (const float*)h_in,
         csc_ptr, csc_eid, csc_dst, (const float*)w, n, H, (float*)dh, (const float*)gate,
-        (float*)out, am_u8);
+        (float*)out, am_u8, w_csc);
   else
     launch_k(k_agg_bwd_scalar<double>, grid_1d((long long)n * H), 256, 0, s,
         (const double*)G, ldg, (const double*)coef, (const double*)dmax, ld, am,
         (const double*)h_in, csc_ptr, csc_eid, csc_dst, (const double*)w, n, H, (double*)dh,
-        (const double*)gate, (double*)out, am_u8);
+        (const double*)gate, (double*)out, am_u8, w_csc);
   return cudaGetLastError();
 }
 
@@ -1115,7 +1096,8 @@ int gfm_agg_bwd(const void* dagg, const void* agg, const void* stat_mean, const 
   cudaError_t e = agg_bwd(dtype, dagg, agg, stat_mean, argmax, h_in, rowptr, csc_ptr, csc_eid,
                           csc_dst, edge_w, n_nodes, H, parts, dh, gate, out, workspace,
                           flags & GFM_FLAG_SCALAR, (flags & GFM_FLAG_ARGMAX_U8) != 0,
-                          (cudaStream_t)stream, (flags & GFM_FLAG_AGG_PREPPED) != 0);
+                          (cudaStream_t)stream, (flags & GFM_FLAG_AGG_PREPPED) != 0,
+                          (flags & GFM_FLAG_W_CSC) != 0);
   if (e != cudaSuccess) set_error("gfm_agg_bwd: %s", cudaGetErrorString(e));
   return (int)e;
 }

@@ -139,6 +139,16 @@ __global__ void k_gather_blocks(const int* __restrict__ idx, int n_out,
   }
 }
 
+// out[q] = in[idx[q]] over q < (n_dev ? *n_dev : n) (4- or 8-byte words)
+template <typename T>
+__global__ void k_permute(const int* __restrict__ idx, int n, const int* __restrict__ n_dev,
+                          const T* __restrict__ in, T* __restrict__ out) {
+  pdl_entry();
+  const int m = n_dev ? min(n, *n_dev) : n;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < m; q += gridDim.x * blockDim.x)
+    out[q] = in[idx[q]];
+}
+
 __global__ void k_iota(int* __restrict__ out, int n) {
   pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
@@ -809,6 +819,20 @@ int gfm_gather_blocks(const int* idx, int n_out, const long long* src_off,
   const int grid = n_out < 148 * 16 ? n_out : 148 * 16;
   launch_k(k_gather_blocks, grid, 128, 0, (cudaStream_t)stream, idx, n_out, src_off, dst_off,
            width, (const unsigned*)in, (unsigned*)out, add);
+  GFM_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gfm_permute(const int* idx, int n, const int* n_dev, const void* in, void* out, int dtype,
+                void* stream) {
+  if (n <= 0) return 0;
+  const int grid = ceil_div(n, 256) < 148 * 8 ? ceil_div(n, 256) : 148 * 8;
+  if (dtype == GFM_F64)
+    launch_k(k_permute<double>, grid, 256, 0, (cudaStream_t)stream, idx, n, n_dev,
+             (const double*)in, (double*)out);
+  else
+    launch_k(k_permute<float>, grid, 256, 0, (cudaStream_t)stream, idx, n, n_dev,
+             (const float*)in, (float*)out);
   GFM_TRY(cudaGetLastError());
   return 0;
 }

@@ -632,6 +632,10 @@ def _scratch_for(owner, device):
     return owner if owner is not None else _Scratch(device)
 
 
+# GFM_W_CSC=0: the backward gathers read w[eid] (A/B runs)
+_W_CSC = os.environ.get("GFM_W_CSC", "1") != "0"
+
+
 def _argmax_flag(batch) -> int:
     """uint8 argmax storage when every CSR row is known to hold <= 256 edges"""
     md = getattr(batch, "max_deg", None)
@@ -961,6 +965,14 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
                   and query("gfm_get_gemm_mode") != 0 and not flags & _lib.FLAG_SCALAR)
     up_ws = sc.bytes("up_ws", query("gfm_layer_bwd_data_agg_workspace_bytes", H)) \
         if fused_prep else None
+    # edge weights in CSC order once per step: the gathers then read w[q]
+    # with their CSC slot instead of a dependent random w[eid]
+    w_agg, w_flag = batch.edge_w, 0
+    if _W_CSC and batch.edge_w.shape[0] > 0:
+        w_agg = sc.get("w_csc", tuple(batch.edge_w.shape), dt)
+        call("gfm_permute", ptr(batch.csc_eid), int(batch.edge_w.shape[0]),
+             ptr(batch.rowptr) + 4 * N, ptr(batch.edge_w), ptr(w_agg), code, s)
+        w_flag = _lib.FLAG_W_CSC
     for l in range(cfg.mpnn_layers - 1, -1, -1):
         lay = cache["layers"][l]
         wgrad(dz, H, H, lay["h_in"], H, H, lay["agg"], K * H, K * H, gp.view(f"layer_{l}.w"),
@@ -980,9 +992,9 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
                  agg_ws.data_ptr() + 4 * N * H, ptr(dmax), ptr(up_ws), s)
             call("gfm_agg_bwd", ptr(dmax), ptr(lay["agg"]), ptr(lay["smean"]), ptr(lay["argmax"]),
                  ptr(lay["h_in"]), ptr(batch.rowptr), ptr(batch.csc_ptr), ptr(batch.csc_eid),
-                 ptr(batch.csc_dst), ptr(batch.edge_w), N, H, parts, ptr(dh_in),
+                 ptr(batch.csc_dst), ptr(w_agg), N, H, parts, ptr(dh_in),
                  ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
-                 flags | _argmax_flag(batch) | _lib.FLAG_AGG_PREPPED, s)
+                 flags | _argmax_flag(batch) | _lib.FLAG_AGG_PREPPED | w_flag, s)
         else:
             dagg = sc.get("dagg", (N, K * H), dt)
             call("gfm_linear_bwd_data", ptr(dz), H, N, None, H, ptr(params.view(f"layer_{l}.w")),
@@ -990,9 +1002,9 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
                  K * H, None, 0, code, s)
             call("gfm_agg_bwd", ptr(dagg), ptr(lay["agg"]), ptr(lay["smean"]), ptr(lay["argmax"]),
                  ptr(lay["h_in"]), ptr(batch.rowptr), ptr(batch.csc_ptr), ptr(batch.csc_eid),
-                 ptr(batch.csc_dst), ptr(batch.edge_w), N, H, parts, ptr(dh_in),
+                 ptr(batch.csc_dst), ptr(w_agg), N, H, parts, ptr(dh_in),
                  ptr(lay["h_in"]) if l > 0 else None, ptr(out), ptr(agg_ws), code,
-                 flags | _argmax_flag(batch), s)
+                 flags | _argmax_flag(batch) | w_flag, s)
         dz = out
     # the batched reduction follows the weight-gradient GEMMs on the side
     # stream while the embedding gradient runs here; join before returning

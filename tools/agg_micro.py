@@ -34,6 +34,8 @@ ap.add_argument("--max-e", type=int, default=100, help="largest E in millions")
 ap.add_argument("--mem-gb", type=float, default=120.0, help="skip configs above this footprint")
 ap.add_argument("--modes", default="fused,materialised")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--e-list", default=None, help="comma list of E in millions (default: all <= --max-e)")
+ap.add_argument("--patterns", default="random,block-local")
 ap.add_argument("--json", default=None)
 a = ap.parse_args()
 _lib.load(require_device=True)
@@ -75,8 +77,13 @@ def graph(E, pattern, rng):
     np.add.at(csc_ptr, src + 1, 1)
     csc_ptr = np.cumsum(csc_ptr)
     t = lambda x, dt=torch.int32: torch.as_tensor(np.ascontiguousarray(x)).to(dtype=dt, device=dev)
+    # the backward reads the weights in CSC order as the step does
+    # (GFM_FLAG_W_CSC; GFM_W_CSC=0: w[eid] gathers)
+    w_csc = os.environ.get("GFM_W_CSC", "1") != "0"
     return N, dict(rowptr=t(rowptr), col_src=t(src), w=t(w, torch.float32), csc_ptr=t(csc_ptr),
-                   csc_eid=t(csc), csc_dst=t(dst[csc]), max_deg=int(np.diff(rowptr).max()))
+                   csc_eid=t(csc), csc_dst=t(dst[csc]), max_deg=int(np.diff(rowptr).max()),
+                   w_bwd=t(w[csc] if w_csc else w, torch.float32),
+                   w_flag=_lib.FLAG_W_CSC if w_csc else 0)
 
 
 def identity_graph(E, g):
@@ -139,9 +146,11 @@ def materialised(E, H, g, kind, parts, K, u8):
 rows = []
 rng = np.random.default_rng(0)
 modes = a.modes.split(",")
-for Em in [m for m in (1, 4, 16, 64, 100) if m <= a.max_e]:
+E_LIST = [int(x) for x in a.e_list.split(",")] if a.e_list else \
+    [m for m in (1, 4, 16, 64, 100) if m <= a.max_e]
+for Em in E_LIST:
     E = Em * 1_000_000
-    for pattern in ("random", "block-local"):
+    for pattern in a.patterns.split(","):
         N, g = graph(E, pattern, rng)
         for H in (64, 128, 256, 512):
             for kind, parts in (("sum", _lib.PART_SUM), ("pna", 15)):
@@ -174,8 +183,9 @@ for Em in [m for m in (1, 4, 16, 64, 100) if m <= a.max_e]:
 
                 def bwd():
                     _lib.call("gfm_agg_bwd", P(dagg), P(agg), P(sm), P(am), P(h), P(g["rowptr"]),
-                              P(g["csc_ptr"]), P(g["csc_eid"]), P(g["csc_dst"]), P(g["w"]), N, H,
-                              parts, P(dh), None, P(out), P(ws), _lib.F32, u8, sh)
+                              P(g["csc_ptr"]), P(g["csc_eid"]), P(g["csc_dst"]), P(g["w_bwd"]), N,
+                              H, parts, P(dh), None, P(out), P(ws), _lib.F32, u8 | g["w_flag"],
+                              sh)
 
                 tf, tb = timeit(fwd), timeit(bwd)
                 # SURVEY 8(d) C5 formulas (s = 4)

@@ -49,10 +49,18 @@ def fwd():
               P(am), P(sm), _lib.F32, flags, sh)
 
 
+# edge weights in CSC order as in the step (GFM_W_CSC=0: w[eid] gathers)
+W_CSC = os.environ.get("GFM_W_CSC", "1") != "0"
+w_b = b.edge_w
+if W_CSC:
+    w_b = torch.empty_like(b.edge_w)
+    _lib.call("gfm_permute", P(b.csc_eid), E, None, P(b.edge_w), P(w_b), _lib.F32, sh)
+
+
 def bwd():
     _lib.call("gfm_agg_bwd", P(dagg), P(agg), P(sm), P(am), P(h), P(b.rowptr), P(b.csc_ptr),
-              P(b.csc_eid), P(b.csc_dst), P(b.edge_w), N, H, parts, P(dh), P(h), P(out), P(ws),
-              _lib.F32, flags, sh)
+              P(b.csc_eid), P(b.csc_dst), P(w_b), N, H, parts, P(dh), P(h), P(out), P(ws),
+              _lib.F32, flags | (_lib.FLAG_W_CSC if W_CSC else 0), sh)
 
 
 def timeit(fn, reps=30):
