@@ -354,16 +354,17 @@ __global__ void __launch_bounds__(256)
         int s[kFU];
         float d[kFU];
         float4 r[kFU][NV];
+        // row indices first: the P loads issue before the dm shuffles wait
+        // on the (dependent) dm loads
 #pragma unroll
-        for (int q = 0; q < kFU; ++q) {
-          const int src = e + q < cnt ? e + q : e;
-          s[q] = __shfl_sync(gm, my_s, src, LPN);
-          d[q] = __shfl_sync(gm, my_dm, src, LPN);
-        }
+        for (int q = 0; q < kFU; ++q)
+          s[q] = __shfl_sync(gm, my_s, e + q < cnt ? e + q : e, LPN);
 #pragma unroll
         for (int q = 0; q < kFU; ++q)
 #pragma unroll
           for (int v = 0; v < NV; ++v) r[q][v] = __ldg(P4 + (long long)s[q] * H4 + v * LPN + cb);
+#pragma unroll
+        for (int q = 0; q < kFU; ++q) d[q] = __shfl_sync(gm, my_dm, e + q < cnt ? e + q : e, LPN);
 #pragma unroll
         for (int q = 0; q < kFU; ++q)
           if (e + q < cnt) edge(r[q], d[q]);
@@ -441,16 +442,17 @@ __global__ void __launch_bounds__(256)
         int i[kFU];
         float d[kFU];
         float4 r[kFU][NV];
+        // row indices first: the P loads issue before the dm shuffles wait
+        // on the (dependent) dm loads
 #pragma unroll
-        for (int q = 0; q < kFU; ++q) {
-          const int src = e + q < cnt ? e + q : e;
-          i[q] = __shfl_sync(gm, my_i, src, LPN);
-          d[q] = __shfl_sync(gm, my_dm, src, LPN);
-        }
+        for (int q = 0; q < kFU; ++q)
+          i[q] = __shfl_sync(gm, my_i, e + q < cnt ? e + q : e, LPN);
 #pragma unroll
         for (int q = 0; q < kFU; ++q)
 #pragma unroll
           for (int v = 0; v < NV; ++v) r[q][v] = __ldg(P4 + (long long)i[q] * H4 + v * LPN + cb);
+#pragma unroll
+        for (int q = 0; q < kFU; ++q) d[q] = __shfl_sync(gm, my_dm, e + q < cnt ? e + q : e, LPN);
 #pragma unroll
         for (int q = 0; q < kFU; ++q)
           if (e + q < cnt) edge(r[q], d[q]);

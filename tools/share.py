@@ -35,3 +35,13 @@ for name, t in rows:
 for c, _ in CATS:
     print(f"{c:20s} {acc[c] / steps:9.1f} us/step  {100 * acc[c] / tot:5.1f}%")
 print(f"{'total':20s} {tot / steps:9.1f} us/step")
+print()
+print("# top kernels (us summed over the step)")
+print(f"launches: {len(rows) // steps}")
+by = defaultdict(lambda: [0.0, 0])
+for name, t in rows:
+    k = name[:100]
+    by[k][0] += t
+    by[k][1] += 1
+for k, (t, n) in sorted(by.items(), key=lambda x: -x[1][0])[:20]:
+    print(f"{t / steps:9.1f} us  {n // steps:4d}x {k}")
