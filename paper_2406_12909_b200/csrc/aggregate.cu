@@ -826,8 +826,8 @@ static bool vec_shape(int H, int& nv, int& lpn, int* slabs = nullptr, bool wide2
   if (slabs) {
     *slabs = 1;
     if (h4 > 32 && h4 % 32 == 0) {
-      // wide2: two float4 per lane (the forward measured 5% faster at
-      // H = 512; the backward 11% slower, it keeps one)
+      // wide2: two float4 per lane (round 1: the forward 5% faster at
+      // H = 512, the backward 11% slower; round 2: both faster with one)
       nv = wide2 && h4 % 64 == 0 ? 2 : 1;
       lpn = 32;
       *slabs = h4 / (32 * nv);
@@ -890,7 +890,10 @@ cudaError_t agg_fwd(int dtype, const void* h, int n, int H, const int* rowptr, c
                                                  (float*)stat_mean, kNb, kCap);
     return cudaGetLastError();
   }
-  if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn, &slabs, true)) {
+  // one float4 per lane and more column slabs (more resident warps): C3
+  // forward 392 -> 364 us vs two float4 per lane (GFM_AGG_FWD_WIDE2=1)
+  static const bool fwd_wide2 = getenv("GFM_AGG_FWD_WIDE2") != nullptr;
+  if (dtype == GFM_F32 && !force_scalar && vec_shape(H, nv, lpn, &slabs, fwd_wide2)) {
     const int nodes_per_block = 8 * (32 / lpn);
     const dim3 grid(ceil_div(n, nodes_per_block), slabs);
 #define GFM_FWD_CASE(NV_, LPN_)                                                                \

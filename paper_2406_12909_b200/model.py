@@ -616,6 +616,8 @@ class _Scratch:
         """second stream for work with no consumer until a later join (one
         per device and thread, shared by every scratch: API calls without a
         scratch object do not create a stream per call)"""
+        if _ONE_STREAM:  # GFM_ONE_STREAM=1: everything on the caller's stream (A/B runs)
+            return torch.cuda.current_stream(self.device)
         if getattr(self, "_side", None) is None:
             key = (str(self.device), threading.get_ident())
             st = _SIDE_STREAMS.get(key)
@@ -626,6 +628,7 @@ class _Scratch:
 
 
 _SIDE_STREAMS: dict = {}
+_ONE_STREAM = os.environ.get("GFM_ONE_STREAM") == "1"
 
 
 def _scratch_for(owner, device):
