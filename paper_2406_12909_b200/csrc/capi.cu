@@ -10,6 +10,13 @@ static thread_local char g_err[512] = "";
 static int g_gemm_mode = GFM_GEMM_TC3;
 
 int gemm_mode() { return g_gemm_mode; }
+// CTA-pair GEMM kernels (default on; GFM_TC_PAIR=0 at first use or
+// gfm_set_tc_pairs(0) selects the single-CTA kernels)
+static int g_tc_pairs = -1;
+bool tc_pairs() {
+  if (g_tc_pairs < 0) g_tc_pairs = getenv("GFM_TC_PAIR") ? atoi(getenv("GFM_TC_PAIR")) : 1;
+  return g_tc_pairs != 0;
+}
 bool pdl_enabled() {
   static const bool v = [] {
     const char* e = getenv("GFM_NO_PDL");
@@ -45,6 +52,12 @@ int gfm_set_gemm_mode(int mode) {
 }
 
 int gfm_get_gemm_mode(void) { return gfm::g_gemm_mode; }
+
+int gfm_set_tc_pairs(int on) {
+  const int prev = gfm::tc_pairs() ? 1 : 0;
+  gfm::g_tc_pairs = on ? 1 : 0;
+  return prev;
+}
 
 int gfm_stream_sync(void* stream) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);

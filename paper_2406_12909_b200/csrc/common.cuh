@@ -16,6 +16,7 @@ void set_error(const char* fmt, ...);
 
 // Process-wide GEMM engine selection for float32 (GFM_GEMM_*).
 int gemm_mode();
+bool tc_pairs();
 
 // ---------------------------------------------------------------------------
 // Exactly-rounded arithmetic.  nvcc contracts a*b+c into FMA by default; the
@@ -232,6 +233,27 @@ inline cudaError_t launch_k(void (*k)(KP...), dim3 grid, dim3 block, size_t smem
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
+// launch_k with a thread-block cluster of `cluster` CTAs along x (CTA pairs)
+template <typename... KP, typename... A>
+inline cudaError_t launch_kc(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             int cluster, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
 }
 

@@ -31,6 +31,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -61,6 +62,10 @@ inline bool at_disabled() {
   if (v < 0) v = getenv("GFM_NO_TMEM_A") ? atoi(getenv("GFM_NO_TMEM_A")) : 0;
   return v != 0;
 }
+
+// CTA-pair (cta_group::2) 3xTF32 kernel for 64/128-wide tiles with a K-major
+// A (default; GFM_TC_PAIR=0 / gfm_set_tc_pairs(0) for the single-CTA kernel)
+inline bool pairs_enabled() { return tc_pairs(); }
 
 // Accumulation flush depth in 32-wide k-blocks (TMA engine).  The tensor
 // core's fp32 accumulator rounds toward zero, so its error grows linearly
@@ -634,13 +639,13 @@ inline bool make_map(CUtensorMap* m, const float* base, long long inner, long lo
 // 3D MN-major view: dims {32, K, extent / 32}, strides {ld, 32} elements,
 // box {32, kBK, 4}
 inline bool make_map3(CUtensorMap* m, const float* base, long long extent, long long K, long long ld,
-                      CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
+                      CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, int atoms = 4) {
   EncodeTiledFn fn = encode_fn();
   if (!fn || !base || extent <= 0 || extent % 32 || K <= 0) return false;
   if (((uintptr_t)base & 15) || ((ld * 4) & 15)) return false;
   cuuint64_t dims[3] = {32, (cuuint64_t)K, (cuuint64_t)(extent / 32)};
   cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), 128};
-  cuuint32_t box[3] = {32, (cuuint32_t)kBK, 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)kBK, (cuuint32_t)atoms};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -682,9 +687,12 @@ inline bool build_tma(const Rows2Ld<T>& l, TmaOp* op, int rows_box, long long ro
                                rows_box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// MN-major operands: the 3D view fetches min(rows_box, 128) / 32 atoms per
+// instruction (64-row B halves of CTA pairs: two)
 template <typename T>
-inline bool build_tma(const ColsLd<T>& l, TmaOp* op, int, long long rows_total, int K,
+inline bool build_tma(const ColsLd<T>& l, TmaOp* op, int rows_box, long long rows_total, int K,
                       CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
+  const int atoms = rows_box >= 128 ? 4 : (rows_box >= 32 ? rows_box / 32 : 1);
   if (sizeof(T) != 4) return false;
   op->mn = 1;
   op->split_at = 1 << 30;
@@ -692,13 +700,14 @@ inline bool build_tma(const ColsLd<T>& l, TmaOp* op, int, long long rows_total, 
   op->has3[0] = op->has3[1] = op->has3[2] = 0;
   if (!make_map(&op->map[0], (const float*)l.p, rows_total, K, l.ld, 32, kBK, sw))
     return false;
-  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p, rows_total, K, l.ld, sw);
+  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p, rows_total, K, l.ld, sw, atoms);
   return true;
 }
 
 template <typename T>
-inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int, long long rows_total, int K,
+inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int rows_box, long long rows_total, int K,
                       CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) {
+  const int atoms = rows_box >= 128 ? 4 : (rows_box >= 32 ? rows_box / 32 : 1);
   // the virtual ones row (bias) needs the caller's ones buffer (a [K][4]
   // tensor whose column 0 is 1: inner extent 1, the rest of each 32-row box
   // is TMA zero fill)
@@ -716,8 +725,8 @@ inline bool build_tma(const Cols2Ld<T>& l, TmaOp* op, int, long long rows_total,
   if (bias && !make_map(&op->map[2], (const float*)l.ones, 1, K, 4, 32, kBK, sw))
     return false;
   if (bias && l.n2 == 0) op->map[1] = op->map[2];  // segment 1 empty: route to the ones map
-  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p1, l.n1, K, l.ld1, sw);
-  op->has3[1] = l.n2 > 0 && make_map3(&op->map3[1], (const float*)l.p2, l.n2, K, l.ld2, sw);
+  op->has3[0] = make_map3(&op->map3[0], (const float*)l.p1, l.n1, K, l.ld1, sw, atoms);
+  op->has3[1] = l.n2 > 0 && make_map3(&op->map3[1], (const float*)l.p2, l.n2, K, l.ld2, sw, atoms);
   op->has3[2] = 0;
   return true;
 }
@@ -750,14 +759,16 @@ __device__ __forceinline__ void tma_tile(const TmaOp& op, uint32_t dst, int r0, 
   } else {
     // one 3D load when the whole tile lies in a segment with a 3D view (rows
     // past the last segment's end are TMA zero fill either way)
-    if constexpr (ROWS % 128 == 0) {
+    // (the 3D view's box is min(ROWS, 128) rows: the op was built for ROWS)
+    if constexpr (ROWS % 32 == 0 && (ROWS % 128 == 0 || ROWS < 128)) {
+      constexpr int kBox = ROWS < 128 ? ROWS : 128;
       const int seg = r0 >= op.split2 ? 2 : (r0 >= op.split_at ? 1 : 0);
       const int s0 = seg == 2 ? op.split2 : (seg == 1 ? op.split_at : 0);
       const int s1 = seg == 0 ? op.split_at : (seg == 1 ? op.split2 : (1 << 30));
       if (op.has3[seg] && (r0 + ROWS <= s1 || s1 >= (1 << 30))) {
 #pragma unroll
-        for (int at = 0; at < ROWS / 128; ++at)
-          tma_load_3d(dst + at * 16384, &op.map3[seg], 0, k0, (r0 - s0) / 32 + at * 4, bar);
+        for (int at = 0; at < ROWS / kBox; ++at)
+          tma_load_3d(dst + at * kBox * 128, &op.map3[seg], 0, k0, (r0 - s0) / 32 + at * (kBox / 32), bar);
         return;
       }
     }
@@ -1224,6 +1235,419 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (warp == 0) tmem_free<NC>(tmem);
 }
 
+// ---------------------------------------------------------------- CTA pairs
+// cta_group::2 variant of the A-in-TMEM 3xTF32 kernel: a cluster of two CTAs
+// (one TPC) computes a 256 x BN tile with M = 256 MMAs issued by the leader.
+// Each CTA stages its own 128 A rows (converted into its own TMEM, as in the
+// single-CTA kernel) and HALF of the BN B rows (raw + lo): the tensor cores
+// read each B half from its owner's smem, so per SM the TMA bytes, the B lo
+// pass and the MMAs' B reads halve (per 32-deep k-block and SM ~80 KB of
+// shared-memory traffic instead of ~128 KB) while the MMA time per SM stays.
+// Barriers: TMA landed / ring free / lo free / accumulator full are per CTA
+// (the leader's commits multicast to both); lo written and accumulator
+// drained live in the leader and count both CTAs' warps.
+template <int BN>
+struct SmemP {
+  static constexpr int kA = kBM * 128;
+  static constexpr int kB = (BN / 2) * 128;  // this CTA's half of the B rows
+  static constexpr int kRaw = kA + kB;
+  static constexpr int kLo = kB;
+  static constexpr int kL = 4;
+  static constexpr int kEpi = 8 * 32 * 20 * 4;
+  static constexpr int kR = (224 * 1024 - kL * kLo - kEpi) / kRaw;
+  static constexpr int kBars = (2 * kR + 2 * kL + 4) * 8 + 16;
+  static constexpr int kBytes = kR * kRaw + kL * kLo + kEpi + 1024 + kBars;
+  static_assert(kBytes <= 232448, "smem");
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of p's twin in CTA `rank` of the pair
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t leader_addr(const void* p) { return peer_addr(p, 0); }
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  // default (.release.cta) semantics, as CUTLASS's ClusterBarrier: a
+  // .release.cluster arrive costs a cluster-scope MEMBAR per k-block
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" :: "r"(caddr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n"
+      :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// commit the leader's MMAs to the barrier at this offset in BOTH CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      :: "r"(smem_u32(bar)), "h"((unsigned short)3) : "memory");
+}
+
+// kb_at3 with M = 256 pair MMAs (A from both CTAs' TMEM, B halves from both
+// CTAs' smem) and multicast commits
+__device__ __forceinline__ void kb_at3_pair(uint32_t d, uint32_t ta, uint64_t bh, uint64_t bl,
+                                            uint64_t binc, uint32_t idesc, uint32_t acc0,
+                                            uint32_t bar0, uint32_t bar1) {
+#define GFM_P_MMA(A, B, EN) \
+  "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [" A "], " B ", %5, " EN ";\n\t"
+#define GFM_P_T3 GFM_P_MMA("l", "b0", "t") GFM_P_MMA("h", "b1", "t") GFM_P_MMA("h", "b0", "t")
+#define GFM_P_STEP \
+  "add.u32 h, h, 8;\n\tadd.u32 l, l, 8;\n\tadd.s64 b0, b0, %4;\n\tadd.s64 b1, b1, %4;\n\t"
+#define GFM_P_COMMIT(BAR) \
+  "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [" BAR "], m;\n\t"
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 b0, b1;\n\t.reg .b32 h, l;\n\t.reg .b16 m;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\tsetp.eq.b32 t, 0, 0;\n\tmov.b16 m, 3;\n\t"
+      "mov.b64 b0, %2;\n\tmov.b64 b1, %3;\n\tmov.b32 h, %1;\n\tadd.u32 l, h, 32;\n\t"
+      GFM_P_MMA("l", "b0", "p") GFM_P_MMA("h", "b1", "t") GFM_P_MMA("h", "b0", "t")
+      GFM_P_STEP GFM_P_T3 GFM_P_STEP GFM_P_T3 GFM_P_STEP GFM_P_T3
+      GFM_P_COMMIT("%7") GFM_P_COMMIT("%8") "}\n"
+      :: "r"(d), "r"(ta), "l"(bh), "l"(bl), "l"(binc), "r"(idesc), "r"(acc0), "r"(bar0),
+         "r"(bar1) : "memory");
+#undef GFM_P_MMA
+#undef GFM_P_T3
+#undef GFM_P_STEP
+#undef GFM_P_COMMIT
+}
+
+template <int BN, class Epi, int AT, bool FLUSH>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    tc_gemm_tma_pair_kernel(int M, const int* __restrict__ M_dev, int N, int K, int k_chunk, int splits,
+                       int split3, int fkb, const __grid_constant__ TmaOp ta,
+                       const __grid_constant__ TmaOp tb, Epi epi) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  static_assert(AT != 0 && BN >= 64, "pairs: A in TMEM, B halves of >= 32 rows");
+  using S = SmemP<BN>;
+  // TMEM: two BN-column accumulators, then (AT) kL A slots of 32 hi + 32 lo columns
+  constexpr int kACol = 2 * BN;
+  constexpr int NC = tmem_cols(2 * BN + (AT ? S::kL * 64 : 0));
+  constexpr int kR = S::kR, kL = S::kL;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* lo_base = base + kR * S::kRaw;
+  float* epi_stage = reinterpret_cast<float*>(lo_base + kL * S::kLo);  // [8][32][20]
+  uint64_t* tfl = reinterpret_cast<uint64_t*>(lo_base + kL * S::kLo + S::kEpi);  // TMA landed [kR]
+  uint64_t* empty = tfl + kR;    // MMAs done with the raw stage [kR]
+  uint64_t* cvt = empty + kR;    // lo written [kL]
+  uint64_t* lofree = cvt + kL;   // MMAs done with the lo slot [kL]
+  uint64_t* tfull = lofree + kL; // accumulator ready [2]
+  uint64_t* tempty = tfull + 2;  // accumulator drained [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool split_on = split3 != 0;
+  constexpr int kMmaWarp = 1 + kConvWarps;
+
+  // prologue (barriers, descriptor prefetch, TMEM) touches no predecessor
+  // output, so it runs before the programmatic-dependency wait
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kR; ++q) {
+      mbar_init(&tfl[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < kL; ++q) {
+      mbar_init(&cvt[q], 2 * kConvWarps);  // both CTAs' converters (leader's copy)
+      mbar_init(&lofree[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&tfull[q], 1);
+      mbar_init(&tempty[q], 2 * kEpiWarps);  // both CTAs' epilogues (leader's copy)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&ta.map[0]) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(&tb.map[0]) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(tmem_slot)), "n"(NC));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barrier inits and the TMEM address visible pair-wide
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_entry();
+
+  const int rank = (int)cluster_rank();
+  const int cid = (int)blockIdx.x >> 1, ncl = (int)gridDim.x >> 1;
+  const int m_total = M_dev ? *M_dev : M;
+  const int m_tiles = (m_total + kBM - 1) / kBM;
+  const int m_pairs = (m_tiles + 1) / 2;  // a pair owns m tiles 2p (leader) and 2p + 1
+  const int n_tiles = (N + BN - 1) / BN;
+  const int n_work = m_pairs * n_tiles * splits;
+
+  auto tile_of = [&](int w, int& bm, int& bn, int& split) {
+    split = w / (m_pairs * n_tiles);
+    bn = (w % (m_pairs * n_tiles)) % n_tiles;
+    bm = 2 * ((w % (m_pairs * n_tiles)) / n_tiles) + rank;
+  };
+  auto nkb_of = [&](int w) { return item_nkb(w, m_pairs * n_tiles, k_chunk, K); };
+  // accumulation chunks of a work item (>= 1: an empty item still completes once)
+  auto nch_of = [&](int nkb) {
+    if constexpr (!FLUSH) return 1;
+    return nkb > 0 ? (nkb + fkb - 1) / fkb : 1;
+  };
+
+  if (cid >= n_work) {
+    // no work for this pair: straight to the teardown
+  } else if (warp == 0) {
+    // ============================================================ TMA producer
+    if (lane == 0) {
+      int p = 0;
+      for (int w = cid; w < n_work; w += ncl) {
+        int bm, bn, split;
+        tile_of(w, bm, bn, split);
+        const int nkb = nkb_of(w);
+        for (int kb = 0; kb < nkb; ++kb, ++p) {
+          const int s = p % kR;
+          if (p >= kR) mbar_wait_cl(&empty[s], ((p / kR) - 1) & 1);
+          const int k0 = split * k_chunk + kb * kBK;
+          const uint32_t st = smem_u32(base + s * S::kRaw);
+          mbar_expect_tx(&tfl[s], S::kRaw);
+          tma_tile<kBM>(ta, st, bm * kBM, k0, &tfl[s]);
+          tma_tile<BN / 2>(tb, st + S::kA, bn * BN + rank * (BN / 2), k0, &tfl[s]);
+        }
+      }
+    }
+  } else if (warp <= kConvWarps) {
+    // ============================================================ lo converters
+    if (split_on) {
+      const int ctid = threadIdx.x - 32;
+      int q = 0;
+      for (int w = cid; w < n_work; w += ncl) {
+        const int nkb = nkb_of(w);
+        for (int kb = 0; kb < nkb; ++kb, ++q) {
+          const int s = q % kR, l = q % kL;
+          mbar_wait(&tfl[s], (q / kR) & 1);
+          if (q >= kL) mbar_wait_cl(&lofree[l], ((q / kL) - 1) & 1);
+          if constexpr (AT != 0) {
+            // A row r = 32 * (warp % 4) + lane (this warp's TMEM lane quarter),
+            // k half h = (warp - 1) / 4 -> 16 hi / lo values
+            const int q4 = warp & 3, h = (warp - 1) >> 2;
+            const int r = q4 * 32 + lane;
+            uint32_t hi[16], lo[16];
+            if constexpr (AT == 1) {  // 4 swizzled 16-byte chunks of the row
+              const uint32_t ra = smem_u32(base + s * S::kRaw) + (uint32_t)(r * 128);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t a = ra + (uint32_t)((((4 * h + j) ^ (r & 7)) & 7) << 4);
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(hi[4 * j]), "=r"(hi[4 * j + 1]), "=r"(hi[4 * j + 2]),
+                               "=r"(hi[4 * j + 3]) : "r"(a));
+              }
+            } else {  // atom q4, column lane, k rows 16h.. (128-byte row stride)
+              const uint32_t ra = smem_u32(base + s * S::kRaw) +
+                                  (uint32_t)(q4 * 4096 + (16 * h) * 128 + lane * 4);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(hi[j]) : "r"(ra + 128u * j));
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t x = hi[e];
+              hi[e] = x & 0xFFFFE000u;
+              lo[e] = __float_as_uint(__uint_as_float(x) - __uint_as_float(hi[e]));
+            }
+            const uint32_t ta_ = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(kACol + l * 64 + 16 * h);
+            tmem_st16(ta_, hi);
+            tmem_st16(ta_ + 32, lo);
+            make_lo<S::kB, kConvWarps * 32>(base + s * S::kRaw + S::kA, lo_base + l * S::kLo, ctid);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+          } else {
+            make_lo<S::kRaw, kConvWarps * 32>(base + s * S::kRaw, lo_base + l * S::kRaw, ctid);
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_addr(&cvt[l]));
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (rank != 0) {
+      // the leader's MMA warp issues for the pair
+    } else {
+    // ============================================================ MMA issuer
+    // (A from TMEM is always row = lane, k = column: K-major in the idesc)
+    const bool a_mn = AT == 0 && ta.mn != 0, b_mn = tb.mn != 0;
+    const uint32_t idesc = make_idesc_tf32(BN, a_mn, b_mn) + ((uint32_t)(kBM >> 4) << 24);  // M = 256
+    // k-step 0 descriptor; later k-steps add ainc / binc (address field is >> 4)
+    auto desc0 = [&](bool mn, uint32_t addr) -> uint64_t {
+      return mn ? make_desc_mn(addr, 4096, 512) : make_desc(addr);
+    };
+    const uint64_t ainc = a_mn ? 1024 >> 4 : 32 >> 4, binc = b_mn ? 1024 >> 4 : 32 >> 4;
+    int q = 0, t = 0;
+    for (int w = cid; w < n_work; w += ncl) {
+     const int nkb = nkb_of(w), nch = nch_of(nkb);
+     for (int ch = 0; ch < nch; ++ch, ++t) {  // one accumulator per chunk
+      const int acc = t & 1;
+      if (t >= 2) mbar_wait_cl(&tempty[acc], ((t >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem + (uint32_t)(acc * BN);
+      const int kb_end = min(nkb, (ch + 1) * fkb);
+      for (int kb = ch * fkb; kb < kb_end; ++kb, ++q) {
+        const int s = q % kR, l = q % kL;
+        mbar_wait_cl(&cvt[l], (q / kL) & 1);  // both CTAs' rows landed and converted
+        tc_fence_after();
+        const uint32_t ah = smem_u32(base + s * S::kRaw), bh = ah + S::kA;
+        const uint32_t al = smem_u32(lo_base + l * S::kLo), bl = AT != 0 ? al : al + S::kA;
+        const uint32_t acc0 = kb > ch * fkb ? 1u : 0u;
+        const uint32_t e_bar = smem_u32(&empty[s]), l_bar = smem_u32(&lofree[l]);
+        (void)ah;
+        kb_at3_pair(d, tmem + (uint32_t)(kACol + l * 64), desc0(b_mn, bh), desc0(b_mn, bl), binc,
+                    idesc, acc0, e_bar, l_bar);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (nkb > 0) {
+          mma_commit_pair(&tfull[acc]);
+        } else {  // empty item: complete both CTAs' accumulators by hand
+          mbar_arrive_cluster(peer_addr(&tfull[acc], 0));
+          mbar_arrive_cluster(peer_addr(&tfull[acc], 1));
+        }
+      }
+      __syncwarp();
+     }
+    }
+    }
+  } else {
+    // ============================================================ epilogue
+    const int quarter = warp & 3;                       // TMEM lanes 32 * quarter ..
+    const int half = (warp - (kMmaWarp + 1)) / 4;       // column half of the tile
+    constexpr int kHalf = BN / 2 >= 16 ? BN / 2 : 16;
+    int t = 0;
+    for (int w = cid; w < n_work; w += ncl, ++t) {
+      int bm, bn, split;
+      tile_of(w, bm, bn, split);
+      const int nkb = nkb_of(w), nch = nch_of(nkb);
+      // chunks before the last: fold each TMEM partial into fp32 registers
+      // (IEEE adds, in chunk order) and hand the accumulator back at once
+      constexpr int kRegs = (BN / 2 >= 16 ? BN / 2 : 16);
+      float racc[kRegs];
+      const int c_lo = half * kHalf, c_hi = min(BN, (half + 1) * kHalf);
+      for (int ch = 0; ch + 1 < nch; ++ch, ++t) {
+        const int acc = t & 1;
+        mbar_wait_cl(&tfull[acc], (t >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int j = 0; j < kRegs / 16; ++j) {
+          if (c_lo + 16 * j >= c_hi) continue;
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c_lo + 16 * j), v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) racc[16 * j + i] = ch == 0 ? v[i] : racc[16 * j + i] + v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+      }
+      const int acc = t & 1;
+      mbar_wait_cl(&tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const int m0 = bm * kBM, n0 = bn * BN;
+      // per 16-column chunk: registers (row = lane) -> this warp's smem stage
+      // -> read back transposed so each store instruction writes 8 rows x 64
+      // contiguous bytes (full sectors) instead of 32 rows x 16 bytes
+      float* stg = epi_stage + (warp - (kMmaWarp + 1)) * (32 * 20);
+      const int m_lim = min(kBM, m_total - m0);
+      auto store16 = [&](int c, const float (&v)[16]) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(stg + lane * 20 + 4 * q) =
+              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        __syncwarp();
+        if constexpr (HasPrefetch<Epi>::value) {
+          decltype(epi.prefetch(0, 0)) pre[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), q = lane & 3;
+            const int col = n0 + c + 4 * q;
+            const int rr = quarter * 32 + r;
+            if (rr < m_lim && col < N) pre[j] = epi.prefetch(m0 + rr, col);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), q = lane & 3;
+            const int col = n0 + c + 4 * q;
+            const int rr = quarter * 32 + r;
+            if (rr < m_lim && col < N)
+              epi.store4(m0 + rr, col, *reinterpret_cast<const float4*>(stg + r * 20 + 4 * q),
+                         min(4, N - col), split, pre[j]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), q = lane & 3;
+            const int col = n0 + c + 4 * q;
+            const int rr = quarter * 32 + r;
+            if (rr < m_lim && col < N)
+              epi.store4(m0 + rr, col, *reinterpret_cast<const float4*>(stg + r * 20 + 4 * q),
+                         min(4, N - col), split);
+          }
+        }
+        __syncwarp();
+      };
+      if (nch > 1) {
+        // last chunk: fold it too and hand the accumulator back BEFORE the
+        // stores, so the next tile's MMAs are not held up by this epilogue
+#pragma unroll
+        for (int j = 0; j < kRegs / 16; ++j) {
+          if (c_lo + 16 * j >= c_hi) continue;
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c_lo + 16 * j), v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) racc[16 * j + i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+#pragma unroll
+        for (int j = 0; j < kRegs / 16; ++j) {
+          const int c = c_lo + 16 * j;
+          if (c >= c_hi || n0 + c >= N) continue;
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = racc[16 * j + i];
+          store16(c, v);
+        }
+        continue;
+      }
+#pragma unroll 1
+      for (int c = c_lo; c < c_hi; c += 16) {
+        float v[16];
+        if (nkb > 0) {
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (n0 + c >= N) continue;
+        store16(c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // the peer no longer touches this CTA's smem / barriers
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(NC));
+}
+
 template <int BN, class AL, class BL, class Epi>
 inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K_dev, int splits,
                              int split3, AL a, BL b, Epi epi, cudaStream_t s) {
@@ -1246,6 +1670,48 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
           build_tma(a, &ta, kBM, M, K);
       }
       const bool flush = ceil_div(k_chunk, kBK) > flush_kb();
+      if constexpr (BN >= 64) {
+        // CTA pairs (cta_group::2): B halves per CTA
+        TmaOp tbh;
+        // (K-major A only: with the MN-major A of the weight gradients the
+        // pair kernel measured 28% slower, forward / backward-data 4-8% faster)
+        if (at == 1 && pairs_enabled() && ceil_div(M, kBM) >= 2 &&
+            build_tma(b, &tbh, BN / 2, N, K)) {
+          auto kp = flush ? (at == 1 ? tc_gemm_tma_pair_kernel<BN, Epi, 1, true>
+                                     : tc_gemm_tma_pair_kernel<BN, Epi, 2, true>)
+                          : (at == 1 ? tc_gemm_tma_pair_kernel<BN, Epi, 1, false>
+                                     : tc_gemm_tma_pair_kernel<BN, Epi, 2, false>);
+          const int smem = SmemP<BN>::kBytes;
+          cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          if (e != cudaSuccess) return e;
+          // persistent: as many pairs as can be co-resident (not every TPC
+          // may take a pair of these 1-CTA-per-SM CTAs at once; a second
+          // wave of pairs would double the time of a persistent kernel)
+          static int max_pairs = 0;
+          if (max_pairs == 0) {
+            cudaLaunchConfig_t qc = {};
+            qc.gridDim = dim3(148);
+            qc.blockDim = dim3(kTmaThreads);
+            qc.dynamicSmemBytes = smem;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = 2;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            qc.attrs = qa;
+            qc.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, kp, &qc) != cudaSuccess || n <= 0) n = 64;
+            max_pairs = n < 74 ? n : 74;
+            if (getenv("GFM_TC_DEBUG")) fprintf(stderr, "tc pairs: %d co-resident (BN %d)\n", n, BN);
+          }
+          const long long pw = (long long)ceil_div(ceil_div(M, kBM), 2) * ceil_div(N, BN) * splits;
+          const int pgrid = 2 * (int)std::min<long long>(pw, (long long)max_pairs);
+          launch_kc(kp, pgrid, kTmaThreads, smem, s, 2, M, M_dev, N, K, k_chunk, splits, split3,
+                    flush_kb(), ta, tbh, epi);
+          return cudaGetLastError();
+        }
+      }
       auto kern = flush ? (at == 1   ? tc_gemm_tma_kernel<BN, Epi, 1, true>
                            : at == 2 ? tc_gemm_tma_kernel<BN, Epi, 2, true>
                                      : tc_gemm_tma_kernel<BN, Epi, 0, true>)
