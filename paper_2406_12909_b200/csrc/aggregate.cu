@@ -26,7 +26,7 @@
 
 #include "common.cuh"
 
-// CSC slots batched per iteration on 32-lane rows, with a max part (3-4
+// CSC slots batched per iteration (32-lane and narrow rows), with a max part (3-4
 // rows per slot) / without: 1 / 2 (C3 pna: 1 is 4% faster than 2; C5 random
 // sum at E = 16M: 2 reaches 0.67 of HBM, 1 0.53; tools/agg_knobs3.sh)
 #ifndef GFM_AGG_BWD_U
@@ -689,8 +689,27 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
       }
     }
   } else {
-    // narrow rows (several nodes per warp): issue-bound, one slot at a time
-    for (int q = qb; q < qe; ++q) {
+    // narrow rows (several nodes per warp): U slots per batch (1 with a max
+    // part: 2 measured 5% slower at C2; 2 without: C5 random sum at H = 64
+    // 0.54 -> 0.73 of HBM)
+    constexpr int UN = U;
+    int q = qb;
+    for (; q + UN <= qe; q += UN) {
+      int p[UN], i[UN];
+      float ww[UN];
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {
+        p[u] = __ldg(csc_eid + q + u);
+        i[u] = __ldg(csc_dst + q + u);
+        ww[u] = __ldg(w + (w_csc ? q + u : p[u]));
+      }
+      Rows r[UN];
+#pragma unroll
+      for (int u = 0; u < UN; ++u) load(i[u], r[u]);
+#pragma unroll
+      for (int u = 0; u < UN; ++u) consume(p[u], i[u], ww[u], r[u]);
+    }
+    for (; q < qe; ++q) {
       const int p = __ldg(csc_eid + q), i = __ldg(csc_dst + q);
       const float wv = __ldg(w + (w_csc ? q : p));
       Rows r;
@@ -998,11 +1017,9 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
            (float*)out, w_csc)
 #define GFM_BWD_LAUNCH(NV_, LPN_, U8_, GC_)                                                  \
   do {                                                                                       \
-    if constexpr (LPN_ == 32) {                                                              \
-      if (deep) {                                                                            \
-        GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U_DEEP);                           \
-        break;                                                                               \
-      }                                                                                      \
+    if (deep) {                                                                              \
+      GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U_DEEP);                             \
+      break;                                                                                 \
     }                                                                                        \
     GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U);                                    \
   } while (0)
