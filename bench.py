@@ -615,7 +615,7 @@ def rooflines(ctx, W, cfg, b, s):
     flags = M._argmax_flag(b)
     h_in = torch.randn(N, H, device=dev)
     agg = torch.empty(N, K * H, device=dev)
-    am = torch.empty(N, H, dtype=torch.uint8 if flags else torch.int32, device=dev)
+    am = torch.empty(N, H, dtype=torch.uint8 if flags & _lib.FLAG_ARGMAX_U8 else torch.int32, device=dev)
     sm_ = torch.empty(N, H, device=dev)
     dagg = torch.randn(N, K * H, device=dev)
     dh_b = torch.randn(N, H, device=dev)

@@ -55,6 +55,11 @@ enum { GFM_FLAG_AGG_PREPPED = 4 };
 /* gfm_agg_bwd: edge_w is in CSC order (w[q] for CSC slot q, e.g. from
  * gfm_permute) -- a coalesced load instead of a dependent gather w[eid] */
 enum { GFM_FLAG_W_CSC = 8 };
+/* gfm_agg_bwd: the gathered rows are local (batches of small graphs: a
+ * node's neighbours sit in the same few hundred rows, mostly L2 hits) --
+ * shallower gather batches; without it the backward keeps more rows in
+ * flight for scattered (HBM-latency-bound) sources */
+enum { GFM_FLAG_GATHER_LOCAL = 16 };
 /* float32 GEMM engine: tcgen05 3xTF32 (default, fp32-level accuracy),
  * tcgen05 1xTF32 (faster, ~1e-3 relative), the SIMT fp32 engine, or MIXED:
  * 3xTF32 everywhere except the weight-gradient GEMMs (gfm_linear_bwd_weight*,

@@ -640,9 +640,19 @@ _W_CSC = os.environ.get("GFM_W_CSC", "1") != "0"
 
 
 def _argmax_flag(batch) -> int:
-    """uint8 argmax storage when every CSR row is known to hold <= 256 edges"""
+    """uint8 argmax storage when every CSR row is known to hold <= 256 edges;
+    local gathers when the batch is made of small graphs"""
     md = getattr(batch, "max_deg", None)
-    return _lib.FLAG_ARGMAX_U8 if md is not None and md <= 256 else 0
+    f = _lib.FLAG_ARGMAX_U8 if md is not None and md <= 256 else 0
+    n_per = getattr(batch, "host_n_per", None)
+    if n_per is not None and len(n_per) and int(np.max(n_per)) <= _LOCAL_GRAPH_ATOMS:
+        f |= _lib.FLAG_GATHER_LOCAL
+    return f
+
+
+# graphs up to this size count as local for the backward gathers (a graph's
+# rows: <= 4096 x H floats, L2-resident while its edges are gathered)
+_LOCAL_GRAPH_ATOMS = 4096
 
 
 def forward_batch(params: ModelParams, batch: Batch, cache: dict | None = None,
@@ -672,7 +682,7 @@ def forward_batch(params: ModelParams, batch: Batch, cache: dict | None = None,
     am_flag = _argmax_flag(batch)
     for l in range(cfg.mpnn_layers):
         agg = sc.get(f"agg{l}", (N, K * H), dt)
-        argmax = sc.get(f"argmax{l}", (N, H), torch.uint8 if am_flag else torch.int32) \
+        argmax = sc.get(f"argmax{l}", (N, H), torch.uint8 if am_flag & _lib.FLAG_ARGMAX_U8 else torch.int32) \
             if parts & _lib.PART_MAX else None
         smean = sc.get(f"smean{l}", (N, H), dt) if parts & _lib.PART_STD else None
         call("gfm_agg_fwd", ptr(h), N, H, ptr(batch.rowptr), ptr(batch.col_src),
