@@ -392,6 +392,24 @@ GFM_API int gfm_colsum(const void* X, int rows, int cols, int ld, void* out, int
 /* y = alpha x */
 GFM_API int gfm_scale(const void* x, long long n, double alpha, void* y, int dtype, void* stream);
 
+
+/* ---- scoring and ensemble reductions (float64 in numpy's order) ------- */
+/* evaluate's per-batch sums (train.py:178-183): acc[4] (device float64
+ * [sum_e, n_graphs, sum_f, n_comp]) += [pairwise sum |(e - e_true) / n|, B,
+ * pairwise sum |f - f_true| over 3N, 3N] */
+GFM_API int gfm_eval_errors(const void* e_pred, const void* e_true, const int* n_per,
+                            int n_graphs, const void* f_pred, const void* f_true, int n_nodes,
+                            double* acc, int dtype, void* stream);
+/* ensemble.py:121-130, 181: over the member axis of stack [K][n]: mean =
+ * (sum in member order) / K, sigma = sqrt(sum (x - mean)^2 / K), 0 where the
+ * members agree bitwise (mean / sigma may be NULL) */
+GFM_API int gfm_member_stats(const void* stack, int n_members, long long n, void* mean,
+                             void* sigma, int dtype, void* stream);
+/* ensemble.py:133-148: per structure, the (n_g, 3) block of component
+ * spreads -> how 0 max, 1 mean, 2 sqrt(mean of squares) */
+GFM_API int gfm_force_sigma_reduce(const void* sigma_comp, const int* node_offsets, int n_graphs,
+                                   int how, void* out, int dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,9 @@ SIGNATURES = {
     "gfm_gather_batch": (_I, [_P, _P, _I, _I] + [_P] * 25 + [_I, _P]),
     "gfm_gather_blocks": (_I, [_P, _I, _P, _P, _I, _P, _P, _P, _P]),
     "gfm_permute": (_I, [_P, _I, _P, _P, _P, _I, _P]),
+    "gfm_eval_errors": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _I, _P]),
+    "gfm_member_stats": (_I, [_P, _I, _L, _P, _P, _I, _P]),
+    "gfm_force_sigma_reduce": (_I, [_P, _P, _I, _I, _P, _I, _P]),
     "gfm_scan_workspace_bytes": (_S, [_I]),
     "gfm_exclusive_scan": (_I, [_P, _I, _P, _P, _P]),
     "gfm_radius_count": (_I, [_P, _P, _P, _I, _P, _D, _I, _P, _P]),

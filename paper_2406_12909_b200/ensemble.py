@@ -3,8 +3,11 @@
 ``ensemble_predict`` builds ONE device batch (CSR/CSC on the device), runs
 each member's forward pass through the sm_100a kernels into a stacked
 (K, B) / (K, N, 3) device buffer, and reduces the member spread on the
-device -- population sigma (divide by K, exactly 0 where all members agree
-bitwise) and the per-structure force-sigma reduction (max | mean | l2).
+device in numpy's float64 operation order -- mean and population sigma
+(divide by K, exactly 0 where all members agree bitwise; gfm_member_stats)
+and the per-structure force-sigma reduction (max | mean | l2 with numpy's
+pairwise sums; gfm_force_sigma_reduce) -- so they are bit-identical to the
+reference's for identical member predictions.
 Only the (B,) results come back to the host, as numpy like the reference.
 """
 
@@ -15,6 +18,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib
+from ._lib import call, ptr, stream_handle
 from .errors import ConfigError, ValidationError
 from .model import ModelParams, forward_batch, make_batch
 
@@ -30,28 +35,44 @@ class EnsemblePrediction:
     member_count: int
 
 
-def population_sigma(stack: torch.Tensor, dim: int = 0) -> torch.Tensor:
-    """ensemble.py:121-130: sqrt(mean((x - mean)^2)) over ``dim``; entries
+def population_sigma(stack: torch.Tensor) -> torch.Tensor:
+    """ensemble.py:121-130 over the member axis 0 of a device stack: numpy's
+    std (ddof 0) in its float64 operation order (gfm_member_stats); entries
     whose members agree bitwise are exactly 0."""
-    sigma = stack.std(dim=dim, correction=0)
-    spread = stack.amax(dim=dim) - stack.amin(dim=dim)
-    return torch.where(spread == 0, torch.zeros_like(sigma), sigma)
+    _, sigma = member_stats(stack, want_mean=False)
+    return sigma
 
 
-def reduce_force_sigma(sigma_comp: torch.Tensor, graph_of_node: torch.Tensor,
-                       n_graphs: int, how: str = "max") -> torch.Tensor:
-    """ensemble.py:133-148 as a segmented reduction over each structure's
-    3·n components (structures are contiguous node ranges)."""
+def member_stats(stack: torch.Tensor, want_mean: bool = True):
+    """(mean, population sigma) over axis 0 of a (K, ...) device stack, one
+    kernel, numpy's order (sum over members in member order, / K)."""
+    if not stack.is_cuda:
+        raise ValidationError("member_stats needs a device tensor")
+    stack = stack.contiguous()
+    K = int(stack.shape[0])
+    n = stack[0].numel()
+    mean = torch.empty(stack.shape[1:], dtype=stack.dtype, device=stack.device) \
+        if want_mean else None
+    sigma = torch.empty(stack.shape[1:], dtype=stack.dtype, device=stack.device)
+    call("gfm_member_stats", ptr(stack), K, n, ptr(mean), ptr(sigma),
+         _lib.dtype_code(stack.dtype), stream_handle())
+    return mean, sigma
+
+
+def reduce_force_sigma(sigma_comp: torch.Tensor, node_offsets: torch.Tensor,
+                       how: str = "max") -> torch.Tensor:
+    """ensemble.py:133-148: each structure's (n, 3) block of component
+    spreads -> max | mean | rms (numpy's pairwise sums), one thread per
+    structure (gfm_force_sigma_reduce).  ``node_offsets``: device int32
+    (B + 1,), structures contiguous."""
     if how not in FORCE_REDUCTIONS:
         raise ConfigError(f"force reduction must be one of {FORCE_REDUCTIONS}")
-    idx = graph_of_node.long()
-    out = torch.zeros(n_graphs, dtype=sigma_comp.dtype, device=sigma_comp.device)
-    if how == "max":
-        return out.scatter_reduce_(0, idx, sigma_comp.amax(dim=1), "amax", include_self=False)
-    count = torch.zeros_like(out).index_add_(0, idx, torch.full_like(sigma_comp[:, 0], 3.0))
-    if how == "mean":
-        return out.index_add_(0, idx, sigma_comp.sum(dim=1)) / count
-    return torch.sqrt(out.index_add_(0, idx, (sigma_comp * sigma_comp).sum(dim=1)) / count)
+    B = int(node_offsets.shape[0]) - 1
+    out = torch.empty(max(B, 0), dtype=sigma_comp.dtype, device=sigma_comp.device)
+    call("gfm_force_sigma_reduce", ptr(sigma_comp.contiguous()), ptr(node_offsets), B,
+         FORCE_REDUCTIONS.index(how), ptr(out), _lib.dtype_code(sigma_comp.dtype),
+         stream_handle())
+    return out
 
 
 def ensemble_predict(members, records, force_reduction: str = "max", device=None,
@@ -72,10 +93,10 @@ def ensemble_predict(members, records, force_reduction: str = "max", device=None
         params = ModelParams.from_flat(member.model_config, member.flat, device=batch.device,
                                        dtype=dtype)
         e_stack[i], f_stack[i] = forward_batch(params, batch)
-    f_sigma = reduce_force_sigma(population_sigma(f_stack), batch.graph_of_node, B,
-                                 force_reduction)
+    f_sigma = reduce_force_sigma(population_sigma(f_stack), batch.node_offsets, force_reduction)
+    e_mean, e_sigma = member_stats(e_stack)
     return EnsemblePrediction(
-        energy_mean=e_stack.mean(dim=0).cpu().numpy().astype(np.float64),
-        energy_sigma=population_sigma(e_stack).cpu().numpy().astype(np.float64),
+        energy_mean=e_mean.cpu().numpy().astype(np.float64),
+        energy_sigma=e_sigma.cpu().numpy().astype(np.float64),
         force_sigma=f_sigma.cpu().numpy().astype(np.float64),
         member_count=len(members))

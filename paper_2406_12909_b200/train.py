@@ -961,10 +961,11 @@ def evaluate(params: ModelParams, store, comm: Comm, group: str = "valset",
         if batch is None:
             continue
         e_pred, f_pred = forward_batch(params, batch)
-        acc[0] += ((e_pred - batch.energy_true) / batch.n_per_graph.to(e_pred.dtype)).abs().sum()
-        acc[1] += batch.n_graphs
-        acc[2] += (f_pred - batch.forces_true).abs().sum()
-        acc[3] += 3.0 * batch.n_nodes
+        # numpy's pairwise sums of this batch added to the running float64
+        # totals in the reference's order (train.py:180-183)
+        call("gfm_eval_errors", ptr(e_pred), ptr(batch.energy_true), ptr(batch.n_per_graph),
+             batch.n_graphs, ptr(f_pred), ptr(batch.forces_true), batch.n_nodes, ptr(acc),
+             _lib.dtype_code(e_pred.dtype), stream_handle())
     totals = comm.allreduce_sum(acc.cpu().numpy())
     energy_mae = totals[0] / totals[1] if totals[1] else 0.0
     force_mae = totals[2] / totals[3] if totals[3] else 0.0

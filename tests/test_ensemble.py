@@ -1,6 +1,7 @@
 """Ensemble inference (ensemble.py:121-186): the device spread reductions
-against the oracle's numpy restatement (CPU tensors), and ensemble_predict
-through the sm_100a forward against the oracle (GPU, float64, 1e-10)."""
+against the oracle's numpy restatement (bitwise, float64), and
+ensemble_predict through the sm_100a forward against the oracle (GPU,
+float64, 1e-10)."""
 
 import numpy as np
 import pytest
@@ -13,24 +14,30 @@ from paper_2406_12909_b200.errors import ConfigError, ValidationError  # noqa: E
 from paper_2406_12909_b200.records import GraphRecord  # noqa: E402
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("how", EN.FORCE_REDUCTIONS)
 def test_spread_reductions_match_oracle(how):
+    """gfm_member_stats / gfm_force_sigma_reduce == numpy (the oracle's
+    restatement of ensemble.py:121-148), bitwise in float64 -- including a
+    structure of 300 atoms (900 components: numpy's pairwise recursion)"""
     rng = np.random.default_rng(0)
-    f = rng.standard_normal((4, 23, 3))
+    f = rng.standard_normal((4, 323, 3))
     f[:, 5] = f[0, 5]  # all members agree on node 5: exactly zero spread
-    offsets = np.array([0, 4, 4 + 9, 23])
-    gnode = torch.from_numpy(np.repeat(np.arange(3), np.diff(offsets)).astype(np.int32))
-    sig = EN.population_sigma(torch.from_numpy(f))
+    offsets = np.array([0, 4, 4 + 9, 23, 323])
+    sig = EN.population_sigma(torch.from_numpy(f).cuda())
     want = O.population_sigma(f)
-    np.testing.assert_allclose(sig.numpy(), want, rtol=1e-14, atol=0)
-    assert np.all(sig.numpy()[5] == 0.0)
-    got = EN.reduce_force_sigma(sig, gnode, 3, how).numpy()
-    np.testing.assert_allclose(got, O.reduce_force_sigma(want, offsets, how), rtol=1e-14)
+    np.testing.assert_array_equal(sig.cpu().numpy(), want)
+    assert np.all(sig.cpu().numpy()[5] == 0.0)
+    mean, _ = EN.member_stats(torch.from_numpy(f).cuda())
+    np.testing.assert_array_equal(mean.cpu().numpy(), f.mean(axis=0))
+    off = torch.as_tensor(offsets.astype(np.int32)).cuda()
+    got = EN.reduce_force_sigma(sig, off, how).cpu().numpy()
+    np.testing.assert_array_equal(got, O.reduce_force_sigma(want, offsets, how))
 
 
 def test_reduction_name_checked():
     with pytest.raises(ConfigError):
-        EN.reduce_force_sigma(torch.zeros(2, 3), torch.zeros(2, dtype=torch.int32), 1, "median")
+        EN.reduce_force_sigma(torch.zeros(2, 3), torch.zeros(2, dtype=torch.int32), "median")
     with pytest.raises(ValidationError):
         EN.ensemble_predict([], [])
 
