@@ -179,6 +179,113 @@ class TorchComm(Comm):
         return box[0]
 
 
+class _PeerHub:
+    """Shared state of the thread ranks of one process."""
+
+    def __init__(self, size: int, timeout: float):
+        import threading
+        self.size = size
+        self.timeout = timeout
+        self.barrier = threading.Barrier(size)
+        self.slots = [None] * size
+
+
+class ThreadPeerComm(Comm):
+    """Thread ranks in ONE process (the reference's thread mode,
+    create_thread_comms, comm.py:219-230; cli.py:297-311): one thread per
+    rank, each driving its own GPU.  Host collectives exchange objects
+    through shared slots and sum float64 vectors in ascending rank order
+    (comm.py:143-147).  The device allreduce copies every peer's tensor over
+    NVLink (peer copies ordered by CUDA events, no host round trip of the
+    data) and sums them in ascending rank order in float64 on every rank, so
+    all ranks hold identical bytes.  The rendezvous is a host barrier, so a
+    step using this comm cannot be captured in a CUDA graph
+    (``capturable = False``: runners step eagerly)."""
+
+    capturable = False
+
+    def __init__(self, rank: int, hub: _PeerHub):
+        self.rank = rank
+        self.size = hub.size
+        self._hub = hub
+
+    def _exchange(self, obj):
+        h = self._hub
+        h.slots[self.rank] = obj
+        h.barrier.wait(h.timeout)
+        out = list(h.slots)
+        h.barrier.wait(h.timeout)  # nobody reposts before everyone has read
+        return out
+
+    def _host_sum(self, vec):
+        vec = np.ascontiguousarray(vec, dtype=np.float64)
+        parts = self._exchange(vec)
+        for r, p in enumerate(parts):
+            if p.shape != vec.shape:
+                raise ValidationError(f"allreduce count mismatch: rank {r} sent {p.shape[0]}, "
+                                      f"rank {self.rank} has {vec.shape[0]}")
+        total = parts[0].astype(np.float64, copy=True)
+        for p in parts[1:]:  # ascending rank order, always
+            total += p
+        return total
+
+    def allreduce_sum(self, vec):
+        return self._host_sum(vec)
+
+    def allreduce_mean(self, vec):
+        return self._host_sum(vec) / self.size
+
+    def allreduce_sum_(self, tensor):
+        if self.size == 1:
+            return tensor
+        dev = tensor.device
+        s = torch.cuda.current_stream(dev)
+        posted = torch.cuda.Event()
+        posted.record(s)
+        parts = self._exchange((tensor, posted))
+        if any(p[0].shape != tensor.shape or p[0].dtype != tensor.dtype for p in parts):
+            raise ValidationError("allreduce_sum_: ranks passed different shapes / dtypes")
+        with torch.cuda.device(dev):
+            for _, ev in parts:
+                s.wait_event(ev)
+            out = parts[0][0].to(dev, torch.float64)
+            for t, _ in parts[1:]:
+                out += t.to(dev, torch.float64)
+            read = torch.cuda.Event()
+            read.record(s)
+        # every rank has read every tensor before any rank overwrites its own
+        done = self._exchange(read)
+        with torch.cuda.device(dev):
+            for ev in done:
+                s.wait_event(ev)
+            tensor.copy_(out.to(tensor.dtype))
+        return tensor
+
+    def barrier(self):
+        self._exchange(None)
+
+    def gather_obj(self, obj, root: int = 0):
+        if root != 0:
+            raise ValidationError("gathers go to rank 0 only (comm.py:182-184)")
+        out = self._exchange(obj)
+        return out if self.rank == 0 else None
+
+    def broadcast_obj(self, obj, root: int = 0):
+        if root != 0:
+            raise ValidationError("broadcasts come from rank 0 only (comm.py:199-201)")
+        return self._exchange(obj if self.rank == 0 else None)[0]
+
+
+def create_thread_comms(size: int, timeout: float = 60.0) -> list:
+    """``size`` thread-rank comms of this process (comm.py:219-230); rank r's
+    thread calls ``torch.cuda.set_device`` for its GPU and trains with
+    ``comms[r]``."""
+    if size == 1:
+        return [LocalComm()]
+    hub = _PeerHub(size, timeout)
+    return [ThreadPeerComm(r, hub) for r in range(size)]
+
+
 def allreduce_gradients(comm: Comm, grad):
     """Average gradients across ranks (comm.py:271-276)."""
     return comm.allreduce_mean(grad)

@@ -571,7 +571,8 @@ class StructureStepRunner:
                          e=torch.zeros(self.B, dtype=dt, device=dev),
                          f=torch.zeros(self.N, 3, dtype=dt, device=dev))
         self.cur = self.shapes[-1]
-        self.use_graph = use_graph
+        # thread-rank comms rendezvous on the host: no graph capture
+        self.use_graph = use_graph and getattr(trainer.comm, "capturable", True)
         self.loss_host = torch.empty(2, dtype=torch.float32).pin_memory()
         # pipelined stepping: two pinned loss slots, each with its copy event
         self._loss_slots = [torch.empty(2, dtype=torch.float32).pin_memory() for _ in range(2)]
