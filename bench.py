@@ -541,6 +541,14 @@ def measure_step(ctx, W, full=True):
              "indices H2D, loss D2H")
     del store
 
+    # ---- sharded store (DDStore's remote fetch over NVLink, N > 1): every
+    # rank holds 1/N of a group of these structures with 29 record edges per
+    # atom; a batch of B random indices (mostly remote) is fetched by one
+    # collective exchange (counts, indices, sizes, packed arrays by NCCL
+    # all_to_all) and assembled into the CSR on the requester
+    if ctx.world > 1:
+        out["sharded_store_fetch"] = measure_sharded_fetch(ctx, W, B, n)
+
     # ---- load balance (scaling.py:54-72): each rank's compute time (batch
     # assembly + forward + backward, no collective) over its pool
     from paper_2406_12909_b200.telemetry import compute_lif, wait_fraction
@@ -711,6 +719,54 @@ def rooflines(ctx, W, cfg, b, s):
     return res
 
 
+def measure_sharded_fetch(ctx, W, B, n):
+    import torch
+
+    from paper_2406_12909_b200.records import GraphRecord
+    from paper_2406_12909_b200.store import ShardedDeviceStore
+    S = 8 * B * ctx.world  # group size: 8 batches per rank
+    own = None
+    rng = np.random.default_rng(123)  # the same group on every rank
+    from paper_2406_12909_b200.store import OwnershipMap
+    own = OwnershipMap(S, ctx.world)
+    lo, hi = own.range_of(ctx.rank)
+    recs = []
+    deg = 29
+    for k in range(S):
+        z, pos = rng.integers(1, 9, n), rng.uniform(0, W["box"], (n, 3))
+        if lo <= k < hi:
+            src = rng.integers(0, n, n * deg)
+            dst = np.repeat(np.arange(n), deg)
+            recs.append(GraphRecord(z, pos, np.stack([src, dst], 1), float(k), pos * 0.1))
+    store = ShardedDeviceStore({"trainset": (recs, S)}, ctx.comm, device=ctx.dev)
+    pick = np.random.default_rng(1000)  # the global schedule: every rank knows every batch
+    steps = [[pick.choice(S, B, replace=False) for _ in range(ctx.world)] for _ in range(12)]
+    res = {}
+    for mode in ("exchanged", "planned"):
+        for k in range(2):
+            store.fetch_device_batch("trainset", steps[k][ctx.rank],
+                                     plan=steps[k] if mode == "planned" else None)
+        ctx.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(2, 12):
+            b = store.fetch_device_batch("trainset", steps[k][ctx.rank],
+                                         plan=steps[k] if mode == "planned" else None)
+        torch.cuda.synchronize()
+        res[mode] = ctx.max_over_ranks(time.perf_counter() - t0) / 10
+    dt = res["planned"]
+    # bytes a rank receives per batch: (N-1)/N of the structures are remote
+    per_struct = n * (4 + 24 + 24) + 8 + n * deg * 8
+    moved = B * per_struct * (ctx.world - 1) / ctx.world
+    return dict(ms_per_batch=dt * 1e3, ms_per_batch_exchanged=res["exchanged"] * 1e3,
+                batch=B, atoms=n, edges_per_atom=deg,
+                remote_bytes_per_rank=moved, remote_gbs_per_rank=moved / dt / 1e9,
+                nodes=b.n_nodes, edges=b.n_edges,
+                note="store.ShardedDeviceStore.fetch_device_batch, wall time, max over ranks: "
+                     "planned = the global schedule known to every rank (payload all_to_all "
+                     "only, no host sync); exchanged = requests, counts exchanged first")
+
+
 def measure_egnn(ctx, W):
     """C4: the EGNN variant's full training step (forward, forces by the
     reverse pass, loss, tangent forward, reverse over primal + tangent,
@@ -849,6 +905,7 @@ def run_native(args):
             e2e=main["e2e"], e2e_device_store=main["e2e_device_store"],
             roofline=main["roofline"], roofline_agg_fwd=main["roofline_agg_fwd"],
             roofline_gemm=main["roofline_gemm"], neighbour_list=main["neighbour_list"],
+            sharded_store_fetch=main.get("sharded_store_fetch"),
             load_balance=main["load_balance"], cpu_baseline=cpu, clocks=main["clocks"],
             gpu_launches=main["gpu_launches"], launches_per_step=main.get("launches_per_step"),
             **nested)

@@ -383,6 +383,7 @@ class ShardedDeviceStore:
                                                  for r in recs)))
             self._g[name] = self._ingest(recs, bool(periodic))
             self._max_deg[name] = self._global_max(self._g[name]["max_deg"])
+            self._g[name]["sizes"] = self._size_table(own, self._g[name])
 
     @classmethod
     def from_container(cls, path: str, comm, groups=None, replication_factor: int = 1,
@@ -404,6 +405,21 @@ class ShardedDeviceStore:
             return int(x)
         vals = self.comm.gather_obj(int(x))
         return int(self.comm.broadcast_obj(max(vals) if self.rank == 0 else None))
+
+    def _size_table(self, own, g):
+        """(atoms, edges) of every structure of the group on every rank (one
+        host exchange at ingest): with it and a global schedule a fetch needs
+        no size or count exchange"""
+        if self.world == 1:
+            return np.stack([g["n"], g["m"]], 1)
+        shards = self.comm.gather_obj(np.stack([g["n"], g["m"]], 1))
+        table = None
+        if self.rank == 0:
+            table = np.zeros((own.n_samples, 2), np.int64)
+            for r in range(own.group_size):  # sub-group 0 covers the group
+                lo, hi = own.local_ranges[r]
+                table[lo:hi] = shards[r]
+        return self.comm.broadcast_obj(table)
 
     def _ingest(self, recs, periodic: bool):
         dev = self.device
@@ -445,68 +461,116 @@ class ShardedDeviceStore:
                                [int(x) for x in send_splits], group=self.comm.group)
         return out
 
-    def _blocks(self, idx_host, sizes, n_blocks_src_off, src, width, add=None):
-        """gather blocks idx of `src` (rows per block from n_blocks_src_off)
-        into a contiguous buffer in idx order"""
-        dev = self.device
-        n_out = int(idx_host.shape[0])
-        rows = sizes[idx_host] if n_out else np.zeros(0, np.int64)
-        dst_off = torch.as_tensor(np.concatenate([[0], np.cumsum(rows)]).astype(np.int64),
-                                  device=dev)
-        out = torch.empty((int(rows.sum()),) + tuple(src.shape[1:]), dtype=src.dtype, device=dev)
+    def _upload(self, arrays: dict) -> dict:
+        """host int32 / int64 arrays -> device views, through ONE pinned
+        staging buffer per dtype and an asynchronous copy (no host sync: the
+        caching host allocator keeps the staging block alive until its copy
+        has run)"""
+        out = {}
+        for dt, tdt in ((np.int64, torch.int64), (np.int32, torch.int32)):
+            items = [(k, np.ascontiguousarray(v, dt).reshape(-1)) for k, v in arrays.items()
+                     if np.dtype(v.dtype) == np.dtype(dt)]
+            if not items:
+                continue
+            total = sum(v.shape[0] for _, v in items)
+            host = torch.empty(max(total, 1), dtype=tdt, pin_memory=True)
+            hv = host.numpy()
+            pos = 0
+            spans = []
+            for k, v in items:
+                hv[pos:pos + v.shape[0]] = v
+                spans.append((k, pos, v.shape[0]))
+                pos += v.shape[0]
+            dev = host.to(self.device, non_blocking=True)
+            for k, p0, n in spans:
+                out[k] = dev[p0:p0 + n]
+        return out
+
+    def _gather(self, idx_dev, n_out, src_off_dev, dst_off_dev, rows, src, width, add=None):
+        """blocks idx of `src` -> a contiguous buffer in idx order"""
+        out = torch.empty((int(rows),) + tuple(src.shape[1:]), dtype=src.dtype, device=self.device)
         if n_out and out.numel():
-            idx = torch.as_tensor(idx_host.astype(np.int32), device=dev)
-            call("gfm_gather_blocks", ptr(idx), n_out, ptr(n_blocks_src_off), ptr(dst_off),
+            call("gfm_gather_blocks", ptr(idx_dev), n_out, ptr(src_off_dev), ptr(dst_off_dev),
                  int(width), ptr(src), ptr(out), ptr(add), stream_handle())
         return out
 
-    def fetch_device_batch(self, group: str, indices, dtype=torch.float32):
+    def fetch_device_batch(self, group: str, indices, dtype=torch.float32, plan=None):
         """Collective.  Returns a model.Batch of structures ``indices`` (in
-        that order) or None when this rank requested nothing."""
+        that order) or None when this rank requested nothing.
+
+        ``plan``: every rank's indices for this call (``plan[rank] ==
+        indices``), as a global schedule (epoch_schedule) provides them --
+        then each rank derives what it serves and receives on the host and
+        the exchange is only the payload: no count / index round trips and
+        no host synchronisation, so the fetch queues behind the previous
+        step's GPU work.  Without it the requests are exchanged first."""
         import torch.distributed as dist
 
         from .model import batch_from_device
         own = self.ownership[group]
         g = self._g[group]
+        table = g["sizes"]
         dev = self.device
-        req, send_counts, arrival_to_batch = plan_fetch(indices, own, self.rank, self.world)
-        # 1. request counts and indices (all_to_all)
-        sc = torch.as_tensor(send_counts, device=dev)
-        rc = torch.empty_like(sc)
-        if self.world > 1:
-            dist.all_to_all_single(rc, sc, group=self.comm.group)
-        else:
-            rc.copy_(sc)
-        recv_counts = rc.cpu().numpy()
-        want = self._a2a(torch.as_tensor(req, device=dev), send_counts, recv_counts, (),
-                         torch.int64)
+        W = self.world
+        req, send_counts, arrival_to_batch = plan_fetch(indices, own, self.rank, W)
         lo, _ = own.range_of(self.rank)
-        serve = want.cpu().numpy() - lo                  # local positions I serve
-        # 2. sizes of the served structures back to the requesters
-        sizes = np.stack([g["n"][serve], g["m"][serve]], 1) if serve.size else \
-            np.zeros((0, 2), np.int64)
-        got_sizes = self._a2a(torch.as_tensor(sizes, device=dev), recv_counts, send_counts, (2,),
-                              torch.int64).cpu().numpy()
-        # per-peer row counts of every array (send side: what I serve per peer)
-        peer_of_serve = np.repeat(np.arange(self.world), recv_counts)
-        s_atoms = np.bincount(peer_of_serve, weights=sizes[:, 0], minlength=self.world) \
-            .astype(np.int64) if serve.size else np.zeros(self.world, np.int64)
-        s_edges = np.bincount(peer_of_serve, weights=sizes[:, 1], minlength=self.world) \
-            .astype(np.int64) if serve.size else np.zeros(self.world, np.int64)
-        peer_of_req = np.repeat(np.arange(self.world), send_counts)
-        r_atoms = np.bincount(peer_of_req, weights=got_sizes[:, 0], minlength=self.world) \
-            .astype(np.int64) if got_sizes.size else np.zeros(self.world, np.int64)
-        r_edges = np.bincount(peer_of_req, weights=got_sizes[:, 1], minlength=self.world) \
-            .astype(np.int64) if got_sizes.size else np.zeros(self.world, np.int64)
-        # 3. pack the served structures (device), exchange, unpack in batch order
+        if plan is not None:
+            if len(plan) != W or not np.array_equal(
+                    np.asarray(plan[self.rank], np.int64).reshape(-1),
+                    np.asarray(indices, np.int64).reshape(-1)):
+                raise ValidationError("plan must hold every rank's indices, this rank's == indices")
+            serve_parts, recv_counts = [], np.zeros(W, np.int64)
+            for p in range(W):
+                rq, cnt, _ = plan_fetch(plan[p], own, p, W)
+                st = int(cnt[:self.rank].sum())
+                serve_parts.append(rq[st:st + int(cnt[self.rank])])
+                recv_counts[p] = cnt[self.rank]
+            serve = np.concatenate(serve_parts) - lo
+        else:
+            # request counts and indices (all_to_all; two host syncs)
+            sc = torch.as_tensor(send_counts, device=dev)
+            rc = torch.empty_like(sc)
+            if W > 1:
+                dist.all_to_all_single(rc, sc, group=self.comm.group)
+            else:
+                rc.copy_(sc)
+            recv_counts = rc.cpu().numpy()
+            want = self._a2a(torch.as_tensor(req, device=dev), send_counts, recv_counts, (),
+                             torch.int64)
+            serve = want.cpu().numpy() - lo                  # local positions I serve
+        # every row count from the global size table (host)
+        sizes = table[serve + lo] if serve.size else np.zeros((0, 2), np.int64)
+        got = table[req] if req.size else np.zeros((0, 2), np.int64)
+        peer_of_serve = np.repeat(np.arange(W), recv_counts)
+        peer_of_req = np.repeat(np.arange(W), send_counts)
+        per_peer = lambda peers, col: np.bincount(peers, weights=col, minlength=W).astype(
+            np.int64) if peers.size else np.zeros(W, np.int64)
+        s_atoms, s_edges = per_peer(peer_of_serve, sizes[:, 0]), per_peer(peer_of_serve, sizes[:, 1])
+        r_atoms, r_edges = per_peer(peer_of_req, got[:, 0]), per_peer(peer_of_req, got[:, 1])
+        B = int(arrival_to_batch.shape[0])
+        cum = lambda x: np.concatenate([[0], np.cumsum(x)]).astype(np.int64)
+        n_arr, m_arr = got[:, 0], got[:, 1]
+        src_slot = arrival_to_batch  # batch position b comes from arrival slot src_slot[b]
+        n_b, m_b = n_arr[src_slot], m_arr[src_slot]
+        host_off = cum(n_b)
+        # every small index / offset array of this fetch in one pinned upload
+        up = self._upload(dict(
+            serve=serve.astype(np.int32), p_noff=cum(sizes[:, 0]), p_eoff=cum(sizes[:, 1]),
+            p_soff=np.arange(serve.shape[0] + 1, dtype=np.int64),
+            slot=src_slot.astype(np.int32), a_noff=cum(n_arr), a_eoff=cum(m_arr),
+            a_soff=np.arange(B + 1, dtype=np.int64), host_off=host_off, e_off64=cum(m_b),
+            node_base=host_off[:-1].astype(np.int32), e_off=cum(m_b).astype(np.int32),
+            off32=host_off.astype(np.int32)))
+        ns = int(serve.shape[0])
+        sv = up.get("serve")
         packed = dict(
-            z=self._blocks(serve, g["n"], g["noff"], g["z"], 1),
-            pos=self._blocks(serve, g["n"], g["noff"], g["pos"], 6),
-            forces=self._blocks(serve, g["n"], g["noff"], g["forces"], 6),
-            energy=self._blocks(serve, np.ones_like(g["n"]), g["soff"], g["energy"], 2),
-            edges=self._blocks(serve, g["m"], g["eoff"], g["edges"], 2),
+            z=self._gather(sv, ns, g["noff"], up["p_noff"], sizes[:, 0].sum(), g["z"], 1),
+            pos=self._gather(sv, ns, g["noff"], up["p_noff"], sizes[:, 0].sum(), g["pos"], 6),
+            forces=self._gather(sv, ns, g["noff"], up["p_noff"], sizes[:, 0].sum(), g["forces"], 6),
+            energy=self._gather(sv, ns, g["soff"], up["p_soff"], ns, g["energy"], 2),
+            edges=self._gather(sv, ns, g["eoff"], up["p_eoff"], sizes[:, 1].sum(), g["edges"], 2),
             shift=None if g["shift"] is None else
-            self._blocks(serve, g["m"], g["eoff"], g["shift"], 6))
+            self._gather(sv, ns, g["eoff"], up["p_eoff"], sizes[:, 1].sum(), g["shift"], 6))
         recv = dict(
             z=self._a2a(packed["z"], s_atoms, r_atoms, (), torch.int32),
             pos=self._a2a(packed["pos"], s_atoms, r_atoms, (3,), torch.float64),
@@ -515,36 +579,22 @@ class ShardedDeviceStore:
             edges=self._a2a(packed["edges"], s_edges, r_edges, (2,), torch.int32),
             shift=None if g["shift"] is None else
             self._a2a(packed["shift"], s_edges, r_edges, (3,), torch.float64))
-        B = int(arrival_to_batch.shape[0])
         if B == 0:
             return None
-        # arrival slot of each batch position; blocks of the arrival buffers
-        n_arr, m_arr = got_sizes[:, 0], got_sizes[:, 1]
-        a_noff = torch.as_tensor(np.concatenate([[0], np.cumsum(n_arr)]).astype(np.int64),
-                                 device=dev)
-        a_eoff = torch.as_tensor(np.concatenate([[0], np.cumsum(m_arr)]).astype(np.int64),
-                                 device=dev)
-        a_soff = torch.as_tensor(np.arange(B + 1, dtype=np.int64), device=dev)
-        src_slot = arrival_to_batch  # batch position b comes from arrival slot src_slot[b]
-        n_b, m_b = n_arr[src_slot], m_arr[src_slot]
-        host_off = np.concatenate([[0], np.cumsum(n_b)]).astype(np.int64)
-        node_base = torch.as_tensor(host_off[:-1].astype(np.int32), device=dev)
-        z = self._blocks(src_slot, n_arr, a_noff, recv["z"], 1)
-        pos = self._blocks(src_slot, n_arr, a_noff, recv["pos"], 6)
-        forces = self._blocks(src_slot, n_arr, a_noff, recv["forces"], 6)
-        energy = self._blocks(src_slot, np.ones(B, np.int64), a_soff, recv["energy"], 2)
+        sl, N, E = up["slot"], int(host_off[-1]), int(m_b.sum())
+        z = self._gather(sl, B, up["a_noff"], up["host_off"], N, recv["z"], 1)
+        pos = self._gather(sl, B, up["a_noff"], up["host_off"], N, recv["pos"], 6)
+        forces = self._gather(sl, B, up["a_noff"], up["host_off"], N, recv["forces"], 6)
+        energy = self._gather(sl, B, up["a_soff"], up["a_soff"], B, recv["energy"], 2)
         # record-local endpoints + the structure's node base in the batch
-        edges = self._blocks(src_slot, m_arr, a_eoff, recv["edges"], 2, add=node_base)
+        edges = self._gather(sl, B, up["a_eoff"], up["e_off64"], E, recv["edges"], 2,
+                             add=up["node_base"])
         shift = None if g["shift"] is None else \
-            self._blocks(src_slot, m_arr, a_eoff, recv["shift"], 6)
-        e_off = np.concatenate([[0], np.cumsum(m_b)]).astype(np.int32)
-        assert int(e_off[-1]) == edges.shape[0]
-        src = edges[:, 0].contiguous()
-        dst = edges[:, 1].contiguous()
-        return batch_from_device(z, pos, energy.to(dtype), forces.to(dtype), src, dst,
-                                 torch.as_tensor(e_off, device=dev),
-                                 torch.as_tensor(host_off.astype(np.int32), device=dev),
-                                 host_off, dtype, shift, self._max_deg[group])
+            self._gather(sl, B, up["a_eoff"], up["e_off64"], E, recv["shift"], 6)
+        return batch_from_device(z, pos, energy.to(dtype), forces.to(dtype),
+                                 edges[:, 0].contiguous(), edges[:, 1].contiguous(),
+                                 up["e_off"], up["off32"], host_off, dtype, shift,
+                                 self._max_deg[group])
 
     def fetch_batch(self, group, indices):
         raise ValidationError("a sharded store fetches collectively: use fetch_device_batch")

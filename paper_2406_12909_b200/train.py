@@ -932,11 +932,12 @@ def load_checkpoint(path: str) -> Checkpoint:
                       epoch=epoch, base_seed=base_seed)
 
 
-def _fetch_batch(store, group: str, indices, device, dtype):
+def _fetch_batch(store, group: str, indices, device, dtype, plan=None):
     """one batch from any store: a collective store (store.ShardedDeviceStore)
-    is called on every rank, with or without indices; None = nothing here"""
+    is called on every rank, with or without indices (``plan``: every rank's
+    indices of this call, from the global schedule); None = nothing here"""
     if getattr(store, "collective", False):
-        return store.fetch_device_batch(group, indices, dtype=dtype)
+        return store.fetch_device_batch(group, indices, dtype=dtype, plan=plan)
     if not len(indices):
         return None
     return make_batch(store.fetch_batch(group, indices), device=device, dtype=dtype)
@@ -958,7 +959,9 @@ def evaluate(params: ModelParams, store, comm: Comm, group: str = "valset",
     # run rank 0's batch count, shorter ones with empty requests
     n_rows = -(-n // comm.size) if collective else mine.shape[0]
     for lo in range(0, n_rows, batch_size):
-        batch = _fetch_batch(store, group, mine[lo:lo + batch_size], dev, params.dtype)
+        plan = [np.arange(r, n, comm.size)[lo:lo + batch_size] for r in range(comm.size)] \
+            if collective else None
+        batch = _fetch_batch(store, group, mine[lo:lo + batch_size], dev, params.dtype, plan)
         if batch is None:
             continue
         e_pred, f_pred = forward_batch(params, batch)
@@ -1024,7 +1027,8 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
         else:
             sched = epoch_schedule(n_train, comm.size, model_config.batch_size, config.base_seed,
                                    epoch)
-            mine = sched.for_rank(comm.rank)
+            per_rank = [sched.for_rank(r) for r in range(comm.size)]
+            mine = per_rank[comm.rank]
             steps = sched.max_batches()
         acc = torch.zeros(2, dtype=torch.float64, device=trainer.device)
         for step in range(steps):
@@ -1041,8 +1045,11 @@ def train(model_config: ModelConfig, store, comm: Comm | None = None,
                     runner.run()
             else:
                 with clock.phase("dataload"), _dphase(dclk, "dataload"):
+                    # the global schedule: a collective store plans its
+                    # exchange without request round trips
+                    plan = [b[step] if step < len(b) else [] for b in per_rank]
                     batch = _fetch_batch(store, "trainset", mine[step] if has else [],
-                                         trainer.device, dtype)
+                                         trainer.device, dtype, plan)
                 if batch is not None:
                     with clock.phase("forward"), _dphase(dclk, "forward"):
                         cache: dict = {}

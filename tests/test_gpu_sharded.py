@@ -84,10 +84,13 @@ def _worker(rank, world, port, q):
         lo, hi = st.ownership["trainset"].range_of(rank)
         out["shard"] = (lo, hi)
         # requests crossing both shards, duplicates, one rank idle in step 2
-        reqs = [[[40, 0, 21, 20, 3, 40], [1, 39]], [[5, 6, 33], []]][rank]
+        all_reqs = [[[40, 0, 21, 20, 3, 40], [1, 39]], [[5, 6, 33], []]]
+        reqs = all_reqs[rank]
         ok = []
-        for idx in reqs:
-            b = st.fetch_device_batch("trainset", idx, dtype=torch.float64)
+        # exchanged requests, then the planned (global schedule) exchange
+        for step, idx in enumerate(reqs + reqs):
+            plan = [all_reqs[r][step % 2] for r in range(world)] if step >= 2 else None
+            b = st.fetch_device_batch("trainset", idx, dtype=torch.float64, plan=plan)
             if not idx:
                 ok.append(b is None)
                 continue
@@ -135,7 +138,7 @@ def test_sharded_fetch_two_ranks_nccl():
         p.join(timeout=60)
     for r in (0, 1):
         assert "error" not in res[r], res[r].get("error")
-        assert res[r]["fetch"] == [True, True], res[r]["fetch"]
+        assert res[r]["fetch"] == [True] * 4, res[r]["fetch"]
     assert res[0]["shard"] == (0, 21) and res[1]["shard"] == (21, 41)
     pa, pb, ma, mb = res[0]["train"]
     np.testing.assert_array_equal(pa, pb)
