@@ -385,7 +385,9 @@ GFM_API int gfm_egnn_head_seed(const void* de, const int* gnode, int n, int rows
                                double edot_seed, const void* a, int G, void* ds, void* yb,
                                int ldyb, int dtype, void* stream);
 /* out[c] (+)= sum_{r < rows} X[r][c] (row stride ld), fixed order (two
- * levels through a float64 workspace of gfm_colsum_workspace_bytes) */
+ * levels in one launch through a workspace of gfm_colsum_workspace_bytes:
+ * float64 chunk partials, then per-slab tickets -- zero the workspace
+ * before its first use; every call leaves the tickets at zero) */
 GFM_API size_t gfm_colsum_workspace_bytes(int rows, int cols);
 GFM_API int gfm_colsum(const void* X, int rows, int cols, int ld, void* out, int accumulate,
                        void* workspace, int dtype, void* stream);

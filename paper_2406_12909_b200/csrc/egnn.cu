@@ -469,16 +469,20 @@ __global__ void k_egnn_head_seed(const T* __restrict__ de, const int* __restrict
   }
 }
 
-// deterministic column sums of rows [0, rows) of X (ld), two levels: block
-// (chunk c, slab s) sums rows [c*kColRows, +kColRows) of 32 columns (8 row
-// groups, fixed-order combine, double) into part[c][cols]; a second launch
-// sums the chunk partials in chunk order.  Result depends only on the shape.
+// deterministic column sums of rows [0, rows) of X (ld), two levels in ONE
+// launch: block (chunk c, slab s) sums rows [c*kColRows, +kColRows) of 32
+// columns (8 row groups, fixed-order combine, double) into part[c][cols];
+// the slab's last block to finish (a ticket per slab) sums the chunk
+// partials in chunk order and resets the ticket.  The result depends only
+// on the shape.
 constexpr int kColRows = 256;
 template <typename T>
-__global__ void k_colsum_part(const T* __restrict__ X, int rows, int cols, int ld,
-                              double* __restrict__ part) {
+__global__ void k_colsum(const T* __restrict__ X, int rows, int cols, int ld,
+                         double* __restrict__ part, unsigned* __restrict__ ticket,
+                         T* __restrict__ out, int accumulate) {
   pdl_entry();
   __shared__ double red[8][33];
+  __shared__ bool last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.y * 32 + tx;
   const int r0 = blockIdx.x * kColRows, r1 = min(rows, r0 + kColRows);
@@ -494,17 +498,19 @@ __global__ void k_colsum_part(const T* __restrict__ X, int rows, int cols, int l
     for (int q = 0; q < 8; ++q) t += red[q][tx];
     part[(long long)blockIdx.x * cols + c] = t;
   }
-}
-
-template <typename T>
-__global__ void k_colsum_final(const double* __restrict__ part, int chunks, int cols,
-                               T* __restrict__ out, int accumulate) {
-  pdl_entry();
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    last = atomicAdd(&ticket[blockIdx.y], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (ty == 0 && c < cols) {
     double t = 0.0;
-    for (int k = 0; k < chunks; ++k) t += part[(long long)k * cols + c];
+    for (int k = 0; k < (int)gridDim.x; ++k) t += __ldcg(part + (long long)k * cols + c);
     out[c] = accumulate ? (T)((double)out[c] + t) : (T)t;
   }
+  if (threadIdx.x == 0) ticket[blockIdx.y] = 0u;  // ready for the next call
 }
 
 template <typename T>
@@ -685,7 +691,8 @@ int gfm_egnn_head_seed(const void* de, const int* gnode, int n, int rows, double
 
 size_t gfm_colsum_workspace_bytes(int rows, int cols) {
   const int chunks = rows > 0 ? (rows + kColRows - 1) / kColRows : 1;
-  return sizeof(double) * (size_t)chunks * (size_t)(cols > 0 ? cols : 1);
+  const size_t slabs = (size_t)((cols > 0 ? cols : 1) + 31) / 32;
+  return sizeof(double) * (size_t)chunks * (size_t)(cols > 0 ? cols : 1) + 4 * slabs;
 }
 
 int gfm_colsum(const void* X, int rows, int cols, int ld, void* out, int accumulate,
@@ -694,12 +701,16 @@ int gfm_colsum(const void* X, int rows, int cols, int ld, void* out, int accumul
   cudaStream_t s = (cudaStream_t)stream;
   const int chunks = rows > 0 ? (rows + kColRows - 1) / kColRows : 1;
   double* part = (double*)workspace;
-  GFM_EDISPATCH(dtype, "gfm_colsum",
-                (rows > 0 ? launch_k(k_colsum_part<T>, dim3(chunks, (cols + 31) / 32), 256, 0, s,
-                                     (const T*)X, rows, cols, ld, part)
-                          : cudaMemsetAsync(part, 0, sizeof(double) * cols, s),
-                 launch_k(k_colsum_final<T>, (cols + 255) / 256, 256, 0, s, (const double*)part,
-                          chunks, cols, (T*)out, accumulate)))
+  unsigned* ticket = (unsigned*)(part + (size_t)chunks * cols);
+  if (rows <= 0) {  // empty: out = 0 (or unchanged when accumulating)
+    if (accumulate) return 0;
+    GFM_EDISPATCH(dtype, "gfm_colsum", cudaMemsetAsync(out, 0, sizeof(T) * cols, s))
+  } else {
+    GFM_EDISPATCH(dtype, "gfm_colsum",
+                  launch_k(k_colsum<T>, dim3(chunks, (cols + 31) / 32), 256, 0, s, (const T*)X,
+                           rows, cols, ld, part, ticket, (T*)out, accumulate))
+  }
+  return 0;
 }
 
 int gfm_scale(const void* x, long long n, double alpha, void* y, int dtype, void* stream) {

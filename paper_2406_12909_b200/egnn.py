@@ -221,7 +221,8 @@ class _Pass:
              ptr(g1), ptr(g2), None, ptr(ws), self.code, self.s)
 
     def colsum(self, X, rows, cols, ld, out):
-        ws = self.sc.bytes(f"eg_cs_{cols}", query("gfm_colsum_workspace_bytes", rows, cols))
+        ws = self.sc.bytes(f"eg_cs_{cols}", query("gfm_colsum_workspace_bytes", rows, cols),
+                           zero=True)
         call("gfm_colsum", X, rows, cols, ld, ptr(out), 0, ptr(ws), self.code, self.s)
 
     # ---- passes -------------------------------------------------------------

@@ -601,16 +601,18 @@ class _Scratch:
         self.bufs = {}
         self.ones_ready = {}  # wgrad workspace -> (address, rows) its ones operand was written for
 
-    def get(self, name, shape, dtype):
+    def get(self, name, shape, dtype, zero: bool = False):
         shape = tuple(int(x) for x in shape)
         t = self.bufs.get(name)
         if t is None or t.dtype != dtype or tuple(t.shape) != shape:
-            t = torch.empty(shape, dtype=dtype, device=self.device)
+            t = (torch.zeros if zero else torch.empty)(shape, dtype=dtype, device=self.device)
             self.bufs[name] = t
         return t
 
-    def bytes(self, name, n):
-        return self.get(name, (max(int(n), 1),), torch.uint8)
+    def bytes(self, name, n, zero: bool = False):
+        """``zero``: zero-filled when (re)allocated (workspaces whose
+        counters the kernels keep at zero between calls)"""
+        return self.get(name, (max(int(n), 1),), torch.uint8, zero)
 
     def side_stream(self):
         """second stream for work with no consumer until a later join (one

@@ -94,3 +94,31 @@ def test_egnn_trainer_runner_step_matches_oracle_adam():
 
 def EG_adam(flat, grad, m, v, t):
     return O.adam(flat, grad, m, v, t)
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (255, 33), (1000, 64), (4097, 130)])
+def test_colsum_one_launch_deterministic(rows, cols):
+    """gfm_colsum (chunk partials + last-block final in one launch): float64
+    sums of the columns, bitwise repeatable with the workspace reused (the
+    tickets reset), accumulate mode adds to the output"""
+    from paper_2406_12909_b200 import _lib
+    rng = np.random.default_rng(rows)
+    ld = cols + 3
+    X = torch.as_tensor(rng.standard_normal((rows, ld)), dtype=torch.float32, device="cuda")
+    ws = torch.zeros(_lib.query("gfm_colsum_workspace_bytes", rows, cols), dtype=torch.uint8,
+                     device="cuda")
+    s = _lib.stream_handle()
+    outs = []
+    for _ in range(3):
+        out = torch.empty(cols, dtype=torch.float32, device="cuda")
+        _lib.call("gfm_colsum", _lib.ptr(X), rows, cols, ld, _lib.ptr(out), 0, _lib.ptr(ws),
+                  _lib.F32, s)
+        outs.append(out.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
+    want = X.double().cpu().numpy()[:, :cols].sum(axis=0)
+    np.testing.assert_allclose(outs[0], want, rtol=1e-6, atol=1e-5)
+    acc = torch.ones(cols, dtype=torch.float32, device="cuda")
+    _lib.call("gfm_colsum", _lib.ptr(X), rows, cols, ld, _lib.ptr(acc), 1, _lib.ptr(ws),
+              _lib.F32, s)
+    np.testing.assert_allclose(acc.cpu().numpy(), want + 1.0, rtol=1e-6, atol=1e-5)
