@@ -759,9 +759,10 @@ __device__ __forceinline__ void tma_tile(const TmaOp& op, uint32_t dst, int r0, 
   } else {
     // one 3D load when the whole tile lies in a segment with a 3D view (rows
     // past the last segment's end are TMA zero fill either way)
-    // (the 3D view's box is min(ROWS, 128) rows: the op was built for ROWS)
-    if constexpr (ROWS % 32 == 0 && (ROWS % 128 == 0 || ROWS < 128)) {
-      constexpr int kBox = ROWS < 128 ? ROWS : 128;
+    // (whole 128-row tiles only: narrower 3D boxes measured slower than
+    // 32-row 2D boxes -- C2 step +2%, pair weight gradients +12%)
+    if constexpr (ROWS % 128 == 0) {
+      constexpr int kBox = 128;
       const int seg = r0 >= op.split2 ? 2 : (r0 >= op.split_at ? 1 : 0);
       const int s0 = seg == 2 ? op.split2 : (seg == 1 ? op.split_at : 0);
       const int s1 = seg == 0 ? op.split_at : (seg == 1 ? op.split2 : (1 << 30));
@@ -1675,7 +1676,9 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
         TmaOp tbh;
         // (K-major A only: with the MN-major A of the weight gradients the
         // pair kernel measured 28% slower, forward / backward-data 4-8% faster)
-        if (at == 1 && pairs_enabled() && ceil_div(M, kBM) >= 2 &&
+        // (deep GEMMs only: below K = 512 -- every C2 GEMM -- the pair's
+        // cluster launch and cross-CTA handshakes cost more than it saves)
+        if (at == 1 && pairs_enabled() && ceil_div(M, kBM) >= 2 && K >= 512 &&
             build_tma(b, &tbh, BN / 2, N, K)) {
           auto kp = flush ? (at == 1 ? tc_gemm_tma_pair_kernel<BN, Epi, 1, true>
                                      : tc_gemm_tma_pair_kernel<BN, Epi, 2, true>)
