@@ -666,7 +666,8 @@ def rooflines(ctx, W, cfg, b, s):
     for rnd in ("r02", "r01"):
         try:
             tr_ = json.load(open(os.path.join(ROOT, "profiles", f"{rnd}_agg_traffic_{name}.json")))
-            if tr_.get("config") == name and tr_.get("flags", 0) == flags:
+            # the captured launch must store argmax the same way (u8 or int32)
+            if tr_.get("config") == name and (tr_.get("flags", 0) & 2) == (flags & 2):
                 traffic = tr_
                 break
         except Exception:
