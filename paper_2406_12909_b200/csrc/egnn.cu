@@ -475,7 +475,7 @@ __global__ void k_egnn_head_seed(const T* __restrict__ de, const int* __restrict
 // the slab's last block to finish (a ticket per slab) sums the chunk
 // partials in chunk order and resets the ticket.  The result depends only
 // on the shape.
-constexpr int kColRows = 256;
+constexpr int kColRows = 64;  // 8 rows per thread: many blocks in flight (latency bound)
 template <typename T>
 __global__ void k_colsum(const T* __restrict__ X, int rows, int cols, int ld,
                          double* __restrict__ part, unsigned* __restrict__ ticket,
@@ -505,10 +505,17 @@ __global__ void k_colsum(const T* __restrict__ X, int rows, int cols, int ld,
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // row group ty sums chunks ty, ty + 8, ... in order; the 8 group sums are
+  // combined in group order (fixed for a shape)
+  double t = 0.0;
+  if (c < cols)
+    for (int k = ty; k < (int)gridDim.x; k += 8) t += __ldcg(part + (long long)k * cols + c);
+  red[ty][tx] = t;
+  __syncthreads();
   if (ty == 0 && c < cols) {
-    double t = 0.0;
-    for (int k = 0; k < (int)gridDim.x; ++k) t += __ldcg(part + (long long)k * cols + c);
-    out[c] = accumulate ? (T)((double)out[c] + t) : (T)t;
+    double u = 0.0;
+    for (int q = 0; q < 8; ++q) u += red[q][tx];
+    out[c] = accumulate ? (T)((double)out[c] + u) : (T)u;
   }
   if (threadIdx.x == 0) ticket[blockIdx.y] = 0u;  // ready for the next call
 }
