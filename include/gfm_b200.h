@@ -412,6 +412,23 @@ GFM_API int gfm_member_stats(const void* stack, int n_members, long long n, void
 GFM_API int gfm_force_sigma_reduce(const void* sigma_comp, const int* node_offsets, int n_graphs,
                                    int how, void* out, int dtype, void* stream);
 
+
+/* ---- container ingest (records.py:126-183 payloads -> device arrays) --- */
+/* one thread per payload (blob + offsets[r], lengths[r] bytes): header,
+ * length and zlib CRC32 checks -> n_atoms[r], n_edges[r], status[r] (0 ok,
+ * 1 truncated, 2 length mismatch, 3 checksum mismatch) */
+GFM_API int gfm_record_scan(const void* blob, const long long* offsets, const long long* lengths,
+                            int n_rec, int* n_atoms, int* n_edges, int* status, void* stream);
+/* one warp per (checked) payload: z (int32), pos / forces (float64 [.,3]),
+ * energy, record edges (int32 [.,2], record-local ids) at the records'
+ * exclusive prefix sums atom_offsets / edge_offsets; deg (optional, zeroed
+ * by the caller) += in-degree of every node (global ids); *bad (optional)
+ * |= 1 when an edge endpoint is not below its record's atom count */
+GFM_API int gfm_record_decode(const void* blob, const long long* offsets, int n_rec,
+                              const long long* atom_offsets, const long long* edge_offsets, int* z,
+                              double* pos, double* forces, double* energy, int* edges, int* deg,
+                              int* bad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,8 @@ SIGNATURES = {
     "gfm_eval_errors": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _I, _P]),
     "gfm_member_stats": (_I, [_P, _I, _L, _P, _P, _I, _P]),
     "gfm_force_sigma_reduce": (_I, [_P, _P, _I, _I, _P, _I, _P]),
+    "gfm_record_scan": (_I, [_P, _P, _P, _I, _P, _P, _P, _P]),
+    "gfm_record_decode": (_I, [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "gfm_scan_workspace_bytes": (_S, [_I]),
     "gfm_exclusive_scan": (_I, [_P, _I, _P, _P, _P]),
     "gfm_radius_count": (_I, [_P, _P, _P, _I, _P, _D, _I, _P, _P]),

@@ -107,6 +107,39 @@ def read_range(manifest: ContainerManifest, group: str, index_range, path: str):
     return out
 
 
+def read_range_raw(manifest: ContainerManifest, group: str, index_range, path: str,
+                   pinned: bool = False):
+    """The undecoded payloads of [lo, hi) as one byte blob + per-record
+    (offset, length) in it (each sub-file read once) -- for decoding on the
+    device (store.decode_payloads).  ``pinned``: the blob lives in page-locked
+    host memory (a torch tensor's numpy view), so its upload runs at full
+    link speed."""
+    lo, hi = index_range
+    g = manifest.group(group)
+    if not (0 <= lo <= hi <= g.record_count):
+        raise ValidationError(f"range [{lo}, {hi}) out of bounds for group {group!r} "
+                              f"with {g.record_count} records")
+    ent = g.entries[lo:hi]
+    lengths = ent["length"].astype(np.int64)
+    offsets = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    if pinned:
+        import torch
+        blob = torch.empty(max(int(offsets[-1]), 1), dtype=torch.uint8,
+                           pin_memory=True).numpy()[:int(offsets[-1])]
+    else:
+        blob = np.empty(int(offsets[-1]), np.uint8)
+    for sub in np.unique(ent["subfile"]):
+        mine = np.nonzero(ent["subfile"] == sub)[0]
+        with open(os.path.join(path, f"data.{int(sub)}"), "rb") as fh:
+            data = np.frombuffer(fh.read(), np.uint8)
+        for k in mine:
+            o, n = int(ent["offset"][k]), int(ent["length"][k])
+            if o + n > data.shape[0]:
+                raise CorruptionError(f"sub-file data.{int(sub)} truncated at offset {o}")
+            blob[offsets[k]:offsets[k] + n] = data[o:o + n]
+    return blob, offsets[:-1].copy(), lengths
+
+
 def read_group(manifest: ContainerManifest, group: str, path: str) -> list[GraphRecord]:
     """container.py:318-319."""
     return read_range(manifest, group, (0, manifest.group(group).record_count), path)

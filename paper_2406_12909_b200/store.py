@@ -257,6 +257,60 @@ def gather_batch(g: "_Group", idx_dev, meta_dev, n_cap_graphs: int, n_nodes: int
 # --------------------------------------------------------------------------
 
 
+def decode_payloads(blob, offsets, lengths, device=None) -> dict:
+    """Record payloads (records.py:126-183) decoded ON THE DEVICE: the blob
+    goes to HBM once, one thread per record checks header, length and CRC32
+    (gfm_record_scan; CorruptionError like decode_record), one warp per
+    record scatters z / positions / edges / energy / forces into
+    concatenated arrays (gfm_record_decode).  Returns the store's group
+    arrays: n, m (host int64), z, pos, forces, energy, edges (device), noff /
+    eoff / soff (device int64 offsets) and max_deg (host)."""
+    from .errors import CorruptionError
+    _lib.load(require_device=True)
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    S = int(len(offsets))
+    # a page-locked blob (container.read_range_raw(pinned=True)) uploads at
+    # link speed; torch.from_numpy keeps the pinned storage's flag
+    host = torch.from_numpy(np.ascontiguousarray(blob, np.uint8))
+    blob_d = host.to(dev, non_blocking=host.is_pinned())
+    off_d = torch.as_tensor(np.asarray(offsets, np.int64), device=dev)
+    len_d = torch.as_tensor(np.asarray(lengths, np.int64), device=dev)
+    nm = torch.empty(3, max(S, 1), dtype=torch.int32, device=dev)
+    s = stream_handle()
+    call("gfm_record_scan", ptr(blob_d), ptr(off_d), ptr(len_d), S, ptr(nm[0]), ptr(nm[1]),
+         ptr(nm[2]), s)
+    n_h, m_h, st = (x[:S].astype(np.int64) for x in nm.cpu().numpy())
+    bad = np.nonzero(st)[0]
+    if bad.size:
+        k = int(bad[0])
+        msg = {1: f"record payload truncated ({int(lengths[k])} bytes)",
+               2: f"record payload length {int(lengths[k])} != expected",
+               3: "record payload checksum mismatch"}[int(st[k])]
+        raise CorruptionError(f"record {k}: {msg}")
+    noff, eoff = (np.concatenate([[0], np.cumsum(x)]).astype(np.int64) for x in (n_h, m_h))
+    N, E = int(noff[-1]), int(eoff[-1])
+    t = lambda a: torch.as_tensor(a, device=dev)
+    z = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
+    pos = torch.empty(max(N, 1), 3, dtype=torch.float64, device=dev)
+    forces = torch.empty(max(N, 1), 3, dtype=torch.float64, device=dev)
+    energy = torch.empty(max(S, 1), dtype=torch.float64, device=dev)
+    edges = torch.empty(max(E, 1), 2, dtype=torch.int32, device=dev)
+    deg = torch.zeros(max(N, 1), dtype=torch.int32, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    noff_d, eoff_d = t(noff), t(eoff)
+    call("gfm_record_decode", ptr(blob_d), ptr(off_d), S, ptr(noff_d), ptr(eoff_d), ptr(z),
+         ptr(pos), ptr(forces), ptr(energy), ptr(edges), ptr(deg), ptr(flag), s)
+    if int(flag.item()):
+        raise ValidationError("edge endpoint out of range")
+    if N and (int(z[:N].min()) < 1 or int(z[:N].max()) > MAX_Z):
+        raise ValidationError(f"atomic numbers must lie in [1, {MAX_Z}]")
+    return dict(n=n_h, m=m_h, noff=noff_d, eoff=eoff_d,
+                soff=t(np.arange(S + 1, dtype=np.int64)), z=z[:N], pos=pos[:N],
+                forces=forces[:N], energy=energy[:S], edges=edges[:E],
+                max_deg=int(deg.max()) if N else 0, shift=None)
+
+
 def partition_for_readers(record_count: int, reader_count: int):
     """container.py:253-268: contiguous, disjoint, sizes differ by at most
     one, the larger ranges on the lower ids."""
@@ -366,12 +420,26 @@ class ShardedDeviceStore:
         self._g = {}
         self._max_deg = {}
         for name, v in groups.items():
-            if isinstance(v, tuple):
+            decoded = None
+            if isinstance(v, tuple) and isinstance(v[0], dict):  # (decoded arrays, total)
+                decoded, total = v
+                recs = None
+            elif isinstance(v, tuple):
                 recs, total = v
             else:
                 recs, total = v, len(v)
             own = OwnershipMap(total, self.world, replication_factor,
                                (chunk_sizes or {}).get(name))
+            if decoded is not None:
+                lo, hi = own.range_of(self.rank)
+                if decoded["n"].shape[0] != hi - lo:
+                    raise ValidationError(f"group {name!r}: shard of rank {self.rank} needs "
+                                          f"{hi - lo} records, got {decoded['n'].shape[0]}")
+                self.ownership[name] = own
+                self._g[name] = decoded
+                self._max_deg[name] = self._global_max(decoded["max_deg"])
+                self._g[name]["sizes"] = self._size_table(own, decoded)
+                continue
             lo, hi = own.range_of(self.rank)
             if not isinstance(v, tuple):
                 recs = recs[lo:hi]
@@ -387,9 +455,11 @@ class ShardedDeviceStore:
 
     @classmethod
     def from_container(cls, path: str, comm, groups=None, replication_factor: int = 1,
-                       device=None) -> "ShardedDeviceStore":
-        """read only this rank's shard of each group (container.read_range)"""
-        from .container import GROUP_NAMES, read_manifest, read_range
+                       device=None, device_decode: bool = True) -> "ShardedDeviceStore":
+        """read only this rank's shard of each group: its payload bytes go to
+        HBM undecoded and are checked and decoded there (decode_payloads);
+        ``device_decode=False`` decodes on the host (container.read_range)"""
+        from .container import GROUP_NAMES, read_manifest, read_range, read_range_raw
         man = read_manifest(path)
         out = {}
         for g in (groups or GROUP_NAMES):
@@ -397,7 +467,11 @@ class ShardedDeviceStore:
             if not n:
                 continue
             lo, hi = OwnershipMap(n, comm.size, replication_factor).range_of(comm.rank)
-            out[g] = (read_range(man, g, (lo, hi), path), n)
+            if device_decode:
+                blob, offs, lens = read_range_raw(man, g, (lo, hi), path, pinned=True)
+                out[g] = (decode_payloads(blob, offs, lens, device), n)
+            else:
+                out[g] = (read_range(man, g, (lo, hi), path), n)
         return cls(out, comm, replication_factor, device)
 
     def _global_max(self, x: int) -> int:
