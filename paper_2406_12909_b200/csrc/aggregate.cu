@@ -635,14 +635,24 @@ __device__ __forceinline__ void agg_bwd_node(LG ldG, LC ldC, LA ldA, bool hasG, 
       if (hasC) dm = fma4(r.cf[v], mul4(hj[v], bcast4(wv)), dm);
       if (hasA) {
         const int4 am = r.a[v];
-        const int pp = am_u8 ? (p & 0xFF) : p;
-        if (am.x == pp || am.y == pp || am.z == pp || am.w == pp) {
+        if (am_u8) {
+          // four low-byte argmaxes packed in am.x: one byte-wise compare
+          const unsigned eq = __vcmpeq4((unsigned)am.x, (unsigned)(p & 0xFF) * 0x01010101u);
+          if (eq) {
+            const float4 d = PF ? r.d[v]
+                                : __ldg(reinterpret_cast<const float4*>(dmax + (long long)i * ldm) + c4);
+            if (eq & 0x000000FFu) dm.x += d.x;
+            if (eq & 0x0000FF00u) dm.y += d.y;
+            if (eq & 0x00FF0000u) dm.z += d.z;
+            if (eq & 0xFF000000u) dm.w += d.w;
+          }
+        } else if (am.x == p || am.y == p || am.z == p || am.w == p) {
           const float4 d = PF ? r.d[v]
                               : __ldg(reinterpret_cast<const float4*>(dmax + (long long)i * ldm) + c4);
-          if (am.x == pp) dm.x += d.x;
-          if (am.y == pp) dm.y += d.y;
-          if (am.z == pp) dm.z += d.z;
-          if (am.w == pp) dm.w += d.w;
+          if (am.x == p) dm.x += d.x;
+          if (am.y == p) dm.y += d.y;
+          if (am.z == p) dm.z += d.z;
+          if (am.w == p) dm.w += d.w;
         }
       }
       acc[v] = fma4(dm, bcast4(wv), acc[v]);
@@ -762,7 +772,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? (LPN == 32 ? (GFM_AGG_BWD_MINB 
           const unsigned b = __ldg(reinterpret_cast<const unsigned*>(
                                        reinterpret_cast<const unsigned char*>(argmax) + (long long)i * H) +
                                    v * LPN + cb);
-          return make_int4(b & 0xFF, (b >> 8) & 0xFF, (b >> 16) & 0xFF, b >> 24);
+          return make_int4((int)b, 0, 0, 0);  // packed: compared with __vcmpeq4
         }
         return __ldg(reinterpret_cast<const int4*>(argmax + (long long)i * H) + v * LPN + cb);
       },
