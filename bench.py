@@ -315,8 +315,10 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in self.rows for k in range(4)
                           if len(r) > 3 + k and r[3 + k].lower() == "active"})
+        pw = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
         return dict(sm_mhz=float(np.median(sm)) if sm else None,
-                    sm_max_mhz=max(mx) if mx else None, reasons=reasons, samples=len(self.rows))
+                    sm_max_mhz=max(mx) if mx else None, reasons=reasons, samples=len(self.rows),
+                    power_w=float(np.median(pw)) if pw else None)
 
 
 # ---------------------------------------------------------------- native leg
