@@ -397,20 +397,26 @@ class ShardedDeviceStore:
     RMA store) rebuilt over NVLink: every rank keeps only
     its OwnershipMap shard of each group in HBM -- structures and their
     records' own edges -- and a batch is assembled by ONE collective
-    exchange: request counts and indices (all_to_all), the owners pack the
-    requested structures on the device (gfm_gather_blocks), the packed
-    arrays travel with all_to_all_single over NCCL, and the requester unpacks
-    them into batch order and builds the CSR/CSC (gfm_csr_build).
+    exchange: the owners pack the requested structures on the device
+    (gfm_gather_blocks), the packed arrays travel with all_to_all_single over
+    NCCL, and the requester unpacks them into batch order and builds the
+    CSR/CSC (gfm_csr_build).  With a plan (every rank's indices, as the
+    global epoch schedule gives them) each rank derives its sends and
+    receives from a global size table; without one, request counts and
+    indices are exchanged first.
 
     ``fetch_device_batch`` is collective: every rank of ``comm`` calls it
-    once per step (an idle rank with no indices)."""
+    once per step (an idle rank with no indices).  Groups come as record
+    lists, (shard records, total) or (decode_payloads arrays, total) --
+    ``from_container`` decodes the rank's payloads on the device."""
 
     collective = True
 
     def __init__(self, groups: dict, comm, replication_factor: int = 1, device=None,
                  chunk_sizes=None):
-        """``groups``: {name: full record list} (each rank keeps its shard)
-        or {name: (records of this rank's shard, total count)}."""
+        """``groups``: {name: full record list} (each rank keeps its shard),
+        {name: (records of this rank's shard, total count)} or {name:
+        (decode_payloads dict of this rank's shard, total count)}."""
         _lib.load(require_device=True)
         self.comm = comm
         self.rank, self.world = comm.rank, comm.size
