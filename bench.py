@@ -716,9 +716,11 @@ def rooflines(ctx, W, cfg, b, s):
     res["roofline_gemm"] = dict(
         kernel="layer weight gradient (tcgen05 3xTF32 split-K + ordered reduce)", bound="tensor",
         achieved=tf, peak=pk, unit="TFLOP/s", frac=tf / pk, launch_ms=wg_ms,
-        algorithmic_flops=flops,
+        algorithmic_flops=flops, issued_tf32_tflops=3.0 * tf, issued_frac_of_tf32=3.0 * tf / (pk / 2),
+        tensor_pipe_active="72% (ncu, profiles/r02_ncu_wgrad.txt)",
         note="useful fp32 flops; each product costs 3 TF32 MMAs (hi*hi + hi*lo + lo*hi); peak "
-             "= MEASURED_PEAKS bf16 sustained")
+             "= MEASURED_PEAKS bf16 sustained; TF32 MMAs run at half the bf16 rate, so the "
+             "issued TF32 rate is compared with peak / 2")
     return res
 
 
