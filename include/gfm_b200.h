@@ -76,6 +76,8 @@ GFM_API int gfm_get_gemm_mode(void);
 /* tcgen05 3xTF32 GEMMs on CTA pairs (cta_group::2, M = 256 MMAs, each CTA
  * staging half of the B tile): 1 on, 0 off; returns the previous setting */
 GFM_API int gfm_set_tc_pairs(int on);
+/* CTA-pair GEMM launches since the library was loaded (diagnostics) */
+GFM_API long long gfm_tc_pair_launches(void);
 
 /* ---- K1/K2: batch geometry (preprocess.py:90-104, model.py:234-285) --- */
 /* gnode[i] = graph of node i (model.py:243) */

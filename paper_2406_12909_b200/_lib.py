@@ -52,6 +52,7 @@ SIGNATURES = {
     "gfm_set_gemm_mode": (_I, [_I]),
     "gfm_get_gemm_mode": (_I, []),
     "gfm_set_tc_pairs": (_I, [_I]),
+    "gfm_tc_pair_launches": (_L, []),
     "gfm_graph_of_node": (_I, [_P, _I, _P, _P]),
     "gfm_gather_structures": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P]),
     "gfm_gather_batch": (_I, [_P, _P, _I, _I] + [_P] * 25 + [_I, _P]),

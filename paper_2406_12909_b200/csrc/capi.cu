@@ -10,6 +10,8 @@ static thread_local char g_err[512] = "";
 static int g_gemm_mode = GFM_GEMM_TC3;
 
 int gemm_mode() { return g_gemm_mode; }
+// launches of the CTA-pair GEMM kernel since load (tests assert the path ran)
+long long g_pair_launches = 0;
 // CTA-pair GEMM kernels (default on; GFM_TC_PAIR=0 at first use or
 // gfm_set_tc_pairs(0) selects the single-CTA kernels)
 static int g_tc_pairs = -1;
@@ -52,6 +54,8 @@ int gfm_set_gemm_mode(int mode) {
 }
 
 int gfm_get_gemm_mode(void) { return gfm::g_gemm_mode; }
+
+long long gfm_tc_pair_launches(void) { return gfm::g_pair_launches; }
 
 int gfm_set_tc_pairs(int on) {
   const int prev = gfm::tc_pairs() ? 1 : 0;

@@ -17,6 +17,7 @@ void set_error(const char* fmt, ...);
 // Process-wide GEMM engine selection for float32 (GFM_GEMM_*).
 int gemm_mode();
 bool tc_pairs();
+extern long long g_pair_launches;
 
 // ---------------------------------------------------------------------------
 // Exactly-rounded arithmetic.  nvcc contracts a*b+c into FMA by default; the

@@ -1712,6 +1712,7 @@ inline cudaError_t launch_bn(int M, const int* M_dev, int N, int K, const int* K
           const int pgrid = 2 * (int)std::min<long long>(pw, (long long)max_pairs);
           launch_kc(kp, pgrid, kTmaThreads, smem, s, 2, M, M_dev, N, K, k_chunk, splits, split3,
                     flush_kb(), ta, tbh, epi);
+          ++g_pair_launches;
           return cudaGetLastError();
         }
       }

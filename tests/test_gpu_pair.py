@@ -20,20 +20,26 @@ def _rand(*shape, seed=0):
     return torch.randn(*shape, device="cuda", generator=g)
 
 
-def _both(fn):
-    """fn() with the single-CTA kernels, then with CTA pairs"""
+def _both(fn, pairs_expected=None):
+    """fn() with the single-CTA kernels, then with CTA pairs (asserting
+    whether the pair kernel ran)"""
     outs = []
     for on in (0, 1):
         prev = _lib.query("gfm_set_tc_pairs", on)
+        n0 = _lib.query("gfm_tc_pair_launches")
         try:
             outs.append([t.cpu().numpy() for t in fn()])
         finally:
             _lib.query("gfm_set_tc_pairs", prev)
+        ran = _lib.query("gfm_tc_pair_launches") > n0
+        assert ran == (bool(on) and bool(pairs_expected)) or pairs_expected is None, (on, ran)
     return outs
 
 
-@pytest.mark.parametrize("M,K1,K2,N", [(1000, 96, 0, 128), (300, 512, 2048, 512), (129, 64, 0, 64),
-                                       (4096, 640, 0, 96)])
+# (pairs run for K >= 512: the shallower shapes check the single-CTA path is
+# still chosen and unchanged)
+@pytest.mark.parametrize("M,K1,K2,N", [(1000, 96, 0, 128), (300, 512, 2048, 512), (129, 64, 448, 64),
+                                       (4096, 640, 0, 96), (1000, 512, 0, 128)])
 def test_pair_forward_bitwise(M, K1, K2, N):
     X1, X2 = _rand(M, K1, seed=1), _rand(M, max(K2, 1), seed=2)
     W1, W2 = _rand(N, K1, seed=3), _rand(N, max(K2, 1), seed=4)
@@ -47,11 +53,11 @@ def test_pair_forward_bitwise(M, K1, K2, N):
         torch.cuda.synchronize()
         return [Y]
 
-    (a,), (c,) = _both(run)
+    (a,), (c,) = _both(run, pairs_expected=K1 + K2 >= 512 and M > 128)
     np.testing.assert_array_equal(a, c)
 
 
-@pytest.mark.parametrize("M,N,K1,K2", [(1000, 128, 128, 512), (333, 64, 64, 0)])
+@pytest.mark.parametrize("M,N,K1,K2", [(1000, 512, 128, 512), (333, 640, 64, 0), (300, 128, 64, 64)])
 def test_pair_backward_data_bitwise(M, N, K1, K2):
     dY = _rand(M, N, seed=6)
     W1, W2 = _rand(N, K1, seed=7), _rand(N, max(K2, 1), seed=8)
@@ -66,7 +72,7 @@ def test_pair_backward_data_bitwise(M, N, K1, K2):
         torch.cuda.synchronize()
         return [o1, o2] if K2 else [o1]
 
-    a, c = _both(run)
+    a, c = _both(run, pairs_expected=N >= 512 and M > 128)
     for x, y in zip(a, c):
         np.testing.assert_array_equal(x, y)
 
@@ -88,7 +94,7 @@ def test_pair_weight_gradient_bitwise(M, N, K1, K2, bias):
         torch.cuda.synchronize()
         return [g1] + ([g2] if K2 else []) + ([gb] if bias else [])
 
-    a, c = _both(run)
+    a, c = _both(run, pairs_expected=False)  # weight gradients stay single-CTA
     for x, y in zip(a, c):
         np.testing.assert_array_equal(x, y)
     ref = dY.double().T @ X1.double()
