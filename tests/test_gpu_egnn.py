@@ -122,3 +122,34 @@ def test_colsum_one_launch_deterministic(rows, cols):
     _lib.call("gfm_colsum", _lib.ptr(X), rows, cols, ld, _lib.ptr(acc), 1, _lib.ptr(ws),
               _lib.F32, s)
     np.testing.assert_allclose(acc.cpu().numpy(), want + 1.0, rtol=1e-6, atol=1e-5)
+
+
+# float32 at this shape (tools/c4_err.py): e 3.8e-6, forces 9.1e-4 (8,192
+# atoms x 20 neighbours: the reverse pass accumulates more 3xTF32 rounding
+# than the small cases), loss 3.6e-8, gradients <= 1.03e-3
+@pytest.mark.parametrize("dtype,rel,frel,grel", [(F64, 1e-9, 1e-9, 1e-9),
+                                                 (F32, 5e-4, 2e-3, 5e-3)], ids=["f64", "f32"])
+def test_egnn_c4_shape_vs_oracle(dtype, rel, frel, grel):
+    """the benched C4 configuration itself: 256 molecules x 32 atoms, EGNN L3
+    H64 fc 2x64, box 8 A, rc 5 A, 20 neighbours -- energies, forces, loss
+    and the full parameter gradient against the float64 oracle"""
+    recs = O.synthetic(256, n_atoms_range=(32, 32), box_length=8.0, rc=5.0, seed=31, max_nbr=20)
+    ocfg = EG.config(layers=3, hidden=64, fc_layers=2, fc_width=64)
+    cfg = EGNNConfig(egnn_layers=3, egnn_width=64, fc_layers=2, fc_width=64, batch_size=256)
+    flat = EG.init_flat(ocfg, 3)
+    bo = O.pack(recs)
+    (tot, _, _), grad_o, (e_o, f_o) = EG.loss_and_grad(ocfg, flat, bo)
+    params = M.ModelParams.from_flat(cfg, flat, dtype=dtype)
+    b = M.make_batch(as_records(recs), dtype=dtype)
+    e, f = M.forward_batch(params, b)
+    fl = 1e-3 if dtype == F64 else 1e-2
+    assert_close_scaled(e.cpu().numpy(), e_o, rel, fl, what="e_pred")
+    assert_close_scaled(f.cpu().numpy(), f_o, frel, fl, what="forces = -dE/dx")
+    lb, grad = M.loss_and_grad(params, b)
+    assert abs(lb.total - tot) <= rel * abs(tot), (lb.total, tot)
+    g = grad.cpu().numpy()
+    off = 0
+    for name, shape in M.param_shapes(cfg):
+        n = int(np.prod(shape))
+        assert_close_scaled(g[off:off + n], grad_o[off:off + n], grel, fl, what=f"grad {name}")
+        off += n
