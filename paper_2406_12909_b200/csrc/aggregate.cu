@@ -35,6 +35,11 @@
 #ifndef GFM_AGG_BWD_U_DEEP
 #define GFM_AGG_BWD_U_DEEP 2
 #endif
+// 32-lane rows without a max part (one or two gathered rows per slot): 3
+// slots (C5 random sum 0.67 -> 0.73 of HBM; narrow rows lose with 3)
+#ifndef GFM_AGG_BWD_U_DEEP32
+#define GFM_AGG_BWD_U_DEEP32 3
+#endif
 // dmax rows loaded with G / coef / argmax (1) or after the argmax compare
 // (0): the dependent load cost 19% at C3 (tools/agg_knobs3.sh, round 2)
 #ifndef GFM_AGG_BWD_PFMAX
@@ -1033,7 +1038,10 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
 #define GFM_BWD_LAUNCH(NV_, LPN_, U8_, GC_)                                                  \
   do {                                                                                       \
     if (deep) {                                                                              \
-      GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U_DEEP);                             \
+      if constexpr (LPN_ == 32)                                                              \
+        GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U_DEEP32);                         \
+      else                                                                                   \
+        GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U_DEEP);                           \
       break;                                                                                 \
     }                                                                                        \
     GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U);                                    \
