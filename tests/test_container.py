@@ -80,3 +80,23 @@ def test_device_store_from_container():
     np.testing.assert_array_equal(pos.cpu().numpy(), np.concatenate([want[4]["pos"],
                                                                       want[0]["pos"]]))
     np.testing.assert_array_equal(e.cpu().numpy(), [want[4]["energy"], want[0]["energy"]])
+
+
+def test_read_range_raw_is_the_payload_bytes():
+    """the device ingest's input: per-record (offset, length) into one blob
+    holding exactly each record's payload bytes, in index order"""
+    man = C.read_manifest(PATH)
+    for g, (lo, hi) in SPLIT.items():
+        n = hi - lo
+        blob, offs, lens = C.read_range_raw(man, g, (0, n), PATH)
+        ent = man.group(g).entries
+        assert offs.shape == lens.shape == (n,) and int(lens.sum()) == blob.shape[0]
+        for k in range(n):
+            with open(os.path.join(PATH, f"data.{int(ent['subfile'][k])}"), "rb") as fh:
+                fh.seek(int(ent["offset"][k]))
+                raw = fh.read(int(ent["length"][k]))
+            assert bytes(blob[offs[k]:offs[k] + lens[k]]) == raw
+        sub = C.read_range_raw(man, g, (1, n), PATH)
+        assert bytes(sub[0]) == bytes(blob[offs[1]:]) if n > 1 else sub[0].size == 0
+    with pytest.raises(Exception):
+        C.read_range_raw(man, "trainset", (0, 99), PATH)
