@@ -31,7 +31,10 @@ class _Ownership:
 
 
 class _Group:
-    def __init__(self, records, device, arrays=None):
+    def __init__(self, records, device, arrays=None, decoded=None):
+        if decoded is not None:
+            self._from_decoded(decoded, device)
+            return
         if arrays is None:
             if not records:
                 raise ValidationError("a store group needs at least one structure")
@@ -61,6 +64,40 @@ class _Group:
         if self.records is not None:
             self._pack_edges(device)
 
+    def _from_decoded(self, d, device):
+        """a group decoded on the device (decode_payloads): the same fields
+        as the record path, its CSR built from the device arrays -- no host
+        records, no host copies of the structures"""
+        from .model import batch_from_device
+        self.records = None
+        n, m = d["n"], d["m"]
+        if n.shape[0] == 0:
+            raise ValidationError("a store group needs at least one structure")
+        self.host_off = np.concatenate([[0], np.cumsum(n)]).astype(np.int32)
+        self.n_samples = n.shape[0]
+        self.max_atoms = int(n.max())
+        self.host_m = m.astype(np.int64)
+        self.max_edges = int(m.max())
+        self.max_deg = int(d["max_deg"])
+        self.periodic = False
+        self.z, self.pos, self.energy, self.forces = d["z"], d["pos"], d["energy"], d["forces"]
+        self.off = torch.as_tensor(self.host_off, device=device)
+        S, E = self.n_samples, int(m.sum())
+        # record-local edge ids + each structure's node base, one block gather
+        edges = torch.empty(max(E, 1), 2, dtype=torch.int32, device=device)
+        if E:
+            idx = torch.arange(S, dtype=torch.int32, device=device)
+            call("gfm_gather_blocks", ptr(idx), S, ptr(d["eoff"]), ptr(d["eoff"]), 2,
+                 ptr(d["edges"]), ptr(edges), ptr(self.off), stream_handle())
+        e_off = torch.as_tensor(np.concatenate([[0], np.cumsum(m)]).astype(np.int32),
+                                device=device)
+        b = batch_from_device(self.z, self.pos, self.energy, self.forces,
+                              edges[:E, 0].contiguous(), edges[:E, 1].contiguous(), e_off,
+                              self.off, self.host_off.astype(np.int64), torch.float64, None,
+                              self.max_deg)
+        self.csr = dict(rowptr=b.rowptr, col_src=b.col_src, edge_w=b.edge_w, edge_dx=b.edge_dx,
+                        csc_ptr=b.csc_ptr, csc_eid=b.csc_eid, csc_dst=b.csc_dst)
+
     def _pack_edges(self, device):
         """the records' own edges (make_batch semantics, model.py:234-285)
         as one float64 CSR / CSC over the whole group, built once on the
@@ -81,13 +118,16 @@ class _Group:
 class DeviceStructureStore:
     """``{group: [GraphRecord]}`` ingested into HBM once."""
 
-    def __init__(self, groups: dict, device=None, _arrays: dict | None = None):
+    def __init__(self, groups: dict, device=None, _arrays: dict | None = None,
+                 _decoded: dict | None = None):
         _lib.load(require_device=True)
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self._groups = {k: _Group(v, self.device) for k, v in groups.items()}
         for k, a in (_arrays or {}).items():
             self._groups[k] = _Group(None, self.device, a)
+        for k, d in (_decoded or {}).items():
+            self._groups[k] = _Group(None, self.device, decoded=d)
         self.ownership = {k: _Ownership(g.n_samples) for k, g in self._groups.items()}
         self._idx = {}
         self._copy_stream = None
@@ -100,12 +140,46 @@ class DeviceStructureStore:
         return cls({}, device, _arrays=groups)
 
     @classmethod
-    def from_container(cls, path: str, groups=None, device=None) -> "DeviceStructureStore":
-        """Ingest a gfmkit container directory (container.py) into HBM."""
-        from .container import GROUP_NAMES, read_group, read_manifest
+    def from_container(cls, path: str, groups=None, device=None,
+                       device_decode: bool = False) -> "DeviceStructureStore":
+        """Ingest a gfmkit container directory (container.py) into HBM.
+        ``device_decode``: payloads checked and decoded on the GPU
+        (decode_payloads); the store then keeps no host records
+        (``fetch_batch`` is unavailable, ``fetch_device_batch`` serves the
+        batches) -- otherwise records are decoded on the host and kept."""
+        from .container import GROUP_NAMES, read_group, read_manifest, read_range_raw
         man = read_manifest(path)
-        return cls({g: read_group(man, g, path) for g in (groups or GROUP_NAMES)
-                    if man.group(g).record_count}, device)
+        names = [g for g in (groups or GROUP_NAMES) if man.group(g).record_count]
+        if device_decode:
+            dec = {}
+            for g in names:
+                blob, offs, lens = read_range_raw(man, g, (0, man.group(g).record_count), path,
+                                                  pinned=True)
+                dec[g] = decode_payloads(blob, offs, lens, device)
+            return cls({}, device, _decoded=dec)
+        return cls({g: read_group(man, g, path) for g in names}, device)
+
+    def fetch_device_batch(self, group, indices, dtype=torch.float32):
+        """Structures ``indices`` as a model.Batch assembled on the device from
+        the group's per-structure CSR blocks (gfm_gather_batch: bitwise the
+        CSR / CSC make_batch builds from the same records)."""
+        g = self._groups[group]
+        if g.csr is None:
+            raise ValidationError(f"group {group!r} holds no record edges")
+        idx = self._check(g, indices)
+        dev = self.device
+        host_off, e_off = self.batch_layout(group, idx)
+        B, N, E = idx.shape[0], int(host_off[-1]), int(e_off[-1])
+        n_per = np.diff(host_off)
+        meta = np.concatenate([[B, N], host_off, n_per, e_off]).astype(np.int32)
+        meta_d = torch.as_tensor(meta, device=dev)
+        idx_d = torch.as_tensor(idx.astype(np.int32), device=dev)
+        slot = dict(z=torch.empty(max(N, 1), dtype=torch.int32, device=dev),
+                    pos=torch.empty(max(N, 1), 3, dtype=torch.float64, device=dev),
+                    e=torch.empty(B, dtype=dtype, device=dev),
+                    f=torch.empty(max(N, 1), 3, dtype=dtype, device=dev))
+        return gather_batch(g, idx_d, meta_d, B, N, E, dtype, {}, slot, meta_d[2:3 + B],
+                            meta_d[3 + B:3 + 2 * B], meta_d[0:2], host_off.astype(np.int64))
 
     # ---- DDStore surface (ddstore.py:316-490) ----------------------------
     def fetch_batch(self, group, indices):

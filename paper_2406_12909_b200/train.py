@@ -940,6 +940,10 @@ def _fetch_batch(store, group: str, indices, device, dtype, plan=None):
         return store.fetch_device_batch(group, indices, dtype=dtype, plan=plan)
     if not len(indices):
         return None
+    from .store import DeviceStructureStore
+    if isinstance(store, DeviceStructureStore) and store.group(group).csr is not None:
+        # assembled on the device from the stored CSR blocks (== make_batch)
+        return store.fetch_device_batch(group, indices, dtype=dtype)
     return make_batch(store.fetch_batch(group, indices), device=device, dtype=dtype)
 
 

@@ -93,3 +93,35 @@ def test_sharded_store_from_container_device_decode():
     for k in ("edge_w", "edge_dx", "csc_eid", "csc_dst"):
         np.testing.assert_array_equal(getattr(a, k).cpu().numpy()[:E],
                                       getattr(ref, k).cpu().numpy()[:E])
+
+
+def test_device_store_device_decode_and_device_batches():
+    """DeviceStructureStore.from_container(device_decode=True): groups built
+    from device-decoded payloads (no host records); fetch_device_batch ==
+    make_batch of the host-decoded records, bitwise; train() + evaluate()
+    run on it"""
+    from paper_2406_12909_b200 import train as T
+    from paper_2406_12909_b200.store import DeviceStructureStore
+    man = C.read_manifest(PATH)
+    recs = C.read_group(man, "trainset", PATH)
+    st = DeviceStructureStore.from_container(PATH, device_decode=True)
+    assert st.group("trainset").records is None
+    idx = [3, 0, 4, 3]
+    a = st.fetch_device_batch("trainset", idx, dtype=torch.float64)
+    ref = M.make_batch([recs[i] for i in idx], dtype=torch.float64)
+    N, E = ref.n_nodes, ref.n_edges
+    for k in ("z", "pos", "energy_true", "forces_true", "graph_of_node"):
+        np.testing.assert_array_equal(getattr(a, k).cpu().numpy()[:N] if k != "energy_true"
+                                      else getattr(a, k).cpu().numpy(),
+                                      getattr(ref, k).cpu().numpy()[:N] if k != "energy_true"
+                                      else getattr(ref, k).cpu().numpy(), err_msg=k)
+    for k in ("rowptr", "csc_ptr"):
+        np.testing.assert_array_equal(getattr(a, k).cpu().numpy()[:N + 1],
+                                      getattr(ref, k).cpu().numpy(), err_msg=k)
+    for k in ("col_src", "edge_dst", "csc_eid", "csc_dst", "edge_w", "edge_dx"):
+        np.testing.assert_array_equal(getattr(a, k).cpu().numpy()[:E],
+                                      getattr(ref, k).cpu().numpy()[:E], err_msg=k)
+    mc = M.ModelConfig(mpnn_kind="pna-agg", mpnn_layers=2, mpnn_width=16, fc_width=16,
+                       batch_size=2)
+    res = T.train(mc, st, config=T.TrainConfig(max_epochs=1), dtype=torch.float64)
+    assert res.epochs_run == 1 and np.isfinite(res.metrics[0].val_mae)
