@@ -972,10 +972,11 @@ def loss_and_grad(params: ModelParams, batch: Batch, precomputed=None,
     dz = dzl
     agg_ws = sc.bytes("agg_bwd_ws", query("gfm_agg_bwd_workspace_bytes", N, H, parts, code))
     # PNA on the float32 tensor-core engine: backward-data GEMM + agg prep
-    # fused (opt-in GFM_FUSED_PREP=1: even with its loads prefetched per chunk
-    # the epilogue measured 6% slower end to end at C2 than the separate
-    # float4 prep pass)
-    fused_prep = (os.environ.get("GFM_FUSED_PREP") == "1" and dt == torch.float32
+    # fused into its epilogue for wide layers (H >= 256: with the CTA-pair
+    # GEMM the C3 step is 1% faster; at C2 (H 64) the separate float4 prep
+    # pass is 1.5% faster).  GFM_FUSED_PREP=1 / 0 forces it on / off.
+    fp_env = os.environ.get("GFM_FUSED_PREP")
+    fused_prep = ((fp_env == "1" or (fp_env is None and H >= 256)) and dt == torch.float32
                   and parts == 15 and H % 4 == 0 and N > 0
                   and query("gfm_get_gemm_mode") != 0 and not flags & _lib.FLAG_SCALAR)
     up_ws = sc.bytes("up_ws", query("gfm_layer_bwd_data_agg_workspace_bytes", H)) \
