@@ -650,7 +650,21 @@ def rooflines(ctx, W, cfg, b, s):
                   P_(dh_b), P_(h_in), P_(out_b), P_(ws_b), _lib.F32, flags | _lib.FLAG_W_CSC, sh)
 
     agg_fwd_call()
-    fwd_ms, bwd_ms = ctx.launch_ms(agg_fwd_call, s), ctx.launch_ms(agg_bwd_call, s)
+    # at H >= 256 the step computes the prep (G | coef, dmax) in the
+    # backward-data GEMM's epilogue and launches the gather alone
+    # (GFM_FLAG_AGG_PREPPED): time that launch; below, prep + gather
+    prepped = H >= 256 and parts == 15 and os.environ.get("GFM_FUSED_PREP") != "0"
+    agg_bwd_call()  # the prep pass fills G | coef in the workspace
+    dmax = dagg.view(N, K, H)[:, 2].contiguous()
+
+    def agg_bwd_gather():
+        _lib.call("gfm_agg_bwd", P_(dmax), P_(agg), P_(sm_), P_(am), P_(h_in), P_(b.rowptr),
+                  P_(b.csc_ptr), P_(b.csc_eid), P_(b.csc_dst), P_(w_csc), N, H, parts,
+                  P_(dh_b), P_(h_in), P_(out_b), P_(ws_b), _lib.F32,
+                  flags | _lib.FLAG_W_CSC | _lib.FLAG_AGG_PREPPED, sh)
+
+    fwd_ms = ctx.launch_ms(agg_fwd_call, s)
+    bwd_ms = ctx.launch_ms(agg_bwd_gather if prepped else agg_bwd_call, s)
     s4 = 4
     # SURVEY 8(d) C5 formulas, fused mode (ii), s = 4 bytes, pna (k = 4, max + std):
     # fwd: E*H*s + 4E (src) + 4E (w) + 4(N+1) + k*N*H*s + 4*N*H argmax
@@ -679,6 +693,10 @@ def rooflines(ctx, W, cfg, b, s):
         ach = nbytes / (ms_ / 1e3) / 1e9
         l2p = l2.get("l2_read_gbs")
         t = traffic.get(key)
+        if key == "agg_bwd_dram_bytes" and prepped and traffic.get("kernels"):
+            # the gather launch alone (the capture lists prep and gather)
+            t = sum(k["dram_bytes"] for k in traffic["kernels"]
+                    if "k_agg_bwd_vec" in k["name"]) or None
         return dict(kernel=kernel, bound="hbm", achieved=ach, peak=peak, unit="GB/s",
                     frac=ach / peak, traffic=t, launch_ms=ms_, algorithmic_bytes=nbytes,
                     dram_frac=(t / (ms_ / 1e3) / 1e9 / peak) if t else None,
@@ -688,7 +706,9 @@ def rooflines(ctx, W, cfg, b, s):
                     note=note)
 
     res = dict(
-        roofline=roof("gfm_agg_bwd (pna CSC gather, uint8 argmax as in the step)", bwd_bytes,
+        roofline=roof("gfm_agg_bwd (pna CSC gather, uint8 argmax as in the step"
+                      + ("; prep fused into the backward-data GEMM: the gather launch alone)"
+                         if prepped else "; prep + gather)"), bwd_bytes,
                       bwd_ms, "agg_bwd_dram_bytes",
                       "frac = SURVEY 8(d) bwd bytes (argmax counted at 4 B/elem as 8(d) "
                       "states; the step stores 1 B) / time / HBM peak.  The per-edge row "
