@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define GFM_ABI_VERSION 2
+#define GFM_ABI_VERSION 3
 
 enum { GFM_F32 = 0, GFM_F64 = 1 };
 enum { GFM_EINVAL = -1 };

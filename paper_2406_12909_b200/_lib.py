@@ -25,7 +25,7 @@ FLAG_ARGMAX_U8 = 2
 FLAG_AGG_PREPPED = 4
 FLAG_W_CSC = 8
 FLAG_GATHER_LOCAL = 16
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
