@@ -37,6 +37,12 @@
 #endif
 // 32-lane rows without a max part (one or two gathered rows per slot): 3
 // slots (C5 random sum 0.67 -> 0.73 of HBM; narrow rows lose with 3)
+// 32-lane rows WITH a max part and scattered (non-local) sources: 2 slots
+// (C5 random pna at E = 16M, H >= 128: 0.58-0.60 -> 0.63-0.64 of HBM; the
+// L2-local C3 batches keep 1)
+#ifndef GFM_AGG_BWD_U_MAXSCAT
+#define GFM_AGG_BWD_U_MAXSCAT 2
+#endif
 #ifndef GFM_AGG_BWD_U_DEEP32
 #define GFM_AGG_BWD_U_DEEP32 3
 #endif
@@ -1043,6 +1049,12 @@ cudaError_t agg_bwd(int dtype, const void* dagg, const void* agg, const void* st
       else                                                                                   \
         GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U_DEEP);                           \
       break;                                                                                 \
+    }                                                                                        \
+    if constexpr (LPN_ == 32 && GFM_AGG_BWD_U_MAXSCAT > 1) {                                  \
+      if (!local) {                                                                          \
+        GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U_MAXSCAT);                        \
+        break;                                                                               \
+      }                                                                                      \
     }                                                                                        \
     GFM_BWD_LAUNCH_U(NV_, LPN_, U8_, GC_, GFM_AGG_BWD_U);                                    \
   } while (0)
