@@ -94,15 +94,15 @@ __global__ void __launch_bounds__(256)
         }
       }
       if (coord) {
-        const T s = warp_sum(sp);
-        up0 += r0 * s;
-        up1 += r1 * s;
-        up2 += r2 * s;
+        // r (and rdot) are uniform over the warp: accumulate this lane's
+        // share of sum_e r_e s_e and reduce once per node, not per edge
+        up0 += r0 * sp;
+        up1 += r1 * sp;
+        up2 += r2 * sp;
         if (DUAL) {
-          const T sd = warp_sum(sdp);
-          ud0 += rd0 * s + r0 * sd;
-          ud1 += rd1 * s + r1 * sd;
-          ud2 += rd2 * s + r2 * sd;
+          ud0 += rd0 * sp + r0 * sdp;
+          ud1 += rd1 * sp + r1 * sdp;
+          ud2 += rd2 * sp + r2 * sdp;
         }
       }
     }
@@ -111,6 +111,16 @@ __global__ void __launch_bounds__(256)
       const int ch = lane + 32 * k;
       if (agg) agg[(long long)i * ldg + ch] = acc[k];
       if (DUAL) aggd[(long long)i * ldg + ch] = accd[k];
+    }
+    if (coord) {
+      up0 = warp_sum(up0);
+      up1 = warp_sum(up1);
+      up2 = warp_sum(up2);
+      if (DUAL) {
+        ud0 = warp_sum(ud0);
+        ud1 = warp_sum(ud1);
+        ud2 = warp_sum(ud2);
+      }
     }
     if (coord && lane == 0) {
       const T ci = T(1) / T(e1 - e0 > 1 ? e1 - e0 : 1);
