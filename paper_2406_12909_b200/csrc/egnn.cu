@@ -138,6 +138,37 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Several warp sums at once by recursive halving: 2 sums with 7 shuffles, 4
+// with 10 (instead of 10 / 20 butterflies); every lane gets every sum.
+template <typename T>
+__device__ __forceinline__ void warp_sum2(T& a, T& b) {
+  const int lane = threadIdx.x & 31;
+  const bool up = lane & 16;
+  T k = up ? b : a;
+  k += __shfl_xor_sync(0xffffffffu, up ? a : b, 16);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  a = __shfl_sync(0xffffffffu, k, 0);
+  b = __shfl_sync(0xffffffffu, k, 16);
+}
+template <typename T>
+__device__ __forceinline__ void warp_sum4(T& a, T& b, T& c, T& d) {
+  const int lane = threadIdx.x & 31;
+  bool up = lane & 16;  // lanes 0-15 keep (a, b), 16-31 keep (c, d)
+  T k0 = up ? c : a, k1 = up ? d : b;
+  k0 += __shfl_xor_sync(0xffffffffu, up ? a : c, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, up ? b : d, 16);
+  up = lane & 8;  // then the first or second of the pair
+  T k = up ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, up ? k0 : k1, 8);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  a = __shfl_sync(0xffffffffu, k, 0);
+  b = __shfl_sync(0xffffffffu, k, 8);
+  c = __shfl_sync(0xffffffffu, k, 16);
+  d = __shfl_sync(0xffffffffu, k, 24);
+}
+
 // Edge adjoints, one warp per dst row i.  Inputs: aggb / aggdb = dL/d agg of
 // the layer (and of its tangent), xbo / xdbo = dL/d x' (layer output
 // coordinates; only read when coord).  Outputs: Ab / Adb (dst part of the
@@ -222,22 +253,13 @@ __global__ void __launch_bounds__(256)
         }
       }
       // coordinate update adjoints: x' = x - ci sum r s, xdot' = xdot - ci sum (rdot s + r sdot)
+      // (sb / sdb are warp-uniform; the four warp sums s, sdot, d2b, d2db
+      // are reduced together after the channel loop)
       T sb = 0, sdb = 0, rb0 = 0, rb1 = 0, rb2 = 0, rdb0 = 0, rdb1 = 0, rdb2 = 0;
       if (coord) {
-        const T s = warp_sum(sp);
         sb = -ci * (r0 * xb0 + r1 * xb1 + r2 * xb2);
-        rb0 = -ci * s * xb0;
-        rb1 = -ci * s * xb1;
-        rb2 = -ci * s * xb2;
         if (DUAL) {
-          const T sd = warp_sum(sdp);
           sb += -ci * (rd0 * xdb0 + rd1 * xdb1 + rd2 * xdb2);
-          rb0 += -ci * sd * xdb0;
-          rb1 += -ci * sd * xdb1;
-          rb2 += -ci * sd * xdb2;
-          rdb0 = -ci * s * xdb0;
-          rdb1 = -ci * s * xdb1;
-          rdb2 = -ci * s * xdb2;
           sdb = -ci * (r0 * xdb0 + r1 * xdb1 + r2 * xdb2);
         }
       }
@@ -264,12 +286,33 @@ __global__ void __launch_bounds__(256)
         d2bp += pb * w[k];
         preb[(long long)e * H + ch] = pb;
       }
-      const T d2b = warp_sum(d2bp);
+      T s = sp, sd = sdp, d2b = d2bp, d2db = d2dbp;
+      if (DUAL && coord) {
+        warp_sum4(s, sd, d2b, d2db);
+      } else if (DUAL) {
+        warp_sum2(d2b, d2db);
+      } else if (coord) {
+        warp_sum2(s, d2b);
+      } else {
+        d2b = warp_sum(d2b);
+      }
+      if (coord) {
+        rb0 = -ci * s * xb0;
+        rb1 = -ci * s * xb1;
+        rb2 = -ci * s * xb2;
+        if (DUAL) {
+          rb0 += -ci * sd * xdb0;
+          rb1 += -ci * sd * xdb1;
+          rb2 += -ci * sd * xdb2;
+          rdb0 = -ci * s * xdb0;
+          rdb1 = -ci * s * xdb1;
+          rdb2 = -ci * s * xdb2;
+        }
+      }
       rb0 += T(2) * r0 * d2b;
       rb1 += T(2) * r1 * d2b;
       rb2 += T(2) * r2 * d2b;
       if (DUAL) {
-        const T d2db = warp_sum(d2dbp);
         rb0 += T(2) * rd0 * d2db;
         rb1 += T(2) * rd1 * d2db;
         rb2 += T(2) * rd2 * d2db;
