@@ -97,3 +97,77 @@ def test_thread_ranks_halves_match_union():
     du, ds = p0 - flat, single - flat
     denom = np.maximum(np.abs(ds), 1e-2 * np.abs(ds).max())
     assert (np.abs(du - ds) / denom).max() <= 5e-4
+
+
+class _Store:
+    def __init__(self, groups):
+        self._g = groups
+        self.ownership = {k: type("O", (), {"n_samples": len(v)})() for k, v in groups.items()}
+
+    def fetch_batch(self, group, idx):
+        return [self._g[group][int(i)] for i in idx]
+
+
+def _groups():
+    from paper_2406_12909_b200.records import GraphRecord
+    dicts = O.synthetic(14, n_atoms_range=(4, 12), seed=8)
+    recs = [GraphRecord(d["z"], d["pos"], d["edges"], d["energy"], d["forces"]) for d in dicts]
+    return {"trainset": recs[:11], "valset": recs[11:]}
+
+
+def _train_cfg():
+    return (M.ModelConfig(mpnn_kind="pna-agg", mpnn_layers=2, mpnn_width=16, fc_width=16,
+                          batch_size=3), T.TrainConfig(max_epochs=2, patience=5))
+
+
+def _nccl_worker(rank, world, port, q):
+    import os
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    import torch.distributed as dist
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        from paper_2406_12909_b200.comm import TorchComm
+        mc, cfg = _train_cfg()
+        res = T.train(mc, _Store(_groups()), comm=TorchComm(deterministic=True), config=cfg)
+        q.put((rank, res.params.flatten(), [m.train_loss for m in res.metrics]))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e), None))
+    q.close()
+    q.join_thread()
+    os._exit(0)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_thread_ranks_train_equals_nccl_processes():
+    """train() with two thread ranks (create_thread_comms) == train() with two
+    NCCL processes in deterministic mode, bitwise: both sum the [grad | loss
+    | 1] payload in ascending rank order in float64"""
+    import socket
+
+    import torch.multiprocessing as mp
+    mc, cfg = _train_cfg()
+
+    def fn(c, dev):
+        res = T.train(mc, _Store(_groups()), comm=c, config=cfg)
+        return res.params.flatten(), [m.train_loss for m in res.metrics]
+
+    thr = _threads(fn)
+    np.testing.assert_array_equal(thr[0][0], thr[1][0])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict((r, (a, b)) for r, a, b in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+    assert not isinstance(out[0][0], str), out[0][0]
+    np.testing.assert_array_equal(out[0][0], thr[0][0])
+    assert out[0][1] == thr[0][1]
